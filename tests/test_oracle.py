@@ -1,0 +1,425 @@
+"""Pins for the CPU oracle: the oracle is checked against
+what the paper and the mathematics fix, never against itself.
+
+* the paper's worked example and case studies (tests/golden/*.txt, cited);
+* closed forms (disjoint clauses, paths, complete graphs, stars);
+* an independent brute force written here over Python *sets* (not masks);
+* Koenig's theorem (min vertex cover = max matching in bipartite graphs);
+* the colex-rank closed form of the level-enumeration candidate count;
+* the defining invariants of a (minimal) hitting set and Johnson's bound.
+"""
+import itertools
+import math
+import random
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2011_08373_b200 import synth
+from gr_testutil import load_golden
+
+SAT, UNSAT, NEGV, BAD = oracle.SAT, oracle.UNSAT, oracle.SAT_NEG_VIOLATED, oracle.BADINPUT
+STATUS = {"SAT": SAT, "UNSAT": UNSAT, "SAT_NEG_VIOLATED": NEGV, "BADINPUT": BAD}
+
+
+def masks_of(pos, neg, W=1):
+    cb = synth.batch_from_lists([(64 * W, pos, neg)], W=W)
+    return cb.masks
+
+
+def vars_of(mask):
+    return synth.mask_to_vars([mask])
+
+
+# ---------------------------------------------------------------- golden pins
+def test_paper_example_p1():
+    g = load_golden("paper_example.txt")
+    m, pos, neg, e = g["m"], g["pos"], g["neg"], g["expect"]
+    mk = masks_of(pos, neg)
+    st, a, picks = oracle.greedy(m, len(pos), mk)
+    assert synth.mask_to_vars(a) == [int(x) for x in e["greedy"]]
+    assert st == STATUS[e["greedy_status"][0]]
+    r = oracle.mhs(m, len(pos), mk)
+    assert vars_of(r.assign) == [int(x) for x in e["mhs"]]
+    assert r.status == STATUS[e["mhs_status"][0]]
+    for reduce in (0, 1):
+        r = oracle.pms(m, len(pos), mk, reduce=reduce)
+        assert r.status == SAT
+        assert vars_of(r.assign) == [int(x) for x in e["pms"]]
+        assert r.cost == int(e["pms_cost"][0])
+
+
+@pytest.mark.parametrize("name", ["unrepairable.txt", "write_write_race.txt"])
+def test_case_study_unsat(name):
+    g = load_golden(name)
+    m, pos, neg, e = g["m"], g["pos"], g["neg"], g["expect"]
+    mk = masks_of(pos, neg)
+    if "pms_status" in e:
+        for reduce in (0, 1):
+            assert oracle.pms(m, len(pos), mk, reduce=reduce).status == STATUS[e["pms_status"][0]]
+        assert oracle.pms_brute(m, len(pos), mk).status == STATUS[e["pms_status"][0]]
+    if "mhs_status" in e:
+        assert oracle.mhs(m, len(pos), mk).status == STATUS[e["mhs_status"][0]]
+    if "greedy_status" in e:
+        assert oracle.greedy(m, len(pos), mk)[0] == STATUS[e["greedy_status"][0]]
+
+
+def colex_rank(vars1):
+    """Combinatorial number system: rank = sum_j C(c_j, j), c_1 < c_2 < ... (0-based)."""
+    return sum(math.comb(c - 1, j + 1) for j, c in enumerate(sorted(vars1)))
+
+
+def test_c1_instances_p2_p3():
+    """C1 instances A and B (m = 8).  The candidate count of the
+    plain levelled enumeration is fixed by the closed form
+    sum_{k<k*} C(m,k) + colex_rank + 1 (first witness ends the search)."""
+    cb = synth.c1_instances()
+    exp = [([2, 3, 4], 14), ([1, 5, 6], 49)]
+    for b in range(2):
+        m, npos, mk, _ = cb.instance(b)
+        r = oracle.pms(m, npos, mk, reduce=0)
+        assert (r.status, r.assign, r.cost) == (SAT, exp[b][1], 3)
+        assert vars_of(r.assign) == exp[b][0]
+        want = sum(math.comb(8, k) for k in range(3)) + colex_rank(exp[b][0]) + 1
+        assert r.decided == want
+    assert [41, 54] == [sum(math.comb(8, k) for k in range(3)) + colex_rank(v) + 1 for v, _ in exp]
+
+
+# ---------------------------------------------------------------- closed forms
+def test_triangle_p4_colex_tiebreak():
+    mk = masks_of([[1, 2], [1, 3], [2, 3]], [])
+    assert vars_of(oracle.mhs(3, 3, mk).assign) == [1, 2]
+    assert vars_of(oracle.pms(3, 3, mk).assign) == [1, 2]
+
+
+@pytest.mark.parametrize("sizes", [[1], [2, 3], [3, 1, 4, 2], [5, 5, 5]])
+def test_disjoint_clauses_p5(sizes):
+    pos, v = [], 1
+    for s in sizes:
+        pos.append(list(range(v, v + s)))
+        v += s
+    m = v - 1
+    mk = masks_of(pos, [])
+    want = [c[0] for c in pos]
+    assert vars_of(oracle.mhs(m, len(pos), mk).assign) == want
+    st, a, _ = oracle.greedy(m, len(pos), mk)
+    assert st == SAT and synth.mask_to_vars(a) == want
+
+
+@pytest.mark.parametrize("m,mhs_vars,greedy_vars", [
+    (2, [1], [1]), (3, [2], [2]), (4, [1, 3], [2, 3]), (5, [2, 4], None), (7, [2, 4, 6], None)])
+def test_path_p6(m, mhs_vars, greedy_vars):
+    pos = [[i, i + 1] for i in range(1, m)]
+    mk = masks_of(pos, [])
+    r = oracle.mhs(m, len(pos), mk)
+    assert r.cost == m // 2  # minimum vertex cover of a path on m vertices
+    assert vars_of(r.assign) == mhs_vars
+    if greedy_vars is not None:
+        assert synth.mask_to_vars(oracle.greedy(m, len(pos), mk)[1]) == greedy_vars
+
+
+@pytest.mark.parametrize("n", [3, 4, 5, 6])
+def test_complete_graph_p7(n):
+    pos = [list(e) for e in itertools.combinations(range(1, n + 1), 2)]
+    r = oracle.mhs(n, len(pos), masks_of(pos, []))
+    assert r.cost == n - 1 and vars_of(r.assign) == list(range(1, n))
+
+
+def test_star_p8():
+    pos = [[1, j] for j in range(2, 6)]
+    assert vars_of(oracle.mhs(5, 4, masks_of(pos, [])).assign) == [1]
+    r = oracle.pms(5, 4, masks_of(pos, [[1]]))
+    assert vars_of(r.assign) == [2, 3, 4, 5] and r.cost == 4
+
+
+def test_unsat_p9_and_empty_clauses():
+    assert oracle.pms(1, 1, masks_of([[1]], [[1]])).status == UNSAT
+    # an empty negative clause: all-true and all-false both violate it
+    assert oracle.pms(3, 1, masks_of([[1]], [[]])).status == UNSAT
+    assert oracle.pms(3, 0, masks_of([], [[]])).status == UNSAT
+
+
+def test_trivial_cases():
+    # m = 0, no clauses -> SAT with the empty assignment
+    r = oracle.pms(0, 0, np.zeros((0, 1), np.uint64))
+    assert (r.status, r.assign, r.cost) == (SAT, 0, 0)
+    # only negative clauses -> all-false (always satisfiable)
+    r = oracle.pms(5, 0, masks_of([], [[1, 2], [3]]))
+    assert (r.status, r.assign, r.cost) == (SAT, 0, 0)
+    # only positive clauses (non-empty) -> always SAT
+    r = oracle.pms(5, 2, masks_of([[1, 2], [5]], []))
+    assert r.status == SAT
+
+
+def test_bad_input():
+    mk = masks_of([[1, 9]], [])  # b9 with m = 8
+    assert oracle.pms(8, 1, mk).status == BAD
+    assert oracle.mhs(8, 1, mk).status == BAD
+    assert oracle.greedy(8, 1, mk)[0] == BAD
+    assert oracle.pms(3, 1, masks_of([[1]], []), w=[1, 0, 2]).status == BAD
+
+
+def test_nonminimal_greedy_p10():
+    pos = [[1, 2, 4], [1, 2, 5], [1, 3, 6], [1, 3, 7], [2], [3]]
+    st, a, picks = oracle.greedy(7, len(pos), masks_of(pos, []))
+    assert picks.tolist() == [0, 1, 2]  # b1 (4 clauses), then b2, b3
+    assert synth.mask_to_vars(a) == [2, 3]  # reverse-delete drops b1
+
+
+def bipartite_family(n):
+    """Johnson's bad family: left = n vertices; for i = 2..n, floor(n/i) right
+    vertices each adjacent to i consecutive left vertices.  Right vertices get
+    the low indices.  Returns (m, edges as 1-based pairs, n_left, n_right)."""
+    right = []
+    for i in range(n, 1, -1):
+        for j in range(n // i):
+            right.append(list(range(j * i, (j + 1) * i)))
+    nr = len(right)
+    edges = [[r + 1, nr + u + 1] for r, nb in enumerate(right) for u in nb]
+    return nr + n, edges, n, nr
+
+
+def max_matching(edges, m):
+    """Kuhn's augmenting paths (independent of the oracle)."""
+    adj = {}
+    for a, b in edges:
+        adj.setdefault(a, []).append(b)
+    match = {}
+
+    def aug(u, seen):
+        for v in adj.get(u, []):
+            if v in seen:
+                continue
+            seen.add(v)
+            if v not in match or aug(match[v], seen):
+                match[v] = u
+                return True
+        return False
+
+    return sum(aug(u, set()) for u in adj)
+
+
+def test_bipartite_family_p11_bound():
+    m, edges, nl, nr = bipartite_family(9)
+    assert (m, len(edges), nr) == (23, 60, 14)
+    mk = masks_of(edges, [])
+    r = oracle.mhs(m, len(edges), mk)
+    assert r.cost == nl == max_matching(edges, m)  # Koenig
+    st, a, picks = oracle.greedy(m, len(edges), mk)
+    g = len(synth.mask_to_vars(a))
+    assert g == 14
+    # greedy/OPT = 14/9 > H(2) = 3/2: the "H(max clause size)" bound is false
+    assert Fraction(g, r.cost) > Fraction(3, 2)
+    delta = max(sum(1 for e in edges if v in e) for v in range(1, m + 1))
+    assert Fraction(g) <= sum(Fraction(1, i) for i in range(1, delta + 1)) * r.cost
+
+
+def test_weights_p12_p13():
+    r = oracle.pms(2, 1, masks_of([[1, 2]], []), w=[100, 1])
+    assert vars_of(r.assign) == [2] and r.cost == 1
+    assert synth.mask_to_vars(oracle.greedy(2, 1, masks_of([[1, 2]], []))[1]) == [1]
+    # P13: w = gw*gb + lw^ld with gw = 12, lw = 10
+    vals = sorted({12 * gb + 10 ** ld for gb in (0, 1) for ld in (0, 1, 2)})
+    assert vals == [1, 10, 13, 22, 100, 112]
+    rng = np.random.default_rng(0)
+    w = synth.paper_weights(rng, 1000)
+    assert set(np.unique(w).tolist()) <= set(vals)
+
+
+# ---------------------------------------------------- independent brute force
+def py_brute(m, pos, neg, w):
+    """Minimum of (weight, size, colex rank) over all assignments, with the
+    clauses as Python sets -- a second, encoding-independent definition."""
+    best = None
+    for bits in itertools.product((0, 1), repeat=m):
+        true = {i + 1 for i in range(m) if bits[i]}
+        if all(set(c) & true for c in pos) and all(not set(c) <= true for c in neg):
+            key = (sum(w[i - 1] for i in true), len(true), colex_rank(true))
+            if best is None or key < best[0]:
+                best = (key, sorted(true))
+    return best
+
+
+def rand_instance(rng, m, n, p_neg=0.3, wmax=0):
+    pos, neg, seen = [], [], set()
+    for _ in range(n):
+        s = rng.randint(1, min(m, 4))
+        c = tuple(sorted(rng.sample(range(1, m + 1), s)))
+        isneg = rng.random() < p_neg
+        if (isneg, c) in seen:
+            continue
+        seen.add((isneg, c))
+        (neg if isneg else pos).append(list(c))
+    w = [rng.randint(1, wmax) for _ in range(m)] if wmax else [1] * m
+    return pos, neg, w
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_levelled_equals_brute_force(seed):
+    rng = random.Random(1000 + seed)
+    for trial in range(60):
+        m = rng.randint(1, 9)
+        wmax = 0 if trial % 2 == 0 else rng.choice([3, 100])
+        pos, neg, w = rand_instance(rng, m, rng.randint(1, 12), wmax=wmax)
+        mk = masks_of(pos, neg)
+        bf = py_brute(m, pos, neg, w)
+        ww = w if wmax else None
+        results = [oracle.pms(m, len(pos), mk, w=ww, reduce=r) for r in (0, 1)]
+        results.append(oracle.pms_brute(m, len(pos), mk, w=ww))
+        for r in results:
+            if bf is None:
+                assert r.status == UNSAT
+            else:
+                assert r.status == SAT
+                assert vars_of(r.assign) == bf[1]
+                assert r.cost == bf[0][0]
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_reduce_matches_plain_larger_m(seed):
+    rng = random.Random(77 + seed)
+    for trial in range(25):
+        m = rng.randint(10, 18)
+        pos, neg, w = rand_instance(rng, m, rng.randint(3, 20), wmax=(50 if trial % 3 == 0 else 0))
+        mk = masks_of(pos, neg)
+        ww = w if trial % 3 == 0 else None
+        a = oracle.pms(m, len(pos), mk, w=ww, reduce=0)
+        b = oracle.pms(m, len(pos), mk, w=ww, reduce=1)
+        c = oracle.pms_brute(m, len(pos), mk, w=ww)
+        assert (a.status, a.assign, a.cost) == (b.status, b.assign, b.cost) == (c.status, c.assign, c.cost)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_koenig_bipartite(seed):
+    rng = random.Random(seed)
+    for _ in range(20):
+        nl, nr = rng.randint(1, 7), rng.randint(1, 7)
+        edges = sorted({(l, nl + r) for l in range(1, nl + 1) for r in range(1, nr + 1)
+                        if rng.random() < 0.35})
+        if not edges:
+            continue
+        edges = [list(e) for e in edges]
+        r = oracle.mhs(nl + nr, len(edges), masks_of(edges, []))
+        assert r.cost == max_matching(edges, nl + nr)
+
+
+def test_decided_closed_form_reduced():
+    """With reduce = 1 and unit weights, the candidates tested are exactly
+    sum_{k<k*} C(m_eff, k) + rank(x*) + 1 in the support-relabelled space."""
+    rng = random.Random(5)
+    for _ in range(80):
+        m = rng.randint(2, 14)
+        pos, neg, _ = rand_instance(rng, m, rng.randint(1, 10))
+        mk = masks_of(pos, neg)
+        r = oracle.pms(m, len(pos), mk, reduce=1)
+        if r.status != SAT:
+            continue
+        sup = sorted({v for c in pos for v in c})
+        relabel = {v: i + 1 for i, v in enumerate(sup)}
+        x = [relabel[v] for v in vars_of(r.assign)]
+        k = len(x)
+        assert r.decided == sum(math.comb(len(sup), j) for j in range(k)) + colex_rank(x) + 1
+
+
+# ------------------------------------------------------------- greedy invariants
+def check_greedy_invariants(m, pos, neg, status, chosen, picks):
+    S = set(chosen)
+    assert all(set(c) & S for c in pos)  # a hitting set of phi+ 
+    for x in S:  # minimal: every element has a private clause
+        assert any(set(c) & S == {x} for c in pos)
+    # pick order: newly covered counts are non-increasing (greedy takes the max)
+    unc = [set(c) for c in pos]
+    gains = []
+    for v in picks:
+        gains.append(sum(1 for c in unc if v + 1 in c))
+        unc = [c for c in unc if v + 1 not in c]
+    assert not unc
+    assert all(g > 0 for g in gains)
+    assert all(a >= b for a, b in zip(gains, gains[1:]))
+    assert set(chosen) <= {v + 1 for v in picks}
+    viol = any(set(c) <= S for c in neg)
+    assert status == (NEGV if viol else SAT)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_greedy_properties_and_bound(seed):
+    rng = random.Random(300 + seed)
+    for _ in range(60):
+        m = rng.randint(2, 12)
+        pos, neg, _ = rand_instance(rng, m, rng.randint(1, 16))
+        if not pos:
+            continue
+        mk = masks_of(pos, neg)
+        st, a, picks = oracle.greedy(m, len(pos), mk)
+        chosen = synth.mask_to_vars(a)
+        check_greedy_invariants(m, pos, neg, st, chosen, picks.tolist())
+        opt = py_brute(m, pos, [], [1] * m)[0][1]
+        assert oracle.mhs(m, len(pos), mk).cost == opt
+        delta = max(sum(1 for c in pos if v in c) for v in range(1, m + 1))
+        H = sum(Fraction(1, i) for i in range(1, delta + 1))
+        assert opt <= len(chosen) <= H * opt
+        # unit PMS relations (P14): |MHS| <= |PMS|; MHS feasible for phi- => PMS == MHS
+        r = oracle.pms(m, len(pos), mk)
+        rm = oracle.mhs(m, len(pos), mk)
+        if r.status == SAT:
+            assert rm.cost <= r.cost
+        if rm.status == SAT:
+            assert (r.status, r.assign) == (SAT, rm.assign)
+
+
+def test_greedy_csr_equals_masks():
+    rng = random.Random(9)
+    for _ in range(30):
+        m = rng.randint(2, 12)
+        pos, neg, _ = rand_instance(rng, m, rng.randint(1, 14))
+        st, a, picks = oracle.greedy(m, len(pos), masks_of(pos, neg))
+        po = np.cumsum([0] + [len(c) for c in pos])
+        no = np.cumsum([0] + [len(c) for c in neg])
+        pv = [v - 1 for c in pos for v in c]
+        nv = [v - 1 for c in neg for v in c]
+        g = oracle.greedy_csr(m, po, np.array(pv, np.int32), no, np.array(nv, np.int32))
+        assert g.status == st
+        assert g.picks.tolist() == picks.tolist()
+        assert [i + 1 for i in np.nonzero(g.in_S)[0]] == synth.mask_to_vars(a)
+
+
+def test_invariance_reorder_relabel():
+    rng = random.Random(11)
+    for _ in range(40):
+        m = rng.randint(2, 10)
+        pos, neg, w = rand_instance(rng, m, rng.randint(1, 12), wmax=20)
+        r0 = oracle.pms(m, len(pos), masks_of(pos, neg), w=w)
+        pos2, neg2 = pos[::-1], neg[::-1]
+        r1 = oracle.pms(m, len(pos), masks_of(pos2, neg2), w=w)
+        assert (r0.status, r0.assign, r0.cost) == (r1.status, r1.assign, r1.cost)
+        # insert an unused variable at position 1 (order-preserving relabel)
+        sh = lambda cs: [[v + 1 for v in c] for c in cs]
+        r2 = oracle.pms(m + 1, len(pos), masks_of(sh(pos), sh(neg)), w=[1] + w)
+        assert r2.status == r0.status
+        if r0.status == SAT:
+            assert vars_of(r2.assign) == [v + 1 for v in vars_of(r0.assign)]
+
+
+# ------------------------------------------------------------ P15 (C3 shape)
+def test_p15_product_reasoning_small():
+    """P15 on a shrunken C3: G disjoint groups -> the canonical optimum is the
+    min feasible one-per-group set; checked against the levelled oracle."""
+    for seed in range(5):
+        cb, H, grp = synth.c3_instance(seed=seed, m=15, groups=5, n_rand_pos=12, n_neg=8)
+        m, npos, mk, _ = cb.instance(0)
+        r = oracle.pms(m, npos, mk)
+        n, best = oracle.min_feasible_product(grp, npos, mk)
+        assert n >= 1 and r.status == SAT and r.cost == 5 and r.assign == best
+
+
+def test_c3_structure():
+    cb, H, grp = synth.c3_instance()
+    m, npos, mk, _ = cb.instance(0)
+    assert (m, npos, mk.shape[0]) == (48, 140, 200)
+    gm = [sum(1 << v for v in g) for g in grp]
+    assert all(a & b == 0 for a, b in itertools.combinations(gm, 2))
+    assert all(int(x) in {int(v) for v in mk[:npos, 0]} for x in gm)  # group clauses present
+    hm = sum(1 << v for v in H)
+    assert oracle.feasible(hm, npos, mk)
