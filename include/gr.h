@@ -1,0 +1,204 @@
+/*
+ * gr.h -- C-ABI of libgrsolve.so: the Solve step of GPURepair (arXiv
+ * 2011.08373) on NVIDIA B200 (sm_100a).
+ *
+ * The Solve step (Alg. 1 line `solve`, Alg:gpurepair) takes the
+ * constraint phi over the barrier variables b_1..b_m -- positive
+ * monotone clauses phi+ from data-race traces and negative monotone clauses
+ * phi- from barrier-divergence traces -- and returns an
+ * assignment <res, sol> that enables as few barriers as possible, or UNSAT
+ * (PAPER.md:131-133).  Three solvers are exported:
+ *
+ *   gr_solve_pms   exact (weighted) partial MaxSAT: phi hard, {not b_i} soft
+ *                  (MaxSAT strategy; PMS/WPMS)
+ *   gr_mhs_exact   exact Minimum-Hitting-Set of phi+ 
+ *   gr_mhs_greedy  Johnson's greedy minimal hitting set of phi+ (mhs
+ *                  strategy), pruned to a *minimal* set
+ *                  (reading R12), phi- checked
+ *   gr_mhs_greedy_matrix   the same greedy for one huge phi+ stored as a
+ *                  variable x clause bit matrix in HBM
+ *
+ * Conventions (all calls):
+ *   - Encoding (reading R1): b_i <-> bit (i-1) of a clause mask; a mask is W
+ *     little-endian uint64 words (b_1 = LSB of word 0).  Polarity is
+ *     positional: the first n_pos[b] clauses of instance b are positive.
+ *   - Pointers inside gr_batch / gr_result / gr_bitmatrix are DEVICE
+ *     pointers unless marked "host"; the caller owns every buffer.  The
+ *     library allocates no device memory per call: scratch comes from the
+ *     caller's workspace (size from gr_*_workspace_bytes, 256-byte aligned).
+ *   - Stream-ordered on `s`.  Calls that run a level / iteration loop on the
+ *     host (gr_solve_pms, gr_mhs_exact, gr_exact_finish,
+ *     gr_mhs_greedy_matrix) synchronise `s` for a few bytes of control state
+ *     per level / per 8 iterations; every result is valid once they return.
+ *   - Return value: GR_OK or a negative call-level error (nothing is
+ *     written to outputs then); per-instance outcomes go to `status`.
+ *     UNSAT is a result, not an error.  gr_last_error() describes the last
+ *     negative return of the calling thread.
+ *   - Re-entrant for distinct workspaces / streams.
+ *   - Canonical answers (readings R2, R3, R11): exact solvers return the
+ *     optimum with the smallest colex rank (= numerically smallest mask
+ *     among optimal sets); WPMS minimises (W, k, mask) lexicographically;
+ *     greedy takes the lowest variable index on count ties.
+ */
+#ifndef GR_H
+#define GR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *gr_stream_t; /* a cudaStream_t; NULL = legacy default stream */
+
+/* call-level return codes */
+enum {
+  GR_OK = 0,
+  GR_EINVAL = -1,      /* null pointer, B < 1, W not in {1,2}, bad flags ... */
+  GR_ETOOBIG = -2,     /* a size beyond what the build supports (see each call) */
+  GR_ECUDA = -3,       /* a CUDA runtime error (gr_last_error has the text) */
+  GR_ENOMEM = -4,      /* reserved */
+  GR_EWORKSPACE = -5   /* ws == NULL or ws_bytes < the queried size */
+};
+
+/* per-instance status */
+enum {
+  GR_SAT = 0,
+  GR_UNSAT = 1,              /* no assignment satisfies the hard clauses (R6, R16) */
+  GR_SAT_NEG_VIOLATED = 2,   /* mhs / MHS hits phi+ but some N in phi- has N subset of S:
+                                the caller falls back to MaxSAT */
+  GR_BADINPUT = 3,           /* a bit >= m is set (R8), a weight is 0 (R4), or the
+                                instance exceeds max_clauses */
+  GR_UNSUPPORTED = 4         /* exact solvers: |support(phi+)| > 64, or a weighted
+                                key (W, rank) that does not fit 63 bits */
+};
+
+/* flags of gr_batch.flags */
+enum {
+  GR_FLAG_EXHAUSTIVE = 1     /* exact unit-weight solvers: enumerate the witness level
+                                completely (deterministic work; benchmarking mode).
+                                Results are identical. */
+};
+
+/* A batch of independent Solve-step instances. */
+typedef struct {
+  int32_t B;                /* host: number of instances, >= 1 */
+  int32_t W;                /* host: uint64 words per clause mask, 1 (m <= 64) or 2 (m <= 128) */
+  int64_t total_clauses;    /* host: off[B] (sizes the workspace) */
+  int32_t max_clauses;      /* host: upper bound on off[b+1]-off[b]; <= 4096 for the exact
+                               solvers and for gr_mhs_greedy */
+  uint32_t flags;           /* host: GR_FLAG_* */
+  const int32_t *m;         /* [B] number of barrier variables, 0 <= m[b] <= 64*W */
+  const int64_t *off;       /* [B+1] instance b owns clauses off[b] .. off[b+1]-1 */
+  const int32_t *n_pos;     /* [B] the first n_pos[b] clauses of b are positive (phi+) */
+  const uint64_t *masks;    /* [off[B]][W] clause masks */
+  const uint32_t *w;        /* [B][wstride] weight w_i >= 1 of soft clause (not b_i), i < m[b];
+                               NULL = unit weights (PMS).  Read by gr_solve_pms only. */
+  int32_t wstride;          /* host: row stride of w in elements (>= max m) */
+} gr_batch;
+
+/* Per-instance results (device buffers, written by the library). */
+typedef struct {
+  uint64_t *assign;   /* [B][W] total assignment, bit i-1 = b_i true; 0 when UNSAT/BADINPUT */
+  uint64_t *cost;     /* [B] sum of w_i over true b_i (popcount if unit); UINT64_MAX if UNSAT */
+  int32_t *status;    /* [B] GR_SAT | GR_UNSAT | GR_SAT_NEG_VIOLATED | GR_BADINPUT | GR_UNSUPPORTED */
+  uint64_t *decided;  /* [B] or NULL: candidate assignments whose feasibility was decided
+                         (exact solvers; DESIGN.md §5 defines the count) */
+} gr_result;
+
+/* Workspace bytes for a call on `in`: which = 0 gr_solve_pms, 1 gr_mhs_exact,
+ * 2 gr_mhs_greedy.  Returns 0 on invalid input. */
+size_t gr_workspace_bytes(const gr_batch *in, int which);
+
+/* (a) Exact PMS / WPMS: minimise the weight of the true
+ * b_i subject to every clause of phi; canonical optimum per R2/R3.
+ * Algorithm: device packing (support restriction, dedup, subsumption,
+ * ascending clause size), then ascending cardinality levels k = 1..k_max with
+ * k_max = min(|support(phi+)|, |phi+ after subsumption|) (reading R13); each
+ * level is enumerated in colex order by the persistent enumeration kernel;
+ * unit weights stop at the first level with a witness, weights stop once the
+ * k smallest weights sum to >= the incumbent. */
+int gr_solve_pms(const gr_batch *in, gr_result *out, void *ws, size_t ws_bytes, gr_stream_t s);
+
+/* (b) Exact MHS of phi+ (PAPER.md:11): cardinality only (w ignored, R10);
+ * status GR_SAT_NEG_VIOLATED flags that the canonical MHS breaks phi-. */
+int gr_mhs_exact(const gr_batch *in, gr_result *out, void *ws, size_t ws_bytes, gr_stream_t s);
+
+/* (c) Greedy mhs of phi+ (Johnson 1974): repeatedly take the
+ * variable hitting the most uncovered positive clauses (lowest index on ties,
+ * R11), then reverse-delete in reverse pick order to a minimal hitting set
+ * (R12); GR_SAT_NEG_VIOLATED if the set contains some N of phi- (PAPER.md:26).
+ * One warp per instance; m <= 128 (W <= 2); duplicates are counted as given (R9).
+ * cost = |S|; decided is not written. */
+int gr_mhs_greedy(const gr_batch *in, gr_result *out, void *ws, size_t ws_bytes, gr_stream_t s);
+
+/* ---- sharded exact solving (the multi-GPU driver owns the collective) ----
+ * gr_solve_pms / gr_mhs_exact are exactly:
+ *     gr_exact_prepare(in, which, ...);
+ *     for (k = 1; ; k++) { gr_exact_level(in, k, 0, 1, ...);
+ *                          gr_exact_finish(in, which, k, out, ..., &n); if (!n) break; }
+ * With G GPUs, rank r calls gr_exact_level(in, k, r, G, ...), then all-reduces
+ * (MIN, int64) the B level keys at gr_exact_level_keys(ws) before
+ * gr_exact_finish -- every rank then holds the same state.  Level k's colex
+ * rank range is cut into fixed chunks; shard r enumerates chunks c with
+ * c % G == r.  which: 0 = PMS/WPMS, 1 = MHS. */
+int gr_exact_prepare(const gr_batch *in, int which, gr_result *out, void *ws, size_t ws_bytes,
+                     gr_stream_t s);
+int gr_exact_level(const gr_batch *in, int which, int k, int shard, int nshard, void *ws,
+                   size_t ws_bytes, gr_stream_t s);
+int64_t *gr_exact_level_keys(const gr_batch *in, int which, void *ws);
+/* commits level k, writes results of instances that finished, plans level
+ * k+1; *n_active (host) = instances still searching.  Synchronises s. */
+int gr_exact_finish(const gr_batch *in, int which, int k, gr_result *out, void *ws,
+                    size_t ws_bytes, gr_stream_t s, int32_t *n_active);
+
+/* ---- greedy at scale: one phi+ as a variable-major bit matrix ----------- */
+typedef struct {
+  int32_t m;              /* host: number of variables (rows), >= 1 */
+  int64_t n_pos;          /* host: number of positive clauses (columns), >= 0 */
+  int64_t ld;             /* host: row stride in uint64 words, >= ceil(n_pos/64), multiple of 64 */
+  const uint64_t *bits;   /* [m][ld] R[v][c/64] bit c%64 <=> b_{v+1} occurs in clause c;
+                             bits at columns >= n_pos must be 0 */
+  int32_t n_neg;          /* host: number of negative clauses */
+  const uint64_t *neg;    /* [n_neg][ceil(m/64)] negative clause masks (may be NULL if n_neg == 0) */
+} gr_bitmatrix;
+
+/* Row stride (words) the library uses for n_pos clauses: a multiple of 64. */
+int64_t gr_bitmatrix_ld(int64_t n_pos);
+
+/* Pack CSR variable lists into the variable-major bit matrix (clause packing
+ * step a1).  off [n+1] int64, var [off[n]] int16 (var_bytes = 2) or int32
+ * (var_bytes = 4), 0-based variable ids.  bits [m][ld] must be zeroed by the
+ * caller.  *d_bad (device int32, may be NULL) is set to 1 if some id is outside
+ * [0, m), to 2 if some clause is empty (phi is then UNSAT, R6). */
+int gr_pack_varmajor(int32_t m, int64_t n, const int64_t *off, const void *var, int var_bytes,
+                     uint64_t *bits, int64_t ld, int32_t *d_bad, gr_stream_t s);
+/* Same, clause-major [n][ceil(m/64)] masks (for phi-); out must be zeroed. */
+int gr_pack_clausemajor(int32_t m, int64_t n, const int64_t *off, const void *var, int var_bytes,
+                        uint64_t *masks, int32_t *d_bad, gr_stream_t s);
+
+size_t gr_greedy_matrix_workspace_bytes(const gr_bitmatrix *in);
+
+/* Greedy mhs over the bit matrix.  assign [ceil(m/64)] words (device);
+ * status (device int32); picks (device, [m], or NULL): pick order before
+ * pruning, padded with -1; n_picks (host, may be NULL) = number of picks.
+ * Empty positive clauses must be reported by the caller (gr_pack_* d_bad). */
+int gr_mhs_greedy_matrix(const gr_bitmatrix *in, uint64_t *assign, int32_t *status,
+                         int32_t *picks, int32_t *n_picks, void *ws, size_t ws_bytes,
+                         gr_stream_t s);
+
+/* Shard hook for the multi-GPU greedy: counts[v] (device, [m] uint32) =
+ * number of clauses c of this shard with U[c] = 1 and v in c. */
+int gr_greedy_count_shard(const gr_bitmatrix *shard, const uint64_t *d_U, uint32_t *d_counts,
+                          gr_stream_t s);
+
+/* thread-local description of the last negative return */
+const char *gr_last_error(void);
+/* build identification, e.g. "grsolve 0.1 sm_100a" */
+const char *gr_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GR_H */

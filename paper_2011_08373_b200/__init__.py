@@ -1,0 +1,16 @@
+"""grsolve: the Solve step of GPURepair (arXiv 2011.08373) on B200 (sm_100a).
+
+Public API (thin marshalling over libgrsolve.so, include/gr.h):
+    DeviceBatch, DeviceResult           device-resident clause batches / results
+    solve_pms, mhs_exact, mhs_greedy    the three solvers
+    ExactSession                        prepare / level / finish for sharded runs
+    pack_bitmatrix, mhs_greedy_matrix   greedy at scale over a bit matrix
+    greedy_count_shard                  shard hook for the multi-GPU greedy
+Seeded synthetic workloads: paper_2011_08373_b200.synth.
+"""
+from ._native import (  # noqa: F401
+    GR_BADINPUT, GR_FLAG_EXHAUSTIVE, GR_SAT, GR_SAT_NEG_VIOLATED, GR_UNSAT, GR_UNSUPPORTED, MHS,
+    PMS, GREEDY, DeviceBatch, DeviceBitMatrix, DeviceResult, ExactSession, GrError,
+    bitmatrix_ld, greedy_count_shard, lib, mhs_exact, mhs_greedy, mhs_greedy_matrix,
+    pack_bitmatrix, solve_pms, version,
+)

@@ -1,0 +1,376 @@
+"""ctypes binding of libgrsolve.so (include/gr.h) -- argument marshalling only.
+
+Every step of the Solve path runs in the CUDA kernels behind the C-ABI; this
+module turns torch device tensors into the plain pointers gr.h declares and
+passes torch's current stream.  There is no CPU fallback: if the library is
+missing or no CUDA device is present, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libgrsolve.so")
+
+GR_OK, GR_EINVAL, GR_ETOOBIG, GR_ECUDA, GR_ENOMEM, GR_EWORKSPACE = 0, -1, -2, -3, -4, -5
+GR_SAT, GR_UNSAT, GR_SAT_NEG_VIOLATED, GR_BADINPUT, GR_UNSUPPORTED = 0, 1, 2, 3, 4
+GR_FLAG_EXHAUSTIVE = 1
+PMS, MHS, GREEDY = 0, 1, 2
+
+EXPORTED = [
+    "gr_workspace_bytes", "gr_solve_pms", "gr_mhs_exact", "gr_mhs_greedy", "gr_exact_prepare",
+    "gr_exact_level", "gr_exact_level_keys", "gr_exact_finish", "gr_bitmatrix_ld",
+    "gr_pack_varmajor", "gr_pack_clausemajor", "gr_greedy_matrix_workspace_bytes",
+    "gr_mhs_greedy_matrix", "gr_greedy_count_shard", "gr_last_error", "gr_version",
+]
+
+
+class GrBatch(C.Structure):
+    _fields_ = [
+        ("B", C.c_int32), ("W", C.c_int32), ("total_clauses", C.c_int64),
+        ("max_clauses", C.c_int32), ("flags", C.c_uint32),
+        ("m", C.c_void_p), ("off", C.c_void_p), ("n_pos", C.c_void_p), ("masks", C.c_void_p),
+        ("w", C.c_void_p), ("wstride", C.c_int32),
+    ]
+
+
+class GrResult(C.Structure):
+    _fields_ = [("assign", C.c_void_p), ("cost", C.c_void_p), ("status", C.c_void_p),
+                ("decided", C.c_void_p)]
+
+
+class GrBitmatrix(C.Structure):
+    _fields_ = [("m", C.c_int32), ("n_pos", C.c_int64), ("ld", C.c_int64), ("bits", C.c_void_p),
+                ("n_neg", C.c_int32), ("neg", C.c_void_p)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libgrsolve.so (raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = C.CDLL(LIB_PATH)
+        vp, i32, i64, sz = C.c_void_p, C.c_int32, C.c_int64, C.c_size_t
+        L.gr_workspace_bytes.argtypes = [vp, C.c_int]
+        L.gr_workspace_bytes.restype = sz
+        for f in (L.gr_solve_pms, L.gr_mhs_exact, L.gr_mhs_greedy):
+            f.argtypes = [vp, vp, vp, sz, vp]
+            f.restype = C.c_int
+        L.gr_exact_prepare.argtypes = [vp, C.c_int, vp, vp, sz, vp]
+        L.gr_exact_level.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, sz, vp]
+        L.gr_exact_level_keys.argtypes = [vp, C.c_int, vp]
+        L.gr_exact_level_keys.restype = vp
+        L.gr_exact_finish.argtypes = [vp, C.c_int, C.c_int, vp, vp, sz, vp, vp]
+        L.gr_bitmatrix_ld.argtypes = [i64]
+        L.gr_bitmatrix_ld.restype = i64
+        L.gr_pack_varmajor.argtypes = [i32, i64, vp, vp, C.c_int, vp, i64, vp, vp]
+        L.gr_pack_clausemajor.argtypes = [i32, i64, vp, vp, C.c_int, vp, vp, vp]
+        L.gr_greedy_matrix_workspace_bytes.argtypes = [vp]
+        L.gr_greedy_matrix_workspace_bytes.restype = sz
+        L.gr_mhs_greedy_matrix.argtypes = [vp, vp, vp, vp, vp, vp, sz, vp]
+        L.gr_greedy_count_shard.argtypes = [vp, vp, vp, vp]
+        L.gr_last_error.restype = C.c_char_p
+        L.gr_version.restype = C.c_char_p
+        for f in (L.gr_exact_prepare, L.gr_exact_level, L.gr_exact_finish, L.gr_pack_varmajor,
+                  L.gr_pack_clausemajor, L.gr_mhs_greedy_matrix, L.gr_greedy_count_shard):
+            f.restype = C.c_int
+        _lib = L
+    return _lib
+
+
+class GrError(RuntimeError):
+    pass
+
+
+def _check(rc: int, what: str):
+    if rc != GR_OK:
+        raise GrError(f"{what} failed ({rc}): {lib().gr_last_error().decode()}")
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise GrError("libgrsolve needs a CUDA device (there is no CPU fallback)")
+    return torch
+
+
+def _ptr(t) -> Optional[int]:
+    return None if t is None else int(t.data_ptr())
+
+
+def _stream(stream=None) -> int:
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+# ---------------------------------------------------------------------------
+# batches
+# ---------------------------------------------------------------------------
+@dataclass
+class DeviceBatch:
+    """A synth.ClauseBatch resident in device memory (torch tensors)."""
+
+    m: "object"
+    off: "object"
+    n_pos: "object"
+    masks: "object"
+    w: "object"
+    B: int
+    W: int
+    total_clauses: int
+    max_clauses: int
+    wstride: int = 0
+    flags: int = 0
+
+    @staticmethod
+    def from_host(cb, device="cuda", flags: int = 0, weighted: bool = True,
+                  non_blocking: bool = False, pinned: bool = False) -> "DeviceBatch":
+        torch = _torch()
+
+        def dev(a, dt):
+            t = torch.from_numpy(np.ascontiguousarray(a).view(dt))
+            if pinned:
+                t = t.pin_memory()
+            return t.to(device, non_blocking=non_blocking)
+
+        n = np.diff(cb.off)
+        w = None
+        ws = 0
+        if weighted and cb.w is not None:
+            w = dev(cb.w.astype(np.uint32).view(np.int32), np.int32)
+            ws = int(cb.w.shape[1])
+        masks = cb.masks if cb.masks.shape[0] else np.zeros((1, cb.W), np.uint64)
+        return DeviceBatch(
+            m=dev(cb.m.astype(np.int32), np.int32), off=dev(cb.off.astype(np.int64), np.int64),
+            n_pos=dev(cb.n_pos.astype(np.int32), np.int32),
+            masks=dev(masks.astype(np.uint64).view(np.int64), np.int64), w=w, B=cb.B, W=cb.W,
+            total_clauses=int(cb.off[-1]), max_clauses=int(n.max()) if n.size else 0,
+            wstride=ws, flags=flags)
+
+    def struct(self, weighted: bool = True) -> GrBatch:
+        return GrBatch(self.B, self.W, self.total_clauses, self.max_clauses, self.flags,
+                       _ptr(self.m), _ptr(self.off), _ptr(self.n_pos), _ptr(self.masks),
+                       _ptr(self.w) if weighted else None, self.wstride if weighted else 0)
+
+
+@dataclass
+class DeviceResult:
+    assign: "object"  # int64 view of uint64 [B, W]
+    cost: "object"
+    status: "object"
+    decided: "object"
+
+    @staticmethod
+    def empty(B: int, W: int, device="cuda") -> "DeviceResult":
+        torch = _torch()
+        return DeviceResult(
+            torch.zeros((B, W), dtype=torch.int64, device=device),
+            torch.zeros(B, dtype=torch.int64, device=device),
+            torch.zeros(B, dtype=torch.int32, device=device),
+            torch.zeros(B, dtype=torch.int64, device=device))
+
+    def struct(self) -> GrResult:
+        return GrResult(_ptr(self.assign), _ptr(self.cost), _ptr(self.status), _ptr(self.decided))
+
+    def to_host(self):
+        """-> dict of numpy arrays (assign/cost/decided as uint64)."""
+        return {
+            "assign": self.assign.cpu().numpy().view(np.uint64),
+            "cost": self.cost.cpu().numpy().view(np.uint64),
+            "status": self.status.cpu().numpy(),
+            "decided": self.decided.cpu().numpy().view(np.uint64),
+        }
+
+
+_ws_cache = {}
+
+
+def workspace(nbytes: int, device="cuda", tag: str = "default"):
+    """A cached uint8 device buffer of at least nbytes."""
+    torch = _torch()
+    key = (str(device), tag)
+    buf = _ws_cache.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+        _ws_cache[key] = buf
+    return buf
+
+
+def _solve(fn_name: str, which: int, db: DeviceBatch, out: Optional[DeviceResult], stream):
+    L = lib()
+    weighted = which == PMS
+    b = db.struct(weighted)
+    nbytes = L.gr_workspace_bytes(C.byref(b), which)
+    if nbytes == 0:
+        raise GrError("gr_workspace_bytes rejected the batch")
+    ws = workspace(nbytes, db.m.device, tag=f"exact{which}")
+    if out is None:
+        out = DeviceResult.empty(db.B, db.W, db.m.device)
+    r = out.struct()
+    _check(getattr(L, fn_name)(C.byref(b), C.byref(r), _ptr(ws), ws.numel(), _stream(stream)),
+           fn_name)
+    return out
+
+
+def solve_pms(db: DeviceBatch, out: Optional[DeviceResult] = None, stream=None) -> DeviceResult:
+    """(a) exact PMS / WPMS (gr_solve_pms)."""
+    return _solve("gr_solve_pms", PMS, db, out, stream)
+
+
+def mhs_exact(db: DeviceBatch, out: Optional[DeviceResult] = None, stream=None) -> DeviceResult:
+    """(b) exact MHS of phi+ (gr_mhs_exact)."""
+    return _solve("gr_mhs_exact", MHS, db, out, stream)
+
+
+def mhs_greedy(db: DeviceBatch, out: Optional[DeviceResult] = None, stream=None) -> DeviceResult:
+    """(c) greedy mhs of phi+ (gr_mhs_greedy)."""
+    return _solve("gr_mhs_greedy", GREEDY, db, out, stream)
+
+
+# ---- sharded exact solving ---------------------------------------------------
+class ExactSession:
+    """Step-wise exact solve (prepare / level / finish) for multi-GPU drivers."""
+
+    def __init__(self, db: DeviceBatch, which: int, out: Optional[DeviceResult] = None,
+                 stream=None):
+        self.L = lib()
+        self.db, self.which = db, which
+        self.b = db.struct(which == PMS)
+        nbytes = self.L.gr_workspace_bytes(C.byref(self.b), which)
+        if nbytes == 0:
+            raise GrError("gr_workspace_bytes rejected the batch")
+        self.ws = workspace(nbytes, db.m.device, tag=f"session{which}")
+        self.out = out if out is not None else DeviceResult.empty(db.B, db.W, db.m.device)
+        self.r = self.out.struct()
+        self.stream = stream
+
+    def prepare(self):
+        _check(self.L.gr_exact_prepare(C.byref(self.b), self.which, C.byref(self.r),
+                                       _ptr(self.ws), self.ws.numel(), _stream(self.stream)),
+               "gr_exact_prepare")
+
+    def level(self, k: int, shard: int = 0, nshard: int = 1):
+        _check(self.L.gr_exact_level(C.byref(self.b), self.which, k, shard, nshard, _ptr(self.ws),
+                                     self.ws.numel(), _stream(self.stream)), "gr_exact_level")
+
+    def level_keys(self):
+        """torch int64 view [B] of the per-instance level keys (for all_reduce MIN)."""
+        torch = _torch()
+        p = self.L.gr_exact_level_keys(C.byref(self.b), self.which, _ptr(self.ws))
+        base = _ptr(self.ws)
+        off = (p - base) // 1
+        return self.ws[off: off + 8 * self.db.B].view(torch.int64)
+
+    def finish(self, k: int) -> int:
+        n = C.c_int32(0)
+        _check(self.L.gr_exact_finish(C.byref(self.b), self.which, k, C.byref(self.r),
+                                      _ptr(self.ws), self.ws.numel(), _stream(self.stream),
+                                      C.byref(n)), "gr_exact_finish")
+        return int(n.value)
+
+
+# ---- greedy at scale ---------------------------------------------------------
+def bitmatrix_ld(n_pos: int) -> int:
+    return int(lib().gr_bitmatrix_ld(n_pos))
+
+
+@dataclass
+class DeviceBitMatrix:
+    m: int
+    n_pos: int
+    ld: int
+    bits: "object"  # int64 [m, ld]
+    n_neg: int
+    neg: "object"  # int64 [n_neg, ceil(m/64)] or None
+    bad: int = 0  # 1: id out of range, 2: empty positive clause
+
+    def struct(self) -> GrBitmatrix:
+        return GrBitmatrix(self.m, self.n_pos, self.ld, _ptr(self.bits), self.n_neg,
+                           _ptr(self.neg))
+
+
+def pack_bitmatrix(m, pos_off, pos_var, neg_off, neg_var, device="cuda", stream=None,
+                   check: bool = True) -> DeviceBitMatrix:
+    """Device clause packing (a1): CSR variable lists -> var-major phi+ bits and
+    clause-major phi- masks (gr_pack_varmajor / gr_pack_clausemajor).  The
+    CSR tensors may be host (numpy) or device (torch) arrays."""
+    torch = _torch()
+    L = lib()
+
+    def dev(a, dt):
+        if isinstance(a, np.ndarray):
+            return torch.from_numpy(np.ascontiguousarray(a)).to(device)
+        return a.to(device)
+
+    po, pv = dev(pos_off, np.int64), dev(pos_var, None)
+    no, nv = dev(neg_off, np.int64), dev(neg_var, None)
+    n_pos, n_neg = int(po.numel() - 1), int(no.numel() - 1)
+    ld = bitmatrix_ld(n_pos)
+    bits = torch.zeros((m, ld), dtype=torch.int64, device=device)
+    mw = (m + 63) // 64
+    neg = torch.zeros((max(n_neg, 1), mw), dtype=torch.int64, device=device)
+    bad = torch.zeros(1, dtype=torch.int32, device=device)
+    st = _stream(stream)
+    _check(L.gr_pack_varmajor(m, n_pos, _ptr(po), _ptr(pv), pv.element_size(), _ptr(bits), ld,
+                              _ptr(bad), st), "gr_pack_varmajor")
+    badn = torch.zeros(1, dtype=torch.int32, device=device)
+    _check(L.gr_pack_clausemajor(m, n_neg, _ptr(no), _ptr(nv), nv.element_size(), _ptr(neg),
+                                 _ptr(badn), st), "gr_pack_clausemajor")
+    b = int(bad.item()) if check else 0
+    b |= int(badn.item()) & 1 if check else 0
+    return DeviceBitMatrix(m, n_pos, ld, bits, n_neg, neg if n_neg else None, b)
+
+
+def greedy_matrix_workspace_bytes(bm: DeviceBitMatrix) -> int:
+    s = bm.struct()
+    return int(lib().gr_greedy_matrix_workspace_bytes(C.byref(s)))
+
+
+@dataclass
+class GreedyMatrixResult:
+    assign: "object"  # int64 [ceil(m/64)]
+    status: "object"  # int32 [1]
+    picks: "object"   # int32 [m]
+    n_picks: int
+
+
+def mhs_greedy_matrix(bm: DeviceBitMatrix, stream=None) -> GreedyMatrixResult:
+    """(c) at scale: greedy mhs over the bit matrix (gr_mhs_greedy_matrix)."""
+    torch = _torch()
+    L = lib()
+    s = bm.struct()
+    nbytes = L.gr_greedy_matrix_workspace_bytes(C.byref(s))
+    if nbytes == 0:
+        raise GrError("gr_greedy_matrix_workspace_bytes rejected the matrix")
+    ws = workspace(nbytes, bm.bits.device, tag="greedy_matrix")
+    dev = bm.bits.device
+    assign = torch.zeros((bm.m + 63) // 64, dtype=torch.int64, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    picks = torch.full((bm.m,), -1, dtype=torch.int32, device=dev)
+    n = C.c_int32(0)
+    _check(L.gr_mhs_greedy_matrix(C.byref(s), _ptr(assign), _ptr(status), _ptr(picks), C.byref(n),
+                                  _ptr(ws), ws.numel(), _stream(stream)), "gr_mhs_greedy_matrix")
+    return GreedyMatrixResult(assign, status, picks, int(n.value))
+
+
+def greedy_count_shard(bm: DeviceBitMatrix, U, counts, stream=None):
+    """counts[v] = |{c in this shard : U[c] and v in c}| (gr_greedy_count_shard)."""
+    s = bm.struct()
+    _check(lib().gr_greedy_count_shard(C.byref(s), _ptr(U), _ptr(counts), _stream(stream)),
+           "gr_greedy_count_shard")
+
+
+def version() -> str:
+    return lib().gr_version().decode()

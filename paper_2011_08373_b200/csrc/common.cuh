@@ -1,0 +1,110 @@
+// common.cuh -- shared device helpers of libgrsolve (CUDA path only).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+
+#include "../../include/gr.h"
+
+typedef uint64_t u64;
+typedef int64_t i64;
+typedef unsigned int u32;
+
+#define GR_KEY_NONE ((i64)0x7fffffffffffffffLL)
+
+// ---- error plumbing (host) ------------------------------------------------
+void gr_set_error(const std::string &msg);
+int gr_cuda_fail(cudaError_t e, const char *where);
+#define GR_CUDA(call)                                        \
+  do {                                                       \
+    cudaError_t _e = (call);                                 \
+    if (_e != cudaSuccess) return gr_cuda_fail(_e, #call);   \
+  } while (0)
+#define GR_CHECK_LAUNCH(name)                                      \
+  do {                                                             \
+    cudaError_t _e = cudaGetLastError();                           \
+    if (_e != cudaSuccess) return gr_cuda_fail(_e, name);          \
+  } while (0)
+
+// ---- binomial table C(n, k), 0 <= n, k <= 64 (C(64,32) < 2^61) ------------
+struct BinomTable {
+  u64 v[65][65];
+  constexpr BinomTable() : v() {
+    for (int n = 0; n <= 64; n++) {
+      v[n][0] = 1;
+      for (int k = 1; k <= n; k++) v[n][k] = v[n - 1][k - 1] + (k <= n - 1 ? v[n - 1][k] : 0);
+    }
+  }
+};
+// one copy per translation unit (no relocatable device code needed)
+static __device__ const BinomTable g_binom = BinomTable();
+
+__device__ __forceinline__ u64 binom(int n, int k) {
+  return (k < 0 || k > n || n < 0) ? 0ull : __ldg(&g_binom.v[n][k]);
+}
+
+// ---- generic bit helpers on 32/64-bit masks --------------------------------
+__device__ __forceinline__ int popc(u32 x) { return __popc(x); }
+__device__ __forceinline__ int popc(u64 x) { return __popcll(x); }
+__device__ __forceinline__ int ctz(u32 x) { return __ffs(x) - 1; }
+__device__ __forceinline__ int ctz(u64 x) { return __ffsll((long long)x) - 1; }
+template <typename M> __device__ __forceinline__ M lowbit(M x) { return x & (~x + 1); }
+
+// order-preserving relabel onto a support set (pext) and back (pdep), 128-bit
+// support given as two words, result <= 64 bits.
+__device__ __forceinline__ u64 pext128(u64 x0, u64 x1, u64 s0, u64 s1) {
+  u64 r = 0;
+  int j = 0;
+  while (s0) {
+    u64 l = s0 & (~s0 + 1);
+    if (x0 & l) r |= 1ull << j;
+    j++;
+    s0 ^= l;
+  }
+  while (s1) {
+    u64 l = s1 & (~s1 + 1);
+    if (x1 & l) r |= 1ull << j;
+    j++;
+    s1 ^= l;
+  }
+  return r;
+}
+__device__ __forceinline__ void pdep128(u64 x, u64 s0, u64 s1, u64 &o0, u64 &o1) {
+  o0 = 0;
+  o1 = 0;
+  int j = 0;
+  while (s0) {
+    u64 l = s0 & (~s0 + 1);
+    if ((x >> j) & 1) o0 |= l;
+    j++;
+    s0 ^= l;
+  }
+  while (s1) {
+    u64 l = s1 & (~s1 + 1);
+    if ((x >> j) & 1) o1 |= l;
+    j++;
+    s1 ^= l;
+  }
+}
+
+// colex unrank: the k-subset of {0..n-1} with rank r = sum_j C(c_j, j)
+__device__ __forceinline__ u64 unrank_colex(u64 r, int k, int n) {
+  u64 x = 0;
+  int hi = n - 1;
+  for (int j = k; j >= 1; j--) {
+    // largest c in [j-1, hi] with C(c, j) <= r  (binary search)
+    int lo = j - 1, h = hi;
+    while (lo < h) {
+      int mid = (lo + h + 1) >> 1;
+      if (binom(mid, j) <= r) lo = mid; else h = mid - 1;
+    }
+    x |= 1ull << lo;
+    r -= binom(lo, j);
+    hi = lo - 1;
+  }
+  return x;
+}
+
+__device__ __forceinline__ u64 sat_add(u64 a, u64 b) { u64 c = a + b; return c < a ? ~0ull : c; }
+
+__host__ __device__ __forceinline__ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }

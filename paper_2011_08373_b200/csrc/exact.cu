@@ -1,0 +1,820 @@
+// exact.cu -- exact PMS / WPMS (gr_solve_pms) and exact MHS (gr_mhs_exact).
+//
+// Method (PAPER.md:15 PMS/WPMS, PAPER.md:11 MHS, PAPER.md:24 MaxSAT
+// strategy): minimise the (weighted) number of true b_i subject to phi.  The
+// canonical optimum is the smallest colex rank at the optimal level (reading
+// R2) or the minimum (W, k, rank) key (reading R3).
+//
+// B200 design:
+//   pack_kernel     one CTA per instance: validation (R4, R6, R8), support
+//                   restriction + order-preserving relabel (R13), dedup and
+//                   subsumption, ascending-size clause order, sorted-weight
+//                   prefix sums S_k.
+//   enum_kernel     persistent CTAs (grid = SMs x occupancy) pull fixed-size
+//                   chunks of the current level's colex rank range from a
+//                   global atomic counter; each lane walks a contiguous
+//                   sub-range.  The walk fixes the k-1 upper elements T (the
+//                   "prefix") and decides all candidates T | {a}, a < min(T),
+//                   at once: their feasible set is a bit mask A, narrowed by
+//                   every positive clause T misses (A &= P) and every negative
+//                   clause with |N \ T| <= 1.  Clause masks are staged in
+//                   shared memory (broadcast reads).  Canonical minimum:
+//                   per-lane first witness -> warp shuffle-min -> CTA min ->
+//                   one 64-bit atomicMin per chunk.
+//   finish_kernel   one CTA: commits level k for every active instance
+//                   (decode, weighted incumbent, S_k stop rule, k_max), writes
+//                   finished results, compacts the active list and plans the
+//                   chunk ranges of level k+1 (block scan).
+#include <cub/block/block_scan.cuh>
+
+#include <algorithm>
+#include <cstdlib>
+#include <mutex>
+
+#include "common.cuh"
+
+namespace {
+
+constexpr int NT = 256;          // enumeration CTA size
+constexpr int FT = 1024;         // finish CTA size
+constexpr int PT = 128;          // pack CTA size
+constexpr int MAXC = 4096;       // max clauses per instance (exact solvers)
+
+struct Ctrl {
+  u64 next_chunk;     // atomic chunk counter of the running level
+  u64 total_chunks;   // chunks of the running level
+  int n_active;       // active instances
+  int pad0;
+  u64 lane_cands;     // candidates per lane per chunk (L)
+  u64 pad1[4];
+};
+
+struct Layout {
+  size_t ctrl, meff, npr, nnr, kmax, done, rb, sup, decided, bestx, bestw, wtot, lvlkey, sk, wr,
+      active, chunk_base, pk, total;
+};
+
+Layout layout_of(const gr_batch *in) {
+  Layout L{};
+  size_t B = (size_t)in->B, o = 0;
+  auto take = [&](size_t bytes) { size_t at = o; o = align256(o + bytes); return at; };
+  L.ctrl = take(sizeof(Ctrl));
+  L.meff = take(4 * B);
+  L.npr = take(4 * B);
+  L.nnr = take(4 * B);
+  L.kmax = take(4 * B);
+  L.done = take(4 * B);
+  L.rb = take(4 * B);
+  L.sup = take(16 * B);
+  L.decided = take(8 * B);
+  L.bestx = take(8 * B);
+  L.bestw = take(8 * B);
+  L.wtot = take(8 * B);
+  L.lvlkey = take(8 * B);
+  L.sk = take(8 * 65 * B);
+  L.wr = take(4 * 64 * B);
+  L.active = take(4 * 2 * B);
+  L.chunk_base = take(8 * (B + 1));
+  L.pk = take(8 * (size_t)std::max<int64_t>(in->total_clauses, 1));
+  L.total = o;
+  return L;
+}
+
+struct WS {
+  Ctrl *ctrl;
+  int *meff, *npr, *nnr, *kmax, *done, *rb;
+  u64 *sup, *decided, *bestx, *bestw, *wtot;
+  i64 *lvlkey;
+  u64 *sk;
+  u32 *wr;
+  int *active;
+  u64 *chunk_base;
+  u64 *pk;
+};
+
+WS ws_of(const gr_batch *in, void *base) {
+  Layout L = layout_of(in);
+  char *p = (char *)base;
+  WS w;
+  w.ctrl = (Ctrl *)(p + L.ctrl);
+  w.meff = (int *)(p + L.meff);
+  w.npr = (int *)(p + L.npr);
+  w.nnr = (int *)(p + L.nnr);
+  w.kmax = (int *)(p + L.kmax);
+  w.done = (int *)(p + L.done);
+  w.rb = (int *)(p + L.rb);
+  w.sup = (u64 *)(p + L.sup);
+  w.decided = (u64 *)(p + L.decided);
+  w.bestx = (u64 *)(p + L.bestx);
+  w.bestw = (u64 *)(p + L.bestw);
+  w.wtot = (u64 *)(p + L.wtot);
+  w.lvlkey = (i64 *)(p + L.lvlkey);
+  w.sk = (u64 *)(p + L.sk);
+  w.wr = (u32 *)(p + L.wr);
+  w.active = (int *)(p + L.active);
+  w.chunk_base = (u64 *)(p + L.chunk_base);
+  w.pk = (u64 *)(p + L.pk);
+  return w;
+}
+
+struct In {
+  int B, W, max_clauses, wstride;
+  const int32_t *m;
+  const int64_t *off;
+  const int32_t *n_pos;
+  const uint64_t *masks;
+  const uint32_t *w;
+};
+struct Out {
+  uint64_t *assign, *cost, *decided;
+  int32_t *status;
+};
+
+In in_of(const gr_batch *b, int which) {
+  In r{b->B, b->W, b->max_clauses, b->wstride, b->m, b->off, b->n_pos, b->masks,
+       which == 0 ? b->w : nullptr};
+  return r;
+}
+Out out_of(const gr_result *o) { return Out{o->assign, o->cost, o->decided, o->status}; }
+
+// ---------------------------------------------------------------------------
+// finalisation of one instance (single thread)
+// ---------------------------------------------------------------------------
+__device__ void write_result(const In &in, const Out &out, int b, int status, u64 x_rel, u64 s0,
+                             u64 s1, u64 cost, u64 decided, int which) {
+  u64 a0 = 0, a1 = 0;
+  if (status == GR_SAT) {
+    pdep128(x_rel, s0, s1, a0, a1);
+    if (which == 1) {  // MHS: flag phi- 
+      int64_t lo = in.off[b], hi = in.off[b + 1];
+      for (int64_t j = lo + in.n_pos[b]; j < hi; j++) {
+        u64 n0 = in.masks[j * in.W], n1 = in.W > 1 ? in.masks[j * in.W + 1] : 0;
+        if ((a0 & n0) == n0 && (a1 & n1) == n1) { status = GR_SAT_NEG_VIOLATED; break; }
+      }
+    }
+  } else {
+    cost = ~0ull;
+  }
+  out.assign[(size_t)b * in.W] = a0;
+  if (in.W > 1) out.assign[(size_t)b * in.W + 1] = a1;
+  out.cost[b] = cost;
+  out.status[b] = status;
+  if (out.decided) out.decided[b] = decided;
+}
+
+// ---------------------------------------------------------------------------
+// pack: one CTA per instance
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(PT) pack_kernel(In in, Out out, WS ws, int which) {
+  extern __shared__ u64 sm[];  // [max_clauses] masks, [max_clauses] int info, [max_clauses] u8 keep
+  __shared__ int s_bad, s_unsat, s_negempty, s_npr, s_nnr;
+  __shared__ unsigned long long s_sup0, s_sup1;
+  __shared__ u32 s_w[64];
+  __shared__ u64 s_ws[64];
+  const int b = blockIdx.x, t = threadIdx.x;
+  u64 *R = sm;
+  int *info = (int *)(sm + in.max_clauses);
+  unsigned char *keep0 = (unsigned char *)(info + in.max_clauses);
+  const int64_t lo = in.off[b], n64 = in.off[b + 1] - lo;
+  const int m = in.m[b], np = in.n_pos[b], W = in.W;
+  if (t == 0) {
+    s_bad = (n64 < 0 || n64 > in.max_clauses || np < 0 || np > n64 || m < 0 || m > 64 * W);
+    s_unsat = 0;
+    s_negempty = 0;
+    s_sup0 = 0;
+    s_sup1 = 0;
+    s_npr = 0;
+    s_nnr = 0;
+  }
+  __syncthreads();
+  const int n = s_bad ? 0 : (int)n64;
+  // validation (R8 bits >= m, R6 empty clause) and support of phi+
+  const u64 al0 = m >= 64 ? ~0ull : ((1ull << m) - 1);
+  const u64 al1 = m >= 128 ? ~0ull : (m <= 64 ? 0ull : ((1ull << (m - 64)) - 1));
+  u64 sup0 = 0, sup1 = 0;
+  for (int j = t; j < n; j += PT) {
+    u64 x0 = in.masks[(lo + j) * W], x1 = W > 1 ? in.masks[(lo + j) * W + 1] : 0;
+    if ((x0 & ~al0) | (x1 & ~al1)) s_bad = 1;
+    if (!(x0 | x1)) {
+      if (j < np) s_unsat = 1;
+      else s_negempty = 1;
+    }
+    if (j < np) { sup0 |= x0; sup1 |= x1; }
+  }
+  if (in.w)
+    for (int i = t; i < m; i += PT)
+      if (in.w[(size_t)b * in.wstride + i] == 0) s_bad = 1;
+  if (sup0) atomicOr(&s_sup0, (unsigned long long)sup0);
+  if (sup1) atomicOr(&s_sup1, (unsigned long long)sup1);
+  __syncthreads();
+  sup0 = s_sup0;
+  sup1 = s_sup1;
+  const int me = __popcll(sup0) + __popcll(sup1);
+  int status = -1;
+  if (s_bad) status = GR_BADINPUT;
+  else if (s_unsat || (which == 0 && s_negempty)) status = GR_UNSAT;
+  else if (me > 64) status = GR_UNSUPPORTED;
+  if (status >= 0) {
+    if (t == 0) {
+      ws.done[b] = 1;
+      write_result(in, out, b, status, 0, 0, 0, 0, 0, which);
+    }
+    return;
+  }
+  // relabel onto the support; negatives that touch a non-support variable are
+  // always satisfied by an optimum (those variables are false) -> dropped (R13)
+  const int nneg_in = which == 0 ? n - np : 0;
+  const int nc = np + nneg_in;
+  for (int j = t; j < nc; j += PT) {
+    u64 x0 = in.masks[(lo + j) * W], x1 = W > 1 ? in.masks[(lo + j) * W + 1] : 0;
+    int keep = 1;
+    if (j >= np && ((x0 & ~sup0) | (x1 & ~sup1))) keep = 0;
+    R[j] = keep ? pext128(x0, x1, sup0, sup1) : 0;
+    keep0[j] = (unsigned char)keep;
+  }
+  __syncthreads();
+  // dedup + subsumption within each polarity: drop j if another kept clause i
+  // of the same polarity has R[i] subset of R[j] (and R[i] != R[j] or i < j).
+  // The feasible set is unchanged (a hitting set of R[i] hits R[j]; an
+  // assignment avoiding all of N_i avoids N_j, N_i subset of N_j).
+  for (int j = t; j < nc; j += PT) {
+    int keep = keep0[j];
+    if (keep) {
+      const int a0 = j < np ? 0 : np, a1 = j < np ? np : nc;
+      const u64 rj = R[j];
+      for (int i = a0; i < a1; i++) {
+        if (i == j || !keep0[i]) continue;
+        const u64 ri = R[i];
+        if ((ri & ~rj) == 0 && (ri != rj || i < j)) { keep = 0; break; }
+      }
+    }
+    info[j] = keep ? (1 | (__popcll(R[j]) << 8)) : 0;
+    if (keep) atomicAdd(j < np ? &s_npr : &s_nnr, 1);
+  }
+  __syncthreads();
+  const int npr = s_npr;
+  // ascending clause size, stable by index, positives first: destination =
+  // number of kept clauses of the same polarity ordered before j
+  for (int j = t; j < nc; j += PT) {
+    const int ij = info[j];
+    if (!ij) continue;
+    const int a0 = j < np ? 0 : np, a1 = j < np ? np : nc;
+    const int pj = ij >> 8;
+    int d = 0;
+    for (int i = a0; i < a1; i++) {
+      const int ii = info[i];
+      if (!ii) continue;
+      const int pi = ii >> 8;
+      d += (pi < pj || (pi == pj && i < j));
+    }
+    ws.pk[lo + (j < np ? 0 : npr) + d] = R[j];
+  }
+  // weights of the support variables (relabelled order) and S_k
+  if (t < 64) {
+    u32 wv = 0;
+    if (t < me) {
+      // original index of the t-th support variable
+      u64 s0 = sup0, s1 = sup1;
+      int idx = -1;
+      for (int q = 0; q <= t; q++) {
+        if (s0) { u64 l = s0 & (~s0 + 1); idx = __ffsll((long long)l) - 1; s0 ^= l; }
+        else { u64 l = s1 & (~s1 + 1); idx = 64 + __ffsll((long long)l) - 1; s1 ^= l; }
+      }
+      wv = in.w ? in.w[(size_t)b * in.wstride + idx] : 1u;
+    }
+    s_w[t] = wv;
+    ws.wr[(size_t)b * 64 + t] = wv;
+  }
+  __syncthreads();
+  if (t < me) {  // rank of weight t among the support weights (ties by index)
+    u32 wt = s_w[t];
+    int r = 0;
+    for (int i = 0; i < me; i++) r += (s_w[i] < wt) || (s_w[i] == wt && i < t);
+    s_ws[r] = wt;
+  }
+  __syncthreads();
+  if (t == 0) {
+    const int nnr = s_nnr;
+    u64 *sk = ws.sk + (size_t)b * 65;
+    u64 acc = 0;
+    sk[0] = 0;
+    for (int i = 0; i < 64; i++) {
+      if (i < me) acc += s_ws[i];
+      sk[i + 1] = acc;
+    }
+    ws.meff[b] = me;
+    ws.npr[b] = npr;
+    ws.nnr[b] = nnr;
+    ws.kmax[b] = me < npr ? me : npr;
+    ws.sup[2 * b] = sup0;
+    ws.sup[2 * b + 1] = sup1;
+    ws.wtot[b] = acc;
+    ws.bestw[b] = ~0ull;
+    ws.bestx[b] = 0;
+    ws.lvlkey[b] = GR_KEY_NONE;
+    ws.decided[b] = 1;  // level 0: the empty assignment
+    if (npr == 0) {
+      // phi+ empty: the all-false assignment satisfies every (non-empty)
+      // negative clause and is optimal
+      ws.done[b] = 1;
+      write_result(in, out, b, GR_SAT, 0, sup0, sup1, 0, 1, which);
+    } else {
+      ws.done[b] = 0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// the level walk of one lane
+// ---------------------------------------------------------------------------
+// Candidates at level k in colex order are grouped by their k-1 upper
+// elements T (the prefix); the candidates of one prefix are T | {a} for
+// a < min(T), consecutive in rank.  x = first candidate, r its rank, cnt the
+// number of candidates left in this lane's sub-range.
+template <typename M>
+__device__ __forceinline__ M prefix_bits(M x, M low, M T, int me, u64 cnt, int &nb) {
+  const M full = (me >= (int)(8 * sizeof(M))) ? ~M(0) : (M)((M(1) << me) - 1);
+  const M lim = T ? lowbit(T) : (M)(full + 1);  // wraps to 0 when me == width
+  M A = (M)(lim - low);                          // bits [a, min(T)) (or [a, me))
+  nb = popc(A);
+  if (cnt < (u64)nb) {
+    A &= (M)((low << cnt) - 1);
+    nb = (int)cnt;
+  }
+  return A;
+}
+
+template <typename M>
+__device__ __forceinline__ M next_prefix_first(M T) {
+  // Gosper's hack on S = T >> 1 (the (k-1)-subsets of [1, me) shifted down)
+  M S = T >> 1;
+  M c = lowbit(S);
+  M r = S + c;
+  S = r | (((r ^ S) >> 2) >> ctz(S));
+  return (M)((S << 1) | 1);
+}
+
+template <typename M>
+__device__ __forceinline__ M narrow_by_clauses(M A, M T, const M *__restrict__ P, int np,
+                                               const M *__restrict__ N, int nn) {
+  int j = 0;
+  for (; j + 4 <= np; j += 4) {
+    const M p0 = P[j], p1 = P[j + 1], p2 = P[j + 2], p3 = P[j + 3];
+    if (!(T & p0)) A &= p0;
+    if (!(T & p1)) A &= p1;
+    if (!(T & p2)) A &= p2;
+    if (!(T & p3)) A &= p3;
+    if (!A) return A;
+  }
+  for (; j < np; j++) {
+    const M p = P[j];
+    if (!(T & p)) A &= p;
+  }
+  if (!A) return A;
+  for (int q = 0; q < nn; q++) {
+    const M R = N[q] & ~T;
+    if (!R) return 0;                 // N subset of T: every candidate has N all true
+    if (!(R & (R - 1))) A &= ~R;      // N \ T = {c}: candidate a = c is excluded
+  }
+  return A;
+}
+
+// unit weights: first feasible rank in the sub-range (EXH: keep walking)
+template <typename M, bool EXH>
+__device__ i64 scan_unit(M x, u64 r, u64 cnt, int me, const M *P, int np, const M *N, int nn) {
+  i64 best = GR_KEY_NONE;
+  for (;;) {
+    const M low = lowbit(x);
+    const M T = x ^ low;
+    int nb;
+    M A = prefix_bits<M>(x, low, T, me, cnt, nb);
+    A = narrow_by_clauses<M>(A, T, P, np, N, nn);
+    if (A) {
+      const u64 rank = r + (u64)popc((M)(lowbit(A) - low));
+      if (!EXH) return (i64)rank;
+      if (best == GR_KEY_NONE) best = (i64)rank;
+    }
+    cnt -= (u64)nb;
+    if (!cnt) return best;
+    r += (u64)nb;
+    x = next_prefix_first<M>(T);
+  }
+}
+
+// weights: min key (W << rb | rank) over the sub-range
+template <typename M>
+__device__ i64 scan_weighted(M x, u64 r, u64 cnt, int me, const M *P, int np, const M *N, int nn,
+                             const u32 *__restrict__ w, int rb) {
+  i64 best = GR_KEY_NONE;
+  for (;;) {
+    const M low = lowbit(x);
+    const M T = x ^ low;
+    int nb;
+    M A = prefix_bits<M>(x, low, T, me, cnt, nb);
+    A = narrow_by_clauses<M>(A, T, P, np, N, nn);
+    if (A) {
+      u64 WT = 0;
+      for (M t = T; t; t &= t - 1) WT += w[ctz(t)];
+      for (M a = A; a; a &= a - 1) {
+        const int bi = ctz(a);
+        const u64 rank = r + (u64)popc((M)(lowbit(a) - low));
+        const i64 key = (i64)(((WT + w[bi]) << rb) | rank);
+        best = key < best ? key : best;
+      }
+    }
+    cnt -= (u64)nb;
+    if (!cnt) return best;
+    r += (u64)nb;
+    x = next_prefix_first<M>(T);
+  }
+}
+
+__device__ __forceinline__ i64 warp_min(i64 v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    i64 u = __shfl_xor_sync(0xffffffffu, v, o);
+    v = u < v ? u : v;
+  }
+  return v;
+}
+
+struct EnumParams {
+  WS ws;
+  const int64_t *off;
+  int k, weighted, exhaustive, shard, nshard;
+};
+
+template <typename M>
+__device__ i64 run_lane(const EnumParams &p, int b, u64 r_lo, u64 cnt, int me, int np, int nn,
+                        const M *P, const M *N, const u32 *w, int rb) {
+  const M x = (M)unrank_colex(r_lo, p.k, me);
+  if (p.weighted) return scan_weighted<M>(x, r_lo, cnt, me, P, np, N, nn, w, rb);
+  if (p.exhaustive) return scan_unit<M, true>(x, r_lo, cnt, me, P, np, N, nn);
+  return scan_unit<M, false>(x, r_lo, cnt, me, P, np, N, nn);
+}
+
+__global__ void __launch_bounds__(NT) enum_kernel(EnumParams p) {
+  extern __shared__ u64 cls[];  // staged clauses (u64 or u32 view)
+  __shared__ u64 s_chunk;
+  __shared__ int s_b, s_cur, s_skip;
+  __shared__ u64 s_r0, s_ck;
+  __shared__ u32 s_w[64];
+  __shared__ i64 s_wmin[NT / 32];
+  const int t = threadIdx.x;
+  if (t == 0) s_cur = -1;
+  const u64 L = p.ws.ctrl->lane_cands;
+  const u64 CH = L * NT;
+  const u64 total = p.ws.ctrl->total_chunks;
+  const int nact = p.ws.ctrl->n_active;
+  const int *active = p.ws.active;  // list of this level (offset by the host)
+  for (;;) {
+    __syncthreads();
+    if (t == 0) {
+      u64 j = atomicAdd((unsigned long long *)&p.ws.ctrl->next_chunk, 1ull);
+      u64 c = j * (u64)p.nshard + (u64)p.shard;
+      s_chunk = c;
+      s_skip = 0;
+      if (c < total) {
+        // active index i: chunk_base[i] <= c < chunk_base[i+1]
+        int lo = 0, hi = nact - 1;
+        while (lo < hi) {
+          int mid = (lo + hi + 1) >> 1;
+          if (p.ws.chunk_base[mid] <= c) lo = mid; else hi = mid - 1;
+        }
+        const int b = active[lo];
+        s_b = b;
+        const u64 r0 = (c - p.ws.chunk_base[lo]) * CH;
+        s_r0 = r0;
+        s_ck = binom(p.ws.meff[b], p.k);
+        if (!p.weighted && !p.exhaustive) {
+          const i64 cur = *(volatile i64 *)&p.ws.lvlkey[b];
+          if (cur != GR_KEY_NONE && (u64)cur < r0) s_skip = 1;  // a lower witness exists
+        }
+      }
+    }
+    __syncthreads();
+    if (s_chunk >= total) break;
+    if (s_skip) continue;
+    const int b = s_b;
+    const int me = p.ws.meff[b], np = p.ws.npr[b], nn = p.ws.nnr[b];
+    const int64_t lo = p.off[b];
+    const bool narrow = me <= 32;
+    if (b != s_cur) {
+      if (narrow) {
+        u32 *c32 = (u32 *)cls;
+        for (int j = t; j < np + nn; j += NT) c32[j] = (u32)p.ws.pk[lo + j];
+      } else {
+        for (int j = t; j < np + nn; j += NT) cls[j] = p.ws.pk[lo + j];
+      }
+      if (t < 64) s_w[t] = p.ws.wr[(size_t)b * 64 + t];
+      __syncthreads();
+      if (t == 0) s_cur = b;
+    }
+    const u64 r_lo = s_r0 + (u64)t * L;
+    const u64 ck = s_ck;
+    i64 key = GR_KEY_NONE;
+    if (r_lo < ck) {
+      const u64 cnt = (ck - r_lo) < L ? (ck - r_lo) : L;
+      const int rb = p.ws.rb[b];
+      if (narrow) {
+        const u32 *c32 = (const u32 *)cls;
+        key = run_lane<u32>(p, b, r_lo, cnt, me, np, nn, c32, c32 + np, s_w, rb);
+      } else {
+        key = run_lane<u64>(p, b, r_lo, cnt, me, np, nn, cls, cls + np, s_w, rb);
+      }
+    }
+    key = warp_min(key);
+    if ((t & 31) == 0) s_wmin[t >> 5] = key;
+    __syncthreads();
+    if (t == 0) {
+      i64 v = s_wmin[0];
+      for (int i = 1; i < NT / 32; i++) v = s_wmin[i] < v ? s_wmin[i] : v;
+      if (v != GR_KEY_NONE) atomicMin((long long *)&p.ws.lvlkey[b], (long long)v);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// finish: commit level k, plan level k+1 (one CTA)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int bitlen(u64 x) { return x ? 64 - __clzll((long long)x) : 0; }
+
+__global__ void __launch_bounds__(FT) finish_kernel(In in, Out out, WS ws, int which, int k,
+                                                    int exhaustive) {
+  typedef cub::BlockScan<u64, FT> Scan;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ u64 s_carry;
+  __shared__ int s_cnt;
+  const int t = threadIdx.x;
+  const bool weighted = in.w != nullptr;
+  const u64 CH = ws.ctrl->lane_cands * NT;
+  const int nact_in = k == 0 ? in.B : ws.ctrl->n_active;
+  int *cur = ws.active + (size_t)(k & 1) * in.B;        // list enumerated at level k
+  int *nxt = ws.active + (size_t)((k + 1) & 1) * in.B;  // list for level k+1
+  // phase 1: commit level k
+  if (k > 0) {
+    for (int i = t; i < nact_in; i += FT) {
+      const int b = cur[i];
+      const int me = ws.meff[b];
+      const u64 ck = binom(me, k);
+      const i64 key = ws.lvlkey[b];
+      const u64 s0 = ws.sup[2 * b], s1 = ws.sup[2 * b + 1];
+      if (!weighted) {
+        if (key != GR_KEY_NONE) {
+          const u64 rank = (u64)key;
+          const u64 x = unrank_colex(rank, k, me);
+          const u64 d = sat_add(ws.decided[b], exhaustive ? ck : rank + 1);
+          ws.done[b] = 1;
+          write_result(in, out, b, GR_SAT, x, s0, s1, (u64)k, d, which);
+        } else {
+          ws.decided[b] = sat_add(ws.decided[b], ck);
+          if (k >= ws.kmax[b]) {
+            ws.done[b] = 1;
+            write_result(in, out, b, GR_UNSAT, 0, s0, s1, 0, ws.decided[b], which);
+          }
+        }
+      } else {
+        ws.decided[b] = sat_add(ws.decided[b], ck);
+        if (key != GR_KEY_NONE) {
+          const int rb = ws.rb[b];
+          const u64 Wk = (u64)key >> rb;
+          const u64 rank = (u64)key & ((rb ? (1ull << rb) : 1ull) - 1ull);
+          if (Wk < ws.bestw[b]) {  // strictly smaller W replaces the incumbent (R3)
+            ws.bestw[b] = Wk;
+            ws.bestx[b] = unrank_colex(rank, k, me);
+          }
+        }
+        const u64 bw = ws.bestw[b];
+        const bool stop = k >= ws.kmax[b] || (bw != ~0ull && ws.sk[(size_t)b * 65 + k + 1] >= bw);
+        if (stop) {
+          ws.done[b] = 1;
+          if (bw != ~0ull) write_result(in, out, b, GR_SAT, ws.bestx[b], s0, s1, bw, ws.decided[b], which);
+          else write_result(in, out, b, GR_UNSAT, 0, s0, s1, 0, ws.decided[b], which);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // phase 2: compact the still-active instances and plan level k+1
+  if (t == 0) { s_carry = 0; s_cnt = 0; }
+  __syncthreads();
+  for (int base = 0; base < nact_in; base += FT) {
+    const int i = base + t;
+    int b = -1;
+    u64 nch = 0;
+    if (i < nact_in) {
+      b = k == 0 ? i : cur[i];
+      if (ws.done[b]) b = -1;
+    }
+    if (b >= 0) {
+      const int me = ws.meff[b];
+      const u64 ck = binom(me, k + 1);
+      if (weighted) {
+        const int rb = bitlen(ck - 1);
+        if (bitlen(ws.wtot[b]) + rb > 63) {  // key (W << rb | rank) would not fit
+          ws.done[b] = 1;
+          write_result(in, out, b, GR_UNSUPPORTED, 0, 0, 0, 0, ws.decided[b], which);
+          b = -1;
+        } else {
+          ws.rb[b] = rb;
+        }
+      }
+      if (b >= 0) {
+        nch = (ck + CH - 1) / CH;
+        ws.lvlkey[b] = GR_KEY_NONE;
+      }
+    }
+    // compaction index (count) and chunk prefix (u64) in one pass
+    u64 flag = b >= 0 ? 1 : 0, pos;
+    Scan(tmp).ExclusiveSum(flag, pos);
+    __syncthreads();
+    u64 cpos;
+    Scan(tmp).ExclusiveSum(nch, cpos);
+    __syncthreads();
+    if (b >= 0) {
+      nxt[s_cnt + (int)pos] = b;
+      ws.chunk_base[s_cnt + (int)pos] = s_carry + cpos;
+    }
+    __syncthreads();
+    // last thread publishes the running totals
+    if (t == FT - 1) {
+      s_cnt += (int)(pos + flag);
+      s_carry += cpos + nch;
+    }
+    __syncthreads();
+  }
+  if (t == 0) {
+    ws.chunk_base[s_cnt] = s_carry;
+    ws.ctrl->n_active = s_cnt;
+    ws.ctrl->total_chunks = s_carry;
+    ws.ctrl->next_chunk = 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+int validate_batch(const gr_batch *in, int which) {
+  if (!in) { gr_set_error("null batch"); return GR_EINVAL; }
+  if (in->B < 1 || (in->W != 1 && in->W != 2)) { gr_set_error("B < 1 or W not in {1,2}"); return GR_EINVAL; }
+  if (!in->m || !in->off || !in->n_pos || (!in->masks && in->total_clauses > 0)) {
+    gr_set_error("null device pointer in batch");
+    return GR_EINVAL;
+  }
+  if (in->total_clauses < 0 || in->max_clauses < 0) { gr_set_error("negative sizes"); return GR_EINVAL; }
+  if (in->max_clauses > MAXC) { gr_set_error("max_clauses > 4096 for the exact solvers"); return GR_ETOOBIG; }
+  if (which == 0 && in->w && in->wstride < 1) { gr_set_error("wstride < 1 with weights"); return GR_EINVAL; }
+  return GR_OK;
+}
+
+std::mutex g_occ_mu;
+int g_enum_grid = 0;
+
+int enum_grid() {
+  std::lock_guard<std::mutex> lk(g_occ_mu);
+  if (g_enum_grid) return g_enum_grid;
+  int dev = 0, sms = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  size_t smem = (size_t)MAXC * 8;
+  cudaFuncSetAttribute(enum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, enum_kernel, NT, smem);
+  if (per < 1) per = 1;
+  g_enum_grid = sms * per;
+  return g_enum_grid;
+}
+
+u64 lane_cands() {
+  static u64 v = 0;
+  if (!v) {
+    const char *e = getenv("GR_LANE_CANDIDATES");
+    v = e ? strtoull(e, nullptr, 10) : 1024ull;
+    if (v < 1) v = 1024;
+  }
+  return v;
+}
+
+}  // namespace
+
+extern "C" size_t gr_workspace_bytes_exact(const gr_batch *in) { return layout_of(in).total; }
+
+extern "C" int gr_exact_prepare(const gr_batch *in, int which, gr_result *out, void *ws,
+                                size_t ws_bytes, gr_stream_t s) {
+  int rc = validate_batch(in, which);
+  if (rc) return rc;
+  if (!out || !out->assign || !out->cost || !out->status) { gr_set_error("null result pointer"); return GR_EINVAL; }
+  if (which != 0 && which != 1) { gr_set_error("which must be 0 (PMS) or 1 (MHS)"); return GR_EINVAL; }
+  Layout L = layout_of(in);
+  if (!ws || ws_bytes < L.total) { gr_set_error("workspace too small"); return GR_EWORKSPACE; }
+  WS w = ws_of(in, ws);
+  cudaStream_t st = (cudaStream_t)s;
+  Ctrl c{};
+  c.lane_cands = lane_cands();
+  GR_CUDA(cudaMemcpyAsync(w.ctrl, &c, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
+  size_t smem = (size_t)std::max(in->max_clauses, 1) * 13 + 16;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MAXC * 13 + 16);
+    attr = true;
+  }
+  pack_kernel<<<in->B, PT, smem, st>>>(in_of(in, which), out_of(out), w, which);
+  GR_CHECK_LAUNCH("pack_kernel");
+  finish_kernel<<<1, FT, 0, st>>>(in_of(in, which), out_of(out), w, which, 0,
+                                   (in->flags & GR_FLAG_EXHAUSTIVE) ? 1 : 0);
+  GR_CHECK_LAUNCH("finish_kernel(plan)");
+  return GR_OK;
+}
+
+extern "C" int gr_exact_level(const gr_batch *in, int which, int k, int shard, int nshard, void *ws,
+                              size_t ws_bytes, gr_stream_t s) {
+  int rc = validate_batch(in, which);
+  if (rc) return rc;
+  if (k < 1 || k > 64 || nshard < 1 || shard < 0 || shard >= nshard) { gr_set_error("bad level/shard"); return GR_EINVAL; }
+  Layout L = layout_of(in);
+  if (!ws || ws_bytes < L.total) { gr_set_error("workspace too small"); return GR_EWORKSPACE; }
+  WS w = ws_of(in, ws);
+  // the list of level k lives at parity k & 1
+  w.active = w.active + (size_t)(k & 1) * in->B;
+  EnumParams p;
+  p.ws = w;
+  p.off = in->off;
+  p.k = k;
+  p.weighted = (which == 0 && in->w) ? 1 : 0;
+  p.exhaustive = (in->flags & GR_FLAG_EXHAUSTIVE) ? 1 : 0;
+  p.shard = shard;
+  p.nshard = nshard;
+  int grid = enum_grid();
+  GR_CUDA(cudaMemsetAsync(&w.ctrl->next_chunk, 0, sizeof(u64), (cudaStream_t)s));
+  enum_kernel<<<grid, NT, (size_t)MAXC * 8, (cudaStream_t)s>>>(p);
+  GR_CHECK_LAUNCH("enum_kernel");
+  return GR_OK;
+}
+
+extern "C" int64_t *gr_exact_level_keys(const gr_batch *in, int which, void *ws) {
+  (void)which;
+  if (!in || !ws) return nullptr;
+  return (int64_t *)ws_of(in, ws).lvlkey;
+}
+
+namespace {
+int *pinned_i32() {
+  static thread_local int *p = nullptr;
+  if (!p) {
+    if (cudaMallocHost((void **)&p, 64) != cudaSuccess) p = nullptr;
+  }
+  return p;
+}
+}  // namespace
+
+extern "C" int gr_exact_finish(const gr_batch *in, int which, int k, gr_result *out, void *ws,
+                               size_t ws_bytes, gr_stream_t s, int32_t *n_active) {
+  int rc = validate_batch(in, which);
+  if (rc) return rc;
+  Layout L = layout_of(in);
+  if (!ws || ws_bytes < L.total) { gr_set_error("workspace too small"); return GR_EWORKSPACE; }
+  if (k < 1 || k > 64) { gr_set_error("bad level"); return GR_EINVAL; }
+  WS w = ws_of(in, ws);
+  cudaStream_t st = (cudaStream_t)s;
+  finish_kernel<<<1, FT, 0, st>>>(in_of(in, which), out_of(out), w, which, k,
+                                   (in->flags & GR_FLAG_EXHAUSTIVE) ? 1 : 0);
+  GR_CHECK_LAUNCH("finish_kernel");
+  int *h = pinned_i32();
+  if (!h) { gr_set_error("cudaMallocHost failed"); return GR_ECUDA; }
+  GR_CUDA(cudaMemcpyAsync(h, &w.ctrl->n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
+  GR_CUDA(cudaStreamSynchronize(st));
+  if (n_active) *n_active = *h;
+  return GR_OK;
+}
+
+static int solve_exact(const gr_batch *in, gr_result *out, void *ws, size_t ws_bytes, gr_stream_t s,
+                       int which) {
+  int rc = gr_exact_prepare(in, which, out, ws, ws_bytes, s);
+  if (rc) return rc;
+  int32_t n = 0;
+  // level 0 handled by the pack; is anything active for level 1?
+  {
+    WS w = ws_of(in, ws);
+    int *h = pinned_i32();
+    if (!h) { gr_set_error("cudaMallocHost failed"); return GR_ECUDA; }
+    GR_CUDA(cudaMemcpyAsync(h, &w.ctrl->n_active, sizeof(int), cudaMemcpyDeviceToHost, (cudaStream_t)s));
+    GR_CUDA(cudaStreamSynchronize((cudaStream_t)s));
+    n = *h;
+  }
+  for (int k = 1; n > 0 && k <= 64; k++) {
+    rc = gr_exact_level(in, which, k, 0, 1, ws, ws_bytes, s);
+    if (rc) return rc;
+    rc = gr_exact_finish(in, which, k, out, ws, ws_bytes, s, &n);
+    if (rc) return rc;
+  }
+  return GR_OK;
+}
+
+extern "C" int gr_solve_pms(const gr_batch *in, gr_result *out, void *ws, size_t ws_bytes,
+                            gr_stream_t s) {
+  return solve_exact(in, out, ws, ws_bytes, s, 0);
+}
+
+extern "C" int gr_mhs_exact(const gr_batch *in, gr_result *out, void *ws, size_t ws_bytes,
+                            gr_stream_t s) {
+  return solve_exact(in, out, ws, ws_bytes, s, 1);
+}

@@ -1,0 +1,577 @@
+// greedy_matrix.cu -- gr_mhs_greedy_matrix: Johnson's greedy mhs
+// over one huge phi+ held in HBM as a variable-major bit matrix
+// R[v][c/64] (bit c%64 <=> b_{v+1} in clause c), then reverse-delete to a
+// minimal set (reading R12) and the phi- check.
+//
+// Pass t (one launch of count_kernel):   counts[v] = sum_c popc(R[v][c] & U_t[c])
+//   with U_t = U_{t-1} & ~R[v*_{t-1}] computed on the fly per column tile
+//   (the mark of the previous pick is fused into this pass's prologue).
+// argmax_kernel:  v*_t = lowest v with the max count (R11); done when max = 0.
+//
+// B200 design: the pass is HBM-bound (m * n/8 bytes, ~1 op per byte).  A
+// persistent CTA per SM runs a warp-specialised pipeline: one producer warp
+// streams 4 KB row segments (one column tile of one row) into a 5-stage
+// shared-memory ring with cp.async.bulk (TMA bulk copies, SASS UBLKCP)
+// completing on mbarriers; 8 consumer warps AND each segment with the
+// register-resident U tile and POPC-accumulate per-row counts in registers,
+// reducing across lanes only once per work item (64 rows x 16 tiles).
+#include <cub/block/block_reduce.cuh>
+
+#include <algorithm>
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+
+namespace {
+
+constexpr int TW = 512;            // words per column tile (4 KB per row segment)
+constexpr int RB = 64;             // rows per work item
+constexpr int TPI = 16;            // tiles per work item
+constexpr int NCW = 8;             // consumer warps
+constexpr int ROWS_PER_STAGE = 8;  // one row per consumer warp
+constexpr int NSTAGE = 5;
+constexpr int CT = 32 * (NCW + 1); // count-kernel CTA size
+constexpr size_t STAGE_BYTES = (size_t)ROWS_PER_STAGE * TW * 8;
+constexpr size_t COUNT_SMEM = NSTAGE * STAGE_BYTES + 2 * NSTAGE * 8 + 64;
+
+struct GCtrl {
+  int done;
+  int npicks;
+  int vprev;       // last pick (-1 = none): its mark is applied by the next pass
+  int upar;        // U buffer parity: pass reads U[upar], writes U[upar ^ 1]
+  unsigned int maxcount;
+  int bad;
+  int pad[2];
+};
+
+struct GLayout {
+  size_t ctrl, U, counts, picks, planes, flags, smask, total;
+  int nplanes;
+};
+
+int bitlen_i(long long x) {
+  int b = 0;
+  while (x) { b++; x >>= 1; }
+  return b;
+}
+
+GLayout glayout(const gr_bitmatrix *in) {
+  GLayout L{};
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t at = o; o = align256(o + bytes); return at; };
+  const size_t ld = (size_t)in->ld;
+  L.nplanes = std::max(1, bitlen_i(in->m));
+  L.ctrl = take(sizeof(GCtrl));
+  L.U = take(2 * ld * 8);
+  L.counts = take(4 * (size_t)in->m);
+  L.picks = take(4 * ((size_t)in->m + 1));
+  L.planes = take((size_t)L.nplanes * ld * 8);
+  L.flags = take(4 * ((size_t)in->m + 1));
+  L.smask = take(8 * (((size_t)in->m + 63) / 64 + 1));
+  L.total = o;
+  return L;
+}
+
+// ---- PTX wrappers: mbarrier + bulk async copy ------------------------------
+__device__ __forceinline__ u32 smem_u32(const void *p) { return (u32)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(u64 *bar, u32 count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(u64 *bar, u32 bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(u64 *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64 *bar, u32 parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, u32 bytes, u64 *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+struct CountParams {
+  const u64 *R;
+  int64_t ld;
+  int m;
+  int ntiles;
+  const u64 *U_in;     // U_{t-1} (or the given U for a shard count)
+  u64 *U_out;          // U_t written by row-block-0 items (nullptr: no write)
+  u32 *counts;
+  GCtrl *ctrl;         // nullptr: no done / mark (shard count)
+  int mark;            // apply U &= ~R[vprev]
+};
+
+// ---- the streaming count pass ------------------------------------------------
+__global__ void __launch_bounds__(CT, 1) count_kernel(CountParams p) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  u64 *stage = (u64 *)smraw;
+  u64 *full = (u64 *)(smraw + NSTAGE * STAGE_BYTES);
+  u64 *empty = full + NSTAGE;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int vprev = -1;
+  if (p.ctrl) {
+    if (*(volatile int *)&p.ctrl->done) return;
+    if (p.mark) vprev = p.ctrl->vprev;
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NSTAGE; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int nrb = (p.m + RB - 1) / RB;
+  const int ntr = (p.ntiles + TPI - 1) / TPI;
+  const int nitems = nrb * ntr;
+  if (warp == NCW) {
+    // ---------------- producer warp: bulk copies into the ring -------------
+    if (lane == 0) {
+      u32 it = 0;
+      for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+        const int rb = item % nrb, tr = item / nrb;
+        const int r0 = rb * RB;
+        const int t0 = tr * TPI, t1 = min(t0 + TPI, p.ntiles);
+        for (int ti = t0; ti < t1; ti++) {
+          const int tw = (int)min((int64_t)TW, p.ld - (int64_t)ti * TW);
+          for (int g = 0; g < RB / ROWS_PER_STAGE; g++, it++) {
+            const int s = it % NSTAGE;
+            mbar_wait(&empty[s], ((it / NSTAGE) & 1) ^ 1);
+            int nrow = min(ROWS_PER_STAGE, p.m - (r0 + g * ROWS_PER_STAGE));
+            nrow = max(nrow, 0);
+            mbar_expect_tx(&full[s], (u32)(nrow * tw * 8));
+            for (int w = 0; w < nrow; w++) {
+              const int row = r0 + g * ROWS_PER_STAGE + w;
+              bulk_g2s(stage + (size_t)s * ROWS_PER_STAGE * TW + (size_t)w * TW,
+                       p.R + (size_t)row * p.ld + (size_t)ti * TW, (u32)(tw * 8), &full[s]);
+            }
+          }
+        }
+      }
+    }
+    return;
+  }
+  // ---------------- consumer warps ------------------------------------------
+  u32 it = 0;
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const int rb = item % nrb, tr = item / nrb;
+    const int r0 = rb * RB;
+    const int t0 = tr * TPI, t1 = min(t0 + TPI, p.ntiles);
+    u32 acc[RB / ROWS_PER_STAGE];
+#pragma unroll
+    for (int g = 0; g < RB / ROWS_PER_STAGE; g++) acc[g] = 0;
+    for (int ti = t0; ti < t1; ti++) {
+      const int tw = (int)min((int64_t)TW, p.ld - (int64_t)ti * TW);
+      const int nstep = tw / 64;
+      // U fragment of this lane: words ti*TW + s*64 + 2*lane + {0,1}
+      ulonglong2 u[TW / 64];
+#pragma unroll
+      for (int s = 0; s < TW / 64; s++) {
+        if (s < nstep) {
+          const size_t wo = (size_t)ti * TW + (size_t)s * 64 + 2 * lane;
+          ulonglong2 x = *(const ulonglong2 *)(p.U_in + wo);
+          if (vprev >= 0) {
+            const ulonglong2 r = *(const ulonglong2 *)(p.R + (size_t)vprev * p.ld + wo);
+            x.x &= ~r.x;
+            x.y &= ~r.y;
+          }
+          u[s] = x;
+          if (p.U_out && rb == 0 && warp == 0) *(ulonglong2 *)(p.U_out + wo) = x;
+        } else {
+          u[s] = make_ulonglong2(0, 0);
+        }
+      }
+#pragma unroll
+      for (int g = 0; g < RB / ROWS_PER_STAGE; g++, it++) {
+        const int s = it % NSTAGE;
+        mbar_wait(&full[s], (it / NSTAGE) & 1);
+        const int row = r0 + g * ROWS_PER_STAGE + warp;
+        if (row < p.m) {
+          const u64 *seg = stage + (size_t)s * ROWS_PER_STAGE * TW + (size_t)warp * TW;
+          u32 c = 0;
+#pragma unroll
+          for (int q = 0; q < TW / 64; q++) {
+            if (q < nstep) {
+              const ulonglong2 d = *(const ulonglong2 *)(seg + q * 64 + 2 * lane);
+              c += __popcll(d.x & u[q].x) + __popcll(d.y & u[q].y);
+            }
+          }
+          acc[g] += c;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+      }
+    }
+    // one reduction per row per item
+#pragma unroll
+    for (int g = 0; g < RB / ROWS_PER_STAGE; g++) {
+      u32 v = acc[g];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      const int row = r0 + g * ROWS_PER_STAGE + warp;
+      if (lane == 0 && row < p.m && v) atomicAdd(&p.counts[row], v);
+    }
+  }
+}
+
+// ---- argmax + bookkeeping (one CTA) ------------------------------------------
+constexpr int AT = 1024;
+__global__ void __launch_bounds__(AT) argmax_kernel(u32 *counts, int m, GCtrl *ctrl, int *picks) {
+  typedef cub::BlockReduce<u64, AT> Red;
+  __shared__ typename Red::TempStorage tmp;
+  if (*(volatile int *)&ctrl->done) return;
+  u64 best = 0;
+  for (int v = threadIdx.x; v < m; v += AT) {
+    const u32 c = counts[v];
+    counts[v] = 0;  // ready for the next pass
+    const u64 key = ((u64)c << 32) | (u64)(0xffffffffu - (u32)v);
+    best = key > best ? key : best;
+  }
+  best = Red(tmp).Reduce(best, cub::Max());
+  if (threadIdx.x == 0) {
+    const u32 c = (u32)(best >> 32);
+    ctrl->maxcount = c;
+    ctrl->upar ^= 1;  // the pass just run wrote U[upar ^ 1]
+    if (c == 0) {
+      ctrl->done = 1;
+      ctrl->vprev = -1;
+    } else {
+      const int v = (int)(0xffffffffu - (u32)(best & 0xffffffffu));
+      picks[ctrl->npicks] = v;
+      ctrl->npicks += 1;
+      ctrl->vprev = v;
+    }
+  }
+}
+
+__global__ void init_kernel(u64 *U0, int64_t ld, int64_t n, GCtrl *ctrl, u32 *counts, int m,
+                            int *picks) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t w = i; w < ld; w += stride) {
+    const int64_t c0 = w * 64;
+    u64 x = 0;
+    if (c0 + 64 <= n) x = ~0ull;
+    else if (c0 < n) x = (1ull << (n - c0)) - 1;
+    U0[w] = x;
+  }
+  for (int64_t v = i; v < m; v += stride) { counts[v] = 0; picks[v] = -1; }
+  if (i == 0) {
+    ctrl->done = 0;
+    ctrl->npicks = 0;
+    ctrl->vprev = -1;
+    ctrl->upar = 0;
+    ctrl->maxcount = 0;
+    ctrl->bad = 0;
+  }
+}
+
+// ---- prune: bit-sliced hit counters over the picks ----------------------------
+// planes[i][w] is bit i of the per-clause hit count; add/sub ripple carries.
+__global__ void planes_build_kernel(const u64 *R, int64_t ld, const int *picks, const GCtrl *ctrl,
+                                    u64 *planes, int nplanes) {
+  const int np = ctrl->npicks;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < ld;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    u64 P[32];
+    for (int i = 0; i < nplanes; i++) P[i] = 0;
+    for (int j = 0; j < np; j++) {
+      u64 carry = R[(size_t)picks[j] * ld + w];
+      for (int i = 0; i < nplanes && carry; i++) {
+        const u64 t = P[i] & carry;
+        P[i] ^= carry;
+        carry = t;
+      }
+    }
+    for (int i = 0; i < nplanes; i++) planes[(size_t)i * ld + w] = P[i];
+  }
+}
+
+// one[w] = clauses hit exactly once (bit 0 set, all higher planes clear)
+__global__ void one_kernel(const u64 *planes, int nplanes, int64_t ld, u64 *one) {
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < ld;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    u64 hi = 0;
+    for (int i = 1; i < nplanes; i++) hi |= planes[(size_t)i * ld + w];
+    one[w] = planes[w] & ~hi;
+  }
+}
+
+// flags[j] |= 1 if pick j (all picks when only < 0, else pick `only`) is the
+// sole hitter of some clause
+__global__ void private_kernel(const u64 *R, int64_t ld, const int *picks, const GCtrl *ctrl,
+                               const u64 *one, int *flags, int only) {
+  const int np = ctrl->npicks;
+  const int j0 = only >= 0 ? only : 0, j1 = only >= 0 ? only + 1 : np;
+  for (int j = j0; j < j1; j++) {
+    const u64 *row = R + (size_t)picks[j] * ld;
+    int found = 0;
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < ld;
+         w += (int64_t)gridDim.x * blockDim.x)
+      if (row[w] & one[w]) { found = 1; break; }
+    if (__syncthreads_or(found) && threadIdx.x == 0) atomicOr(&flags[j], 1);
+  }
+}
+
+// drop pick x: subtract its row from the bit-sliced counters, refresh one[]
+__global__ void remove_kernel(const u64 *R, int64_t ld, int x, u64 *planes, int nplanes, u64 *one) {
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < ld;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    u64 borrow = R[(size_t)x * ld + w];
+    if (!borrow) continue;
+    for (int i = 0; i < nplanes && borrow; i++) {
+      const u64 p = planes[(size_t)i * ld + w];
+      const u64 t = ~p & borrow;
+      planes[(size_t)i * ld + w] = p ^ borrow;
+      borrow = t;
+    }
+    u64 hi = 0;
+    for (int i = 1; i < nplanes; i++) hi |= planes[(size_t)i * ld + w];
+    one[w] = planes[w] & ~hi;
+  }
+}
+
+__global__ void finalize_kernel(const int *picks, const GCtrl *ctrl, const int *removed, int m,
+                                const u64 *neg, int n_neg, u64 *assign, int32_t *status,
+                                u64 *smask) {
+  const int mw = (m + 63) / 64;
+  const int np = ctrl->npicks;
+  __shared__ int s_viol;
+  for (int q = threadIdx.x; q < mw; q += blockDim.x) smask[q] = 0;
+  if (threadIdx.x == 0) s_viol = 0;
+  __syncthreads();
+  for (int j = threadIdx.x; j < np; j += blockDim.x)
+    if (!removed[j]) atomicOr((unsigned long long *)&smask[picks[j] >> 6], 1ull << (picks[j] & 63));
+  __syncthreads();
+  for (int q = threadIdx.x; q < mw; q += blockDim.x) assign[q] = smask[q];
+  for (int j = threadIdx.x; j < n_neg; j += blockDim.x) {
+    int sub = 1;
+    for (int q = 0; q < mw; q++)
+      if (neg[(size_t)j * mw + q] & ~smask[q]) { sub = 0; break; }
+    if (sub) s_viol = 1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *status = s_viol ? GR_SAT_NEG_VIOLATED : GR_SAT;
+}
+
+// ---- CSR packing ------------------------------------------------------------------
+template <typename V>
+__global__ void pack_vm_kernel(int m, int64_t n, const int64_t *off, const V *var, u64 *bits,
+                               int64_t ld, int32_t *bad, int varmajor) {
+  const int mw = (m + 63) / 64;
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e0 = off[c], e1 = off[c + 1];
+    if (e1 <= e0 && bad) atomicOr(bad, 2);
+    for (int64_t e = e0; e < e1; e++) {
+      const int v = (int)var[e];
+      if (v < 0 || v >= m) {
+        if (bad) atomicOr(bad, 1);
+        continue;
+      }
+      if (varmajor)
+        atomicOr((unsigned long long *)&bits[(size_t)v * ld + (c >> 6)], 1ull << (c & 63));
+      else
+        atomicOr((unsigned long long *)&bits[(size_t)c * mw + (v >> 6)], 1ull << (v & 63));
+    }
+  }
+}
+
+std::mutex g_mu;
+int g_count_grid = 0;
+int count_grid() {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g_count_grid) return g_count_grid;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaFuncSetAttribute(count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)COUNT_SMEM);
+  g_count_grid = sms;
+  return g_count_grid;
+}
+
+int validate_matrix(const gr_bitmatrix *in) {
+  if (!in || !in->bits) { gr_set_error("null matrix"); return GR_EINVAL; }
+  if (in->m < 1 || in->n_pos < 0 || in->n_neg < 0 || (in->n_neg > 0 && !in->neg)) {
+    gr_set_error("bad matrix sizes");
+    return GR_EINVAL;
+  }
+  if (in->ld < (in->n_pos + 63) / 64 || in->ld % 64 != 0 || in->ld < 64) {
+    gr_set_error("ld must be >= ceil(n_pos/64), >= 64 and a multiple of 64");
+    return GR_EINVAL;
+  }
+  return GR_OK;
+}
+
+int *pinned_ctrl() {
+  static thread_local int *p = nullptr;
+  if (!p && cudaMallocHost((void **)&p, sizeof(GCtrl) + 64) != cudaSuccess) p = nullptr;
+  return p;
+}
+
+}  // namespace
+
+extern "C" int64_t gr_bitmatrix_ld(int64_t n_pos) {
+  int64_t w = (n_pos + 63) / 64;
+  w = (w + 63) / 64 * 64;
+  return w < 64 ? 64 : w;
+}
+
+extern "C" int gr_pack_varmajor(int32_t m, int64_t n, const int64_t *off, const void *var,
+                                int var_bytes, uint64_t *bits, int64_t ld, int32_t *d_bad,
+                                gr_stream_t s) {
+  if (m < 1 || n < 0 || !off || (!var && n > 0) || !bits || ld < (n + 63) / 64 ||
+      (var_bytes != 2 && var_bytes != 4)) {
+    gr_set_error("gr_pack_varmajor: bad arguments");
+    return GR_EINVAL;
+  }
+  if (n == 0) return GR_OK;
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  if (var_bytes == 2)
+    pack_vm_kernel<int16_t><<<grid, 256, 0, (cudaStream_t)s>>>(m, n, off, (const int16_t *)var, bits, ld, d_bad, 1);
+  else
+    pack_vm_kernel<int32_t><<<grid, 256, 0, (cudaStream_t)s>>>(m, n, off, (const int32_t *)var, bits, ld, d_bad, 1);
+  GR_CHECK_LAUNCH("pack_vm_kernel");
+  return GR_OK;
+}
+
+extern "C" int gr_pack_clausemajor(int32_t m, int64_t n, const int64_t *off, const void *var,
+                                   int var_bytes, uint64_t *masks, int32_t *d_bad, gr_stream_t s) {
+  if (m < 1 || n < 0 || !off || (!var && n > 0) || !masks || (var_bytes != 2 && var_bytes != 4)) {
+    gr_set_error("gr_pack_clausemajor: bad arguments");
+    return GR_EINVAL;
+  }
+  if (n == 0) return GR_OK;
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  if (var_bytes == 2)
+    pack_vm_kernel<int16_t><<<grid, 256, 0, (cudaStream_t)s>>>(m, n, off, (const int16_t *)var, masks, 0, d_bad, 0);
+  else
+    pack_vm_kernel<int32_t><<<grid, 256, 0, (cudaStream_t)s>>>(m, n, off, (const int32_t *)var, masks, 0, d_bad, 0);
+  GR_CHECK_LAUNCH("pack_cm_kernel");
+  return GR_OK;
+}
+
+extern "C" size_t gr_greedy_matrix_workspace_bytes(const gr_bitmatrix *in) {
+  if (validate_matrix(in)) return 0;
+  return glayout(in).total;
+}
+
+extern "C" int gr_greedy_count_shard(const gr_bitmatrix *shard, const uint64_t *d_U,
+                                     uint32_t *d_counts, gr_stream_t s) {
+  int rc = validate_matrix(shard);
+  if (rc) return rc;
+  if (!d_U || !d_counts) { gr_set_error("null U / counts"); return GR_EINVAL; }
+  cudaStream_t st = (cudaStream_t)s;
+  GR_CUDA(cudaMemsetAsync(d_counts, 0, sizeof(u32) * shard->m, st));
+  CountParams p{shard->bits, shard->ld, shard->m, (int)((shard->ld + TW - 1) / TW), d_U, nullptr,
+                d_counts, nullptr, 0};
+  count_kernel<<<count_grid(), CT, COUNT_SMEM, st>>>(p);
+  GR_CHECK_LAUNCH("count_kernel(shard)");
+  return GR_OK;
+}
+
+extern "C" int gr_mhs_greedy_matrix(const gr_bitmatrix *in, uint64_t *assign, int32_t *status,
+                                    int32_t *picks, int32_t *n_picks, void *ws, size_t ws_bytes,
+                                    gr_stream_t s) {
+  int rc = validate_matrix(in);
+  if (rc) return rc;
+  if (!assign || !status) { gr_set_error("null assign / status"); return GR_EINVAL; }
+  GLayout L = glayout(in);
+  if (!ws || ws_bytes < L.total) { gr_set_error("workspace too small"); return GR_EWORKSPACE; }
+  char *base = (char *)ws;
+  GCtrl *ctrl = (GCtrl *)(base + L.ctrl);
+  u64 *U = (u64 *)(base + L.U);
+  u32 *counts = (u32 *)(base + L.counts);
+  int *wpicks = (int *)(base + L.picks);
+  u64 *planes = (u64 *)(base + L.planes);
+  int *flags = (int *)(base + L.flags);
+  u64 *smask = (u64 *)(base + L.smask);
+  cudaStream_t st = (cudaStream_t)s;
+  const int64_t ld = in->ld;
+  const int ntiles = (int)((ld + TW - 1) / TW);
+  init_kernel<<<592, 256, 0, st>>>(U, ld, in->n_pos, ctrl, counts, in->m, wpicks);
+  GR_CHECK_LAUNCH("init_kernel");
+  const int grid = count_grid();
+  int *h = pinned_ctrl();
+  if (!h) { gr_set_error("cudaMallocHost failed"); return GR_ECUDA; }
+  // pass t reads U[t & 1] and writes U[(t & 1) ^ 1]; parity is host-known
+  // because every pass (even a no-op after done) flips it in argmax_kernel.
+  const int CHUNK = 8;
+  int t = 0;
+  for (;;) {
+    for (int j = 0; j < CHUNK; j++, t++) {
+      CountParams p{in->bits, ld, in->m, ntiles, U + (size_t)(t & 1) * ld,
+                    U + (size_t)((t & 1) ^ 1) * ld, counts, ctrl, 1};
+      count_kernel<<<grid, CT, COUNT_SMEM, st>>>(p);
+      GR_CHECK_LAUNCH("count_kernel");
+      argmax_kernel<<<1, AT, 0, st>>>(counts, in->m, ctrl, wpicks);
+      GR_CHECK_LAUNCH("argmax_kernel");
+    }
+    GR_CUDA(cudaMemcpyAsync(h, ctrl, sizeof(GCtrl), cudaMemcpyDeviceToHost, st));
+    GR_CUDA(cudaStreamSynchronize(st));
+    if (((GCtrl *)h)->done) break;
+    if (t > in->m + 2 * CHUNK) { gr_set_error("greedy did not terminate"); return GR_ECUDA; }
+  }
+  const int np = ((GCtrl *)h)->npicks;
+  if (n_picks) *n_picks = np;
+  // prune (reverse-delete, R12)
+  GR_CUDA(cudaMemsetAsync(flags, 0, sizeof(int) * (in->m + 1), st));
+  planes_build_kernel<<<(int)std::min<int64_t>((ld + 255) / 256, 148 * 8), 256, 0, st>>>(
+      in->bits, ld, wpicks, ctrl, planes, L.nplanes);
+  GR_CHECK_LAUNCH("planes_build_kernel");
+  u64 *one = U;  // the U buffers are free once the greedy loop is done
+  const int egrid = (int)std::min<int64_t>((ld + 255) / 256, 148 * 8);
+  one_kernel<<<egrid, 256, 0, st>>>(planes, L.nplanes, ld, one);
+  GR_CHECK_LAUNCH("one_kernel");
+  private_kernel<<<148 * 4, 256, 0, st>>>(in->bits, ld, wpicks, ctrl, one, flags, -1);
+  GR_CHECK_LAUNCH("private_kernel");
+  std::vector<int> hflags(np + 1), hpicks(np + 1);
+  if (np > 0) {
+    GR_CUDA(cudaMemcpyAsync(hflags.data(), flags, sizeof(int) * np, cudaMemcpyDeviceToHost, st));
+    GR_CUDA(cudaMemcpyAsync(hpicks.data(), wpicks, sizeof(int) * np, cudaMemcpyDeviceToHost, st));
+    GR_CUDA(cudaStreamSynchronize(st));
+  }
+  // a pick that is the sole hitter of some clause stays so (counts only
+  // decrease); the others are re-checked in reverse pick order
+  std::vector<int> removed(np + 1, 0);
+  int *hf = pinned_ctrl() + 8;
+  for (int j = np - 1; j >= 0; j--) {
+    if (hflags[j]) continue;
+    GR_CUDA(cudaMemsetAsync(flags + j, 0, sizeof(int), st));
+    private_kernel<<<148 * 4, 256, 0, st>>>(in->bits, ld, wpicks, ctrl, one, flags, j);
+    GR_CHECK_LAUNCH("private_kernel(one)");
+    GR_CUDA(cudaMemcpyAsync(hf, flags + j, sizeof(int), cudaMemcpyDeviceToHost, st));
+    GR_CUDA(cudaStreamSynchronize(st));
+    if (!*hf) {
+      removed[j] = 1;
+      remove_kernel<<<egrid, 256, 0, st>>>(in->bits, ld, hpicks[j], planes, L.nplanes, one);
+      GR_CHECK_LAUNCH("remove_kernel");
+    }
+  }
+  // removed flags -> device (reuse `flags`)
+  if (np > 0) {
+    GR_CUDA(cudaMemcpyAsync(flags, removed.data(), sizeof(int) * np, cudaMemcpyHostToDevice, st));
+    GR_CUDA(cudaStreamSynchronize(st));
+  }
+  finalize_kernel<<<1, 256, 0, st>>>(wpicks, ctrl, flags, in->m, in->neg, in->n_neg, assign,
+                                     status, smask);
+  GR_CHECK_LAUNCH("finalize_kernel");
+  if (picks) GR_CUDA(cudaMemcpyAsync(picks, wpicks, sizeof(int) * in->m, cudaMemcpyDeviceToDevice, st));
+  GR_CUDA(cudaStreamSynchronize(st));
+  return GR_OK;
+}

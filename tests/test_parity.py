@@ -1,0 +1,272 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle,
+element by element (status, assignment mask, cost; greedy pick order) on the
+same seeded inputs.  Everything here is integer: the bar is bit-exact."""
+import os
+import random
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2011_08373_b200 as gr
+from paper_2011_08373_b200 import synth
+from gr_testutil import load_golden
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+try:
+    import torch
+
+    HAVE_GPU = torch.cuda.is_available()
+except Exception:  # pragma: no cover
+    HAVE_GPU = False
+
+if not HAVE_GPU:
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+
+def gpu_solve(cb, which, flags=0):
+    db = gr.DeviceBatch.from_host(cb, flags=flags)
+    fn = {"pms": gr.solve_pms, "mhs": gr.mhs_exact, "greedy": gr.mhs_greedy}[which]
+    r = fn(db).to_host()
+    torch.cuda.synchronize()
+    return r
+
+
+def assert_same(g, o, which, idx=None, decided=False):
+    st = o.status if idx is None else o.status[idx]
+    bad = np.nonzero(g["status"] != st)[0]
+    assert bad.size == 0, f"{which}: status differs at {bad[:10]} gpu={g['status'][bad[:10]]} oracle={st[bad[:10]]}"
+    a = o.assign if idx is None else o.assign[idx]
+    bad = np.nonzero((g["assign"] != a).any(axis=1))[0]
+    assert bad.size == 0, f"{which}: assignment differs at {bad[:10]}"
+    c = o.cost if idx is None else o.cost[idx]
+    bad = np.nonzero(g["cost"] != c)[0]
+    assert bad.size == 0, f"{which}: cost differs at {bad[:10]}"
+    if decided:
+        d = o.decided if idx is None else o.decided[idx]
+        sat = (g["status"] == 0) | (g["status"] == 2)
+        bad = np.nonzero(sat & (g["decided"] != d))[0]
+        assert bad.size == 0, f"{which}: decided differs at {bad[:10]}"
+
+
+def oracle_all(cb, weighted=True):
+    return (oracle.batch("pms", cb, weighted=weighted), oracle.batch("mhs", cb),
+            oracle.batch("greedy", cb))
+
+
+def check_batch(cb, decided=True):
+    p, h, g = oracle_all(cb)
+    assert_same(gpu_solve(cb, "pms"), p, "pms", decided=decided and cb.w is None)
+    assert_same(gpu_solve(cb, "mhs"), h, "mhs", decided=decided)
+    assert_same(gpu_solve(cb, "greedy"), g, "greedy")
+
+
+# ------------------------------------------------------------------ golden
+@pytest.mark.parametrize("name", ["paper_example.txt", "unrepairable.txt", "write_write_race.txt"])
+def test_golden(name):
+    gd = load_golden(name)
+    cb = synth.batch_from_lists([(gd["m"], gd["pos"], gd["neg"])], W=1)
+    check_batch(cb)
+    if name == "paper_example.txt":
+        r = gpu_solve(cb, "pms")
+        assert synth.mask_to_vars(r["assign"][0]) == [2, 3, 4]
+        assert synth.mask_to_vars(gpu_solve(cb, "greedy")["assign"][0]) == [1, 2]
+
+
+def test_c1():
+    cb = synth.c1_instances()
+    e = np.load(os.path.join(GOLDEN, "expected_c1.npz"))
+    r = gpu_solve(cb, "pms")
+    assert (r["status"] == e["pms_status"]).all() and (r["assign"] == e["pms_assign"]).all()
+    assert (r["cost"] == e["pms_cost"]).all() and (r["decided"] == e["pms_decided"]).all()
+    assert r["assign"][:, 0].tolist() == [14, 49]
+    h = gpu_solve(cb, "mhs")
+    assert (h["status"] == e["mhs_status"]).all() and (h["assign"] == e["mhs_assign"]).all()
+    g = gpu_solve(cb, "greedy")
+    assert (g["status"] == e["greedy_status"]).all() and (g["assign"] == e["greedy_assign"]).all()
+
+
+# ------------------------------------------------------------------ fuzz
+def rand_batch(seed, B, mmax, nmax, W=1, weighted=False, p_neg=0.3, edge=True):
+    rng = random.Random(seed)
+    insts, ws = [], []
+    for i in range(B):
+        m = rng.randint(0, mmax)
+        pos, neg, seen = [], [], set()
+        n = rng.randint(0, nmax) if m else rng.randint(0, 1)
+        for _ in range(n):
+            if m == 0:
+                break
+            s = rng.randint(1, min(m, rng.choice([2, 3, 4, 8])))
+            c = tuple(sorted(rng.sample(range(1, m + 1), s)))
+            isneg = rng.random() < p_neg
+            if (isneg, c) in seen:
+                continue
+            seen.add((isneg, c))
+            (neg if isneg else pos).append(list(c))
+        if edge and rng.random() < 0.03:
+            (pos if rng.random() < 0.5 else neg).append([])  # empty clause (R6)
+        if edge and rng.random() < 0.03 and pos:
+            pos.append(list(pos[0]))  # duplicate clause (R9)
+        insts.append((m, pos, neg))
+        ws.append([rng.randint(1, 100) for _ in range(max(m, 1))])
+    return synth.batch_from_lists(insts, weights=ws if weighted else None, W=W)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_fuzz_small_unit(seed):
+    check_batch(rand_batch(seed, 300, 14, 16))
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_fuzz_small_weighted(seed):
+    check_batch(rand_batch(100 + seed, 300, 14, 16, weighted=True))
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_fuzz_wide_masks(seed):
+    # 33..64 variables (u64 lane path) with sparse clauses, and W = 2 inputs
+    check_batch(rand_batch(200 + seed, 60, 40, 10, weighted=(seed == 1)))
+    check_batch(rand_batch(300 + seed, 40, 100, 6, W=2))
+
+
+def test_bad_inputs_and_unsupported():
+    insts = [(4, [[1, 5]], []), (3, [[1]], [[2]]), (0, [], []), (2, [], [[1]]), (2, [[1, 2]], [[]])]
+    cb = synth.batch_from_lists(insts, weights=[[1, 0], [1, 1, 1], [1], [5, 5], [1, 1]], W=1)
+    cb.m[0] = 4  # b5 with m = 4 -> BADINPUT
+    check_batch(cb)
+    # > 64 support variables: exact solvers report UNSUPPORTED, greedy still works
+    wide = synth.batch_from_lists([(100, [[i] for i in range(1, 80)], [])], W=2)
+    r = gpu_solve(wide, "pms")
+    assert r["status"][0] == gr.GR_UNSUPPORTED
+    g = gpu_solve(wide, "greedy")
+    st, a, _ = oracle.greedy(100, 79, wide.masks, W=2)
+    assert g["status"][0] == st and (g["assign"][0] == a).all()
+
+
+# ------------------------------------------------------------------ configs
+def check_expected(cb, e, which, prefix, decided=False):
+    r = gpu_solve(cb, which)
+    for f in ("status", "assign", "cost"):
+        exp = e[f"{prefix}_{f}"]
+        got = r[f]
+        bad = np.nonzero((got != exp).reshape(got.shape[0], -1).any(axis=1))[0]
+        assert bad.size == 0, f"{prefix}.{f} differs at {bad[:10]}"
+    if decided:
+        sat = (r["status"] == 0) | (r["status"] == 2)
+        bad = np.nonzero(sat & (r["decided"] != e[f"{prefix}_decided"]))[0]
+        assert bad.size == 0, f"{prefix}.decided differs at {bad[:10]}"
+    return r
+
+
+def test_c2_full_batch():
+    cb = synth.c2_batch()
+    e = np.load(os.path.join(GOLDEN, "expected_c2.npz"))
+    import hashlib
+
+    h = hashlib.sha256()
+    for a in (cb.m, cb.off, cb.n_pos, cb.masks):
+        h.update(np.ascontiguousarray(a).tobytes())
+    assert str(e["digest"]) == h.hexdigest(), "generator drift: re-run scripts/make_expected.py"
+    check_expected(cb, e, "pms", "pms", decided=True)
+    check_expected(cb, e, "mhs", "mhs", decided=True)
+    check_expected(cb, e, "greedy", "greedy")
+    # live oracle on a random sample of small instances
+    idx = [b for b in range(cb.B) if cb.m[b] <= 16][:200]
+    sub = cb.subset(idx)
+    check_batch(sub)
+
+
+def test_c3_first_witness_exhaustive_and_shards():
+    cb, H, grp = synth.c3_instance()
+    e = np.load(os.path.join(GOLDEN, "expected_c3.npz"))
+    for flags in (0, gr.GR_FLAG_EXHAUSTIVE):
+        r = gpu_solve(cb, "pms", flags=flags)
+        assert r["status"][0] == gr.GR_SAT
+        assert int(r["assign"][0, 0]) == int(e["assign"])
+        assert int(r["cost"][0]) == 16
+    m, npos, mk, _ = cb.instance(0)
+    assert oracle.feasible(int(r["assign"][0, 0]), npos, mk)
+    # shard emulation: G sequential shards + host min == one GPU
+    db = gr.DeviceBatch.from_host(cb)
+    for G in (2, 3):
+        s = gr.ExactSession(db, gr.PMS)
+        s.prepare()
+        n, k = 1, 0
+        while n:
+            k += 1
+            keys = []
+            for shard in range(G):
+                s.level_keys().fill_(2**63 - 1)
+                s.level(k, shard, G)
+                keys.append(s.level_keys().clone())
+            s.level_keys().copy_(torch.stack(keys).min(0).values)
+            n = s.finish(k)
+        got = s.out.to_host()
+        assert int(got["assign"][0, 0]) == int(e["assign"]) and got["status"][0] == 0
+
+
+def test_c4_subset_and_full_batch():
+    e = np.load(os.path.join(GOLDEN, "expected_c4.npz"))
+    full = synth.c4_batch()
+    sub = full.subset(range(256))
+    check_expected(sub, e, "pms", "pms")
+    r = gpu_solve(full, "pms")
+    assert (r["status"] == 0).all()  # SAT by construction (planted H)
+    for f in ("status", "assign", "cost"):
+        assert (r[f][:256] == e[f"pms_{f}"]).all()
+    # any output: feasible, and its cost is its weight
+    rng = np.random.default_rng(0)
+    for b in rng.choice(full.B, 300, replace=False):
+        m, npos, mk, w = full.instance(int(b))
+        x = int(r["assign"][b, 0])
+        assert oracle.feasible(x, npos, mk)
+        assert int(r["cost"][b]) == sum(int(w[i]) for i in range(m) if (x >> i) & 1)
+
+
+# ------------------------------------------------------------------ greedy at scale
+def csr_from_lists(cls):
+    off = np.cumsum([0] + [len(c) for c in cls]).astype(np.int64)
+    var = np.array([v for c in cls for v in c], np.int32)
+    return off, var
+
+
+def check_matrix(m, pos, neg):
+    po, pv = csr_from_lists(pos)
+    no, nv = csr_from_lists(neg)
+    o = oracle.greedy_csr(m, po, pv, no, nv)
+    bm = gr.pack_bitmatrix(m, po, pv, no, nv)
+    assert bm.bad == 0
+    r = gr.mhs_greedy_matrix(bm)
+    torch.cuda.synchronize()
+    assert r.n_picks == len(o.picks)
+    assert r.picks.cpu().numpy()[: r.n_picks].tolist() == o.picks.tolist()
+    a = r.assign.cpu().numpy().view(np.uint64)
+    got = [i for i in range(m) if (int(a[i // 64]) >> (i % 64)) & 1]
+    assert got == np.nonzero(o.in_S)[0].tolist()
+    assert int(r.status.item()) == o.status
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_greedy_matrix_random(seed):
+    rng = random.Random(seed)
+    m = rng.choice([7, 64, 65, 300])
+    n = rng.choice([1, 100, 5000, 40000])
+    pos = [sorted(rng.sample(range(m), rng.randint(1, min(m, 6)))) for _ in range(n)]
+    neg = [sorted(rng.sample(range(m), min(m, 2))) for _ in range(5)]
+    check_matrix(m, pos, neg)
+
+
+def test_greedy_matrix_c5_shape_reduced():
+    csr, H = synth.c5_clauses(m=4096, n=1 << 18)
+    o = oracle.greedy_csr(csr.m, csr.pos_off, csr.pos_var.astype(np.int32), csr.neg_off, csr.neg_var)
+    bm = gr.pack_bitmatrix(csr.m, csr.pos_off, csr.pos_var, csr.neg_off, csr.neg_var)
+    r = gr.mhs_greedy_matrix(bm)
+    torch.cuda.synchronize()
+    assert r.picks.cpu().numpy()[: r.n_picks].tolist() == o.picks.tolist()
+    a = r.assign.cpu().numpy().view(np.uint64)
+    got = [i for i in range(csr.m) if (int(a[i // 64]) >> (i % 64)) & 1]
+    assert got == np.nonzero(o.in_S)[0].tolist()
+    assert int(r.status.item()) == o.status
