@@ -190,7 +190,7 @@ def main():
                    "parallelism": f"batch-sharded x{world}" if world > 1 else "single GPU"},
         "instances_per_s": inst_all * a.steps / sec,
         "candidates_per_step": cands_all,
-        "status_counts": {k: int(v) for k, v in zip(*np.unique(res[0]["status"], return_counts=True))},
+        "status_counts": {int(k): int(v) for k, v in zip(*np.unique(res[0]["status"], return_counts=True))},
         "clocks": clk.summary(),
         "gpu_launches": None,
     }

@@ -80,10 +80,14 @@ def set_threads(t: int) -> None:
 
 @dataclass
 class Result:
-    status: int
-    assign: int  # mask (word 0 for W = 1 inputs); 0 when UNSAT
+    status: int  # -1: support of phi+ > 64 variables (no oracle value)
+    assign: int  # mask (all W words joined); 0 when UNSAT
     cost: int  # U64MAX when UNSAT
     decided: int = 0
+
+
+def _join(words) -> int:
+    return sum(int(x) << (64 * i) for i, x in enumerate(words))
 
 
 def _inst(masks, W):
@@ -95,13 +99,13 @@ def pms(m: int, n_pos: int, masks, w=None, reduce: int = 1, W: int = 1) -> Resul
     """Exact PMS (w None) / WPMS of one instance; masks [n, W] positives first."""
     mk = _inst(masks, W)
     wa = None if w is None else np.ascontiguousarray(np.asarray(w, np.uint32))
-    a, c, s, d = (np.zeros(1, np.uint64), np.zeros(1, np.uint64), np.zeros(1, np.int32),
+    a, c, s, d = (np.zeros(W, np.uint64), np.zeros(1, np.uint64), np.zeros(1, np.int32),
                   np.zeros(1, np.uint64))
     rc = lib().or_pms(m, W, n_pos, mk.shape[0] - n_pos, _ptr(mk), _ptr(wa), reduce,
                       _ptr(a), _ptr(c), _ptr(s), _ptr(d))
     if rc:
         raise RuntimeError(f"or_pms failed: {rc}")
-    return Result(int(s[0]), int(a[0]), int(c[0]), int(d[0]))
+    return Result(int(s[0]), _join(a), int(c[0]), int(d[0]))
 
 
 def pms_brute(m: int, n_pos: int, masks, w=None, W: int = 1) -> Result:
@@ -118,13 +122,13 @@ def pms_brute(m: int, n_pos: int, masks, w=None, W: int = 1) -> Result:
 
 def mhs(m: int, n_pos: int, masks, reduce: int = 1, W: int = 1) -> Result:
     mk = _inst(masks, W)
-    a, c, s, d = (np.zeros(1, np.uint64), np.zeros(1, np.uint64), np.zeros(1, np.int32),
+    a, c, s, d = (np.zeros(W, np.uint64), np.zeros(1, np.uint64), np.zeros(1, np.int32),
                   np.zeros(1, np.uint64))
     rc = lib().or_mhs(m, W, n_pos, mk.shape[0] - n_pos, _ptr(mk), reduce, _ptr(a), _ptr(c),
                       _ptr(s), _ptr(d))
     if rc:
         raise RuntimeError(f"or_mhs failed: {rc}")
-    return Result(int(s[0]), int(a[0]), int(c[0]), int(d[0]))
+    return Result(int(s[0]), _join(a), int(c[0]), int(d[0]))
 
 
 @dataclass

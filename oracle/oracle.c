@@ -159,33 +159,42 @@ static int validate(int m, int W, int n, const uint64_t *masks, const uint32_t *
  */
 int or_pms(int m, int W, int n_pos, int n_neg, const uint64_t *masks, const uint32_t *w,
            int reduce, uint64_t *assign, uint64_t *cost, int32_t *status, uint64_t *decided) {
-  if (m < 0 || W < 1 || n_pos < 0 || n_neg < 0) return OR_EINVAL;
-  *assign = 0; *cost = UINT64_MAX; *decided = 0;
+  if (m < 0 || W < 1 || W > 2 || n_pos < 0 || n_neg < 0) return OR_EINVAL;
+  for (int t = 0; t < W; t++) assign[t] = 0;
+  *cost = UINT64_MAX; *decided = 0;
   int n = n_pos + n_neg;
   int v = validate(m, W, n, masks, w);
   if (v >= 0) { *status = v; return OR_OK; }
-  if (m > 64) return OR_ETOOBIG;
+  if (!reduce && m > 64) return OR_ETOOBIG;
   uint64_t *pos = (uint64_t *)malloc(sizeof(uint64_t) * (n_pos + 1));
   uint64_t *neg = (uint64_t *)malloc(sizeof(uint64_t) * (n_neg + 1));
   uint32_t wr[64];
   if (!pos || !neg) { free(pos); free(neg); return OR_ENOMEM; }
-  for (int j = 0; j < n_pos; j++) pos[j] = masks[(size_t)j * W];
-  uint64_t sup = (m == 64) ? ~0ull : ((1ull << m) - 1);
+  /* sup[t]: the enumerated variables (word t) */
+  uint64_t sup[2] = {0, 0};
   int np = n_pos, nn = 0, me = m, kmax = m;
   if (reduce) {
-    sup = 0;
-    for (int j = 0; j < n_pos; j++) sup |= pos[j];
-    for (int j = 0; j < n_pos; j++) pos[j] = compress(pos[j], sup);
+    for (int j = 0; j < n_pos; j++) for (int t = 0; t < W; t++) sup[t] |= masks[(size_t)j * W + t];
+    me = popc64(sup[0]) + popc64(sup[1]);
+    if (me > 64) { free(pos); free(neg); return OR_ETOOBIG; }
+    for (int j = 0; j < n_pos; j++)
+      pos[j] = compress(masks[(size_t)j * W], sup[0]) |
+               (W > 1 ? compress(masks[(size_t)j * W + 1], sup[1]) << popc64(sup[0]) : 0);
     for (int j = 0; j < n_neg; j++) {
-      uint64_t N = masks[(size_t)(n_pos + j) * W];
-      if ((N & ~sup) == 0) neg[nn++] = compress(N, sup);
+      const uint64_t *N = masks + (size_t)(n_pos + j) * W;
+      int inside = 1;
+      for (int t = 0; t < W; t++) if (N[t] & ~sup[t]) inside = 0;
+      if (inside)
+        neg[nn++] = compress(N[0], sup[0]) | (W > 1 ? compress(N[1], sup[1]) << popc64(sup[0]) : 0);
     }
-    me = popc64(sup);
     kmax = me < n_pos ? me : n_pos;
   } else {
+    sup[0] = (m == 64) ? ~0ull : ((1ull << m) - 1);
+    for (int j = 0; j < n_pos; j++) pos[j] = masks[(size_t)j * W];
     for (int j = 0; j < n_neg; j++) neg[nn++] = masks[(size_t)(n_pos + j) * W];
   }
-  { int j = 0; for (int i = 0; i < 64; i++) if ((sup >> i) & 1) wr[j++] = w ? w[i] : 1u; }
+  { int j = 0;
+    for (int t = 0; t < 2; t++) for (int i = 0; i < 64; i++) if ((sup[t] >> i) & 1) wr[j++] = w ? w[64 * t + i] : 1u; }
   /* sorted weights for S_k (insertion sort, me <= 64) */
   uint32_t ws[64];
   for (int i = 0; i < me; i++) ws[i] = wr[i];
@@ -215,8 +224,13 @@ int or_pms(int m, int W, int n_pos, int n_neg, const uint64_t *masks, const uint
   }
   *decided = nd;
   if (found) {
-    *assign = reduce ? expand(best_x, sup) : best_x;
-    *cost = cost_of(*assign, w);
+    if (reduce) {
+      assign[0] = expand(best_x, sup[0]);
+      if (W > 1) assign[1] = expand(best_x >> popc64(sup[0]), sup[1]);
+    } else {
+      assign[0] = best_x;
+    }
+    *cost = cost_of(assign[0], w) + (W > 1 ? cost_of(assign[1], w ? w + 64 : NULL) : 0);
     *status = OR_SAT;
   } else {
     *status = OR_UNSAT;
@@ -253,14 +267,17 @@ int or_pms_brute(int m, int W, int n_pos, int n_neg, const uint64_t *masks, cons
  * clause N has all its b_i true in the MHS (N subset of S). */
 int or_mhs(int m, int W, int n_pos, int n_neg, const uint64_t *masks, int reduce,
            uint64_t *assign, uint64_t *cost, int32_t *status, uint64_t *decided) {
-  *assign = 0; *cost = UINT64_MAX; *decided = 0;
+  for (int t = 0; t < W; t++) assign[t] = 0;
+  *cost = UINT64_MAX; *decided = 0;
   if (bad_input(m, W, n_pos + n_neg, masks, NULL)) { *status = OR_BADINPUT; return OR_OK; }
   if (has_empty(W, n_pos, masks)) { *status = OR_UNSAT; return OR_OK; }
   int rc = or_pms(m, W, n_pos, 0, masks, NULL, reduce, assign, cost, status, decided);
   if (rc != OR_OK || *status != OR_SAT) return rc;
   for (int j = 0; j < n_neg; j++) {
-    uint64_t N = masks[(size_t)(n_pos + j) * W];
-    if (!clause_neg_sat(*assign, N)) { *status = OR_SAT_NEG_VIOLATED; break; }
+    const uint64_t *N = masks + (size_t)(n_pos + j) * W;
+    int all_true = 1;
+    for (int t = 0; t < W; t++) if ((assign[t] & N[t]) != N[t]) all_true = 0;
+    if (all_true) { *status = OR_SAT_NEG_VIOLATED; break; }
   }
   return OR_OK;
 }
@@ -387,10 +404,11 @@ int or_batch(int which, int B, int W, const int32_t *m, const int64_t *off, cons
     int n = (int)(off[b + 1] - off[b]);
     const uint64_t *mk = masks + (size_t)off[b] * W;
     int np = n_pos[b], nn = n - n_pos[b];
-    uint64_t a = 0, c = UINT64_MAX, d = 0; int32_t s = 0; int rc = OR_OK;
-    for (int t = 0; t < W; t++) assign[(size_t)b * W + t] = 0;
-    if (which == 0) rc = or_pms(m[b], W, np, nn, mk, w ? w + (size_t)b * wstride : NULL, reduce, &a, &c, &s, &d);
-    else if (which == 1) rc = or_mhs(m[b], W, np, nn, mk, reduce, &a, &c, &s, &d);
+    uint64_t c = UINT64_MAX, d = 0; int32_t s = 0; int rc = OR_OK;
+    uint64_t *a = assign + (size_t)b * W;
+    for (int t = 0; t < W; t++) a[t] = 0;
+    if (which == 0) rc = or_pms(m[b], W, np, nn, mk, w ? w + (size_t)b * wstride : NULL, reduce, a, &c, &s, &d);
+    else if (which == 1) rc = or_mhs(m[b], W, np, nn, mk, reduce, a, &c, &s, &d);
     else {
       int32_t *pk = malloc(sizeof(int32_t) * (m[b] + 1)); int32_t nu;
       rc = or_greedy_masks(m[b], W, np, nn, mk, assign + (size_t)b * W, pk, &nu, &s);
@@ -398,8 +416,9 @@ int or_batch(int which, int B, int W, const int32_t *m, const int64_t *off, cons
       if (s == OR_UNSAT || s == OR_BADINPUT) c = UINT64_MAX;
       free(pk);
     }
-    if (which != 2) assign[(size_t)b * W] = a;
     cost[b] = c; status[b] = s; if (decided) decided[b] = d;
+    if (rc == OR_ETOOBIG) { s = -1; rc = OR_OK; }  /* support > 64: no oracle value */
+    status[b] = s;
     if (rc != OR_OK) {
 #pragma omp critical
       err = rc;
