@@ -5,15 +5,21 @@
                     [--impl ours|reference] [--no-cpu-baseline]
 
 A *step* is one pass of the whole hot path over
-one batch: device clause packing, exact PMS (a), exact MHS (b) and greedy mhs
-(c) of every instance.  The default workload is BASELINE.json configs[1]
-("c2": 748 suite-shaped instances, m <= 32, <= 64 clauses).  Under torchrun
-every rank solves its own seeded 748-instance batch (weak scaling, no
-data-path collective); the timed region is bracketed by a barrier and a
-synchronize, and the time is the max over ranks.
+one batch of synthetic input: device clause packing, exact PMS (a), exact MHS
+(b) and greedy mhs (c) of every instance.  The default workload is
+BASELINE.json configs[1] ("c2": 748 suite-shaped instances, m <= 32, <= 64
+clauses), the configuration the metric is quoted on.  Under torchrun every
+rank solves its own seeded 748-instance batch (weak scaling, no data-path
+collective; "c3" instead splits each level's colex rank range across the
+ranks with an NCCL all-reduce MIN per level -- strong scaling).
 
-One JSON line on rank 0.  value = candidate assignments decided per second
-(exact PMS + MHS) over all ranks; instances_per_s alongside.
+The timed region is device-resident inputs -> device results, CUDA events on
+the launching stream, L2 flushed (256 MiB write) between steps, barrier +
+synchronize on both sides, max over ranks.  `e2e` repeats the step through the
+public API from pinned host buffers with the H2D / D2H copies inside.
+
+value = candidate assignments decided per second over all ranks (exact PMS +
+MHS; DESIGN.md §5 defines the count); instances_per_s alongside.
 """
 from __future__ import annotations
 
@@ -32,6 +38,8 @@ sys.path.insert(0, ROOT)
 
 METRIC = "candidate assignments checked/sec and instances solved/sec at 1/2/4/8 B200"
 L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
+ALU_LANES_PER_SM_CLK = 64   # LOP3/IADD3/ISETP: alu pipe, 16 lanes/clk per SMSP
+TEST_OPS = {32: 2, 64: 4}   # SASS ALU ops per clause test: (T & P) == 0 ? A &= P (per 32-bit word: 2)
 
 
 def parse():
@@ -42,14 +50,36 @@ def parse():
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--profile-kernels", action="store_true",
-                    help="record per-kernel CUDA-event durations inside the library")
+    ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
+
+
+def peaks():
+    p = {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "source": "fallback (B200_PROFILING.md)"}
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        p.update(hbm_gbs=float(d.get("hbm_gbs", p["hbm_gbs"])),
+                 sm_max_mhz=float(d.get("sm_max_mhz", p["sm_max_mhz"])),
+                 source="MEASURED_PEAKS.json")
+    return p
+
+
+def traffic_of(kernel: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the
+    committed ncu --set full capture (profiles/traffic.json), else None."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        d = json.load(f)
+    return d.get(kernel)
 
 
 # ---------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -62,10 +92,11 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            time.sleep(0.3)
         except FileNotFoundError:
             self.proc = None
         return self
@@ -83,15 +114,21 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm = [float(r[1]) for r in self.rows if len(r) > 8 and r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if len(r) > 8 and r[2].replace(".", "").isdigit()]
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+
+        rows = [r for r in self.rows if len(r) > 8]
+        sm = [num(r[1]) for r in rows if num(r[1])]
+        mx = [num(r[2]) for r in rows if num(r[2])]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = set()
-        for r in self.rows:
-            if len(r) > 8:
-                for i, n in enumerate(names):
-                    if r[5 + i].lower().startswith("active"):
-                        reasons.add(n)
+        for r in rows:
+            for i, n in enumerate(names):
+                if r[5 + i].lower().startswith("active"):
+                    reasons.add(n)
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
                 "samples": len(sm)}
@@ -102,17 +139,44 @@ def make_workload(cfg: str, rank: int):
     from paper_2011_08373_b200 import synth
 
     if cfg == "c1":
-        return synth.c1_instances(), "C1: paper example in m=8 (2 instances)"
+        return synth.c1_instances(), "C1: the paper's example (PAPER.md:26) in m=8, instances A+B"
     if cfg == "c2":
         return (synth.c2_batch(seed=synth.seed_for(2, rank)),
                 "C2: 748 suite-shaped instances, m<=32, <=64 clauses (PAPER.md:194, 593-602)")
     if cfg == "c3":
         cb, _, _ = synth.c3_instance()
-        return cb, "C3: m=48, 200 clauses, k*=16, exhaustive levels"
+        return cb, "C3: one instance m=48, 200 clauses, k*=16, levels 0..16 exhaustive"
     if cfg == "c4":
         return (synth.c4_batch(seed=synth.seed_for(4, rank)),
                 "C4: 10000 WPMS instances, m=40, w~U{50..100}, planted SAT")
     raise ValueError(cfg)
+
+
+def host_tensors(cb, pinned: bool):
+    import torch
+
+    def t(a, dt):
+        x = torch.from_numpy(np.ascontiguousarray(a).view(dt))
+        return x.pin_memory() if pinned else x
+
+    masks = cb.masks if cb.masks.shape[0] else np.zeros((1, cb.W), np.uint64)
+    h = {"m": t(cb.m.astype(np.int32), np.int32), "off": t(cb.off.astype(np.int64), np.int64),
+         "n_pos": t(cb.n_pos.astype(np.int32), np.int32),
+         "masks": t(masks.astype(np.uint64).view(np.int64), np.int64)}
+    if cb.w is not None:
+        h["w"] = t(cb.w.astype(np.uint32).view(np.int32), np.int32)
+    return h
+
+
+def device_batch(h, cb, dev, flags):
+    import paper_2011_08373_b200 as gr
+
+    n = np.diff(cb.off)
+    d = {k: v.to(dev, non_blocking=True) for k, v in h.items()}
+    return gr.DeviceBatch(m=d["m"], off=d["off"], n_pos=d["n_pos"], masks=d["masks"],
+                          w=d.get("w"), B=cb.B, W=cb.W, total_clauses=int(cb.off[-1]),
+                          max_clauses=int(n.max()) if n.size else 0,
+                          wstride=int(cb.w.shape[1]) if cb.w is not None else 0, flags=flags)
 
 
 def main():
@@ -126,115 +190,271 @@ def main():
     import torch.distributed as dist
 
     import paper_2011_08373_b200 as gr
+    from paper_2011_08373_b200 import multigpu
 
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     if a.config == "c5":
-        return run_c5(a, rank, world, dev)
+        return run_c5(a, rank, world, local, dev)
     cb, desc = make_workload(a.config, rank)
     flags = gr.GR_FLAG_EXHAUSTIVE if a.config == "c3" else 0
-    db = gr.DeviceBatch.from_host(cb, device=dev, flags=flags)
+    hb = host_tensors(cb, pinned=True)
+    db = device_batch(hb, cb, dev, flags)
+    torch.cuda.synchronize()
     outs = [gr.DeviceResult.empty(cb.B, cb.W, dev) for _ in range(3)]
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
+    sharded = a.config == "c3" and world > 1
 
-    def step():
-        gr.solve_pms(db, outs[0])
-        gr.mhs_exact(db, outs[1])
-        gr.mhs_greedy(db, outs[2])
+    def step(dbx, o):
+        if sharded:  # rank-range sharding of each level, NCCL all-reduce MIN per level
+            multigpu.solve_exact_sharded(dbx, gr.PMS, rank, world, out=o[0])
+            multigpu.solve_exact_sharded(dbx, gr.MHS, rank, world, out=o[1])
+        else:
+            gr.solve_pms(dbx, o[0])
+            gr.mhs_exact(dbx, o[1])
+        gr.mhs_greedy(dbx, o[2])
 
     for _ in range(a.warmup):
-        step()
+        step(db, outs)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    gr_prof = gr.profiler() if a.profile_kernels else None
+    # ---------------- timed region (device-resident inputs) ----------------
+    prof = gr.profiler(1).start()
+    l0 = gr.launch_count()
     total_ms = 0.0
     with ClockSampler(local) as clk:
-        if gr_prof:
-            gr_prof.start()
         for _ in range(a.steps):
             flush.fill_(1)  # L2 flush between timed iterations (untimed)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            step()
+            step(db, outs)
             e1.record(stream)
             e1.synchronize()
             total_ms += e0.elapsed_time(e1)
-        if gr_prof:
-            kern = gr_prof.stop()
+    launches = gr.launch_count() - l0
+    kern = prof.stop()
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
     res = [o.to_host() for o in outs]
-    cands = int(res[0]["decided"].astype(np.float64).sum() + res[1]["decided"].astype(np.float64).sum())
-    t = torch.tensor([total_ms, float(cands), float(cb.B)], dtype=torch.float64, device=dev)
-    if world > 1:
-        tmax = t.clone()
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-        tsum = t.clone()
-        dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
-        total_ms, cands_all, inst_all = float(tmax[0]), float(tsum[1]), float(tsum[2])
+    cands = float(res[0]["decided"].astype(np.float64).sum() + res[1]["decided"].astype(np.float64).sum())
+    if sharded:
+        cands_rank = cands / world  # every rank holds the full result
     else:
-        cands_all, inst_all = float(cands), float(cb.B)
+        cands_rank = cands
+    # ---------------- work counters (untimed, counting instantiation) ------
+    wprof = gr.profiler(2).start()
+    step(db, outs)
+    wk = wprof.stop()
+    # ---------------- e2e through the public API from pinned host buffers --
+    e2e_ms, h2d, d2h = None, 0, 0
+    if not a.no_e2e:
+        h2d = sum(int(v.numel() * v.element_size()) for v in hb.values())
+        for s in range(a.warmup + a.steps):
+            flush.fill_(1)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            dbx = device_batch(hb, cb, dev, flags)
+            step(dbx, outs)
+            host = [o.to_host() for o in outs]
+            e1.record(stream)
+            e1.synchronize()
+            if s >= a.warmup:
+                e2e_ms = (e2e_ms or 0.0) + e0.elapsed_time(e1)
+        d2h = sum(int(x.nbytes) for r in host for x in r.values())
+    # ---------------- reduce over ranks ---------------------------------------
+    t = torch.tensor([total_ms, cands_rank, float(cb.B if not sharded else cb.B / world),
+                      e2e_ms or 0.0], dtype=torch.float64, device=dev)
+    if world > 1:
+        tmax, tsum = t.clone(), t.clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+        total_ms, cands_all, inst_all, e2e_ms = float(tmax[0]), float(tsum[1]), float(tsum[2]), float(tmax[3])
+    else:
+        cands_all, inst_all = cands_rank, float(cb.B)
     sec = total_ms / 1e3
     value = cands_all * a.steps / sec
+    # ---------------- roofline of the dominant kernel (enum_kernel) ---------
+    pk = peaks()
+    ek = kern.get("enum_kernel", {"launches": 0, "ms": 0.0})
+    ew = wk.get("enum_kernel", {"launches": 0, "work": [0, 0, 0, 0]})
+    tests, blocks, wcands, tests64 = ew["work"]
+    ops = TEST_OPS[32] * (tests - tests64) + TEST_OPS[64] * tests64
+    roof = None
+    if ek["launches"] and ew["launches"]:
+        per_launch_ops = ops / ew["launches"]
+        per_launch_s = ek["ms"] / ek["launches"] / 1e3
+        achieved = per_launch_ops / per_launch_s / 1e12
+        peak_tops = 148 * ALU_LANES_PER_SM_CLK * pk["sm_max_mhz"] * 1e6 / 1e12
+        roof = {"bound": "alu", "achieved": achieved, "peak": peak_tops, "unit": "Tops/s",
+                "frac": achieved / peak_tops, "traffic": traffic_of("enum_kernel"),
+                "kernel": "enum_kernel",
+                "per_launch": {"ops": per_launch_ops, "ms": per_launch_s * 1e3,
+                               "clause_tests": tests / ew["launches"],
+                               "candidate_blocks": blocks / ew["launches"],
+                               "candidates": wcands / ew["launches"]},
+                "peak_source": f"148 SMs x {ALU_LANES_PER_SM_CLK} ALU lanes/clk x {pk['sm_max_mhz']:.0f} MHz "
+                               f"({pk['source']})",
+                "share_of_step": ek["ms"] / total_ms if total_ms else None}
     line = {
         "metric": METRIC, "value": value, "unit": "candidates/s", "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": total_ms / a.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "higher_is_better": True, "scaling": "strong" if sharded else "weak",
+        "vs_baseline": None, "dtype": "u64",
         "data": "synthetic (seeded, SURVEY.md §8(d) recipe; DESIGN.md §6)",
-        "config": {"workload": desc, "instances_per_gpu": cb.B, "l2": "flushed between steps (256 MiB write)",
-                   "parallelism": f"batch-sharded x{world}" if world > 1 else "single GPU"},
+        "config": {"workload": desc, "instances_per_gpu": cb.B,
+                   "l2": "flushed between timed steps (256 MiB write)",
+                   "parallelism": (f"level rank-range sharded x{world} (NCCL allreduce MIN per level)"
+                                   if sharded else (f"batch x{world} (one seeded batch per rank)"
+                                                    if world > 1 else "single GPU"))},
         "instances_per_s": inst_all * a.steps / sec,
         "candidates_per_step": cands_all,
-        "status_counts": {int(k): int(v) for k, v in zip(*np.unique(res[0]["status"], return_counts=True))},
+        "e2e": ({"value": cands_all * a.steps / (e2e_ms / 1e3), "unit": "candidates/s",
+                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                 "ms_per_step": e2e_ms / a.steps} if e2e_ms else None),
+        "gpu_launches": launches,
+        "roofline": roof,
         "clocks": clk.summary(),
-        "gpu_launches": None,
+        "status_counts": {str(int(k)): int(v) for k, v in zip(*np.unique(res[0]["status"], return_counts=True))},
+        "kernels": {k: {"launches": v["launches"], "ms_per_step": v["ms"] / a.steps} for k, v in kern.items()},
     }
-    if gr_prof:
-        line["kernels"] = kern
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(a.config, cb)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
-def run_c5(a, rank, world, dev):
-    raise SystemExit("c5 bench: not yet wired")
+# ---------------------------------------------------------------- C5
+def run_c5(a, rank, world, local, dev):
+    import torch
+
+    import paper_2011_08373_b200 as gr
+    from paper_2011_08373_b200 import synth
+
+    csr, H = synth.c5_clauses(seed=synth.seed_for(5, rank))
+    d = {"po": torch.from_numpy(csr.pos_off).to(dev), "pv": torch.from_numpy(csr.pos_var).to(dev),
+         "no": torch.from_numpy(csr.neg_off).to(dev), "nv": torch.from_numpy(csr.neg_var).to(dev)}
+    stream = torch.cuda.current_stream()
+
+    def step():
+        bm = gr.pack_bitmatrix(csr.m, d["po"], d["pv"], d["no"], d["nv"], device=dev, check=False)
+        return bm, gr.mhs_greedy_matrix(bm)
+
+    for _ in range(max(1, min(a.warmup, 2))):
+        bm, r = step()
+        del bm
+    torch.cuda.synchronize()
+    prof = gr.profiler(1).start()
+    l0 = gr.launch_count()
+    total_ms = 0.0
+    with ClockSampler(local) as clk:
+        for _ in range(a.steps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            bm, r = step()
+            e1.record(stream)
+            e1.synchronize()
+            total_ms += e0.elapsed_time(e1)
+            ld = bm.ld
+            del bm
+    launches = gr.launch_count() - l0
+    kern = prof.stop()
+    pk = peaks()
+    ck = kern["count_kernel"]
+    bytes_per_launch = csr.m * ld * 8 + 3 * ld * 8  # R + U_in + U_out + R[v*] row (mark)
+    ach = bytes_per_launch / (ck["ms"] / ck["launches"] / 1e3) / 1e9
+    a_ = r.assign.cpu().numpy().view(np.uint64)
+    size = int(sum(bin(int(x)).count("1") for x in a_))
+    n = csr.n_pos
+    line = {
+        "metric": METRIC, "value": n * a.steps / (total_ms / 1e3), "unit": "clauses/s (greedy)",
+        "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": total_ms / a.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic", "config": {"workload": "C5: greedy mhs, m=4096, n=2^24 positive clauses (8 GiB bit matrix)",
+                                        "l2": "inputs (8 GiB) larger than L2"},
+        "greedy": {"picks": r.n_picks, "size": size, "status": int(r.status.item()), "planted": 256,
+                   "passes": ck["launches"] / a.steps},
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                     "frac": ach / pk["hbm_gbs"], "traffic": traffic_of("count_kernel"),
+                     "kernel": "count_kernel", "share_of_step": ck["ms"] / total_ms},
+        "clocks": clk.summary(),
+        "kernels": {k: {"launches": v["launches"], "ms_per_step": v["ms"] / a.steps} for k, v in kern.items()},
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- CPU oracle legs
+def oracle_sample(cfg, cb):
+    """Bounded sample of the workload for the CPU oracle (about 10-30 s)."""
+    if cfg == "c2":
+        idx = [b for b in range(cb.B) if cb.m[b] <= 26]
+        return cb.subset(idx), f"{len(idx)} of {cb.B} C2 instances (those with m <= 26), PMS+MHS+greedy"
+    if cfg == "c4":
+        idx = list(range(48))
+        return cb.subset(idx), f"first 48 of {cb.B} C4 instances, WPMS"
+    return cb, "whole workload"
+
+
+def run_oracle_once(cfg, sub):
+    import oracle
+
+    t0 = time.perf_counter()
+    p = oracle.batch("pms", sub)
+    cands = float(p.decided.astype(np.float64).sum())
+    if cfg != "c4":
+        h = oracle.batch("mhs", sub)
+        oracle.batch("greedy", sub)
+        cands += float(h.decided.astype(np.float64).sum())
+    return time.perf_counter() - t0, cands
+
+
+def cpu_baseline(cfg, cb):
+    import oracle
+
+    if cfg == "c3":
+        return {"value": None, "unit": "candidates/s", "cores": oracle.num_threads(), "kind": "oracle",
+                "sample": "not run: 4.1e12 candidates (~hours on the host); see DESIGN.md §7"}
+    sub, desc = oracle_sample(cfg, cb)
+    sec, cands, reps = 0.0, 0.0, 0
+    while sec < 10.0 and reps < 50:
+        dt, c = run_oracle_once(cfg, sub)
+        sec += dt
+        cands += c
+        reps += 1
+    return {"value": cands / sec, "unit": "candidates/s", "cores": oracle.num_threads(),
+            "kind": "oracle", "sample": f"{reps} pass(es) over {desc}", "seconds": sec}
 
 
 def run_reference(a, rank, world):
-    """The oracle (the CPU reference of this tier) on a bounded sample."""
+    """--impl reference: the CPU oracle (this tier's reference) on the host."""
     if rank != 0:
         return
     import oracle
-    from paper_2011_08373_b200 import synth
 
-    cb, desc = make_workload(a.config, 0)
-    idx = [b for b in range(cb.B) if cb.m[b] <= 24]
-    sub = cb.subset(idx)
-    ts, cands = [], 0
+    cfg = a.config if a.config in ("c1", "c2", "c4") else "c2"
+    cb, desc = make_workload(cfg, 0)
+    sub, sdesc = oracle_sample(cfg, cb)
+    ts, cands = [], 0.0
     for s in range(a.warmup + a.steps):
-        t0 = time.perf_counter()
-        p = oracle.batch("pms", sub)
-        h = oracle.batch("mhs", sub)
-        g = oracle.batch("greedy", sub)
-        dt = time.perf_counter() - t0
+        dt, c = run_oracle_once(cfg, sub)
         if s >= a.warmup:
             ts.append(dt)
-            cands = float(p.decided.astype(np.float64).sum() + h.decided.astype(np.float64).sum())
+            cands += c
     sec = float(np.sum(ts))
-    v = cands * a.steps / sec
+    v = cands / sec
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "candidates/s", "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * sec / a.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
         "data": "synthetic", "config": {"workload": desc},
         "cpu_baseline": {"value": v, "unit": "candidates/s", "cores": oracle.num_threads(),
-                         "kind": "oracle", "sample": f"{len(idx)} of {cb.B} instances (m <= 24)"},
+                         "kind": "oracle", "sample": sdesc},
         "e2e": {"value": v, "unit": "candidates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 

@@ -135,16 +135,19 @@ int gr_mhs_greedy(const gr_batch *in, gr_result *out, void *ws, size_t ws_bytes,
 
 /* ---- sharded exact solving (the multi-GPU driver owns the collective) ----
  * gr_solve_pms / gr_mhs_exact are exactly:
- *     gr_exact_prepare(in, which, ...);
- *     for (k = 1; ; k++) { gr_exact_level(in, k, 0, 1, ...);
- *                          gr_exact_finish(in, which, k, out, ..., &n); if (!n) break; }
+ *     gr_exact_prepare(in, which, out, ..., &n);
+ *     for (k = 1; n > 0; k++) { gr_exact_level(in, which, k, 0, 1, ...);
+ *                               gr_exact_finish(in, which, k, out, ..., &n); }
  * With G GPUs, rank r calls gr_exact_level(in, k, r, G, ...), then all-reduces
  * (MIN, int64) the B level keys at gr_exact_level_keys(ws) before
  * gr_exact_finish -- every rank then holds the same state.  Level k's colex
  * rank range is cut into fixed chunks; shard r enumerates chunks c with
  * c % G == r.  which: 0 = PMS/WPMS, 1 = MHS. */
+/* packs the batch, writes the results of trivially decided instances and
+ * plans level 1; *n_active (host, may be NULL; if given the call synchronises
+ * s) = instances that still search. */
 int gr_exact_prepare(const gr_batch *in, int which, gr_result *out, void *ws, size_t ws_bytes,
-                     gr_stream_t s);
+                     gr_stream_t s, int32_t *n_active);
 int gr_exact_level(const gr_batch *in, int which, int k, int shard, int nshard, void *ws,
                    size_t ws_bytes, gr_stream_t s);
 int64_t *gr_exact_level_keys(const gr_batch *in, int which, void *ws);
@@ -192,6 +195,24 @@ int gr_mhs_greedy_matrix(const gr_bitmatrix *in, uint64_t *assign, int32_t *stat
  * number of clauses c of this shard with U[c] = 1 and v in c. */
 int gr_greedy_count_shard(const gr_bitmatrix *shard, const uint64_t *d_U, uint32_t *d_counts,
                           gr_stream_t s);
+
+/* ---- launch accounting and profiling ------------------------------------
+ * Every kernel launch of the library is counted (gr_launch_count).  With
+ * gr_profile(1) each launch is bracketed by CUDA events recorded on the
+ * stream it is launched on; gr_profile(2) additionally runs the enumeration
+ * kernel's work-counting instantiation (slower; for the roofline numerator).
+ * gr_profile(mode) resets the statistics; gr_profile_read synchronises the
+ * recorded events and returns one entry per kernel name. */
+typedef struct {
+  char name[48];
+  int64_t launches;
+  double ms;          /* summed event-timed duration of the launches */
+  uint64_t work[4];   /* enum_kernel in mode 2: [0] clause tests, [1] candidate blocks
+                         (prefixes), [2] candidates decided, [3] tests on 64-bit lanes */
+} gr_kernel_stat;
+int gr_profile(int mode);
+int gr_profile_read(gr_kernel_stat *out, int max_stats);
+unsigned long long gr_launch_count(void);
 
 /* thread-local description of the last negative return */
 const char *gr_last_error(void);

@@ -12,5 +12,5 @@ from ._native import (  # noqa: F401
     GR_BADINPUT, GR_FLAG_EXHAUSTIVE, GR_SAT, GR_SAT_NEG_VIOLATED, GR_UNSAT, GR_UNSUPPORTED, MHS,
     PMS, GREEDY, DeviceBatch, DeviceBitMatrix, DeviceResult, ExactSession, GrError,
     bitmatrix_ld, greedy_count_shard, lib, mhs_exact, mhs_greedy, mhs_greedy_matrix,
-    pack_bitmatrix, solve_pms, version,
+    pack_bitmatrix, solve_pms, version, launch_count, profiler, Profiler,
 )

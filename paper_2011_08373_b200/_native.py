@@ -27,6 +27,7 @@ EXPORTED = [
     "gr_exact_level", "gr_exact_level_keys", "gr_exact_finish", "gr_bitmatrix_ld",
     "gr_pack_varmajor", "gr_pack_clausemajor", "gr_greedy_matrix_workspace_bytes",
     "gr_mhs_greedy_matrix", "gr_greedy_count_shard", "gr_last_error", "gr_version",
+    "gr_profile", "gr_profile_read", "gr_launch_count",
 ]
 
 
@@ -42,6 +43,11 @@ class GrBatch(C.Structure):
 class GrResult(C.Structure):
     _fields_ = [("assign", C.c_void_p), ("cost", C.c_void_p), ("status", C.c_void_p),
                 ("decided", C.c_void_p)]
+
+
+class GrKernelStat(C.Structure):
+    _fields_ = [("name", C.c_char * 48), ("launches", C.c_int64), ("ms", C.c_double),
+                ("work", C.c_uint64 * 4)]
 
 
 class GrBitmatrix(C.Structure):
@@ -66,7 +72,12 @@ def lib():
         for f in (L.gr_solve_pms, L.gr_mhs_exact, L.gr_mhs_greedy):
             f.argtypes = [vp, vp, vp, sz, vp]
             f.restype = C.c_int
-        L.gr_exact_prepare.argtypes = [vp, C.c_int, vp, vp, sz, vp]
+        L.gr_exact_prepare.argtypes = [vp, C.c_int, vp, vp, sz, vp, vp]
+        L.gr_profile.argtypes = [C.c_int]
+        L.gr_profile.restype = C.c_int
+        L.gr_profile_read.argtypes = [vp, C.c_int]
+        L.gr_profile_read.restype = C.c_int
+        L.gr_launch_count.restype = C.c_ulonglong
         L.gr_exact_level.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, sz, vp]
         L.gr_exact_level_keys.argtypes = [vp, C.c_int, vp]
         L.gr_exact_level_keys.restype = vp
@@ -256,10 +267,13 @@ class ExactSession:
         self.r = self.out.struct()
         self.stream = stream
 
-    def prepare(self):
+    def prepare(self) -> int:
+        """Pack + plan level 1; returns the number of instances still searching."""
+        n = C.c_int32(0)
         _check(self.L.gr_exact_prepare(C.byref(self.b), self.which, C.byref(self.r),
-                                       _ptr(self.ws), self.ws.numel(), _stream(self.stream)),
-               "gr_exact_prepare")
+                                       _ptr(self.ws), self.ws.numel(), _stream(self.stream),
+                                       C.byref(n)), "gr_exact_prepare")
+        return int(n.value)
 
     def level(self, k: int, shard: int = 0, nshard: int = 1):
         _check(self.L.gr_exact_level(C.byref(self.b), self.which, k, shard, nshard, _ptr(self.ws),
@@ -374,3 +388,40 @@ def greedy_count_shard(bm: DeviceBitMatrix, U, counts, stream=None):
 
 def version() -> str:
     return lib().gr_version().decode()
+
+
+# ---- launch accounting / profiling ---------------------------------------------
+def launch_count() -> int:
+    """Kernel launches made by libgrsolve since it was loaded."""
+    return int(lib().gr_launch_count())
+
+
+class Profiler:
+    """gr_profile(mode): 1 = CUDA-event duration of every launch (on its own
+    stream), 2 = also the enumeration kernel's work-counting instantiation."""
+
+    def __init__(self, mode: int = 1):
+        self.mode = mode
+
+    def start(self):
+        _check(lib().gr_profile(self.mode), "gr_profile")
+        return self
+
+    def read(self) -> dict:
+        arr = (GrKernelStat * 64)()
+        n = lib().gr_profile_read(C.cast(arr, C.c_void_p), 64)
+        out = {}
+        for i in range(n):
+            st = arr[i]
+            out[st.name.decode()] = {"launches": int(st.launches), "ms": float(st.ms),
+                                     "work": [int(x) for x in st.work]}
+        return out
+
+    def stop(self) -> dict:
+        r = self.read()
+        lib().gr_profile(0)
+        return r
+
+
+def profiler(mode: int = 1) -> Profiler:
+    return Profiler(mode)

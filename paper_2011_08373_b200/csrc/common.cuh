@@ -26,6 +26,24 @@ int gr_cuda_fail(cudaError_t e, const char *where);
     if (_e != cudaSuccess) return gr_cuda_fail(_e, name);          \
   } while (0)
 
+// ---- launch accounting / profiling (api.cu) --------------------------------
+// Every kernel launch of the library goes through GR_LAUNCH: it is counted
+// (gr_launch_count) and, when profiling is on (gr_profile), bracketed by CUDA
+// events recorded on the launch stream.
+int gr_prof_mode();
+void gr_prof_pre(const char *name, cudaStream_t s);
+void gr_prof_post(const char *name, cudaStream_t s);
+#define GR_LAUNCH(name, st, ...)                                   \
+  do {                                                             \
+    gr_prof_pre(name, st);                                         \
+    __VA_ARGS__;                                                   \
+    cudaError_t _e = cudaGetLastError();                           \
+    gr_prof_post(name, st);                                        \
+    if (_e != cudaSuccess) return gr_cuda_fail(_e, name);          \
+  } while (0)
+// work counters of the enumeration kernel's counting instantiation (exact.cu)
+void gr_exact_work_read(unsigned long long out[4], int reset);
+
 // ---- binomial table C(n, k), 0 <= n, k <= 64 (C(64,32) < 2^61) ------------
 struct BinomTable {
   u64 v[65][65];

@@ -354,9 +354,15 @@ __device__ __forceinline__ M next_prefix_first(M T) {
   return (M)((S << 1) | 1);
 }
 
-template <typename M>
+// Work counters of the counting instantiation (COUNT = true): clause tests,
+// candidate blocks (prefixes), candidates decided.
+struct Work {
+  u64 tests = 0, blocks = 0, cands = 0;
+};
+
+template <typename M, bool COUNT>
 __device__ __forceinline__ M narrow_by_clauses(M A, M T, const M *__restrict__ P, int np,
-                                               const M *__restrict__ N, int nn) {
+                                               const M *__restrict__ N, int nn, Work &wk) {
   int j = 0;
   for (; j + 4 <= np; j += 4) {
     const M p0 = P[j], p1 = P[j + 1], p2 = P[j + 2], p3 = P[j + 3];
@@ -364,15 +370,18 @@ __device__ __forceinline__ M narrow_by_clauses(M A, M T, const M *__restrict__ P
     if (!(T & p1)) A &= p1;
     if (!(T & p2)) A &= p2;
     if (!(T & p3)) A &= p3;
+    if (COUNT) wk.tests += 4;
     if (!A) return A;
   }
   for (; j < np; j++) {
     const M p = P[j];
     if (!(T & p)) A &= p;
+    if (COUNT) wk.tests += 1;
   }
   if (!A) return A;
   for (int q = 0; q < nn; q++) {
     const M R = N[q] & ~T;
+    if (COUNT) wk.tests += 1;
     if (!R) return 0;                 // N subset of T: every candidate has N all true
     if (!(R & (R - 1))) A &= ~R;      // N \ T = {c}: candidate a = c is excluded
   }
@@ -380,15 +389,17 @@ __device__ __forceinline__ M narrow_by_clauses(M A, M T, const M *__restrict__ P
 }
 
 // unit weights: first feasible rank in the sub-range (EXH: keep walking)
-template <typename M, bool EXH>
-__device__ i64 scan_unit(M x, u64 r, u64 cnt, int me, const M *P, int np, const M *N, int nn) {
+template <typename M, bool EXH, bool COUNT>
+__device__ i64 scan_unit(M x, u64 r, u64 cnt, int me, const M *P, int np, const M *N, int nn,
+                         Work &wk) {
   i64 best = GR_KEY_NONE;
   for (;;) {
     const M low = lowbit(x);
     const M T = x ^ low;
     int nb;
     M A = prefix_bits<M>(x, low, T, me, cnt, nb);
-    A = narrow_by_clauses<M>(A, T, P, np, N, nn);
+    if (COUNT) { wk.blocks++; wk.cands += (u64)nb; }
+    A = narrow_by_clauses<M, COUNT>(A, T, P, np, N, nn, wk);
     if (A) {
       const u64 rank = r + (u64)popc((M)(lowbit(A) - low));
       if (!EXH) return (i64)rank;
@@ -402,16 +413,17 @@ __device__ i64 scan_unit(M x, u64 r, u64 cnt, int me, const M *P, int np, const 
 }
 
 // weights: min key (W << rb | rank) over the sub-range
-template <typename M>
+template <typename M, bool COUNT>
 __device__ i64 scan_weighted(M x, u64 r, u64 cnt, int me, const M *P, int np, const M *N, int nn,
-                             const u32 *__restrict__ w, int rb) {
+                             const u32 *__restrict__ w, int rb, Work &wk) {
   i64 best = GR_KEY_NONE;
   for (;;) {
     const M low = lowbit(x);
     const M T = x ^ low;
     int nb;
     M A = prefix_bits<M>(x, low, T, me, cnt, nb);
-    A = narrow_by_clauses<M>(A, T, P, np, N, nn);
+    if (COUNT) { wk.blocks++; wk.cands += (u64)nb; }
+    A = narrow_by_clauses<M, COUNT>(A, T, P, np, N, nn, wk);
     if (A) {
       u64 WT = 0;
       for (M t = T; t; t &= t - 1) WT += w[ctz(t)];
@@ -444,15 +456,18 @@ struct EnumParams {
   int k, weighted, exhaustive, shard, nshard;
 };
 
-template <typename M>
+template <typename M, bool COUNT>
 __device__ i64 run_lane(const EnumParams &p, int b, u64 r_lo, u64 cnt, int me, int np, int nn,
-                        const M *P, const M *N, const u32 *w, int rb) {
+                        const M *P, const M *N, const u32 *w, int rb, Work &wk) {
   const M x = (M)unrank_colex(r_lo, p.k, me);
-  if (p.weighted) return scan_weighted<M>(x, r_lo, cnt, me, P, np, N, nn, w, rb);
-  if (p.exhaustive) return scan_unit<M, true>(x, r_lo, cnt, me, P, np, N, nn);
-  return scan_unit<M, false>(x, r_lo, cnt, me, P, np, N, nn);
+  if (p.weighted) return scan_weighted<M, COUNT>(x, r_lo, cnt, me, P, np, N, nn, w, rb, wk);
+  if (p.exhaustive) return scan_unit<M, true, COUNT>(x, r_lo, cnt, me, P, np, N, nn, wk);
+  return scan_unit<M, false, COUNT>(x, r_lo, cnt, me, P, np, N, nn, wk);
 }
 
+__device__ unsigned long long g_work[4];  // counting instantiation totals
+
+template <bool COUNT>
 __global__ void __launch_bounds__(NT) enum_kernel(EnumParams p) {
   extern __shared__ u64 cls[];  // staged clauses (u64 or u32 view)
   __shared__ u64 s_chunk;
@@ -513,15 +528,22 @@ __global__ void __launch_bounds__(NT) enum_kernel(EnumParams p) {
     const u64 r_lo = s_r0 + (u64)t * L;
     const u64 ck = s_ck;
     i64 key = GR_KEY_NONE;
+    Work wk;
     if (r_lo < ck) {
       const u64 cnt = (ck - r_lo) < L ? (ck - r_lo) : L;
       const int rb = p.ws.rb[b];
       if (narrow) {
         const u32 *c32 = (const u32 *)cls;
-        key = run_lane<u32>(p, b, r_lo, cnt, me, np, nn, c32, c32 + np, s_w, rb);
+        key = run_lane<u32, COUNT>(p, b, r_lo, cnt, me, np, nn, c32, c32 + np, s_w, rb, wk);
       } else {
-        key = run_lane<u64>(p, b, r_lo, cnt, me, np, nn, cls, cls + np, s_w, rb);
+        key = run_lane<u64, COUNT>(p, b, r_lo, cnt, me, np, nn, cls, cls + np, s_w, rb, wk);
       }
+    }
+    if (COUNT) {
+      atomicAdd(&g_work[0], (unsigned long long)wk.tests);
+      atomicAdd(&g_work[1], (unsigned long long)wk.blocks);
+      atomicAdd(&g_work[2], (unsigned long long)wk.cands);
+      if (!narrow) atomicAdd(&g_work[3], (unsigned long long)wk.tests);
     }
     key = warp_min(key);
     if ((t & 31) == 0) s_wmin[t >> 5] = key;
@@ -677,8 +699,9 @@ int enum_grid() {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   size_t smem = (size_t)MAXC * 8;
-  cudaFuncSetAttribute(enum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, enum_kernel, NT, smem);
+  cudaFuncSetAttribute(enum_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(enum_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, enum_kernel<false>, NT, smem);
   if (per < 1) per = 1;
   g_enum_grid = sms * per;
   return g_enum_grid;
@@ -698,8 +721,30 @@ u64 lane_cands() {
 
 extern "C" size_t gr_workspace_bytes_exact(const gr_batch *in) { return layout_of(in).total; }
 
+void gr_exact_work_read(unsigned long long out[4], int reset) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) { for (int i = 0; i < 4; i++) out[i] = 0; return; }
+  cudaDeviceSynchronize();
+  if (cudaMemcpyFromSymbol(out, g_work, sizeof(unsigned long long) * 4) != cudaSuccess)
+    for (int i = 0; i < 4; i++) out[i] = 0;
+  if (reset) {
+    unsigned long long z[4] = {0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_work, z, sizeof(z));
+  }
+}
+
+namespace {
+int *pinned_i32() {
+  static thread_local int *p = nullptr;
+  if (!p) {
+    if (cudaMallocHost((void **)&p, 64) != cudaSuccess) p = nullptr;
+  }
+  return p;
+}
+}  // namespace
+
 extern "C" int gr_exact_prepare(const gr_batch *in, int which, gr_result *out, void *ws,
-                                size_t ws_bytes, gr_stream_t s) {
+                                size_t ws_bytes, gr_stream_t s, int32_t *n_active) {
   int rc = validate_batch(in, which);
   if (rc) return rc;
   if (!out || !out->assign || !out->cost || !out->status) { gr_set_error("null result pointer"); return GR_EINVAL; }
@@ -717,11 +762,16 @@ extern "C" int gr_exact_prepare(const gr_batch *in, int which, gr_result *out, v
     cudaFuncSetAttribute(pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MAXC * 13 + 16);
     attr = true;
   }
-  pack_kernel<<<in->B, PT, smem, st>>>(in_of(in, which), out_of(out), w, which);
-  GR_CHECK_LAUNCH("pack_kernel");
-  finish_kernel<<<1, FT, 0, st>>>(in_of(in, which), out_of(out), w, which, 0,
-                                   (in->flags & GR_FLAG_EXHAUSTIVE) ? 1 : 0);
-  GR_CHECK_LAUNCH("finish_kernel(plan)");
+  GR_LAUNCH("pack_kernel", (cudaStream_t)s, pack_kernel<<<in->B, PT, smem, st>>>(in_of(in, which), out_of(out), w, which));
+  GR_LAUNCH("finish_kernel", (cudaStream_t)s, finish_kernel<<<1, FT, 0, st>>>(in_of(in, which), out_of(out), w, which, 0,
+                                   (in->flags & GR_FLAG_EXHAUSTIVE) ? 1 : 0));
+  if (n_active) {
+    int *h = pinned_i32();
+    if (!h) { gr_set_error("cudaMallocHost failed"); return GR_ECUDA; }
+    GR_CUDA(cudaMemcpyAsync(h, &w.ctrl->n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
+    GR_CUDA(cudaStreamSynchronize(st));
+    *n_active = *h;
+  }
   return GR_OK;
 }
 
@@ -745,8 +795,10 @@ extern "C" int gr_exact_level(const gr_batch *in, int which, int k, int shard, i
   p.nshard = nshard;
   int grid = enum_grid();
   GR_CUDA(cudaMemsetAsync(&w.ctrl->next_chunk, 0, sizeof(u64), (cudaStream_t)s));
-  enum_kernel<<<grid, NT, (size_t)MAXC * 8, (cudaStream_t)s>>>(p);
-  GR_CHECK_LAUNCH("enum_kernel");
+  if (gr_prof_mode() == 2)
+    GR_LAUNCH("enum_kernel", (cudaStream_t)s, enum_kernel<true><<<grid, NT, (size_t)MAXC * 8, (cudaStream_t)s>>>(p));
+  else
+    GR_LAUNCH("enum_kernel", (cudaStream_t)s, enum_kernel<false><<<grid, NT, (size_t)MAXC * 8, (cudaStream_t)s>>>(p));
   return GR_OK;
 }
 
@@ -755,16 +807,6 @@ extern "C" int64_t *gr_exact_level_keys(const gr_batch *in, int which, void *ws)
   if (!in || !ws) return nullptr;
   return (int64_t *)ws_of(in, ws).lvlkey;
 }
-
-namespace {
-int *pinned_i32() {
-  static thread_local int *p = nullptr;
-  if (!p) {
-    if (cudaMallocHost((void **)&p, 64) != cudaSuccess) p = nullptr;
-  }
-  return p;
-}
-}  // namespace
 
 extern "C" int gr_exact_finish(const gr_batch *in, int which, int k, gr_result *out, void *ws,
                                size_t ws_bytes, gr_stream_t s, int32_t *n_active) {
@@ -775,9 +817,8 @@ extern "C" int gr_exact_finish(const gr_batch *in, int which, int k, gr_result *
   if (k < 1 || k > 64) { gr_set_error("bad level"); return GR_EINVAL; }
   WS w = ws_of(in, ws);
   cudaStream_t st = (cudaStream_t)s;
-  finish_kernel<<<1, FT, 0, st>>>(in_of(in, which), out_of(out), w, which, k,
-                                   (in->flags & GR_FLAG_EXHAUSTIVE) ? 1 : 0);
-  GR_CHECK_LAUNCH("finish_kernel");
+  GR_LAUNCH("finish_kernel", (cudaStream_t)s, finish_kernel<<<1, FT, 0, st>>>(in_of(in, which), out_of(out), w, which, k,
+                                   (in->flags & GR_FLAG_EXHAUSTIVE) ? 1 : 0));
   int *h = pinned_i32();
   if (!h) { gr_set_error("cudaMallocHost failed"); return GR_ECUDA; }
   GR_CUDA(cudaMemcpyAsync(h, &w.ctrl->n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -788,18 +829,9 @@ extern "C" int gr_exact_finish(const gr_batch *in, int which, int k, gr_result *
 
 static int solve_exact(const gr_batch *in, gr_result *out, void *ws, size_t ws_bytes, gr_stream_t s,
                        int which) {
-  int rc = gr_exact_prepare(in, which, out, ws, ws_bytes, s);
+  int32_t n = 0;  // level 0 is handled by the pack; instances active for level 1
+  int rc = gr_exact_prepare(in, which, out, ws, ws_bytes, s, &n);
   if (rc) return rc;
-  int32_t n = 0;
-  // level 0 handled by the pack; is anything active for level 1?
-  {
-    WS w = ws_of(in, ws);
-    int *h = pinned_i32();
-    if (!h) { gr_set_error("cudaMallocHost failed"); return GR_ECUDA; }
-    GR_CUDA(cudaMemcpyAsync(h, &w.ctrl->n_active, sizeof(int), cudaMemcpyDeviceToHost, (cudaStream_t)s));
-    GR_CUDA(cudaStreamSynchronize((cudaStream_t)s));
-    n = *h;
-  }
   for (int k = 1; n > 0 && k <= 64; k++) {
     rc = gr_exact_level(in, which, k, 0, 1, ws, ws_bytes, s);
     if (rc) return rc;

@@ -443,10 +443,9 @@ extern "C" int gr_pack_varmajor(int32_t m, int64_t n, const int64_t *off, const 
   if (n == 0) return GR_OK;
   const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
   if (var_bytes == 2)
-    pack_vm_kernel<int16_t><<<grid, 256, 0, (cudaStream_t)s>>>(m, n, off, (const int16_t *)var, bits, ld, d_bad, 1);
+    GR_LAUNCH("pack_vm_kernel", (cudaStream_t)s, pack_vm_kernel<int16_t><<<grid, 256, 0, (cudaStream_t)s>>>(m, n, off, (const int16_t *)var, bits, ld, d_bad, 1));
   else
-    pack_vm_kernel<int32_t><<<grid, 256, 0, (cudaStream_t)s>>>(m, n, off, (const int32_t *)var, bits, ld, d_bad, 1);
-  GR_CHECK_LAUNCH("pack_vm_kernel");
+    GR_LAUNCH("pack_vm_kernel", (cudaStream_t)s, pack_vm_kernel<int32_t><<<grid, 256, 0, (cudaStream_t)s>>>(m, n, off, (const int32_t *)var, bits, ld, d_bad, 1));
   return GR_OK;
 }
 
@@ -459,10 +458,9 @@ extern "C" int gr_pack_clausemajor(int32_t m, int64_t n, const int64_t *off, con
   if (n == 0) return GR_OK;
   const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
   if (var_bytes == 2)
-    pack_vm_kernel<int16_t><<<grid, 256, 0, (cudaStream_t)s>>>(m, n, off, (const int16_t *)var, masks, 0, d_bad, 0);
+    GR_LAUNCH("pack_cm_kernel", (cudaStream_t)s, pack_vm_kernel<int16_t><<<grid, 256, 0, (cudaStream_t)s>>>(m, n, off, (const int16_t *)var, masks, 0, d_bad, 0));
   else
-    pack_vm_kernel<int32_t><<<grid, 256, 0, (cudaStream_t)s>>>(m, n, off, (const int32_t *)var, masks, 0, d_bad, 0);
-  GR_CHECK_LAUNCH("pack_cm_kernel");
+    GR_LAUNCH("pack_cm_kernel", (cudaStream_t)s, pack_vm_kernel<int32_t><<<grid, 256, 0, (cudaStream_t)s>>>(m, n, off, (const int32_t *)var, masks, 0, d_bad, 0));
   return GR_OK;
 }
 
@@ -480,8 +478,7 @@ extern "C" int gr_greedy_count_shard(const gr_bitmatrix *shard, const uint64_t *
   GR_CUDA(cudaMemsetAsync(d_counts, 0, sizeof(u32) * shard->m, st));
   CountParams p{shard->bits, shard->ld, shard->m, (int)((shard->ld + TW - 1) / TW), d_U, nullptr,
                 d_counts, nullptr, 0};
-  count_kernel<<<count_grid(), CT, COUNT_SMEM, st>>>(p);
-  GR_CHECK_LAUNCH("count_kernel(shard)");
+  GR_LAUNCH("count_kernel", (cudaStream_t)s, count_kernel<<<count_grid(), CT, COUNT_SMEM, st>>>(p));
   return GR_OK;
 }
 
@@ -504,8 +501,7 @@ extern "C" int gr_mhs_greedy_matrix(const gr_bitmatrix *in, uint64_t *assign, in
   cudaStream_t st = (cudaStream_t)s;
   const int64_t ld = in->ld;
   const int ntiles = (int)((ld + TW - 1) / TW);
-  init_kernel<<<592, 256, 0, st>>>(U, ld, in->n_pos, ctrl, counts, in->m, wpicks);
-  GR_CHECK_LAUNCH("init_kernel");
+  GR_LAUNCH("init_kernel", (cudaStream_t)s, init_kernel<<<592, 256, 0, st>>>(U, ld, in->n_pos, ctrl, counts, in->m, wpicks));
   const int grid = count_grid();
   int *h = pinned_ctrl();
   if (!h) { gr_set_error("cudaMallocHost failed"); return GR_ECUDA; }
@@ -517,10 +513,8 @@ extern "C" int gr_mhs_greedy_matrix(const gr_bitmatrix *in, uint64_t *assign, in
     for (int j = 0; j < CHUNK; j++, t++) {
       CountParams p{in->bits, ld, in->m, ntiles, U + (size_t)(t & 1) * ld,
                     U + (size_t)((t & 1) ^ 1) * ld, counts, ctrl, 1};
-      count_kernel<<<grid, CT, COUNT_SMEM, st>>>(p);
-      GR_CHECK_LAUNCH("count_kernel");
-      argmax_kernel<<<1, AT, 0, st>>>(counts, in->m, ctrl, wpicks);
-      GR_CHECK_LAUNCH("argmax_kernel");
+      GR_LAUNCH("count_kernel", (cudaStream_t)s, count_kernel<<<grid, CT, COUNT_SMEM, st>>>(p));
+      GR_LAUNCH("argmax_kernel", (cudaStream_t)s, argmax_kernel<<<1, AT, 0, st>>>(counts, in->m, ctrl, wpicks));
     }
     GR_CUDA(cudaMemcpyAsync(h, ctrl, sizeof(GCtrl), cudaMemcpyDeviceToHost, st));
     GR_CUDA(cudaStreamSynchronize(st));
@@ -531,15 +525,12 @@ extern "C" int gr_mhs_greedy_matrix(const gr_bitmatrix *in, uint64_t *assign, in
   if (n_picks) *n_picks = np;
   // prune (reverse-delete, R12)
   GR_CUDA(cudaMemsetAsync(flags, 0, sizeof(int) * (in->m + 1), st));
-  planes_build_kernel<<<(int)std::min<int64_t>((ld + 255) / 256, 148 * 8), 256, 0, st>>>(
-      in->bits, ld, wpicks, ctrl, planes, L.nplanes);
-  GR_CHECK_LAUNCH("planes_build_kernel");
+  GR_LAUNCH("planes_build_kernel", (cudaStream_t)s, planes_build_kernel<<<(int)std::min<int64_t>((ld + 255) / 256, 148 * 8), 256, 0, st>>>(
+      in->bits, ld, wpicks, ctrl, planes, L.nplanes));
   u64 *one = U;  // the U buffers are free once the greedy loop is done
   const int egrid = (int)std::min<int64_t>((ld + 255) / 256, 148 * 8);
-  one_kernel<<<egrid, 256, 0, st>>>(planes, L.nplanes, ld, one);
-  GR_CHECK_LAUNCH("one_kernel");
-  private_kernel<<<148 * 4, 256, 0, st>>>(in->bits, ld, wpicks, ctrl, one, flags, -1);
-  GR_CHECK_LAUNCH("private_kernel");
+  GR_LAUNCH("one_kernel", (cudaStream_t)s, one_kernel<<<egrid, 256, 0, st>>>(planes, L.nplanes, ld, one));
+  GR_LAUNCH("private_kernel", (cudaStream_t)s, private_kernel<<<148 * 4, 256, 0, st>>>(in->bits, ld, wpicks, ctrl, one, flags, -1));
   std::vector<int> hflags(np + 1), hpicks(np + 1);
   if (np > 0) {
     GR_CUDA(cudaMemcpyAsync(hflags.data(), flags, sizeof(int) * np, cudaMemcpyDeviceToHost, st));
@@ -553,14 +544,12 @@ extern "C" int gr_mhs_greedy_matrix(const gr_bitmatrix *in, uint64_t *assign, in
   for (int j = np - 1; j >= 0; j--) {
     if (hflags[j]) continue;
     GR_CUDA(cudaMemsetAsync(flags + j, 0, sizeof(int), st));
-    private_kernel<<<148 * 4, 256, 0, st>>>(in->bits, ld, wpicks, ctrl, one, flags, j);
-    GR_CHECK_LAUNCH("private_kernel(one)");
+    GR_LAUNCH("private_kernel", (cudaStream_t)s, private_kernel<<<148 * 4, 256, 0, st>>>(in->bits, ld, wpicks, ctrl, one, flags, j));
     GR_CUDA(cudaMemcpyAsync(hf, flags + j, sizeof(int), cudaMemcpyDeviceToHost, st));
     GR_CUDA(cudaStreamSynchronize(st));
     if (!*hf) {
       removed[j] = 1;
-      remove_kernel<<<egrid, 256, 0, st>>>(in->bits, ld, hpicks[j], planes, L.nplanes, one);
-      GR_CHECK_LAUNCH("remove_kernel");
+      GR_LAUNCH("remove_kernel", (cudaStream_t)s, remove_kernel<<<egrid, 256, 0, st>>>(in->bits, ld, hpicks[j], planes, L.nplanes, one));
     }
   }
   // removed flags -> device (reuse `flags`)
@@ -568,9 +557,8 @@ extern "C" int gr_mhs_greedy_matrix(const gr_bitmatrix *in, uint64_t *assign, in
     GR_CUDA(cudaMemcpyAsync(flags, removed.data(), sizeof(int) * np, cudaMemcpyHostToDevice, st));
     GR_CUDA(cudaStreamSynchronize(st));
   }
-  finalize_kernel<<<1, 256, 0, st>>>(wpicks, ctrl, flags, in->m, in->neg, in->n_neg, assign,
-                                     status, smask);
-  GR_CHECK_LAUNCH("finalize_kernel");
+  GR_LAUNCH("finalize_kernel", (cudaStream_t)s, finalize_kernel<<<1, 256, 0, st>>>(wpicks, ctrl, flags, in->m, in->neg, in->n_neg, assign,
+                                     status, smask));
   if (picks) GR_CUDA(cudaMemcpyAsync(picks, wpicks, sizeof(int) * in->m, cudaMemcpyDeviceToDevice, st));
   GR_CUDA(cudaStreamSynchronize(st));
   return GR_OK;

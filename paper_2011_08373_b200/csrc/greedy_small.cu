@@ -139,7 +139,6 @@ extern "C" int gr_mhs_greedy(const gr_batch *in, gr_result *out, void *ws, size_
                          MAXC * 16 + MAXC / 32 * 4 + 16);
     attr = true;
   }
-  greedy_small_kernel<<<in->B, 32, smem, (cudaStream_t)s>>>(*in, *out);
-  GR_CHECK_LAUNCH("greedy_small_kernel");
+  GR_LAUNCH("greedy_small_kernel", (cudaStream_t)s, greedy_small_kernel<<<in->B, 32, smem, (cudaStream_t)s>>>(*in, *out));
   return GR_OK;
 }
