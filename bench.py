@@ -380,7 +380,7 @@ def run_c5(a, rank, world, local, dev):
                    "passes": ck["launches"] / a.steps},
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                     "frac": ach / pk["hbm_gbs"], "traffic": traffic_of("count_kernel"),
+                     "frac": ach / pk["hbm_gbs"], "traffic": traffic_of("count_kernel_c5"),
                      "kernel": "count_kernel", "share_of_step": ck["ms"] / total_ms},
         "clocks": clk.summary(),
         "kernels": {k: {"launches": v["launches"], "ms_per_step": v["ms"] / a.steps} for k, v in kern.items()},
