@@ -51,7 +51,7 @@ struct Ctrl {
 
 struct Layout {
   size_t ctrl, meff, npr, nnr, kmax, done, rb, sup, decided, bestx, bestw, wtot, lvlkey, sk, wr,
-      active, chunk_base, pk, total;
+      active, chunk_base, pk, h2, h3, total;
 };
 
 Layout layout_of(const gr_batch *in) {
@@ -76,6 +76,8 @@ Layout layout_of(const gr_batch *in) {
   L.active = take(4 * 2 * B);
   L.chunk_base = take(8 * (B + 1));
   L.pk = take(8 * (size_t)std::max<int64_t>(in->total_clauses, 1));
+  L.h2 = take(8 * (size_t)std::max<int64_t>(in->total_clauses, 1));
+  L.h3 = take(8 * (size_t)std::max<int64_t>(in->total_clauses, 1));
   L.total = o;
   return L;
 }
@@ -89,7 +91,7 @@ struct WS {
   u32 *wr;
   int *active;
   u64 *chunk_base;
-  u64 *pk;
+  u64 *pk, *h2, *h3;  // packed clause masks; pairs / triples meeting each positive clause
 };
 
 WS ws_of(const gr_batch *in, void *base) {
@@ -114,6 +116,8 @@ WS ws_of(const gr_batch *in, void *base) {
   w.active = (int *)(p + L.active);
   w.chunk_base = (u64 *)(p + L.chunk_base);
   w.pk = (u64 *)(p + L.pk);
+  w.h2 = (u64 *)(p + L.h2);
+  w.h3 = (u64 *)(p + L.h3);
   return w;
 }
 
@@ -161,6 +165,9 @@ __device__ void write_result(const In &in, const Out &out, int b, int status, u6
   out.status[b] = status;
   if (out.decided) out.decided[b] = decided;
 }
+
+__device__ u64 pairs_hitting(u32 p);
+__device__ u64 triples_hitting(u32 p);
 
 // ---------------------------------------------------------------------------
 // pack: one CTA per instance
@@ -267,7 +274,12 @@ __global__ void __launch_bounds__(PT) pack_kernel(In in, Out out, WS ws, int whi
       const int pi = ii >> 8;
       d += (pi < pj || (pi == pj && i < j));
     }
-    ws.pk[lo + (j < np ? 0 : npr) + d] = R[j];
+    const int64_t dst = lo + (j < np ? 0 : npr) + d;
+    ws.pk[dst] = R[j];
+    if (j < np) {
+      ws.h2[dst] = pairs_hitting((u32)(R[j] & 0x7ffu));
+      ws.h3[dst] = triples_hitting((u32)(R[j] & 0xffu));
+    }
   }
   // weights of the support variables (relabelled order) and S_k
   if (t < 64) {
@@ -325,119 +337,235 @@ __global__ void __launch_bounds__(PT) pack_kernel(In in, Out out, WS ws, int whi
 }
 
 // ---------------------------------------------------------------------------
-// the level walk of one lane
+// the level walk of one lane: bit-parallel decision of the j lowest elements
 // ---------------------------------------------------------------------------
-// Candidates at level k in colex order are grouped by their k-1 upper
-// elements T (the prefix); the candidates of one prefix are T | {a} for
-// a < min(T), consecutive in rank.  x = first candidate, r its rank, cnt the
-// number of candidates left in this lane's sub-range.
-template <typename M>
-__device__ __forceinline__ M prefix_bits(M x, M low, M T, int me, u64 cnt, int &nb) {
-  const M full = (me >= (int)(8 * sizeof(M))) ? ~M(0) : (M)((M(1) << me) - 1);
-  const M lim = T ? lowbit(T) : (M)(full + 1);  // wraps to 0 when me == width
-  M A = (M)(lim - low);                          // bits [a, min(T)) (or [a, me))
-  nb = popc(A);
-  if (cnt < (u64)nb) {
-    A &= (M)((low << cnt) - 1);
-    nb = (int)cnt;
-  }
-  return A;
-}
+// Candidates at level k are k-subsets x of [0, m_eff) in colex order (rank =
+// sum_i C(c_i, i)).  Split x = U | S where S holds the j = min(3, k) lowest
+// elements: all candidates sharing U form one contiguous rank block (U in
+// colex order, then S in colex order), S ranging over the j-subsets of
+// [0, min U).  The block is decided as a few *sub-blocks* whose candidates
+// are one bit each of a 64-bit mask F, the bit index being the colex offset
+// idx_j(S) = sum_i C(s_i, i):
+//   j = 3: triples inside [0, 8)   (C(8,3) = 56 bits), then for t >= 8 the
+//          pairs block of U | {t};
+//   j = 2: pairs inside [0, 11)    (C(11,2) = 55 bits), then for t >= 11 the
+//          singles block of U | {t};
+//   j = 1: singles a < e           (<= 64 bits).
+// A positive clause P missed by U leaves the candidates that hit P:
+// F &= H_j(P) with H_1(P) = P, H_2(P) = {pairs meeting P & 0x7ff},
+// H_3(P) = {triples meeting P & 0xff} (precomputed per clause by the pack).
+// A negative clause N with N \ U inside the region kills the S with
+// S superset of N & region.
+constexpr int R2 = 11, R3 = 8;
 
-template <typename M>
-__device__ __forceinline__ M next_prefix_first(M T) {
-  // Gosper's hack on S = T >> 1 (the (k-1)-subsets of [1, me) shifted down)
-  M S = T >> 1;
-  M c = lowbit(S);
-  M r = S + c;
-  S = r | (((r ^ S) >> 2) >> ctz(S));
-  return (M)((S << 1) | 1);
+__device__ __forceinline__ int c2i(int b) { return b * (b - 1) / 2; }
+__device__ __forceinline__ int c3i(int c) { return c * (c - 1) * (c - 2) / 6; }
+
+// {pairs a < b < 11 meeting p}, bit a + C(b,2)
+__device__ u64 pairs_hitting(u32 p) {
+  u64 r = 0;
+  for (int b = 1; b < R2; b++)
+    for (int a = 0; a < b; a++)
+      if (((p >> a) | (p >> b)) & 1u) r |= 1ull << (a + c2i(b));
+  return r;
+}
+// {triples a < b < c < 8 meeting p}, bit a + C(b,2) + C(c,3)
+__device__ u64 triples_hitting(u32 p) {
+  u64 r = 0;
+  for (int c = 2; c < R3; c++)
+    for (int b = 1; b < c; b++)
+      for (int a = 0; a < b; a++)
+        if (((p >> a) | (p >> b) | (p >> c)) & 1u) r |= 1ull << (a + c2i(b) + c3i(c));
+  return r;
+}
+__device__ __forceinline__ u64 nbits(u64 n) { return n >= 64 ? ~0ull : ((1ull << n) - 1ull); }
+__device__ __forceinline__ u64 small_binom(int e, int j) {
+  return j == 1 ? (u64)e : (j == 2 ? (u64)c2i(e) : (u64)c3i(e));
+}
+// the j-subsets of [0, e) that contain every element of q (a subset of [0, e))
+__device__ u64 supersets(int j, u64 q, int e) {
+  const int c = __popcll(q);
+  if (c > j) return 0;
+  u64 r = nbits(small_binom(e, j));
+  while (q) {
+    const int x = __ffsll((long long)q) - 1;
+    q &= q - 1;
+    r &= j == 1 ? (1ull << x) : (j == 2 ? pairs_hitting(1u << x) : triples_hitting(1u << x));
+  }
+  return r;
 }
 
 // Work counters of the counting instantiation (COUNT = true): clause tests,
-// candidate blocks (prefixes), candidates decided.
+// sub-blocks tested, candidates in the tested sub-blocks.
 struct Work {
   u64 tests = 0, blocks = 0, cands = 0;
 };
 
+template <typename M>
+struct Clauses {
+  const M *P;      // [np + nn] positives then negatives
+  const u64 *H2;   // [np] pairs meeting P
+  const u64 *H3;   // [np] triples meeting P
+  int np, nn;
+};
+
 template <typename M, bool COUNT>
-__device__ __forceinline__ M narrow_by_clauses(M A, M T, const M *__restrict__ P, int np,
-                                               const M *__restrict__ N, int nn, Work &wk) {
-  int j = 0;
-  for (; j + 4 <= np; j += 4) {
-    const M p0 = P[j], p1 = P[j + 1], p2 = P[j + 2], p3 = P[j + 3];
-    if (!(T & p0)) A &= p0;
-    if (!(T & p1)) A &= p1;
-    if (!(T & p2)) A &= p2;
-    if (!(T & p3)) A &= p3;
-    if (COUNT) wk.tests += 4;
-    if (!A) return A;
+__device__ __forceinline__ u64 test_sub(int j, M U, int e, u64 F, const Clauses<M> &c, Work &wk) {
+  const int np = c.np;
+  int q = 0;
+  if (j == 1) {
+    for (; q + 4 <= np; q += 4) {
+      const M p0 = c.P[q], p1 = c.P[q + 1], p2 = c.P[q + 2], p3 = c.P[q + 3];
+      if (!(U & p0)) F &= (u64)p0;
+      if (!(U & p1)) F &= (u64)p1;
+      if (!(U & p2)) F &= (u64)p2;
+      if (!(U & p3)) F &= (u64)p3;
+      if (COUNT) wk.tests += 4;
+      if (!F) return 0;
+    }
+    for (; q < np; q++) {
+      const M p0 = c.P[q];
+      if (!(U & p0)) F &= (u64)p0;
+      if (COUNT) wk.tests += 1;
+    }
+  } else {
+    const u64 *H = j == 2 ? c.H2 : c.H3;
+    for (; q + 4 <= np; q += 4) {
+      const M p0 = c.P[q], p1 = c.P[q + 1], p2 = c.P[q + 2], p3 = c.P[q + 3];
+      const u64 h0 = H[q], h1 = H[q + 1], h2 = H[q + 2], h3 = H[q + 3];
+      if (!(U & p0)) F &= h0;
+      if (!(U & p1)) F &= h1;
+      if (!(U & p2)) F &= h2;
+      if (!(U & p3)) F &= h3;
+      if (COUNT) wk.tests += 4;
+      if (!F) return 0;
+    }
+    for (; q < np; q++) {
+      const M p0 = c.P[q];
+      if (!(U & p0)) F &= H[q];
+      if (COUNT) wk.tests += 1;
+    }
   }
-  for (; j < np; j++) {
-    const M p = P[j];
-    if (!(T & p)) A &= p;
+  if (!F) return 0;
+  const M lowm = (M)nbits((u64)e);
+  for (int t = 0; t < c.nn; t++) {
+    const M N = c.P[np + t];
     if (COUNT) wk.tests += 1;
+    if (N & ~U & ~lowm) continue;  // a variable of N outside U | region is false
+    F &= ~supersets(j, (u64)(N & lowm), e);
+    if (!F) return 0;
   }
-  if (!A) return A;
-  for (int q = 0; q < nn; q++) {
-    const M R = N[q] & ~T;
-    if (COUNT) wk.tests += 1;
-    if (!R) return 0;                 // N subset of T: every candidate has N all true
-    if (!(R & (R - 1))) A &= ~R;      // N \ T = {c}: candidate a = c is excluded
-  }
-  return A;
+  return F;
 }
 
-// unit weights: first feasible rank in the sub-range (EXH: keep walking)
-template <typename M, bool EXH, bool COUNT>
-__device__ i64 scan_unit(M x, u64 r, u64 cnt, int me, const M *P, int np, const M *N, int nn,
-                         Work &wk) {
-  i64 best = GR_KEY_NONE;
-  for (;;) {
-    const M low = lowbit(x);
-    const M T = x ^ low;
-    int nb;
-    M A = prefix_bits<M>(x, low, T, me, cnt, nb);
-    if (COUNT) { wk.blocks++; wk.cands += (u64)nb; }
-    A = narrow_by_clauses<M, COUNT>(A, T, P, np, N, nn, wk);
-    if (A) {
-      const u64 rank = r + (u64)popc((M)(lowbit(A) - low));
-      if (!EXH) return (i64)rank;
-      if (best == GR_KEY_NONE) best = (i64)rank;
-    }
-    cnt -= (u64)nb;
-    if (!cnt) return best;
-    r += (u64)nb;
-    x = next_prefix_first<M>(T);
+struct LaneCtx {
+  u64 r_lo, r_hi;  // this lane's rank window
+  int rb;          // weighted key shift
+  i64 best;
+};
+
+// weighted: W(U) + weights of the j low elements encoded by bit idx
+template <typename M>
+__device__ __forceinline__ u64 weight_of(int j, int idx, M U, const u32 *w) {
+  u64 W = 0;
+  for (M t = U; t; t &= t - 1) W += w[ctz(t)];
+  if (j == 1) return W + w[idx];
+  int c = -1;
+  if (j == 3) {
+    c = 2;
+    while (c + 1 < R3 && c3i(c + 1) <= idx) c++;
+    idx -= c3i(c);
   }
+  int b = 1;
+  while (b + 1 < R2 && c2i(b + 1) <= idx) b++;
+  const int a = idx - c2i(b);
+  W += w[a] + w[b];
+  if (c >= 0) W += w[c];
+  return W;
 }
 
-// weights: min key (W << rb | rank) over the sub-range
-template <typename M, bool COUNT>
-__device__ i64 scan_weighted(M x, u64 r, u64 cnt, int me, const M *P, int np, const M *N, int nn,
-                             const u32 *__restrict__ w, int rb, Work &wk) {
-  i64 best = GR_KEY_NONE;
-  for (;;) {
-    const M low = lowbit(x);
-    const M T = x ^ low;
-    int nb;
-    M A = prefix_bits<M>(x, low, T, me, cnt, nb);
-    if (COUNT) { wk.blocks++; wk.cands += (u64)nb; }
-    A = narrow_by_clauses<M, COUNT>(A, T, P, np, N, nn, wk);
-    if (A) {
-      u64 WT = 0;
-      for (M t = T; t; t &= t - 1) WT += w[ctz(t)];
-      for (M a = A; a; a &= a - 1) {
-        const int bi = ctz(a);
-        const u64 rank = r + (u64)popc((M)(lowbit(a) - low));
-        const i64 key = (i64)(((WT + w[bi]) << rb) | rank);
-        best = key < best ? key : best;
-      }
+// one sub-block: U | S, S a j-subset of [0, e), ranks base + idx_j(S).
+// MODE 0: unit first witness (returns true when found), 1: unit exhaustive,
+// 2: weighted (min key).
+template <typename M, int MODE, bool COUNT>
+__device__ __forceinline__ bool do_sub(int j, M U, int e, u64 base, LaneCtx &L,
+                                       const Clauses<M> &c, const u32 *w, Work &wk) {
+  const u64 n = small_binom(e, j);
+  if (base >= L.r_hi || base + n <= L.r_lo || n == 0) return false;
+  u64 F = nbits(n);
+  if (L.r_lo > base) F &= ~nbits(L.r_lo - base);
+  if (L.r_hi < base + n) F &= nbits(L.r_hi - base);
+  if (COUNT) { wk.blocks++; wk.cands += (u64)__popcll(F); }
+  F = test_sub<M, COUNT>(j, U, e, F, c, wk);
+  if (!F) return false;
+  if (MODE == 2) {
+    for (u64 f = F; f; f &= f - 1) {
+      const int idx = __ffsll((long long)f) - 1;
+      const i64 key = (i64)((weight_of<M>(j, idx, U, w) << L.rb) | (base + (u64)idx));
+      L.best = key < L.best ? key : L.best;
     }
-    cnt -= (u64)nb;
-    if (!cnt) return best;
-    r += (u64)nb;
-    x = next_prefix_first<M>(T);
+    return false;
+  }
+  if (L.best == GR_KEY_NONE) L.best = (i64)(base + (u64)(__ffsll((long long)F) - 1));
+  return MODE == 0;
+}
+
+template <typename M, int MODE, bool COUNT>
+__device__ __forceinline__ bool do_block2(M U, int e, u64 base, LaneCtx &L, const Clauses<M> &c,
+                                          const u32 *w, Work &wk) {
+  if (do_sub<M, MODE, COUNT>(2, U, e < R2 ? e : R2, base, L, c, w, wk)) return true;
+  for (int t = R2; t < e; t++) {
+    const u64 bt = base + (u64)c2i(t);
+    if (bt >= L.r_hi) break;
+    if (do_sub<M, MODE, COUNT>(1, (M)(U | ((M)1 << t)), t, bt, L, c, w, wk)) return true;
+  }
+  return false;
+}
+
+template <typename M, int MODE, bool COUNT>
+__device__ __forceinline__ bool do_block3(M U, int e, u64 base, LaneCtx &L, const Clauses<M> &c,
+                                          const u32 *w, Work &wk) {
+  if (do_sub<M, MODE, COUNT>(3, U, e < R3 ? e : R3, base, L, c, w, wk)) return true;
+  for (int t = R3; t < e; t++) {
+    const u64 bt = base + (u64)c3i(t);
+    if (bt >= L.r_hi) break;
+    if (bt + (u64)c2i(t) <= L.r_lo) continue;
+    if (do_block2<M, MODE, COUNT>((M)(U | ((M)1 << t)), t, bt, L, c, w, wk)) return true;
+  }
+  return false;
+}
+
+// walk ranks [r_lo, r_lo + cnt) of level k
+template <typename M, int MODE, bool COUNT>
+__device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const u32 *w, int rb,
+                    Work &wk) {
+  const int j = k < 3 ? k : 3;
+  LaneCtx L{r_lo, r_lo + cnt, rb, GR_KEY_NONE};
+  const u64 x = unrank_colex(r_lo, k, me);
+  u64 Ux = x;
+  u64 off = 0;
+  for (int i = 1; i <= j; i++) {  // strip the j lowest elements, their colex offset
+    const int s = __ffsll((long long)Ux) - 1;
+    Ux &= Ux - 1;
+    off += binom(s, i);
+  }
+  M U = (M)Ux;
+  u64 base = r_lo - off;
+  for (;;) {
+    const int e = U ? ctz(U) : me;
+    bool done;
+    if (j == 3) done = do_block3<M, MODE, COUNT>(U, e, base, L, c, w, wk);
+    else if (j == 2) done = do_block2<M, MODE, COUNT>(U, e, base, L, c, w, wk);
+    else done = do_sub<M, MODE, COUNT>(1, U, e, base, L, c, w, wk);
+    if (done) return L.best;
+    base += binom(e, j);
+    if (base >= L.r_hi || !U) return L.best;
+    // next U: Gosper's hack on the (k-j)-subsets of [j, me) (shifted down by j)
+    M S = U >> j;
+    const M lb = lowbit(S);
+    const M r = S + lb;
+    S = r | (((r ^ S) >> 2) >> ctz(S));
+    U = (M)(S << j);
   }
 }
 
@@ -457,19 +585,21 @@ struct EnumParams {
 };
 
 template <typename M, bool COUNT>
-__device__ i64 run_lane(const EnumParams &p, int b, u64 r_lo, u64 cnt, int me, int np, int nn,
-                        const M *P, const M *N, const u32 *w, int rb, Work &wk) {
-  const M x = (M)unrank_colex(r_lo, p.k, me);
-  if (p.weighted) return scan_weighted<M, COUNT>(x, r_lo, cnt, me, P, np, N, nn, w, rb, wk);
-  if (p.exhaustive) return scan_unit<M, true, COUNT>(x, r_lo, cnt, me, P, np, N, nn, wk);
-  return scan_unit<M, false, COUNT>(x, r_lo, cnt, me, P, np, N, nn, wk);
+__device__ i64 run_lane(const EnumParams &p, u64 r_lo, u64 cnt, int me, const Clauses<M> &c,
+                        const u32 *w, int rb, Work &wk) {
+  if (p.weighted) return walk<M, 2, COUNT>(p.k, me, r_lo, cnt, c, w, rb, wk);
+  if (p.exhaustive) return walk<M, 1, COUNT>(p.k, me, r_lo, cnt, c, w, rb, wk);
+  return walk<M, 0, COUNT>(p.k, me, r_lo, cnt, c, w, rb, wk);
 }
 
 __device__ unsigned long long g_work[4];  // counting instantiation totals
 
+constexpr int SMC = 1024;  // clauses staged in shared memory (larger instances read L1/L2)
+constexpr size_t ENUM_SMEM = (size_t)SMC * 24;
+
 template <bool COUNT>
 __global__ void __launch_bounds__(NT) enum_kernel(EnumParams p) {
-  extern __shared__ u64 cls[];  // staged clauses (u64 or u32 view)
+  extern __shared__ u64 cls[];  // [np] H2, [np] H3, [np + nn] P (u32 or u64)
   __shared__ u64 s_chunk;
   __shared__ int s_b, s_cur, s_skip;
   __shared__ u64 s_r0, s_ck;
@@ -477,28 +607,28 @@ __global__ void __launch_bounds__(NT) enum_kernel(EnumParams p) {
   __shared__ i64 s_wmin[NT / 32];
   const int t = threadIdx.x;
   if (t == 0) s_cur = -1;
-  const u64 L = p.ws.ctrl->lane_cands;
-  const u64 CH = L * NT;
+  const u64 Lc = p.ws.ctrl->lane_cands;
+  const u64 CH = Lc * NT;
   const u64 total = p.ws.ctrl->total_chunks;
   const int nact = p.ws.ctrl->n_active;
   const int *active = p.ws.active;  // list of this level (offset by the host)
   for (;;) {
     __syncthreads();
     if (t == 0) {
-      u64 j = atomicAdd((unsigned long long *)&p.ws.ctrl->next_chunk, 1ull);
-      u64 c = j * (u64)p.nshard + (u64)p.shard;
-      s_chunk = c;
+      u64 jn = atomicAdd((unsigned long long *)&p.ws.ctrl->next_chunk, 1ull);
+      u64 ch = jn * (u64)p.nshard + (u64)p.shard;
+      s_chunk = ch;
       s_skip = 0;
-      if (c < total) {
-        // active index i: chunk_base[i] <= c < chunk_base[i+1]
+      if (ch < total) {
+        // active index i: chunk_base[i] <= ch < chunk_base[i+1]
         int lo = 0, hi = nact - 1;
         while (lo < hi) {
           int mid = (lo + hi + 1) >> 1;
-          if (p.ws.chunk_base[mid] <= c) lo = mid; else hi = mid - 1;
+          if (p.ws.chunk_base[mid] <= ch) lo = mid; else hi = mid - 1;
         }
         const int b = active[lo];
         s_b = b;
-        const u64 r0 = (c - p.ws.chunk_base[lo]) * CH;
+        const u64 r0 = (ch - p.ws.chunk_base[lo]) * CH;
         s_r0 = r0;
         s_ck = binom(p.ws.meff[b], p.k);
         if (!p.weighted && !p.exhaustive) {
@@ -513,30 +643,42 @@ __global__ void __launch_bounds__(NT) enum_kernel(EnumParams p) {
     const int b = s_b;
     const int me = p.ws.meff[b], np = p.ws.npr[b], nn = p.ws.nnr[b];
     const int64_t lo = p.off[b];
-    const bool narrow = me <= 32;
+    const bool staged = np + nn <= SMC;
+    const bool narrow = staged && me <= 32;
+    u64 *sH2 = cls, *sH3 = cls + np;
     if (b != s_cur) {
-      if (narrow) {
-        u32 *c32 = (u32 *)cls;
-        for (int j = t; j < np + nn; j += NT) c32[j] = (u32)p.ws.pk[lo + j];
-      } else {
-        for (int j = t; j < np + nn; j += NT) cls[j] = p.ws.pk[lo + j];
+      if (staged) {
+        for (int q = t; q < np; q += NT) {
+          sH2[q] = p.ws.h2[lo + q];
+          sH3[q] = p.ws.h3[lo + q];
+        }
+        if (narrow) {
+          u32 *c32 = (u32 *)(cls + 2 * np);
+          for (int q = t; q < np + nn; q += NT) c32[q] = (u32)p.ws.pk[lo + q];
+        } else {
+          for (int q = t; q < np + nn; q += NT) cls[2 * np + q] = p.ws.pk[lo + q];
+        }
       }
       if (t < 64) s_w[t] = p.ws.wr[(size_t)b * 64 + t];
       __syncthreads();
       if (t == 0) s_cur = b;
     }
-    const u64 r_lo = s_r0 + (u64)t * L;
+    const u64 r_lo = s_r0 + (u64)t * Lc;
     const u64 ck = s_ck;
     i64 key = GR_KEY_NONE;
     Work wk;
     if (r_lo < ck) {
-      const u64 cnt = (ck - r_lo) < L ? (ck - r_lo) : L;
+      const u64 cnt = (ck - r_lo) < Lc ? (ck - r_lo) : Lc;
       const int rb = p.ws.rb[b];
       if (narrow) {
-        const u32 *c32 = (const u32 *)cls;
-        key = run_lane<u32, COUNT>(p, b, r_lo, cnt, me, np, nn, c32, c32 + np, s_w, rb, wk);
+        Clauses<u32> c{(const u32 *)(cls + 2 * np), sH2, sH3, np, nn};
+        key = run_lane<u32, COUNT>(p, r_lo, cnt, me, c, s_w, rb, wk);
+      } else if (staged) {
+        Clauses<u64> c{cls + 2 * np, sH2, sH3, np, nn};
+        key = run_lane<u64, COUNT>(p, r_lo, cnt, me, c, s_w, rb, wk);
       } else {
-        key = run_lane<u64, COUNT>(p, b, r_lo, cnt, me, np, nn, cls, cls + np, s_w, rb, wk);
+        Clauses<u64> c{p.ws.pk + lo, p.ws.h2 + lo, p.ws.h3 + lo, np, nn};
+        key = run_lane<u64, COUNT>(p, r_lo, cnt, me, c, s_w, rb, wk);
       }
     }
     if (COUNT) {
@@ -698,7 +840,7 @@ int enum_grid() {
   int dev = 0, sms = 0, per = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  size_t smem = (size_t)MAXC * 8;
+  size_t smem = ENUM_SMEM;
   cudaFuncSetAttribute(enum_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(enum_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, enum_kernel<false>, NT, smem);
@@ -711,8 +853,8 @@ u64 lane_cands() {
   static u64 v = 0;
   if (!v) {
     const char *e = getenv("GR_LANE_CANDIDATES");
-    v = e ? strtoull(e, nullptr, 10) : 1024ull;
-    if (v < 1) v = 1024;
+    v = e ? strtoull(e, nullptr, 10) : 4096ull;
+    if (v < 1) v = 4096;
   }
   return v;
 }
@@ -796,9 +938,9 @@ extern "C" int gr_exact_level(const gr_batch *in, int which, int k, int shard, i
   int grid = enum_grid();
   GR_CUDA(cudaMemsetAsync(&w.ctrl->next_chunk, 0, sizeof(u64), (cudaStream_t)s));
   if (gr_prof_mode() == 2)
-    GR_LAUNCH("enum_kernel", (cudaStream_t)s, enum_kernel<true><<<grid, NT, (size_t)MAXC * 8, (cudaStream_t)s>>>(p));
+    GR_LAUNCH("enum_kernel", (cudaStream_t)s, enum_kernel<true><<<grid, NT, ENUM_SMEM, (cudaStream_t)s>>>(p));
   else
-    GR_LAUNCH("enum_kernel", (cudaStream_t)s, enum_kernel<false><<<grid, NT, (size_t)MAXC * 8, (cudaStream_t)s>>>(p));
+    GR_LAUNCH("enum_kernel", (cudaStream_t)s, enum_kernel<false><<<grid, NT, ENUM_SMEM, (cudaStream_t)s>>>(p));
   return GR_OK;
 }
 
