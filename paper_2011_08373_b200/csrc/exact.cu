@@ -51,7 +51,7 @@ struct Ctrl {
 
 struct Layout {
   size_t ctrl, meff, npr, nnr, kmax, done, rb, sup, decided, bestx, bestw, wtot, lvlkey, sk, wr,
-      active, chunk_base, pk, h2, h3, total;
+      active, chunk_base, pk, hrec, total;
 };
 
 Layout layout_of(const gr_batch *in) {
@@ -76,8 +76,7 @@ Layout layout_of(const gr_batch *in) {
   L.active = take(4 * 2 * B);
   L.chunk_base = take(8 * (B + 1));
   L.pk = take(8 * (size_t)std::max<int64_t>(in->total_clauses, 1));
-  L.h2 = take(8 * (size_t)std::max<int64_t>(in->total_clauses, 1));
-  L.h3 = take(8 * (size_t)std::max<int64_t>(in->total_clauses, 1));
+  L.hrec = take(8 * 5 * (size_t)std::max<int64_t>(in->total_clauses, 1));
   L.total = o;
   return L;
 }
@@ -91,7 +90,7 @@ struct WS {
   u32 *wr;
   int *active;
   u64 *chunk_base;
-  u64 *pk, *h2, *h3;  // packed clause masks; pairs / triples meeting each positive clause
+  u64 *pk, *hrec;  // packed clause masks; [clause][5] H_j(P) records of the positives
 };
 
 WS ws_of(const gr_batch *in, void *base) {
@@ -116,8 +115,7 @@ WS ws_of(const gr_batch *in, void *base) {
   w.active = (int *)(p + L.active);
   w.chunk_base = (u64 *)(p + L.chunk_base);
   w.pk = (u64 *)(p + L.pk);
-  w.h2 = (u64 *)(p + L.h2);
-  w.h3 = (u64 *)(p + L.h3);
+  w.hrec = (u64 *)(p + L.hrec);
   return w;
 }
 
@@ -166,8 +164,7 @@ __device__ void write_result(const In &in, const Out &out, int b, int status, u6
   if (out.decided) out.decided[b] = decided;
 }
 
-__device__ u64 pairs_hitting(u32 p);
-__device__ u64 triples_hitting(u32 p);
+__device__ u64 hitting(int j, u64 p);
 
 // ---------------------------------------------------------------------------
 // pack: one CTA per instance
@@ -276,10 +273,8 @@ __global__ void __launch_bounds__(PT) pack_kernel(In in, Out out, WS ws, int whi
     }
     const int64_t dst = lo + (j < np ? 0 : npr) + d;
     ws.pk[dst] = R[j];
-    if (j < np) {
-      ws.h2[dst] = pairs_hitting((u32)(R[j] & 0x7ffu));
-      ws.h3[dst] = triples_hitting((u32)(R[j] & 0xffu));
-    }
+    if (j < np)
+      for (int jj = 1; jj <= 5; jj++) ws.hrec[dst * 5 + jj - 1] = hitting(jj, R[j]);
   }
   // weights of the support variables (relabelled order) and S_k
   if (t < 64) {
@@ -337,60 +332,55 @@ __global__ void __launch_bounds__(PT) pack_kernel(In in, Out out, WS ws, int whi
 }
 
 // ---------------------------------------------------------------------------
-// the level walk of one lane: bit-parallel decision of the j lowest elements
+// the level walk of one lane: bit-parallel decision of the J lowest elements
 // ---------------------------------------------------------------------------
 // Candidates at level k are k-subsets x of [0, m_eff) in colex order (rank =
-// sum_i C(c_i, i)).  Split x = U | S where S holds the j = min(3, k) lowest
-// elements: all candidates sharing U form one contiguous rank block (U in
-// colex order, then S in colex order), S ranging over the j-subsets of
-// [0, min U).  The block is decided as a few *sub-blocks* whose candidates
-// are one bit each of a 64-bit mask F, the bit index being the colex offset
-// idx_j(S) = sum_i C(s_i, i):
-//   j = 3: triples inside [0, 8)   (C(8,3) = 56 bits), then for t >= 8 the
-//          pairs block of U | {t};
-//   j = 2: pairs inside [0, 11)    (C(11,2) = 55 bits), then for t >= 11 the
-//          singles block of U | {t};
-//   j = 1: singles a < e           (<= 64 bits).
-// A positive clause P missed by U leaves the candidates that hit P:
-// F &= H_j(P) with H_1(P) = P, H_2(P) = {pairs meeting P & 0x7ff},
-// H_3(P) = {triples meeting P & 0xff} (precomputed per clause by the pack).
-// A negative clause N with N \ U inside the region kills the S with
-// S superset of N & region.
-constexpr int R2 = 11, R3 = 8;
+// sum_i C(c_i, i)).  With J = min(JMAX, k), split x = U | S, S = the J lowest
+// elements.  All candidates sharing U form one contiguous rank block, S
+// ranging over the J-subsets of [0, min U) in colex order.  Recursively,
+//   node(j, U, e, base) = part A: the j-subsets of [0, min(e, R_j))   (one
+//                                 sub-block, <= 64 candidates)
+//                         part B: for t in [R_j, e): node(j-1, U | {t}, t,
+//                                 base + C(t, j))
+// where R_j is the largest R with C(R, j) <= 64 (R_1 = 64, R_2 = 11, R_3 = 8,
+// R_4 = 7, R_5 = 8).  A sub-block's candidates are the bits of one 64-bit
+// mask F whose bit index is the colex offset idx_j(S) = sum_i C(s_i, i), so
+// rank = base + bit.  A positive clause P missed by U keeps the candidates
+// that meet P: F &= H_j(P), H_j(P) = {j-subsets of [0, R_j) meeting P}
+// (precomputed per clause by the pack; H_1(P) = P).  A negative clause N
+// whose variables outside the region all lie in U kills the S that contain
+// N's region part.  Each lane visits one sub-block per loop iteration (a flat
+// depth-first iterator over the node tree), so the lanes of a warp run the
+// same clause-test code in lock step.
+constexpr int JMAX = 5;
+constexpr int HREC = 5;  // per-clause record: H_1 (= P), H_2, H_3, H_4, H_5
 
-__device__ __forceinline__ int c2i(int b) { return b * (b - 1) / 2; }
-__device__ __forceinline__ int c3i(int c) { return c * (c - 1) * (c - 2) / 6; }
-
-// {pairs a < b < 11 meeting p}, bit a + C(b,2)
-__device__ u64 pairs_hitting(u32 p) {
-  u64 r = 0;
-  for (int b = 1; b < R2; b++)
-    for (int a = 0; a < b; a++)
-      if (((p >> a) | (p >> b)) & 1u) r |= 1ull << (a + c2i(b));
-  return r;
-}
-// {triples a < b < c < 8 meeting p}, bit a + C(b,2) + C(c,3)
-__device__ u64 triples_hitting(u32 p) {
-  u64 r = 0;
-  for (int c = 2; c < R3; c++)
-    for (int b = 1; b < c; b++)
-      for (int a = 0; a < b; a++)
-        if (((p >> a) | (p >> b) | (p >> c)) & 1u) r |= 1ull << (a + c2i(b) + c3i(c));
-  return r;
+__host__ __device__ constexpr int region_of(int j) {
+  return j == 1 ? 64 : (j == 2 ? 11 : (j == 3 ? 8 : (j == 4 ? 7 : 8)));
 }
 __device__ __forceinline__ u64 nbits(u64 n) { return n >= 64 ? ~0ull : ((1ull << n) - 1ull); }
-__device__ __forceinline__ u64 small_binom(int e, int j) {
-  return j == 1 ? (u64)e : (j == 2 ? (u64)c2i(e) : (u64)c3i(e));
+
+// H_j(p): bit i set iff the i-th j-subset of [0, R_j) (colex order) meets p
+__device__ u64 hitting(int j, u64 p) {
+  if (j == 1) return p;
+  const int R = region_of(j);
+  const u64 n = binom(R, j);
+  u64 x = (1ull << j) - 1, r = 0;
+  for (u64 i = 0; i < n; i++) {
+    if (x & p) r |= 1ull << i;
+    const u64 c = x & (~x + 1), y = x + c;  // Gosper: next j-subset
+    x = y | (((y ^ x) >> 2) >> (__ffsll((long long)c) - 1));
+  }
+  return r;
 }
-// the j-subsets of [0, e) that contain every element of q (a subset of [0, e))
+// the j-subsets of [0, e) (e <= R_j) that contain every element of q
 __device__ u64 supersets(int j, u64 q, int e) {
-  const int c = __popcll(q);
-  if (c > j) return 0;
-  u64 r = nbits(small_binom(e, j));
+  if (__popcll(q) > j) return 0;
+  u64 r = nbits(binom(e, j));
   while (q) {
     const int x = __ffsll((long long)q) - 1;
     q &= q - 1;
-    r &= j == 1 ? (1ull << x) : (j == 2 ? pairs_hitting(1u << x) : triples_hitting(1u << x));
+    r &= hitting(j, 1ull << x);
   }
   return r;
 }
@@ -403,48 +393,30 @@ struct Work {
 
 template <typename M>
 struct Clauses {
-  const M *P;      // [np + nn] positives then negatives
-  const u64 *H2;   // [np] pairs meeting P
-  const u64 *H3;   // [np] triples meeting P
+  const M *P;       // [np + nn] positives then negatives (uniform reads)
+  const u64 *H;     // [np][HREC] H_j(P) at H[q * HREC + j - 1]
   int np, nn;
 };
 
 template <typename M, bool COUNT>
 __device__ __forceinline__ u64 test_sub(int j, M U, int e, u64 F, const Clauses<M> &c, Work &wk) {
   const int np = c.np;
+  const u64 *H = c.H + (j - 1);
   int q = 0;
-  if (j == 1) {
-    for (; q + 4 <= np; q += 4) {
-      const M p0 = c.P[q], p1 = c.P[q + 1], p2 = c.P[q + 2], p3 = c.P[q + 3];
-      if (!(U & p0)) F &= (u64)p0;
-      if (!(U & p1)) F &= (u64)p1;
-      if (!(U & p2)) F &= (u64)p2;
-      if (!(U & p3)) F &= (u64)p3;
-      if (COUNT) wk.tests += 4;
-      if (!F) return 0;
-    }
-    for (; q < np; q++) {
-      const M p0 = c.P[q];
-      if (!(U & p0)) F &= (u64)p0;
-      if (COUNT) wk.tests += 1;
-    }
-  } else {
-    const u64 *H = j == 2 ? c.H2 : c.H3;
-    for (; q + 4 <= np; q += 4) {
-      const M p0 = c.P[q], p1 = c.P[q + 1], p2 = c.P[q + 2], p3 = c.P[q + 3];
-      const u64 h0 = H[q], h1 = H[q + 1], h2 = H[q + 2], h3 = H[q + 3];
-      if (!(U & p0)) F &= h0;
-      if (!(U & p1)) F &= h1;
-      if (!(U & p2)) F &= h2;
-      if (!(U & p3)) F &= h3;
-      if (COUNT) wk.tests += 4;
-      if (!F) return 0;
-    }
-    for (; q < np; q++) {
-      const M p0 = c.P[q];
-      if (!(U & p0)) F &= H[q];
-      if (COUNT) wk.tests += 1;
-    }
+  for (; q + 4 <= np; q += 4) {
+    const M p0 = c.P[q], p1 = c.P[q + 1], p2 = c.P[q + 2], p3 = c.P[q + 3];
+    const u64 h0 = H[HREC * q], h1 = H[HREC * (q + 1)], h2 = H[HREC * (q + 2)],
+              h3 = H[HREC * (q + 3)];
+    if (!(U & p0)) F &= h0;
+    if (!(U & p1)) F &= h1;
+    if (!(U & p2)) F &= h2;
+    if (!(U & p3)) F &= h3;
+    if (COUNT) wk.tests += 4;
+    if (!F) return 0;
+  }
+  for (; q < np; q++) {
+    if (!(U & c.P[q])) F &= H[HREC * q];
+    if (COUNT) wk.tests += 1;
   }
   if (!F) return 0;
   const M lowm = (M)nbits((u64)e);
@@ -458,114 +430,122 @@ __device__ __forceinline__ u64 test_sub(int j, M U, int e, u64 F, const Clauses<
   return F;
 }
 
-struct LaneCtx {
-  u64 r_lo, r_hi;  // this lane's rank window
-  int rb;          // weighted key shift
-  i64 best;
-};
-
-// weighted: W(U) + weights of the j low elements encoded by bit idx
+// weighted: W(U) + the weights of the j low elements encoded by bit idx
 template <typename M>
-__device__ __forceinline__ u64 weight_of(int j, int idx, M U, const u32 *w) {
+__device__ __forceinline__ u64 weight_of(int j, u64 idx, M U, const u32 *w) {
   u64 W = 0;
   for (M t = U; t; t &= t - 1) W += w[ctz(t)];
-  if (j == 1) return W + w[idx];
-  int c = -1;
-  if (j == 3) {
-    c = 2;
-    while (c + 1 < R3 && c3i(c + 1) <= idx) c++;
-    idx -= c3i(c);
+  for (int i = j; i >= 1; i--) {  // colex unrank of idx within [0, R_j)
+    int c = i - 1;
+    while (binom(c + 1, i) <= idx) c++;
+    W += w[c];
+    idx -= binom(c, i);
   }
-  int b = 1;
-  while (b + 1 < R2 && c2i(b + 1) <= idx) b++;
-  const int a = idx - c2i(b);
-  W += w[a] + w[b];
-  if (c >= 0) W += w[c];
   return W;
 }
 
-// one sub-block: U | S, S a j-subset of [0, e), ranks base + idx_j(S).
-// MODE 0: unit first witness (returns true when found), 1: unit exhaustive,
-// 2: weighted (min key).
-template <typename M, int MODE, bool COUNT>
-__device__ __forceinline__ bool do_sub(int j, M U, int e, u64 base, LaneCtx &L,
-                                       const Clauses<M> &c, const u32 *w, Work &wk) {
-  const u64 n = small_binom(e, j);
-  if (base >= L.r_hi || base + n <= L.r_lo || n == 0) return false;
-  u64 F = nbits(n);
-  if (L.r_lo > base) F &= ~nbits(L.r_lo - base);
-  if (L.r_hi < base + n) F &= nbits(L.r_hi - base);
-  if (COUNT) { wk.blocks++; wk.cands += (u64)__popcll(F); }
-  F = test_sub<M, COUNT>(j, U, e, F, c, wk);
-  if (!F) return false;
-  if (MODE == 2) {
-    for (u64 f = F; f; f &= f - 1) {
-      const int idx = __ffsll((long long)f) - 1;
-      const i64 key = (i64)((weight_of<M>(j, idx, U, w) << L.rb) | (base + (u64)idx));
-      L.best = key < L.best ? key : L.best;
-    }
-    return false;
-  }
-  if (L.best == GR_KEY_NONE) L.best = (i64)(base + (u64)(__ffsll((long long)F) - 1));
-  return MODE == 0;
-}
-
-template <typename M, int MODE, bool COUNT>
-__device__ __forceinline__ bool do_block2(M U, int e, u64 base, LaneCtx &L, const Clauses<M> &c,
-                                          const u32 *w, Work &wk) {
-  if (do_sub<M, MODE, COUNT>(2, U, e < R2 ? e : R2, base, L, c, w, wk)) return true;
-  for (int t = R2; t < e; t++) {
-    const u64 bt = base + (u64)c2i(t);
-    if (bt >= L.r_hi) break;
-    if (do_sub<M, MODE, COUNT>(1, (M)(U | ((M)1 << t)), t, bt, L, c, w, wk)) return true;
-  }
-  return false;
-}
-
-template <typename M, int MODE, bool COUNT>
-__device__ __forceinline__ bool do_block3(M U, int e, u64 base, LaneCtx &L, const Clauses<M> &c,
-                                          const u32 *w, Work &wk) {
-  if (do_sub<M, MODE, COUNT>(3, U, e < R3 ? e : R3, base, L, c, w, wk)) return true;
-  for (int t = R3; t < e; t++) {
-    const u64 bt = base + (u64)c3i(t);
-    if (bt >= L.r_hi) break;
-    if (bt + (u64)c2i(t) <= L.r_lo) continue;
-    if (do_block2<M, MODE, COUNT>((M)(U | ((M)1 << t)), t, bt, L, c, w, wk)) return true;
-  }
-  return false;
-}
-
-// walk ranks [r_lo, r_lo + cnt) of level k
+// walk ranks [r_lo, r_lo + cnt) of level k.  MODE 0: unit weights, first
+// witness; 1: unit, exhaustive; 2: weighted (min key W << rb | rank).
 template <typename M, int MODE, bool COUNT>
 __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const u32 *w, int rb,
                     Work &wk) {
-  const int j = k < 3 ? k : 3;
-  LaneCtx L{r_lo, r_lo + cnt, rb, GR_KEY_NONE};
+  const int J = k < JMAX ? k : JMAX;
+  const u64 r_hi = r_lo + cnt;
+  i64 best = GR_KEY_NONE;
+  // ---- position the iterator on the sub-block that holds rank r_lo
   const u64 x = unrank_colex(r_lo, k, me);
+  int s[JMAX];  // the J lowest elements of x, ascending
   u64 Ux = x;
-  u64 off = 0;
-  for (int i = 1; i <= j; i++) {  // strip the j lowest elements, their colex offset
-    const int s = __ffsll((long long)Ux) - 1;
+  for (int i = 0; i < J; i++) {
+    s[i] = __ffsll((long long)Ux) - 1;
     Ux &= Ux - 1;
-    off += binom(s, i);
   }
-  M U = (M)Ux;
-  u64 base = r_lo - off;
+  u64 off = 0;
+  for (int i = 0; i < J; i++) off += binom(s[i], i + 1);
+  M Utop = (M)Ux;
+  u64 base_top = r_lo - off;
+  int e_top = Utop ? ctz(Utop) : me;
+  // descend: at depth d (node j = J - d) x lies in part B iff its j-th lowest
+  // element s[j-1] >= R_j; then t_d = s[j-1]
+  M U = Utop;
+  u64 base = base_top;
+  int d = 0;
+  u64 tp = 0;  // t_0 .. t_{d-1}, 8 bits each
   for (;;) {
-    const int e = U ? ctz(U) : me;
-    bool done;
-    if (j == 3) done = do_block3<M, MODE, COUNT>(U, e, base, L, c, w, wk);
-    else if (j == 2) done = do_block2<M, MODE, COUNT>(U, e, base, L, c, w, wk);
-    else done = do_sub<M, MODE, COUNT>(1, U, e, base, L, c, w, wk);
-    if (done) return L.best;
-    base += binom(e, j);
-    if (base >= L.r_hi || !U) return L.best;
-    // next U: Gosper's hack on the (k-j)-subsets of [j, me) (shifted down by j)
-    M S = U >> j;
+    const int j = J - d;
+    if (j < 2 || s[j - 1] < region_of(j)) break;
+    const int t = s[j - 1];
+    tp |= (u64)t << (8 * d);
+    U |= (M)1 << t;
+    base += binom(t, j);
+    d++;
+  }
+  // ---- iterate over sub-blocks in rank order
+  for (;;) {
+    const int j = J - d;
+    const int e = d == 0 ? e_top : (int)((tp >> (8 * (d - 1))) & 255);
+    const int R = region_of(j);
+    const int ea = e < R ? e : R;
+    if (base >= r_hi) return best;
+    const u64 n = binom(ea, j);
+    if (n && base + n > r_lo) {
+      u64 F = nbits(n);
+      if (r_lo > base) F &= ~nbits(r_lo - base);
+      if (r_hi < base + n) F &= nbits(r_hi - base);
+      if (COUNT) { wk.blocks++; wk.cands += (u64)__popcll(F); }
+      F = test_sub<M, COUNT>(j, U, ea, F, c, wk);
+      if (F) {
+        if (MODE == 2) {
+          for (u64 f = F; f; f &= f - 1) {
+            const u64 idx = (u64)(__ffsll((long long)f) - 1);
+            const i64 key = (i64)((weight_of<M>(j, idx, U, w) << rb) | (base + idx));
+            best = key < best ? key : best;
+          }
+        } else {
+          if (best == GR_KEY_NONE) best = (i64)(base + (u64)(__ffsll((long long)F) - 1));
+          if (MODE == 0) return best;
+        }
+      }
+    }
+    // ---- advance: first child of this node, else next sibling up the path
+    if (j >= 2 && R < e) {
+      tp |= (u64)R << (8 * d);
+      U |= (M)1 << R;
+      base += binom(R, j);
+      d++;
+      continue;
+    }
+    bool moved = false;
+    while (d > 0) {
+      const int t = (int)((tp >> (8 * (d - 1))) & 255);
+      const int jp = J - (d - 1);
+      const int ep = d == 1 ? e_top : (int)((tp >> (8 * (d - 2))) & 255);
+      U &= ~((M)1 << t);
+      base -= binom(t, jp);
+      tp &= ~(255ull << (8 * (d - 1)));
+      if (t + 1 < ep) {
+        tp |= (u64)(t + 1) << (8 * (d - 1));
+        U |= (M)1 << (t + 1);
+        base += binom(t + 1, jp);
+        moved = true;
+        break;
+      }
+      d--;
+    }
+    if (moved) continue;
+    // ---- next top-level U (Gosper on the (k-J)-subsets of [J, me))
+    base_top += binom(e_top, J);
+    if (base_top >= r_hi || !Utop) return best;
+    M S = Utop >> J;
     const M lb = lowbit(S);
     const M r = S + lb;
     S = r | (((r ^ S) >> 2) >> ctz(S));
-    U = (M)(S << j);
+    Utop = (M)(S << J);
+    e_top = ctz(Utop);
+    U = Utop;
+    base = base_top;
+    d = 0;
+    tp = 0;
   }
 }
 
@@ -594,12 +574,12 @@ __device__ i64 run_lane(const EnumParams &p, u64 r_lo, u64 cnt, int me, const Cl
 
 __device__ unsigned long long g_work[4];  // counting instantiation totals
 
-constexpr int SMC = 1024;  // clauses staged in shared memory (larger instances read L1/L2)
-constexpr size_t ENUM_SMEM = (size_t)SMC * 24;
+constexpr int SMC = 512;  // clauses staged in shared memory (larger instances read L1/L2)
+constexpr size_t ENUM_SMEM = (size_t)SMC * (8 * HREC + 8);
 
 template <bool COUNT>
 __global__ void __launch_bounds__(NT) enum_kernel(EnumParams p) {
-  extern __shared__ u64 cls[];  // [np] H2, [np] H3, [np + nn] P (u32 or u64)
+  extern __shared__ u64 cls[];  // [np][HREC] H records, [np + nn] P (u32 or u64)
   __shared__ u64 s_chunk;
   __shared__ int s_b, s_cur, s_skip;
   __shared__ u64 s_r0, s_ck;
@@ -645,18 +625,16 @@ __global__ void __launch_bounds__(NT) enum_kernel(EnumParams p) {
     const int64_t lo = p.off[b];
     const bool staged = np + nn <= SMC;
     const bool narrow = staged && me <= 32;
-    u64 *sH2 = cls, *sH3 = cls + np;
+    u64 *sH = cls;                       // [np][HREC]
+    u64 *sP = cls + (size_t)HREC * np;   // [np + nn] as u32 or u64
     if (b != s_cur) {
       if (staged) {
-        for (int q = t; q < np; q += NT) {
-          sH2[q] = p.ws.h2[lo + q];
-          sH3[q] = p.ws.h3[lo + q];
-        }
+        for (int q = t; q < np * HREC; q += NT) sH[q] = p.ws.hrec[lo * HREC + q];
         if (narrow) {
-          u32 *c32 = (u32 *)(cls + 2 * np);
+          u32 *c32 = (u32 *)sP;
           for (int q = t; q < np + nn; q += NT) c32[q] = (u32)p.ws.pk[lo + q];
         } else {
-          for (int q = t; q < np + nn; q += NT) cls[2 * np + q] = p.ws.pk[lo + q];
+          for (int q = t; q < np + nn; q += NT) sP[q] = p.ws.pk[lo + q];
         }
       }
       if (t < 64) s_w[t] = p.ws.wr[(size_t)b * 64 + t];
@@ -671,13 +649,13 @@ __global__ void __launch_bounds__(NT) enum_kernel(EnumParams p) {
       const u64 cnt = (ck - r_lo) < Lc ? (ck - r_lo) : Lc;
       const int rb = p.ws.rb[b];
       if (narrow) {
-        Clauses<u32> c{(const u32 *)(cls + 2 * np), sH2, sH3, np, nn};
+        Clauses<u32> c{(const u32 *)sP, sH, np, nn};
         key = run_lane<u32, COUNT>(p, r_lo, cnt, me, c, s_w, rb, wk);
       } else if (staged) {
-        Clauses<u64> c{cls + 2 * np, sH2, sH3, np, nn};
+        Clauses<u64> c{sP, sH, np, nn};
         key = run_lane<u64, COUNT>(p, r_lo, cnt, me, c, s_w, rb, wk);
       } else {
-        Clauses<u64> c{p.ws.pk + lo, p.ws.h2 + lo, p.ws.h3 + lo, np, nn};
+        Clauses<u64> c{p.ws.pk + lo, p.ws.hrec + lo * HREC, np, nn};
         key = run_lane<u64, COUNT>(p, r_lo, cnt, me, c, s_w, rb, wk);
       }
     }
