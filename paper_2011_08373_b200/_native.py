@@ -15,7 +15,7 @@ from typing import Optional
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libgrsolve.so")
+LIB_PATH = os.environ.get("GRSOLVE_LIB") or os.path.join(HERE, "libgrsolve.so")  # override: dev A/B builds
 
 GR_OK, GR_EINVAL, GR_ETOOBIG, GR_ECUDA, GR_ENOMEM, GR_EWORKSPACE = 0, -1, -2, -3, -4, -5
 GR_SAT, GR_UNSAT, GR_SAT_NEG_VIOLATED, GR_BADINPUT, GR_UNSUPPORTED = 0, 1, 2, 3, 4
