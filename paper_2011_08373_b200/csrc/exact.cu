@@ -356,7 +356,7 @@ constexpr int JMAX = 5;
 constexpr int HREC = 5;  // per-clause record: H_1 (= P), H_2, H_3, H_4, H_5
 
 __host__ __device__ constexpr int region_of(int j) {
-  return j == 1 ? 64 : (j == 2 ? 11 : (j == 3 ? 8 : (j == 4 ? 7 : 8)));
+  return (int)((0x0807080B40ull >> (8 * (j - 1))) & 0xffull);  // 64, 11, 8, 7, 8
 }
 __device__ __forceinline__ u64 nbits(u64 n) { return n >= 64 ? ~0ull : ((1ull << n) - 1ull); }
 
@@ -380,24 +380,15 @@ struct Work {
   u64 tests = 0, blocks = 0, cands = 0;
 };
 
-__device__ __forceinline__ i64 warp_min(i64 v) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    i64 u = __shfl_xor_sync(0xffffffffu, v, o);
-    v = u < v ? u : v;
-  }
-  return v;
-}
-
 template <typename M>
 struct Clauses {
-  const M *P;       // [np + nn] positives then negatives
+  const M *P;       // [np + nn] positives then negatives (uniform reads)
   const u64 *H;     // [np][HREC] H_j(P) at H[q * HREC + j - 1]
   const u64 *hitx;  // [6][64] HIT_j({x}) (0 when x >= R_j), shared memory
+  const u32 *cs;    // [65][8] C(n, j) for j <= 5 (fits 32 bits), shared memory
   int np, nn;
 };
 
-// decide one sub-block: positives, then negatives (F &= ~AND_{x in N \ U} HIT_j({x}))
 template <typename M, bool COUNT>
 __device__ __forceinline__ u64 test_sub(int j, M U, int e, u64 F, const Clauses<M> &c, Work &wk) {
   const int np = c.np;
@@ -427,7 +418,7 @@ __device__ __forceinline__ u64 test_sub(int j, M U, int e, u64 F, const Clauses<
     if ((rest & ~lowm) || popc(rest) > j) continue;  // some variable of N stays false
     u64 kill = ~0ull;
     for (; rest; rest &= rest - 1) kill &= hx[ctz(rest)];
-    F &= ~kill;
+    F &= ~kill;  // the S holding every variable of N outside U
     if (!F) return 0;
   }
   return F;
@@ -447,159 +438,124 @@ __device__ __forceinline__ u64 weight_of(int j, u64 idx, M U, const u32 *w) {
   return W;
 }
 
-// flat depth-first iterator over the sub-blocks of level k, in rank order
-template <typename M>
-struct SubIter {
-  int J, me, e_top, d;
-  M Utop, U;
-  u64 base_top, base, tp;  // tp: t_0 .. t_{d-1}, 8 bits each
-
-  // position on the sub-block holding rank r
-  __device__ __forceinline__ void init(int k, int m_eff, u64 r) {
-    J = k < JMAX ? k : JMAX;
-    me = m_eff;
-    const u64 x = unrank_colex(r, k, me);
-    u64 Ux = x, off = 0;
-    int s[JMAX];
-    for (int i = 0; i < J; i++) {
-      s[i] = __ffsll((long long)Ux) - 1;
-      Ux &= Ux - 1;
-      off += binom(s[i], i + 1);
-    }
-    Utop = (M)Ux;
-    base_top = r - off;
-    e_top = Utop ? ctz(Utop) : me;
-    U = Utop;
-    base = base_top;
-    d = 0;
-    tp = 0;
-    for (;;) {  // x lies in part B of the node at depth d iff s[j-1] >= R_j
-      const int j = J - d;
-      if (j < 2 || s[j - 1] < region_of(j)) break;
-      const int t = s[j - 1];
-      tp |= (u64)t << (8 * d);
-      U |= (M)1 << t;
-      base += binom(t, j);
-      d++;
-    }
+// walk ranks [r_lo, r_lo + cnt) of level k.  MODE 0: unit weights, first
+// witness; 1: unit, exhaustive; 2: weighted (min key W << rb | rank).
+// Iterator state: the top-level U (k - J elements) with its first rank
+// base_top, the path t_0 > t_1 > ... of part-B choices below it (6 bits
+// each in tp), the current U and the current sub-block's first rank base.
+template <typename M, int MODE, bool COUNT>
+__device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const u32 *w, int rb,
+                    Work &wk) {
+  const int J = k < JMAX ? k : JMAX;
+  const u32 *cs = c.cs;  // C(n, j), j <= 5
+#define CS(n, j) ((u64)cs[(n) * 8 + (j)])
+  const u64 r_hi = r_lo + cnt;
+  i64 best = GR_KEY_NONE;
+  // ---- position the iterator on the sub-block that holds rank r_lo
+  const u64 x = unrank_colex(r_lo, k, me);
+  int s[JMAX];  // the J lowest elements of x, ascending
+  u64 Ux = x, off = 0;
+  for (int i = 0; i < J; i++) {
+    s[i] = __ffsll((long long)Ux) - 1;
+    Ux &= Ux - 1;
+    off += CS(s[i], i + 1);
   }
-  __device__ __forceinline__ int j() const { return J - d; }
-  __device__ __forceinline__ int e() const {
-    return d == 0 ? e_top : (int)((tp >> (8 * (d - 1))) & 255);
+  M Utop = (M)Ux;
+  u64 base_top = r_lo - off;
+  int e_top = Utop ? ctz(Utop) : me;
+  // descend: at depth d (node j = J - d) x lies in part B iff its j-th lowest
+  // element s[j-1] >= R_j; then t_d = s[j-1]
+  M U = Utop;
+  u64 base = base_top;
+  int d = 0;
+  u32 tp = 0;  // t_0 .. t_{d-1}, 6 bits each
+  for (;;) {
+    const int j = J - d;
+    if (j < 2 || s[j - 1] < region_of(j)) break;
+    const int t = s[j - 1];
+    tp |= (u32)t << (6 * d);
+    U |= (M)1 << t;
+    base += CS(t, j);
+    d++;
   }
-  // advance to the next sub-block; false when the level is exhausted
-  __device__ __forceinline__ bool next() {
-    const int jj = J - d, ee = e(), R = region_of(jj);
-    if (jj >= 2 && R < ee) {  // first child: t = R_j
-      tp |= (u64)R << (8 * d);
-      U |= (M)1 << R;
-      base += binom(R, jj);
-      d++;
-      return true;
-    }
-    while (d > 0) {  // next sibling up the path
-      const int t = (int)((tp >> (8 * (d - 1))) & 255);
-      const int jp = J - (d - 1);
-      const int ep = d == 1 ? e_top : (int)((tp >> (8 * (d - 2))) & 255);
-      U &= ~((M)1 << t);
-      base -= binom(t, jp);
-      tp &= ~(255ull << (8 * (d - 1)));
-      if (t + 1 < ep) {
-        tp |= (u64)(t + 1) << (8 * (d - 1));
-        U |= (M)1 << (t + 1);
-        base += binom(t + 1, jp);
-        return true;
+  // ---- iterate over sub-blocks in rank order
+  for (;;) {
+    const int j = J - d;
+    const int e = d == 0 ? e_top : (int)((tp >> (6 * (d - 1))) & 63u);
+    const int R = region_of(j);
+    const int ea = e < R ? e : R;
+    if (base >= r_hi) return best;
+    const u64 n = CS(ea, j);
+    if (n && base + n > r_lo) {
+      u64 F = nbits(n);
+      if (r_lo > base) F &= ~nbits(r_lo - base);
+      if (r_hi < base + n) F &= nbits(r_hi - base);
+      if (COUNT) { wk.blocks++; wk.cands += (u64)__popcll(F); }
+      F = test_sub<M, COUNT>(j, U, ea, F, c, wk);
+      if (F) {
+        if (MODE == 2) {
+          for (u64 f = F; f; f &= f - 1) {
+            const u64 idx = (u64)(__ffsll((long long)f) - 1);
+            const i64 key = (i64)((weight_of<M>(j, idx, U, w) << rb) | (base + idx));
+            best = key < best ? key : best;
+          }
+        } else {
+          if (best == GR_KEY_NONE) best = (i64)(base + (u64)(__ffsll((long long)F) - 1));
+          if (MODE == 0) return best;
+        }
       }
+    }
+    // ---- advance: first child of this node, else next sibling up the path
+    if (j >= 2 && R < e) {
+      tp |= (u32)R << (6 * d);
+      U |= (M)1 << R;
+      base += CS(R, j);
+      d++;
+      continue;
+    }
+    bool moved = false;
+    while (d > 0) {
+      const int sh = 6 * (d - 1);
+      const int t = (int)((tp >> sh) & 63u);
+      const int jp = J - (d - 1);
+      const int ep = d == 1 ? e_top : (int)((tp >> (sh - 6)) & 63u);
+      tp &= ~(63u << sh);
+      if (t + 1 < ep) {  // next sibling: t -> t + 1
+        tp |= (u32)(t + 1) << sh;
+        U ^= (M)3 << t;
+        base += CS(t + 1, jp) - CS(t, jp);
+        moved = true;
+        break;
+      }
+      U &= ~((M)1 << t);
+      base -= CS(t, jp);
       d--;
     }
-    base_top += binom(e_top, J);  // next top-level U: Gosper on (k-J)-subsets of [J, me)
-    if (!Utop) return false;
+    if (moved) continue;
+    // ---- next top-level U (Gosper on the (k-J)-subsets of [J, me))
+    base_top += CS(e_top, J);
+    if (base_top >= r_hi || !Utop) return best;
     M S = Utop >> J;
     const M lb = lowbit(S);
     const M r = S + lb;
     S = r | (((r ^ S) >> 2) >> ctz(S));
     Utop = (M)(S << J);
-    if (!Utop) return false;
     e_top = ctz(Utop);
     U = Utop;
     base = base_top;
-    return true;
+    d = 0;
+    tp = 0;
   }
-};
+#undef CS
+}
 
-constexpr u64 STEAL_MIN = 512;  // smallest remaining window worth an unrank
-
-// One warp walks 32 lane windows [lo, hi) of level k (called by all 32 lanes).
-// Each iteration every busy lane decides one sub-block; when at least 4 lanes
-// ran out of work, one of them steals the upper half of the busiest lane's
-// remaining window (one unrank per steal).
-// MODE 0: unit weights, first witness; 1: unit, exhaustive; 2: weighted.
-template <typename M, int MODE, bool COUNT>
-__device__ i64 walk_warp(int k, int me, u64 lo, u64 hi, const Clauses<M> &c, const u32 *w,
-                         int rb, Work &wk) {
-  const int lane = threadIdx.x & 31;
-  i64 best = GR_KEY_NONE;
-  SubIter<M> it;
-  bool done = lo >= hi;
-  if (!done) it.init(k, me, lo);
-  for (;;) {
-    unsigned dm = __ballot_sync(0xffffffffu, done);
-    if (dm == 0xffffffffu) break;
-    if (MODE == 0 && __any_sync(0xffffffffu, best != GR_KEY_NONE)) {
-      // a witness below a lane's window ends that lane
-      const i64 f = warp_min(best);
-      if (!done && it.base > (u64)f) done = true;
-      dm = __ballot_sync(0xffffffffu, done);
-      if (dm == 0xffffffffu) break;
-    }
-    if (__popc(dm) >= 4) {  // work stealing: enough idle lanes
-      const u64 rem = (!done && hi > it.base) ? hi - it.base : 0;
-      const u32 r32 = rem > 0xffffffffull ? 0xffffffffu : (u32)rem;
-      const u32 mx = __reduce_max_sync(0xffffffffu, r32);
-      if (mx >= STEAL_MIN) {
-        const int ml = __ffs(__ballot_sync(0xffffffffu, r32 == mx)) - 1;
-        const int thief = __ffs(dm) - 1;
-        u64 mid = it.base + rem / 2;
-        mid = __shfl_sync(0xffffffffu, mid, ml);
-        const u64 vhi = __shfl_sync(0xffffffffu, hi, ml);
-        if (lane == ml) hi = mid;
-        if (lane == thief) {
-          lo = mid;
-          hi = vhi;
-          it.init(k, me, mid);
-          done = false;
-        }
-      }
-    }
-    if (done) continue;
-    // ---- decide the current sub-block
-    const int j = it.j(), e = it.e(), R = region_of(j);
-    const int ea = e < R ? e : R;
-    const u64 base = it.base;
-    const u64 n = binom(ea, j);
-    if (n && base + n > lo) {
-      u64 F = nbits(n);
-      if (lo > base) F &= ~nbits(lo - base);
-      if (hi < base + n) F &= nbits(hi - base);
-      if (COUNT) { wk.blocks++; wk.cands += (u64)__popcll(F); }
-      F = test_sub<M, COUNT>(j, it.U, ea, F, c, wk);
-      if (F) {
-        if (MODE == 2) {
-          for (u64 f = F; f; f &= f - 1) {
-            const u64 idx = (u64)(__ffsll((long long)f) - 1);
-            const i64 key = (i64)((weight_of<M>(j, idx, it.U, w) << rb) | (base + idx));
-            best = key < best ? key : best;
-          }
-        } else {
-          const i64 r = (i64)(base + (u64)(__ffsll((long long)F) - 1));
-          best = r < best ? r : best;  // a stolen window may lie below an earlier witness
-          if (MODE == 0) done = true;
-        }
-      }
-    }
-    if (!done && (!it.next() || it.base >= hi)) done = true;
+__device__ __forceinline__ i64 warp_min(i64 v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    i64 u = __shfl_xor_sync(0xffffffffu, v, o);
+    v = u < v ? u : v;
   }
-  return best;
+  return v;
 }
 
 struct EnumParams {
@@ -608,113 +564,124 @@ struct EnumParams {
   int k, weighted, exhaustive, shard, nshard;
 };
 
+template <typename M, bool COUNT>
+__device__ i64 run_lane(const EnumParams &p, u64 r_lo, u64 cnt, int me, const Clauses<M> &c,
+                        const u32 *w, int rb, Work &wk) {
+  if (p.weighted) return walk<M, 2, COUNT>(p.k, me, r_lo, cnt, c, w, rb, wk);
+  if (p.exhaustive) return walk<M, 1, COUNT>(p.k, me, r_lo, cnt, c, w, rb, wk);
+  return walk<M, 0, COUNT>(p.k, me, r_lo, cnt, c, w, rb, wk);
+}
+
 __device__ unsigned long long g_work[4];  // counting instantiation totals
 
-#ifndef GR_ENUM_MINB
-#define GR_ENUM_MINB 3
-#endif
-constexpr int NWARP = NT / 32;
-constexpr size_t WARP_SMEM = 8704;  // per-warp clause slice (larger instances read L1/L2)
-constexpr size_t ENUM_SMEM = 6 * 64 * 8 + NWARP * WARP_SMEM;
+constexpr int SMC = 512;  // clauses staged in shared memory (larger instances read L1/L2)
+constexpr size_t TAB_SMEM = 6 * 64 * 8 + 65 * 8 * 4;  // HIT table + small binomials
+constexpr size_t ENUM_SMEM = TAB_SMEM + (size_t)SMC * (8 * HREC + 8);
 
-// Persistent CTAs; every warp independently pulls chunks of 32 x L colex
-// ranks of the current level from one global atomic counter (chunk c goes to
-// shard c % nshard), stages its instance's clause records in its own
-// shared-memory slice, walks, and publishes the chunk minimum with one
-// atomicMin.
-template <bool COUNT, int MODE>
-__global__ void __launch_bounds__(NT, GR_ENUM_MINB) enum_kernel(EnumParams p) {
-  extern __shared__ u64 smem[];  // [6][64] HIT table, then one slice per warp
-  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
-  for (int q = t; q < 6 * 64; q += NT) {  // HIT_j({x}): j-subsets of [0, R_j) containing x
+template <bool COUNT>
+__global__ void __launch_bounds__(NT) enum_kernel(EnumParams p) {
+  extern __shared__ u64 cls[];  // [np][HREC] H records, [np + nn] P (u32 or u64)
+  __shared__ u64 s_chunk;
+  __shared__ int s_b, s_cur, s_skip;
+  __shared__ u64 s_r0, s_ck;
+  __shared__ u32 s_w[64];
+  __shared__ i64 s_wmin[NT / 32];
+  const int t = threadIdx.x;
+  if (t == 0) s_cur = -1;
+  u64 *hitx = cls;                     // [6][64] HIT_j({x}): j-subsets of [0, R_j) containing x
+  u32 *cs = (u32 *)(cls + 6 * 64);     // [65][8] C(n, j), j <= 5
+  for (int q = t; q < 6 * 64; q += NT) {
     const int jj = q / 64, x = q % 64;
-    smem[q] = (jj >= 1 && x < region_of(jj)) ? hitting(jj, 1ull << x) : 0ull;
+    hitx[q] = (jj >= 1 && x < region_of(jj)) ? hitting(jj, 1ull << x) : 0ull;
   }
-  __syncthreads();
-  const u64 *hitx = smem;
-  u64 *slice = smem + 6 * 64 + (size_t)wid * (WARP_SMEM / 8);
+  for (int q = t; q < 65 * 8; q += NT) cs[q] = (q % 8) <= 5 ? (u32)binom(q / 8, q % 8) : 0u;
+  u64 *stage = cls + TAB_SMEM / 8;  // staged clause records
   const u64 Lc = p.ws.ctrl->lane_cands;
-  const u64 CH = Lc * 32;
+  const u64 CH = Lc * NT;
   const u64 total = p.ws.ctrl->total_chunks;
   const int nact = p.ws.ctrl->n_active;
   const int *active = p.ws.active;  // list of this level (offset by the host)
-  int cur = -1;
-  Work wk;
   for (;;) {
-    u64 ch = 0;
-    int b = -1;
-    u64 r0 = 0;
-    int skip = 0;
-    if (lane == 0) {
-      const u64 jn = atomicAdd((unsigned long long *)&p.ws.ctrl->next_chunk, 1ull);
-      ch = jn * (u64)p.nshard + (u64)p.shard;
+    __syncthreads();
+    if (t == 0) {
+      u64 jn = atomicAdd((unsigned long long *)&p.ws.ctrl->next_chunk, 1ull);
+      u64 ch = jn * (u64)p.nshard + (u64)p.shard;
+      s_chunk = ch;
+      s_skip = 0;
       if (ch < total) {
-        int lo = 0, hi = nact - 1;  // active index i: chunk_base[i] <= ch < chunk_base[i+1]
+        // active index i: chunk_base[i] <= ch < chunk_base[i+1]
+        int lo = 0, hi = nact - 1;
         while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
+          int mid = (lo + hi + 1) >> 1;
           if (p.ws.chunk_base[mid] <= ch) lo = mid; else hi = mid - 1;
         }
-        b = active[lo];
-        r0 = (ch - p.ws.chunk_base[lo]) * CH;
-        if (MODE == 0) {
-          const i64 f = *(volatile i64 *)&p.ws.lvlkey[b];
-          skip = f != GR_KEY_NONE && (u64)f < r0;  // a lower witness exists
+        const int b = active[lo];
+        s_b = b;
+        const u64 r0 = (ch - p.ws.chunk_base[lo]) * CH;
+        s_r0 = r0;
+        s_ck = binom(p.ws.meff[b], p.k);
+        if (!p.weighted && !p.exhaustive) {
+          const i64 cur = *(volatile i64 *)&p.ws.lvlkey[b];
+          if (cur != GR_KEY_NONE && (u64)cur < r0) s_skip = 1;  // a lower witness exists
         }
       }
     }
-    ch = __shfl_sync(0xffffffffu, ch, 0);
-    if (ch >= total) break;
-    b = __shfl_sync(0xffffffffu, b, 0);
-    r0 = __shfl_sync(0xffffffffu, r0, 0);
-    skip = __shfl_sync(0xffffffffu, skip, 0);
-    if (skip) continue;
+    __syncthreads();
+    if (s_chunk >= total) break;
+    if (s_skip) continue;
+    const int b = s_b;
     const int me = p.ws.meff[b], np = p.ws.npr[b], nn = p.ws.nnr[b];
     const int64_t lo = p.off[b];
-    const bool staged = (size_t)(HREC * np + np + nn) * 8 + 256 <= WARP_SMEM;
+    const bool staged = np + nn <= SMC;
     const bool narrow = staged && me <= 32;
-    u64 *sH = slice;                                // [np][HREC]
-    u64 *sP = slice + (size_t)HREC * np;            // [np + nn] as u32 or u64
-    u32 *sW = (u32 *)(slice + WARP_SMEM / 8) - 64;  // [64] weights (tail of the slice)
-    if (b != cur) {
-      __syncwarp();
+    u64 *sH = stage;                       // [np][HREC]
+    u64 *sP = stage + (size_t)HREC * np;   // [np + nn] as u32 or u64
+    if (b != s_cur) {
       if (staged) {
-        for (int q = lane; q < np * HREC; q += 32) sH[q] = p.ws.hrec[lo * HREC + q];
+        for (int q = t; q < np * HREC; q += NT) sH[q] = p.ws.hrec[lo * HREC + q];
         if (narrow) {
           u32 *c32 = (u32 *)sP;
-          for (int q = lane; q < np + nn; q += 32) c32[q] = (u32)p.ws.pk[lo + q];
+          for (int q = t; q < np + nn; q += NT) c32[q] = (u32)p.ws.pk[lo + q];
         } else {
-          for (int q = lane; q < np + nn; q += 32) sP[q] = p.ws.pk[lo + q];
+          for (int q = t; q < np + nn; q += NT) sP[q] = p.ws.pk[lo + q];
         }
       }
-      if (MODE == 2) {
-        sW[lane] = p.ws.wr[(size_t)b * 64 + lane];
-        sW[lane + 32] = p.ws.wr[(size_t)b * 64 + lane + 32];
-      }
-      __syncwarp();
-      cur = b;
+      if (t < 64) s_w[t] = p.ws.wr[(size_t)b * 64 + t];
+      __syncthreads();
+      if (t == 0) s_cur = b;
     }
-    const u64 ck = binom(me, p.k);
-    const u64 r_lo = r0 + (u64)lane * Lc;
-    const u64 r_hi = r_lo < ck ? (ck - r_lo < Lc ? ck : r_lo + Lc) : r_lo;
-    const int rb = p.ws.rb[b];
-    i64 key;
-    if (narrow) {
-      Clauses<u32> c{(const u32 *)sP, sH, hitx, np, nn};
-      key = walk_warp<u32, MODE, COUNT>(p.k, me, r_lo, r_hi, c, sW, rb, wk);
-    } else if (staged) {
-      Clauses<u64> c{sP, sH, hitx, np, nn};
-      key = walk_warp<u64, MODE, COUNT>(p.k, me, r_lo, r_hi, c, sW, rb, wk);
-    } else {  // clause records and weights straight from global memory (L1)
-      Clauses<u64> c{p.ws.pk + lo, p.ws.hrec + lo * HREC, hitx, np, nn};
-      key = walk_warp<u64, MODE, COUNT>(p.k, me, r_lo, r_hi, c, p.ws.wr + (size_t)b * 64, rb, wk);
+    const u64 r_lo = s_r0 + (u64)t * Lc;
+    const u64 ck = s_ck;
+    i64 key = GR_KEY_NONE;
+    Work wk;
+    if (r_lo < ck) {
+      const u64 cnt = (ck - r_lo) < Lc ? (ck - r_lo) : Lc;
+      const int rb = p.ws.rb[b];
+      if (narrow) {
+        Clauses<u32> c{(const u32 *)sP, sH, hitx, cs, np, nn};
+        key = run_lane<u32, COUNT>(p, r_lo, cnt, me, c, s_w, rb, wk);
+      } else if (staged) {
+        Clauses<u64> c{sP, sH, hitx, cs, np, nn};
+        key = run_lane<u64, COUNT>(p, r_lo, cnt, me, c, s_w, rb, wk);
+      } else {
+        Clauses<u64> c{p.ws.pk + lo, p.ws.hrec + lo * HREC, hitx, cs, np, nn};
+        key = run_lane<u64, COUNT>(p, r_lo, cnt, me, c, s_w, rb, wk);
+      }
+    }
+    if (COUNT) {
+      atomicAdd(&g_work[0], (unsigned long long)wk.tests);
+      atomicAdd(&g_work[1], (unsigned long long)wk.blocks);
+      atomicAdd(&g_work[2], (unsigned long long)wk.cands);
+      if (!narrow) atomicAdd(&g_work[3], (unsigned long long)wk.tests);
     }
     key = warp_min(key);
-    if (lane == 0 && key != GR_KEY_NONE) atomicMin((long long *)&p.ws.lvlkey[b], (long long)key);
-  }
-  if (COUNT) {
-    atomicAdd(&g_work[0], (unsigned long long)wk.tests);
-    atomicAdd(&g_work[1], (unsigned long long)wk.blocks);
-    atomicAdd(&g_work[2], (unsigned long long)wk.cands);
+    if ((t & 31) == 0) s_wmin[t >> 5] = key;
+    __syncthreads();
+    if (t == 0) {
+      i64 v = s_wmin[0];
+      for (int i = 1; i < NT / 32; i++) v = s_wmin[i] < v ? s_wmin[i] : v;
+      if (v != GR_KEY_NONE) atomicMin((long long *)&p.ws.lvlkey[b], (long long)v);
+    }
   }
 }
 
@@ -731,7 +698,7 @@ __global__ void __launch_bounds__(FT) finish_kernel(In in, Out out, WS ws, int w
   __shared__ int s_cnt;
   const int t = threadIdx.x;
   const bool weighted = in.w != nullptr;
-  const u64 CH = ws.ctrl->lane_cands * 32;  // one chunk = one warp's 32 lane windows
+  const u64 CH = ws.ctrl->lane_cands * NT;
   const int nact_in = k == 0 ? in.B : ws.ctrl->n_active;
   int *cur = ws.active + (size_t)(k & 1) * in.B;        // list enumerated at level k
   int *nxt = ws.active + (size_t)((k + 1) & 1) * in.B;  // list for level k+1
@@ -861,11 +828,9 @@ int enum_grid() {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   size_t smem = ENUM_SMEM;
-#define GR_ENUM_ATTR(C, Mo) cudaFuncSetAttribute(enum_kernel<C, Mo>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
-  GR_ENUM_ATTR(false, 0); GR_ENUM_ATTR(false, 1); GR_ENUM_ATTR(false, 2);
-  GR_ENUM_ATTR(true, 0); GR_ENUM_ATTR(true, 1); GR_ENUM_ATTR(true, 2);
-#undef GR_ENUM_ATTR
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, enum_kernel<false, 0>, NT, smem);
+  cudaFuncSetAttribute(enum_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(enum_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, enum_kernel<false>, NT, smem);
   if (per < 1) per = 1;
   g_enum_grid = sms * per;
   return g_enum_grid;
@@ -959,20 +924,10 @@ extern "C" int gr_exact_level(const gr_batch *in, int which, int k, int shard, i
   p.nshard = nshard;
   int grid = enum_grid();
   GR_CUDA(cudaMemsetAsync(&w.ctrl->next_chunk, 0, sizeof(u64), (cudaStream_t)s));
-  const int mode = p.weighted ? 2 : (p.exhaustive ? 1 : 0);
-  const bool count = gr_prof_mode() == 2;
-  cudaStream_t st = (cudaStream_t)s;
-#define GR_ENUM_LAUNCH(C, Mo) GR_LAUNCH("enum_kernel", st, enum_kernel<C, Mo><<<grid, NT, ENUM_SMEM, st>>>(p))
-  if (count) {
-    if (mode == 0) GR_ENUM_LAUNCH(true, 0);
-    else if (mode == 1) GR_ENUM_LAUNCH(true, 1);
-    else GR_ENUM_LAUNCH(true, 2);
-  } else {
-    if (mode == 0) GR_ENUM_LAUNCH(false, 0);
-    else if (mode == 1) GR_ENUM_LAUNCH(false, 1);
-    else GR_ENUM_LAUNCH(false, 2);
-  }
-#undef GR_ENUM_LAUNCH
+  if (gr_prof_mode() == 2)
+    GR_LAUNCH("enum_kernel", (cudaStream_t)s, enum_kernel<true><<<grid, NT, ENUM_SMEM, (cudaStream_t)s>>>(p));
+  else
+    GR_LAUNCH("enum_kernel", (cudaStream_t)s, enum_kernel<false><<<grid, NT, ENUM_SMEM, (cudaStream_t)s>>>(p));
   return GR_OK;
 }
 
