@@ -152,7 +152,10 @@ int gr_exact_level(const gr_batch *in, int which, int k, int shard, int nshard, 
                    size_t ws_bytes, gr_stream_t s);
 int64_t *gr_exact_level_keys(const gr_batch *in, int which, void *ws);
 /* commits level k, writes results of instances that finished, plans level
- * k+1; *n_active (host) = instances still searching.  Synchronises s. */
+ * k+1 (chunk size adapted to the level's candidate count); *n_active (host)
+ * = instances still searching.  Synchronises s only when n_active != NULL;
+ * levels enumerated after every instance finished are no-ops, so a driver may
+ * queue several levels per read-back (gr_solve_pms queues 4). */
 int gr_exact_finish(const gr_batch *in, int which, int k, gr_result *out, void *ws,
                     size_t ws_bytes, gr_stream_t s, int32_t *n_active);
 

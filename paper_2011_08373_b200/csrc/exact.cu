@@ -691,14 +691,14 @@ __global__ void __launch_bounds__(NT) enum_kernel(EnumParams p) {
 __device__ __forceinline__ int bitlen(u64 x) { return x ? 64 - __clzll((long long)x) : 0; }
 
 __global__ void __launch_bounds__(FT) finish_kernel(In in, Out out, WS ws, int which, int k,
-                                                    int exhaustive) {
+                                                    int exhaustive, int enum_lanes,
+                                                    u64 fixed_lane) {
   typedef cub::BlockScan<u64, FT> Scan;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ u64 s_carry;
   __shared__ int s_cnt;
   const int t = threadIdx.x;
   const bool weighted = in.w != nullptr;
-  const u64 CH = ws.ctrl->lane_cands * NT;
   const int nact_in = k == 0 ? in.B : ws.ctrl->n_active;
   int *cur = ws.active + (size_t)(k & 1) * in.B;        // list enumerated at level k
   int *nxt = ws.active + (size_t)((k + 1) & 1) * in.B;  // list for level k+1
@@ -752,11 +752,11 @@ __global__ void __launch_bounds__(FT) finish_kernel(In in, Out out, WS ws, int w
   for (int base = 0; base < nact_in; base += FT) {
     const int i = base + t;
     int b = -1;
-    u64 nch = 0;
     if (i < nact_in) {
       b = k == 0 ? i : cur[i];
       if (ws.done[b]) b = -1;
     }
+    u64 csz = 0;
     if (b >= 0) {
       const int me = ws.meff[b];
       const u64 ck = binom(me, k + 1);
@@ -771,34 +771,51 @@ __global__ void __launch_bounds__(FT) finish_kernel(In in, Out out, WS ws, int w
         }
       }
       if (b >= 0) {
-        nch = (ck + CH - 1) / CH;
         ws.lvlkey[b] = GR_KEY_NONE;
+        csz = ck;
       }
     }
-    // compaction index (count) and chunk prefix (u64) in one pass
-    u64 flag = b >= 0 ? 1 : 0, pos;
+    u64 flag = b >= 0 ? 1 : 0, pos, tot;
     Scan(tmp).ExclusiveSum(flag, pos);
     __syncthreads();
-    u64 cpos;
-    Scan(tmp).ExclusiveSum(nch, cpos);
+    Scan(tmp).ExclusiveSum(csz, tot);
     __syncthreads();
-    if (b >= 0) {
-      nxt[s_cnt + (int)pos] = b;
-      ws.chunk_base[s_cnt + (int)pos] = s_carry + cpos;
-    }
+    if (b >= 0) nxt[s_cnt + (int)pos] = b;
     __syncthreads();
-    // last thread publishes the running totals
     if (t == FT - 1) {
       s_cnt += (int)(pos + flag);
-      s_carry += cpos + nch;
+      s_carry += tot + csz;  // candidates of level k+1 (saturation is harmless: only sizes L)
     }
     __syncthreads();
   }
+  // lane window L: about 4 windows per lane of the enumeration grid, a power
+  // of two in [256, 4096]
+  u64 L = s_carry / ((u64)enum_lanes * 4);
+  L = L < 256 ? 256 : (L > 4096 ? 4096 : L);
+  L = 1ull << (63 - __clzll((long long)L));
+  const u64 CH = L * NT;
+  const int nact = s_cnt;
+  __syncthreads();
+  if (t == 0) s_carry = 0;
+  __syncthreads();
+  for (int base = 0; base < nact; base += FT) {
+    const int i = base + t;
+    u64 nch = 0;
+    if (i < nact) nch = (binom(ws.meff[nxt[i]], k + 1) + CH - 1) / CH;
+    u64 cpos;
+    Scan(tmp).ExclusiveSum(nch, cpos);
+    __syncthreads();
+    if (i < nact) ws.chunk_base[i] = s_carry + cpos;
+    __syncthreads();
+    if (t == FT - 1) s_carry += cpos + nch;
+    __syncthreads();
+  }
   if (t == 0) {
-    ws.chunk_base[s_cnt] = s_carry;
-    ws.ctrl->n_active = s_cnt;
+    ws.chunk_base[nact] = s_carry;
+    ws.ctrl->n_active = nact;
     ws.ctrl->total_chunks = s_carry;
     ws.ctrl->next_chunk = 0;
+    ws.ctrl->lane_cands = fixed_lane ? fixed_lane : L;
   }
 }
 
@@ -836,14 +853,18 @@ int enum_grid() {
   return g_enum_grid;
 }
 
-u64 lane_cands() {
+u64 lane_cands_raw() {
   static u64 v = 0;
   if (!v) {
     const char *e = getenv("GR_LANE_CANDIDATES");
-    v = e ? strtoull(e, nullptr, 10) : 4096ull;
-    if (v < 1) v = 4096;
+    v = e ? strtoull(e, nullptr, 10) : 0ull;  // 0: adaptive per level
+    if (!e) v = ~0ull;
   }
   return v;
+}
+u64 lane_cands() {  // 0 = adaptive (GR_LANE_CANDIDATES overrides)
+  const u64 v = lane_cands_raw();
+  return v == ~0ull ? 0ull : v;
 }
 
 }  // namespace
@@ -893,7 +914,7 @@ extern "C" int gr_exact_prepare(const gr_batch *in, int which, gr_result *out, v
   }
   GR_LAUNCH("pack_kernel", (cudaStream_t)s, pack_kernel<<<in->B, PT, smem, st>>>(in_of(in, which), out_of(out), w, which));
   GR_LAUNCH("finish_kernel", (cudaStream_t)s, finish_kernel<<<1, FT, 0, st>>>(in_of(in, which), out_of(out), w, which, 0,
-                                   (in->flags & GR_FLAG_EXHAUSTIVE) ? 1 : 0));
+                                   (in->flags & GR_FLAG_EXHAUSTIVE) ? 1 : 0, enum_grid() * NT, lane_cands()));
   if (n_active) {
     int *h = pinned_i32();
     if (!h) { gr_set_error("cudaMallocHost failed"); return GR_ECUDA; }
@@ -947,12 +968,14 @@ extern "C" int gr_exact_finish(const gr_batch *in, int which, int k, gr_result *
   WS w = ws_of(in, ws);
   cudaStream_t st = (cudaStream_t)s;
   GR_LAUNCH("finish_kernel", (cudaStream_t)s, finish_kernel<<<1, FT, 0, st>>>(in_of(in, which), out_of(out), w, which, k,
-                                   (in->flags & GR_FLAG_EXHAUSTIVE) ? 1 : 0));
-  int *h = pinned_i32();
-  if (!h) { gr_set_error("cudaMallocHost failed"); return GR_ECUDA; }
-  GR_CUDA(cudaMemcpyAsync(h, &w.ctrl->n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
-  GR_CUDA(cudaStreamSynchronize(st));
-  if (n_active) *n_active = *h;
+                                   (in->flags & GR_FLAG_EXHAUSTIVE) ? 1 : 0, enum_grid() * NT, lane_cands()));
+  if (n_active) {
+    int *h = pinned_i32();
+    if (!h) { gr_set_error("cudaMallocHost failed"); return GR_ECUDA; }
+    GR_CUDA(cudaMemcpyAsync(h, &w.ctrl->n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
+    GR_CUDA(cudaStreamSynchronize(st));
+    *n_active = *h;
+  }
   return GR_OK;
 }
 
@@ -961,11 +984,17 @@ static int solve_exact(const gr_batch *in, gr_result *out, void *ws, size_t ws_b
   int32_t n = 0;  // level 0 is handled by the pack; instances active for level 1
   int rc = gr_exact_prepare(in, which, out, ws, ws_bytes, s, &n);
   if (rc) return rc;
-  for (int k = 1; n > 0 && k <= 64; k++) {
-    rc = gr_exact_level(in, which, k, 0, 1, ws, ws_bytes, s);
-    if (rc) return rc;
-    rc = gr_exact_finish(in, which, k, out, ws, ws_bytes, s, &n);
-    if (rc) return rc;
+  // levels are queued SPEC at a time and n_active is read back once per batch;
+  // levels past the last active one are no-ops (empty active list)
+  const int SPEC = 4;
+  for (int k = 1; n > 0 && k <= 64;) {
+    for (int i = 0; i < SPEC && k <= 64; i++, k++) {
+      rc = gr_exact_level(in, which, k, 0, 1, ws, ws_bytes, s);
+      if (rc) return rc;
+      const bool last = i == SPEC - 1 || k == 64;
+      rc = gr_exact_finish(in, which, k, out, ws, ws_bytes, s, last ? &n : nullptr);
+      if (rc) return rc;
+    }
   }
   return GR_OK;
 }
