@@ -39,7 +39,7 @@ sys.path.insert(0, ROOT)
 METRIC = "candidate assignments checked/sec and instances solved/sec at 1/2/4/8 B200"
 L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
 ALU_LANES_PER_SM_CLK = 64   # LOP3/IADD3/ISETP: alu pipe, 16 lanes/clk per SMSP
-TEST_OPS = {32: 2, 64: 4}   # SASS ALU ops per clause test: (T & P) == 0 ? A &= P (per 32-bit word: 2)
+TEST_OPS = {32: 3, 64: 4}   # SASS ALU ops per clause test: LOP3.P (U & P) + 2 predicated LOP3 (F &= H); u64 lanes +1
 
 
 def parse():

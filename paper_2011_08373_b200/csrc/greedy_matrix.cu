@@ -30,10 +30,12 @@ constexpr int RB = 64;             // rows per work item
 constexpr int TPI = 16;            // tiles per work item
 constexpr int NCW = 8;             // consumer warps
 constexpr int ROWS_PER_STAGE = 8;  // one row per consumer warp
-constexpr int NSTAGE = 5;
+#ifndef GR_NSTAGE
+#define GR_NSTAGE 5
+#endif
+constexpr int NSTAGE = GR_NSTAGE;
 constexpr int CT = 32 * (NCW + 1); // count-kernel CTA size
 constexpr size_t STAGE_BYTES = (size_t)ROWS_PER_STAGE * TW * 8;
-constexpr size_t COUNT_SMEM = NSTAGE * STAGE_BYTES + 2 * NSTAGE * 8 + 64;
 
 struct GCtrl {
   int done;
@@ -117,11 +119,21 @@ struct CountParams {
 };
 
 // ---- the streaming count pass ------------------------------------------------
+// Shared memory: NSTAGE row-segment stages (8 rows x 4 KB) and two tile-header
+// slots (the U_{t-1} tile and the R[v*_{t-1}] tile, 4 KB each), all filled by
+// the producer lane with cp.async.bulk and completed on mbarriers.
+constexpr size_t TILE_BYTES = (size_t)TW * 8;
+constexpr size_t HDR_BYTES = 2 * TILE_BYTES;
+constexpr size_t COUNT_SMEM_V2 = NSTAGE * STAGE_BYTES + 2 * HDR_BYTES + (2 * NSTAGE + 4) * 8 + 64;
+
 __global__ void __launch_bounds__(CT, 1) count_kernel(CountParams p) {
   extern __shared__ __align__(128) unsigned char smraw[];
   u64 *stage = (u64 *)smraw;
-  u64 *full = (u64 *)(smraw + NSTAGE * STAGE_BYTES);
+  u64 *hdr = (u64 *)(smraw + NSTAGE * STAGE_BYTES);   // [2][U tile | R tile]
+  u64 *full = (u64 *)(smraw + NSTAGE * STAGE_BYTES + 2 * HDR_BYTES);
   u64 *empty = full + NSTAGE;
+  u64 *hfull = empty + NSTAGE;   // [2]
+  u64 *hempty = hfull + 2;       // [2]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int vprev = -1;
   if (p.ctrl) {
@@ -133,6 +145,10 @@ __global__ void __launch_bounds__(CT, 1) count_kernel(CountParams p) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], NCW);
     }
+    for (int s = 0; s < 2; s++) {
+      mbar_init(&hfull[s], 1);
+      mbar_init(&hempty[s], NCW);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -140,15 +156,23 @@ __global__ void __launch_bounds__(CT, 1) count_kernel(CountParams p) {
   const int ntr = (p.ntiles + TPI - 1) / TPI;
   const int nitems = nrb * ntr;
   if (warp == NCW) {
-    // ---------------- producer warp: bulk copies into the ring -------------
+    // ---------------- producer lane: bulk copies into the rings -----------
     if (lane == 0) {
-      u32 it = 0;
+      u32 it = 0, ht = 0;
       for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
         const int rb = item % nrb, tr = item / nrb;
         const int r0 = rb * RB;
         const int t0 = tr * TPI, t1 = min(t0 + TPI, p.ntiles);
-        for (int ti = t0; ti < t1; ti++) {
+        for (int ti = t0; ti < t1; ti++, ht++) {
           const int tw = (int)min((int64_t)TW, p.ld - (int64_t)ti * TW);
+          // tile header: U_{t-1} tile (+ R[v*] tile when marking)
+          const int hs = ht & 1;
+          mbar_wait(&hempty[hs], ((ht >> 1) & 1) ^ 1);
+          u64 *h = hdr + (size_t)hs * (HDR_BYTES / 8);
+          mbar_expect_tx(&hfull[hs], (u32)((vprev >= 0 ? 2 : 1) * tw * 8));
+          bulk_g2s(h, p.U_in + (size_t)ti * TW, (u32)(tw * 8), &hfull[hs]);
+          if (vprev >= 0)
+            bulk_g2s(h + TW, p.R + (size_t)vprev * p.ld + (size_t)ti * TW, (u32)(tw * 8), &hfull[hs]);
           for (int g = 0; g < RB / ROWS_PER_STAGE; g++, it++) {
             const int s = it % NSTAGE;
             mbar_wait(&empty[s], ((it / NSTAGE) & 1) ^ 1);
@@ -167,7 +191,7 @@ __global__ void __launch_bounds__(CT, 1) count_kernel(CountParams p) {
     return;
   }
   // ---------------- consumer warps ------------------------------------------
-  u32 it = 0;
+  u32 it = 0, ht = 0;
   for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
     const int rb = item % nrb, tr = item / nrb;
     const int r0 = rb * RB;
@@ -175,27 +199,32 @@ __global__ void __launch_bounds__(CT, 1) count_kernel(CountParams p) {
     u32 acc[RB / ROWS_PER_STAGE];
 #pragma unroll
     for (int g = 0; g < RB / ROWS_PER_STAGE; g++) acc[g] = 0;
-    for (int ti = t0; ti < t1; ti++) {
+    for (int ti = t0; ti < t1; ti++, ht++) {
       const int tw = (int)min((int64_t)TW, p.ld - (int64_t)ti * TW);
       const int nstep = tw / 64;
-      // U fragment of this lane: words ti*TW + s*64 + 2*lane + {0,1}
+      // U_t fragment of this lane (words s*64 + 2*lane + {0,1} of the tile)
+      const int hs = ht & 1;
+      mbar_wait(&hfull[hs], (ht >> 1) & 1);
+      const u64 *h = hdr + (size_t)hs * (HDR_BYTES / 8);
       ulonglong2 u[TW / 64];
 #pragma unroll
       for (int s = 0; s < TW / 64; s++) {
         if (s < nstep) {
-          const size_t wo = (size_t)ti * TW + (size_t)s * 64 + 2 * lane;
-          ulonglong2 x = *(const ulonglong2 *)(p.U_in + wo);
+          ulonglong2 x = *(const ulonglong2 *)(h + s * 64 + 2 * lane);
           if (vprev >= 0) {
-            const ulonglong2 r = *(const ulonglong2 *)(p.R + (size_t)vprev * p.ld + wo);
+            const ulonglong2 r = *(const ulonglong2 *)(h + TW + s * 64 + 2 * lane);
             x.x &= ~r.x;
             x.y &= ~r.y;
           }
           u[s] = x;
-          if (p.U_out && rb == 0 && warp == 0) *(ulonglong2 *)(p.U_out + wo) = x;
+          if (p.U_out && rb == 0 && warp == 0)
+            *(ulonglong2 *)(p.U_out + (size_t)ti * TW + (size_t)s * 64 + 2 * lane) = x;
         } else {
           u[s] = make_ulonglong2(0, 0);
         }
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&hempty[hs]);
 #pragma unroll
       for (int g = 0; g < RB / ROWS_PER_STAGE; g++, it++) {
         const int s = it % NSTAGE;
@@ -400,7 +429,7 @@ int count_grid() {
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaFuncSetAttribute(count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)COUNT_SMEM);
+  cudaFuncSetAttribute(count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)COUNT_SMEM_V2);
   g_count_grid = sms;
   return g_count_grid;
 }
@@ -478,7 +507,7 @@ extern "C" int gr_greedy_count_shard(const gr_bitmatrix *shard, const uint64_t *
   GR_CUDA(cudaMemsetAsync(d_counts, 0, sizeof(u32) * shard->m, st));
   CountParams p{shard->bits, shard->ld, shard->m, (int)((shard->ld + TW - 1) / TW), d_U, nullptr,
                 d_counts, nullptr, 0};
-  GR_LAUNCH("count_kernel", (cudaStream_t)s, count_kernel<<<count_grid(), CT, COUNT_SMEM, st>>>(p));
+  GR_LAUNCH("count_kernel", (cudaStream_t)s, count_kernel<<<count_grid(), CT, COUNT_SMEM_V2, st>>>(p));
   return GR_OK;
 }
 
@@ -513,7 +542,7 @@ extern "C" int gr_mhs_greedy_matrix(const gr_bitmatrix *in, uint64_t *assign, in
     for (int j = 0; j < CHUNK; j++, t++) {
       CountParams p{in->bits, ld, in->m, ntiles, U + (size_t)(t & 1) * ld,
                     U + (size_t)((t & 1) ^ 1) * ld, counts, ctrl, 1};
-      GR_LAUNCH("count_kernel", (cudaStream_t)s, count_kernel<<<grid, CT, COUNT_SMEM, st>>>(p));
+      GR_LAUNCH("count_kernel", (cudaStream_t)s, count_kernel<<<grid, CT, COUNT_SMEM_V2, st>>>(p));
       GR_LAUNCH("argmax_kernel", (cudaStream_t)s, argmax_kernel<<<1, AT, 0, st>>>(counts, in->m, ctrl, wpicks));
     }
     GR_CUDA(cudaMemcpyAsync(h, ctrl, sizeof(GCtrl), cudaMemcpyDeviceToHost, st));
