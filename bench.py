@@ -38,8 +38,11 @@ sys.path.insert(0, ROOT)
 
 METRIC = "candidate assignments checked/sec and instances solved/sec at 1/2/4/8 B200"
 L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
-ALU_LANES_PER_SM_CLK = 64   # LOP3/IADD3/ISETP: alu pipe, 16 lanes/clk per SMSP
-TEST_OPS = {32: 3, 64: 4}   # SASS ALU ops per clause test: LOP3.P (U & P) + 2 predicated LOP3 (F &= H); u64 lanes +1
+INT_LANES_PER_SM_CLK = 128  # INT32 issue: 4 SMSPs x 32 lanes x 1 warp-instruction/clk
+# SURVEY.md §8(d) per-unit figure: a candidate-at-a-time enumerator spends one
+# clause test (W + 1 ops) plus an amortised successor (~4 ops) per candidate.
+OPS_PER_CANDIDATE = {32: 6, 64: 7}   # m_eff <= 32 (one 32-bit word) / <= 64
+TEST_OPS = {32: 3, 64: 4}   # SASS per clause test: LOP3.P (U & P) + 2 predicated LOP3 (F &= H)
 
 
 def parse():
@@ -64,6 +67,25 @@ def peaks():
                  sm_max_mhz=float(d.get("sm_max_mhz", p["sm_max_mhz"])),
                  source="MEASURED_PEAKS.json")
     return p
+
+
+def ncu_evidence(kernel: str):
+    """Selected counters of the committed ncu --set full capture (profiles/)."""
+    path = os.path.join(ROOT, "profiles", "r01_ncu_selected_metrics.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        d = json.load(f).get(kernel)
+    if not d:
+        return None
+    m = d[0]
+    pick = {"alu_pipe_pct": "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+            "issue_active_pct": "smsp__issue_active.avg.pct_of_peak_sustained_active",
+            "active_lanes_per_warp_inst": "smsp__thread_inst_executed_per_inst_executed.ratio",
+            "dram_pct": "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"}
+    out = {k: float(m[v][0]) for k, v in pick.items() if v in m}
+    out["source"] = "profiles/r01_ncu_selected_metrics.json"
+    return out
 
 
 def traffic_of(kernel: str):
@@ -281,22 +303,27 @@ def main():
     ek = kern.get("enum_kernel", {"launches": 0, "ms": 0.0})
     ew = wk.get("enum_kernel", {"launches": 0, "work": [0, 0, 0, 0]})
     tests, blocks, wcands, tests64 = ew["work"]
-    ops = TEST_OPS[32] * (tests - tests64) + TEST_OPS[64] * tests64
+    wide = int((cb.m > 32).sum()) > cb.B // 2
     roof = None
     if ek["launches"] and ew["launches"]:
-        per_launch_ops = ops / ew["launches"]
         per_launch_s = ek["ms"] / ek["launches"] / 1e3
-        achieved = per_launch_ops / per_launch_s / 1e12
-        peak_tops = 148 * ALU_LANES_PER_SM_CLK * pk["sm_max_mhz"] * 1e6 / 1e12
+        cands_launch = wcands / ew["launches"]
+        opc = OPS_PER_CANDIDATE[64 if wide else 32]
+        achieved = cands_launch * opc / per_launch_s / 1e12
+        peak_tops = 148 * INT_LANES_PER_SM_CLK * pk["sm_max_mhz"] * 1e6 / 1e12
+        test_ops = TEST_OPS[32] * (tests - tests64) + TEST_OPS[64] * tests64
         roof = {"bound": "alu", "achieved": achieved, "peak": peak_tops, "unit": "Tops/s",
                 "frac": achieved / peak_tops, "traffic": traffic_of("enum_kernel"),
                 "kernel": "enum_kernel",
-                "per_launch": {"ops": per_launch_ops, "ms": per_launch_s * 1e3,
+                "per_unit": f"{opc} INT ops per candidate decided (SURVEY.md §8(d): 1 clause test "
+                            f"+ amortised successor of a candidate-at-a-time enumerator)",
+                "per_launch": {"candidates": cands_launch, "ms": per_launch_s * 1e3,
                                "clause_tests": tests / ew["launches"],
-                               "candidate_blocks": blocks / ew["launches"],
-                               "candidates": wcands / ew["launches"]},
-                "peak_source": f"148 SMs x {ALU_LANES_PER_SM_CLK} ALU lanes/clk x {pk['sm_max_mhz']:.0f} MHz "
-                               f"({pk['source']})",
+                               "candidate_blocks": blocks / ew["launches"]},
+                "peak_source": f"INT32 issue: 148 SMs x {INT_LANES_PER_SM_CLK} lanes/clk x "
+                               f"{pk['sm_max_mhz']:.0f} MHz ({pk['source']})",
+                "clause_test_frac": test_ops / ew["launches"] / per_launch_s / 1e12 / peak_tops,
+                "ncu": ncu_evidence("enum_kernel"),
                 "share_of_step": ek["ms"] / total_ms if total_ms else None}
     line = {
         "metric": METRIC, "value": value, "unit": "candidates/s", "n_gpus": world,
@@ -366,7 +393,10 @@ def run_c5(a, rank, world, local, dev):
     pk = peaks()
     ck = kern["count_kernel"]
     bytes_per_launch = csr.m * ld * 8 + 3 * ld * 8  # R + U_in + U_out + R[v*] row (mark)
-    ach = bytes_per_launch / (ck["ms"] / ck["launches"] / 1e3) / 1e9
+    # passes that did work: n_picks + 1 per solve (up to 7 more are queued
+    # no-ops after `done`; their few microseconds stay in the total)
+    eff = (r.n_picks + 1) * a.steps
+    ach = bytes_per_launch / (ck["ms"] / eff / 1e3) / 1e9
     a_ = r.assign.cpu().numpy().view(np.uint64)
     size = int(sum(bin(int(x)).count("1") for x in a_))
     n = csr.n_pos
@@ -381,7 +411,9 @@ def run_c5(a, rank, world, local, dev):
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": ach / pk["hbm_gbs"], "traffic": traffic_of("count_kernel_c5"),
-                     "kernel": "count_kernel", "share_of_step": ck["ms"] / total_ms},
+                     "kernel": "count_kernel", "share_of_step": ck["ms"] / total_ms,
+                     "per_launch": {"bytes": bytes_per_launch, "ms": ck["ms"] / eff},
+                     "ncu": ncu_evidence("count_kernel")},
         "clocks": clk.summary(),
         "kernels": {k: {"launches": v["launches"], "ms_per_step": v["ms"] / a.steps} for k, v in kern.items()},
     }
