@@ -793,6 +793,7 @@ __global__ void __launch_bounds__(FT) finish_kernel(In in, Out out, WS ws, int w
   u64 L = s_carry / ((u64)enum_lanes * 4);
   L = L < 256 ? 256 : (L > 4096 ? 4096 : L);
   L = 1ull << (63 - __clzll((long long)L));
+  if (fixed_lane) L = fixed_lane;  // GR_LANE_CANDIDATES override
   const u64 CH = L * NT;
   const int nact = s_cnt;
   __syncthreads();
@@ -815,7 +816,7 @@ __global__ void __launch_bounds__(FT) finish_kernel(In in, Out out, WS ws, int w
     ws.ctrl->n_active = nact;
     ws.ctrl->total_chunks = s_carry;
     ws.ctrl->next_chunk = 0;
-    ws.ctrl->lane_cands = fixed_lane ? fixed_lane : L;
+    ws.ctrl->lane_cands = L;
   }
 }
 
