@@ -692,7 +692,7 @@ __device__ __forceinline__ int bitlen(u64 x) { return x ? 64 - __clzll((long lon
 
 __global__ void __launch_bounds__(FT) finish_kernel(In in, Out out, WS ws, int which, int k,
                                                     int exhaustive, int enum_lanes,
-                                                    u64 fixed_lane) {
+                                                    u64 fixed_lane, int windows_per_lane) {
   typedef cub::BlockScan<u64, FT> Scan;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ u64 s_carry;
@@ -790,7 +790,7 @@ __global__ void __launch_bounds__(FT) finish_kernel(In in, Out out, WS ws, int w
   }
   // lane window L: about 4 windows per lane of the enumeration grid, a power
   // of two in [256, 4096]
-  u64 L = s_carry / ((u64)enum_lanes * 4);
+  u64 L = s_carry / ((u64)enum_lanes * (u64)windows_per_lane);
   L = L < 256 ? 256 : (L > 4096 ? 4096 : L);
   L = 1ull << (63 - __clzll((long long)L));
   if (fixed_lane) L = fixed_lane;  // GR_LANE_CANDIDATES override
@@ -863,6 +863,15 @@ u64 lane_cands_raw() {
   }
   return v;
 }
+int windows_per_lane() {  // adaptive lane window: windows per lane per level
+  static int v = 0;
+  if (!v) {
+    const char *e = getenv("GR_WINDOWS_PER_LANE");
+    v = e ? atoi(e) : 4;
+    if (v < 1) v = 4;
+  }
+  return v;
+}
 u64 lane_cands() {  // 0 = adaptive (GR_LANE_CANDIDATES overrides)
   const u64 v = lane_cands_raw();
   return v == ~0ull ? 0ull : v;
@@ -915,7 +924,7 @@ extern "C" int gr_exact_prepare(const gr_batch *in, int which, gr_result *out, v
   }
   GR_LAUNCH("pack_kernel", (cudaStream_t)s, pack_kernel<<<in->B, PT, smem, st>>>(in_of(in, which), out_of(out), w, which));
   GR_LAUNCH("finish_kernel", (cudaStream_t)s, finish_kernel<<<1, FT, 0, st>>>(in_of(in, which), out_of(out), w, which, 0,
-                                   (in->flags & GR_FLAG_EXHAUSTIVE) ? 1 : 0, enum_grid() * NT, lane_cands()));
+                                   (in->flags & GR_FLAG_EXHAUSTIVE) ? 1 : 0, enum_grid() * NT, lane_cands(), windows_per_lane()));
   if (n_active) {
     int *h = pinned_i32();
     if (!h) { gr_set_error("cudaMallocHost failed"); return GR_ECUDA; }
@@ -969,7 +978,7 @@ extern "C" int gr_exact_finish(const gr_batch *in, int which, int k, gr_result *
   WS w = ws_of(in, ws);
   cudaStream_t st = (cudaStream_t)s;
   GR_LAUNCH("finish_kernel", (cudaStream_t)s, finish_kernel<<<1, FT, 0, st>>>(in_of(in, which), out_of(out), w, which, k,
-                                   (in->flags & GR_FLAG_EXHAUSTIVE) ? 1 : 0, enum_grid() * NT, lane_cands()));
+                                   (in->flags & GR_FLAG_EXHAUSTIVE) ? 1 : 0, enum_grid() * NT, lane_cands(), windows_per_lane()));
   if (n_active) {
     int *h = pinned_i32();
     if (!h) { gr_set_error("cudaMallocHost failed"); return GR_ECUDA; }
