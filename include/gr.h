@@ -133,6 +133,20 @@ int gr_mhs_exact(const gr_batch *in, gr_result *out, void *ws, size_t ws_bytes, 
  * cost = |S|; decided is not written. */
 int gr_mhs_greedy(const gr_batch *in, gr_result *out, void *ws, size_t ws_bytes, gr_stream_t s);
 
+/* ---- the composite Solve (Alg. 1 line `solve`) -------------
+ * strategy GR_STRATEGY_MAXSAT: the (weighted) partial-MaxSAT optimum
+ *   (= gr_solve_pms).
+ * strategy GR_STRATEGY_MHS (the paper's default): the greedy mhs of phi+
+ *   (= gr_mhs_greedy); every instance whose greedy set breaks phi- falls back
+ *   to the MaxSAT solver and gets the gr_solve_pms result.
+ *   With weights, a greedy answer's cost is its weight.
+ * fell_back (device [B] int32, may be NULL): 1 where the fallback ran.
+ * decided is 0 for instances answered by the greedy.  Workspace:
+ * gr_workspace_bytes(in, 0). */
+enum { GR_STRATEGY_MHS = 0, GR_STRATEGY_MAXSAT = 1 };
+int gr_solve(const gr_batch *in, int strategy, gr_result *out, int32_t *fell_back, void *ws,
+             size_t ws_bytes, gr_stream_t s);
+
 /* ---- sharded exact solving (the multi-GPU driver owns the collective) ----
  * gr_solve_pms / gr_mhs_exact are exactly:
  *     gr_exact_prepare(in, which, out, ..., &n);

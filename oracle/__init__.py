@@ -177,8 +177,10 @@ class BatchResult:
 
 
 def batch(which: str, cb, reduce: int = 1, weighted: bool = True) -> BatchResult:
-    """Solve every instance of a synth.ClauseBatch: which in {pms, mhs, greedy}."""
-    code = {"pms": 0, "mhs": 1, "greedy": 2}[which]
+    """Solve every instance of a synth.ClauseBatch: which in {pms, mhs, greedy, solve}
+    (solve = composite mhs strategy with MaxSAT fallback; its ``decided`` holds
+    the fallback flag)."""
+    code = {"pms": 0, "mhs": 1, "greedy": 2, "solve": 3}[which]
     W = cb.W
     B = cb.B
     assign = np.zeros((B, W), np.uint64)
@@ -191,7 +193,7 @@ def batch(which: str, cb, reduce: int = 1, weighted: bool = True) -> BatchResult
     masks = np.ascontiguousarray(cb.masks, np.uint64)
     w = None
     ws = 0
-    if weighted and cb.w is not None and which == "pms":
+    if weighted and cb.w is not None and which in ("pms", "solve"):
         w = np.ascontiguousarray(cb.w, np.uint32)
         ws = w.shape[1]
     rc = lib().or_batch(code, B, W, _ptr(m), _ptr(off), _ptr(npos), _ptr(masks), _ptr(w), ws,

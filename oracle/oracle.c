@@ -393,8 +393,33 @@ int or_greedy_masks(int m, int W, int n_pos, int n_neg, const uint64_t *masks,
   return rc;
 }
 
+/* The composite Solve: mhs strategy = greedy over phi+; if
+ * the greedy set breaks phi- ("results in unsatisfiability"), fall back to
+ * the MaxSAT solver (or_pms).  cost: weight (or size) of the returned set. */
+int or_solve_mhs(int m, int W, int n_pos, int n_neg, const uint64_t *masks, const uint32_t *w,
+                 int reduce, uint64_t *assign, uint64_t *cost, int32_t *status, uint64_t *decided,
+                 int32_t *fell_back) {
+  int32_t *pk = malloc(sizeof(int32_t) * (m + 1)), nu;
+  int rc = or_greedy_masks(m, W, n_pos, n_neg, masks, assign, pk, &nu, status);
+  free(pk);
+  *decided = 0;
+  *fell_back = 0;
+  if (rc != OR_OK) return rc;
+  if (*status == OR_SAT_NEG_VIOLATED) {
+    *fell_back = 1;
+    return or_pms(m, W, n_pos, n_neg, masks, w, reduce, assign, cost, status, decided);
+  }
+  if (*status != OR_SAT) { *cost = UINT64_MAX; return OR_OK; }
+  uint64_t c = 0;
+  for (int t = 0; t < W; t++) c += cost_of(assign[t], w ? w + 64 * t : NULL);
+  *cost = c;
+  return OR_OK;
+}
+
 /* ---- batch drivers: independent instances in parallel ------------------ */
-/* which: 0 = PMS/WPMS (w may be NULL), 1 = MHS (weights ignored), 2 = greedy */
+/* which: 0 = PMS/WPMS (w may be NULL), 1 = MHS (weights ignored), 2 = greedy,
+ * 3 = composite Solve, mhs strategy with MaxSAT fallback (decided[b] = 1 where
+ * the fallback ran, else 0 -- the fallback flag, not a candidate count) */
 int or_batch(int which, int B, int W, const int32_t *m, const int64_t *off, const int32_t *n_pos,
              const uint64_t *masks, const uint32_t *w, int wstride, int reduce,
              uint64_t *assign /*[B][W]*/, uint64_t *cost, int32_t *status, uint64_t *decided) {
@@ -409,6 +434,11 @@ int or_batch(int which, int B, int W, const int32_t *m, const int64_t *off, cons
     for (int t = 0; t < W; t++) a[t] = 0;
     if (which == 0) rc = or_pms(m[b], W, np, nn, mk, w ? w + (size_t)b * wstride : NULL, reduce, a, &c, &s, &d);
     else if (which == 1) rc = or_mhs(m[b], W, np, nn, mk, reduce, a, &c, &s, &d);
+    else if (which == 3) {
+      int32_t fb = 0;
+      rc = or_solve_mhs(m[b], W, np, nn, mk, w ? w + (size_t)b * wstride : NULL, reduce, a, &c, &s, &d, &fb);
+      d = (uint64_t)fb;
+    }
     else {
       int32_t *pk = malloc(sizeof(int32_t) * (m[b] + 1)); int32_t nu;
       rc = or_greedy_masks(m[b], W, np, nn, mk, assign + (size_t)b * W, pk, &nu, &s);

@@ -3,6 +3,7 @@
 Public API (thin marshalling over libgrsolve.so, include/gr.h):
     DeviceBatch, DeviceResult           device-resident clause batches / results
     solve_pms, mhs_exact, mhs_greedy    the three solvers
+    solve                               the composite Solve with the MaxSAT fallback
     ExactSession                        prepare / level / finish for sharded runs
     pack_bitmatrix, mhs_greedy_matrix   greedy at scale over a bit matrix
     greedy_count_shard                  shard hook for the multi-GPU greedy
@@ -12,5 +13,6 @@ from ._native import (  # noqa: F401
     GR_BADINPUT, GR_FLAG_EXHAUSTIVE, GR_SAT, GR_SAT_NEG_VIOLATED, GR_UNSAT, GR_UNSUPPORTED, MHS,
     PMS, GREEDY, DeviceBatch, DeviceBitMatrix, DeviceResult, ExactSession, GrError,
     bitmatrix_ld, greedy_count_shard, lib, mhs_exact, mhs_greedy, mhs_greedy_matrix,
-    pack_bitmatrix, solve_pms, version, launch_count, profiler, Profiler,
+    pack_bitmatrix, solve_pms, version, launch_count, profiler, Profiler, solve,
+    GR_STRATEGY_MHS, GR_STRATEGY_MAXSAT,
 )

@@ -27,8 +27,9 @@ EXPORTED = [
     "gr_exact_level", "gr_exact_level_keys", "gr_exact_finish", "gr_bitmatrix_ld",
     "gr_pack_varmajor", "gr_pack_clausemajor", "gr_greedy_matrix_workspace_bytes",
     "gr_mhs_greedy_matrix", "gr_greedy_count_shard", "gr_last_error", "gr_version",
-    "gr_profile", "gr_profile_read", "gr_launch_count",
+    "gr_profile", "gr_profile_read", "gr_launch_count", "gr_solve",
 ]
+GR_STRATEGY_MHS, GR_STRATEGY_MAXSAT = 0, 1
 
 
 class GrBatch(C.Structure):
@@ -73,6 +74,8 @@ def lib():
             f.argtypes = [vp, vp, vp, sz, vp]
             f.restype = C.c_int
         L.gr_exact_prepare.argtypes = [vp, C.c_int, vp, vp, sz, vp, vp]
+        L.gr_solve.argtypes = [vp, C.c_int, vp, vp, vp, sz, vp]
+        L.gr_solve.restype = C.c_int
         L.gr_profile.argtypes = [C.c_int]
         L.gr_profile.restype = C.c_int
         L.gr_profile_read.argtypes = [vp, C.c_int]
@@ -248,6 +251,24 @@ def mhs_exact(db: DeviceBatch, out: Optional[DeviceResult] = None, stream=None) 
 def mhs_greedy(db: DeviceBatch, out: Optional[DeviceResult] = None, stream=None) -> DeviceResult:
     """(c) greedy mhs of phi+ (gr_mhs_greedy)."""
     return _solve("gr_mhs_greedy", GREEDY, db, out, stream)
+
+
+def solve(db: DeviceBatch, strategy: int = GR_STRATEGY_MHS, out: Optional[DeviceResult] = None,
+          fell_back=None, stream=None) -> DeviceResult:
+    """The composite Solve (gr_solve): mhs strategy with MaxSAT fallback, or MaxSAT."""
+    torch = _torch()
+    L = lib()
+    b = db.struct(True)
+    nbytes = L.gr_workspace_bytes(C.byref(b), PMS)
+    if nbytes == 0:
+        raise GrError("gr_workspace_bytes rejected the batch")
+    ws = workspace(nbytes, db.m.device, tag="exact0")
+    if out is None:
+        out = DeviceResult.empty(db.B, db.W, db.m.device)
+    r = out.struct()
+    _check(L.gr_solve(C.byref(b), strategy, C.byref(r), _ptr(fell_back), _ptr(ws), ws.numel(),
+                      _stream(stream)), "gr_solve")
+    return out
 
 
 # ---- sharded exact solving ---------------------------------------------------

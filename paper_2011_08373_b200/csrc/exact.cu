@@ -126,15 +126,20 @@ struct In {
   const int32_t *n_pos;
   const uint64_t *masks;
   const uint32_t *w;
+  const int32_t *sel;  // optional: solve only instances with sel[b] == sel_val (others untouched)
+  int sel_val;
 };
 struct Out {
   uint64_t *assign, *cost, *decided;
   int32_t *status;
 };
 
+thread_local const int32_t *t_sel = nullptr;  // set by gr_solve around its fallback solve
+thread_local int t_sel_val = 0;
+
 In in_of(const gr_batch *b, int which) {
   In r{b->B, b->W, b->max_clauses, b->wstride, b->m, b->off, b->n_pos, b->masks,
-       which == 0 ? b->w : nullptr};
+       which == 0 ? b->w : nullptr, t_sel, t_sel_val};
   return r;
 }
 Out out_of(const gr_result *o) { return Out{o->assign, o->cost, o->decided, o->status}; }
@@ -176,6 +181,10 @@ __global__ void __launch_bounds__(PT) pack_kernel(In in, Out out, WS ws, int whi
   __shared__ u32 s_w[64];
   __shared__ u64 s_ws[64];
   const int b = blockIdx.x, t = threadIdx.x;
+  if (in.sel && in.sel[b] != in.sel_val) {  // not selected: leave its results alone
+    if (t == 0) ws.done[b] = 1;
+    return;
+  }
   u64 *R = sm;
   int *info = (int *)(sm + in.max_clauses);
   unsigned char *keep0 = (unsigned char *)(info + in.max_clauses);
@@ -1007,6 +1016,15 @@ static int solve_exact(const gr_batch *in, gr_result *out, void *ws, size_t ws_b
     }
   }
   return GR_OK;
+}
+
+int gr_exact_solve_selected(const gr_batch *in, gr_result *out, void *ws, size_t ws_bytes,
+                            gr_stream_t s, const int32_t *sel, int sel_val) {
+  t_sel = sel;
+  t_sel_val = sel_val;
+  const int rc = solve_exact(in, out, ws, ws_bytes, s, 0);
+  t_sel = nullptr;
+  return rc;
 }
 
 extern "C" int gr_solve_pms(const gr_batch *in, gr_result *out, void *ws, size_t ws_bytes,

@@ -423,3 +423,33 @@ def test_c3_structure():
     assert all(int(x) in {int(v) for v in mk[:npos, 0]} for x in gm)  # group clauses present
     hm = sum(1 << v for v in H)
     assert oracle.feasible(hm, npos, mk)
+
+
+# ------------------------------------------------------- composite Solve (f1)
+def test_composite_solve_paper_fallback():
+    """PAPER.md:26 / SPEC.md:411 (acceptance #6): the mhs strategy on the paper's
+    example triggers the MaxSAT fallback and returns 3 true variables."""
+    g = load_golden("paper_example.txt")
+    cb = synth.batch_from_lists([(g["m"], g["pos"], g["neg"])], W=1)
+    r = oracle.batch("solve", cb)
+    assert r.decided[0] == 1  # fell back
+    assert (r.status[0], r.cost[0]) == (SAT, 3)
+    assert synth.mask_to_vars(r.assign[0]) == [2, 3, 4]
+
+
+def test_composite_solve_properties():
+    """Fallback completeness (SPEC.md:281): Solve is UNSAT iff PMS is UNSAT;
+    without fallback the answer is the greedy set, with it the PMS optimum."""
+    rng = random.Random(21)
+    insts = []
+    for _ in range(200):
+        m = rng.randint(1, 10)
+        pos, neg, _ = rand_instance(rng, m, rng.randint(1, 12))
+        insts.append((m, pos, neg))
+    cb = synth.batch_from_lists(insts, W=1)
+    s, p, g = oracle.batch("solve", cb), oracle.batch("pms", cb), oracle.batch("greedy", cb)
+    assert ((s.status == UNSAT) == (p.status == UNSAT)).all()
+    fb = s.decided == 1
+    assert (fb == (g.status == NEGV)).all()
+    assert (s.assign[fb] == p.assign[fb]).all() and (s.assign[~fb] == g.assign[~fb]).all()
+    assert (s.status != NEGV).all()

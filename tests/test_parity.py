@@ -405,3 +405,21 @@ def test_greedy_count_shard_hook():
         for v in cls[c]:
             want[v] += 1
     assert (counts.cpu().numpy() == want).all()
+
+
+@pytest.mark.parametrize("weighted", [False, True])
+def test_composite_solve(weighted):
+    """gr_solve (mhs strategy with MaxSAT fallback) == oracle."""
+    cb = rand_batch(400 + weighted, 300, 14, 16, weighted=weighted)
+    db = gr.DeviceBatch.from_host(cb)
+    fb = torch.zeros(cb.B, dtype=torch.int32, device="cuda")
+    g = gr.solve(db, gr.GR_STRATEGY_MHS, fell_back=fb).to_host()
+    o = oracle.batch("solve", cb)
+    assert (g["status"] == o.status).all()
+    assert (g["assign"] == o.assign).all()
+    assert (g["cost"] == o.cost).all()
+    assert (fb.cpu().numpy() == o.decided.astype(np.int32)).all()
+    assert fb.sum().item() > 0  # the fallback path ran
+    m = gr.solve(db, gr.GR_STRATEGY_MAXSAT).to_host()
+    p = oracle.batch("pms", cb)
+    assert (m["status"] == p.status).all() and (m["assign"] == p.assign).all()
