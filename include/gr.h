@@ -182,6 +182,14 @@ typedef struct {
                              bits at columns >= n_pos must be 0 */
   int32_t n_neg;          /* host: number of negative clauses */
   const uint64_t *neg;    /* [n_neg][ceil(m/64)] negative clause masks (may be NULL if n_neg == 0) */
+  /* optional clause-major view of the same phi+ (the CSR given to
+   * gr_pack_varmajor): with it the greedy keeps exact counts incrementally
+   * (one 2 MiB row + the newly covered clauses' lists per pick, SURVEY
+   * §8(f) f3) instead of re-streaming the matrix each pick; picks identical.
+   * A clause must not list a variable twice.  NULL = recounting passes. */
+  const int64_t *pos_off; /* [n_pos+1] or NULL */
+  const void *pos_var;    /* [pos_off[n_pos]] int16 / int32 variable ids, or NULL */
+  int32_t var_bytes;      /* 2 or 4 when pos_var is given; m <= 50000 (shared histogram) */
 } gr_bitmatrix;
 
 /* Row stride (words) the library uses for n_pos clauses: a multiple of 64. */
@@ -189,9 +197,11 @@ int64_t gr_bitmatrix_ld(int64_t n_pos);
 
 /* Pack CSR variable lists into the variable-major bit matrix (clause packing
  * step a1).  off [n+1] int64, var [off[n]] int16 (var_bytes = 2) or int32
- * (var_bytes = 4), 0-based variable ids.  bits [m][ld] must be zeroed by the
- * caller.  *d_bad (device int32, may be NULL) is set to 1 if some id is outside
- * [0, m), to 2 if some clause is empty (phi is then UNSAT, R6). */
+ * (var_bytes = 4), 0-based variable ids.  For m <= 4096 every word of
+ * bits [m][ld] is written (shared-memory tiles, no need to clear it); for
+ * larger m bits must be zeroed by the caller.  *d_bad (device int32, may be NULL) gets bit 1 if some id is outside
+ * [0, m), bit 2 if some clause is empty (phi is then UNSAT, R6), bit 4 if a
+ * clause lists a variable twice. */
 int gr_pack_varmajor(int32_t m, int64_t n, const int64_t *off, const void *var, int var_bytes,
                      uint64_t *bits, int64_t ld, int32_t *d_bad, gr_stream_t s);
 /* Same, clause-major [n][ceil(m/64)] masks (for phi-); out must be zeroed. */

@@ -53,7 +53,8 @@ class GrKernelStat(C.Structure):
 
 class GrBitmatrix(C.Structure):
     _fields_ = [("m", C.c_int32), ("n_pos", C.c_int64), ("ld", C.c_int64), ("bits", C.c_void_p),
-                ("n_neg", C.c_int32), ("neg", C.c_void_p)]
+                ("n_neg", C.c_int32), ("neg", C.c_void_p), ("pos_off", C.c_void_p),
+                ("pos_var", C.c_void_p), ("var_bytes", C.c_int32)]
 
 
 _lib = None
@@ -329,15 +330,18 @@ class DeviceBitMatrix:
     bits: "object"  # int64 [m, ld]
     n_neg: int
     neg: "object"  # int64 [n_neg, ceil(m/64)] or None
-    bad: int = 0  # 1: id out of range, 2: empty positive clause
+    bad: int = 0  # 1: id out of range, 2: empty positive clause, 4: repeated id in a clause
+    pos_off: "object" = None  # device CSR of phi+ (enables the incremental greedy)
+    pos_var: "object" = None
 
     def struct(self) -> GrBitmatrix:
+        vb = 0 if self.pos_var is None else self.pos_var.element_size()
         return GrBitmatrix(self.m, self.n_pos, self.ld, _ptr(self.bits), self.n_neg,
-                           _ptr(self.neg))
+                           _ptr(self.neg), _ptr(self.pos_off), _ptr(self.pos_var), vb)
 
 
 def pack_bitmatrix(m, pos_off, pos_var, neg_off, neg_var, device="cuda", stream=None,
-                   check: bool = True) -> DeviceBitMatrix:
+                   check: bool = True, keep_csr: bool = True) -> DeviceBitMatrix:
     """Device clause packing (a1): CSR variable lists -> var-major phi+ bits and
     clause-major phi- masks (gr_pack_varmajor / gr_pack_clausemajor).  The
     CSR tensors may be host (numpy) or device (torch) arrays."""
@@ -353,7 +357,8 @@ def pack_bitmatrix(m, pos_off, pos_var, neg_off, neg_var, device="cuda", stream=
     no, nv = dev(neg_off, np.int64), dev(neg_var, None)
     n_pos, n_neg = int(po.numel() - 1), int(no.numel() - 1)
     ld = bitmatrix_ld(n_pos)
-    bits = torch.zeros((m, ld), dtype=torch.int64, device=device)
+    # m <= 4096: the tiled device pack writes every word (no clearing pass)
+    bits = (torch.empty if m <= 4096 else torch.zeros)((m, ld), dtype=torch.int64, device=device)
     mw = (m + 63) // 64
     neg = torch.zeros((max(n_neg, 1), mw), dtype=torch.int64, device=device)
     bad = torch.zeros(1, dtype=torch.int32, device=device)
@@ -365,7 +370,8 @@ def pack_bitmatrix(m, pos_off, pos_var, neg_off, neg_var, device="cuda", stream=
                                  _ptr(badn), st), "gr_pack_clausemajor")
     b = int(bad.item()) if check else 0
     b |= int(badn.item()) & 1 if check else 0
-    return DeviceBitMatrix(m, n_pos, ld, bits, n_neg, neg if n_neg else None, b)
+    return DeviceBitMatrix(m, n_pos, ld, bits, n_neg, neg if n_neg else None, b,
+                           po if keep_csr else None, pv if keep_csr else None)
 
 
 def greedy_matrix_workspace_bytes(bm: DeviceBitMatrix) -> int:

@@ -18,6 +18,7 @@
 #include <cub/block/block_reduce.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -44,6 +45,11 @@ struct GCtrl {
   int upar;        // U buffer parity: pass reads U[upar], writes U[upar ^ 1]
   unsigned int maxcount;
   int bad;
+  // lazy greedy (lazy_step_kernel)
+  int pending;     // pick whose mark the next step applies (-1 = none)
+  unsigned int fresh;   // recount accumulator of the current step
+  unsigned int ticket;  // last-CTA ticket of the current step
+  int steps;
   int pad[2];
 };
 
@@ -307,6 +313,105 @@ __global__ void init_kernel(u64 *U0, int64_t ld, int64_t n, GCtrl *ctrl, u32 *co
     ctrl->upar = 0;
     ctrl->maxcount = 0;
     ctrl->bad = 0;
+    ctrl->pending = -1;
+    ctrl->fresh = 0;
+    ctrl->ticket = 0;
+    ctrl->steps = 0;
+  }
+}
+
+// ---- incremental greedy -----------------------------------
+// With the clause-major variable lists (CSR) at hand the counts are kept exact
+// without re-streaming the matrix: count[v] starts as the number of clauses
+// containing v (a histogram of the CSR), and when v* is picked every newly
+// covered clause c (U ∩ R[v*], one 2 MiB row) decrements the count of each of
+// its variables.  Picks are identical to the recounting loop (same counts,
+// same lowest-index argmax); the bytes per pick drop from m·n/8 to about
+// n/8 + |newly covered|·(clause length + 1)·(var bytes).
+template <typename V>
+__global__ void csr_hist_kernel(int64_t n, const int64_t *off, const V *var, int m, u32 *counts) {
+  extern __shared__ u32 hist[];
+  for (int v = threadIdx.x; v < m; v += blockDim.x) hist[v] = 0;
+  __syncthreads();
+  const int64_t e0 = off[0], e1 = off[n];
+  for (int64_t e = e0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < e1;
+       e += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&hist[(int)var[e]], 1u);
+  __syncthreads();
+  for (int v = threadIdx.x; v < m; v += blockDim.x)
+    if (hist[v]) atomicAdd(&counts[v], hist[v]);
+}
+
+constexpr int IT = 512;
+// the argmax of the counts (lowest index on ties) -> ctrl (pick or done)
+__device__ __forceinline__ void pick_argmax(const u32 *counts, int m, GCtrl *ctrl, int *picks) {
+  typedef cub::BlockReduce<u64, IT> Red;
+  __shared__ typename Red::TempStorage tmp;
+  u64 key = 0;
+  for (int v = threadIdx.x; v < m; v += IT) {
+    const u64 k = ((u64)__ldcg(&counts[v]) << 32) | (u64)(0xffffffffu - (u32)v);
+    key = k > key ? k : key;
+  }
+  key = Red(tmp).Reduce(key, cub::Max());
+  if (threadIdx.x == 0) {
+    if ((key >> 32) == 0) {  // every count is 0: U is empty
+      ctrl->done = 1;
+      ctrl->pending = -1;
+    } else {
+      const int v = (int)(0xffffffffu - (u32)(key & 0xffffffffu));
+      picks[ctrl->npicks] = v;
+      ctrl->npicks += 1;
+      ctrl->pending = v;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(IT) first_pick_kernel(const u32 *counts, int m, GCtrl *ctrl,
+                                                       int *picks) {
+  pick_argmax(counts, m, ctrl, picks);
+}
+
+// one pick: apply the pending pick v (cover its clauses, decrement counts),
+// then the last CTA chooses the next pick
+template <typename V>
+__global__ void __launch_bounds__(IT) incr_step_kernel(const u64 *R, int64_t ld, int m, u64 *U,
+                                                      u32 *counts, const int64_t *off,
+                                                      const V *var, GCtrl *ctrl, int *picks) {
+  extern __shared__ u32 hist[];
+  __shared__ int s_last;
+  if (*(volatile int *)&ctrl->done) return;
+  const int v = ctrl->pending;
+  for (int u = threadIdx.x; u < m; u += IT) hist[u] = 0;
+  __syncthreads();
+  const int64_t a = ld * blockIdx.x / gridDim.x, b = ld * (blockIdx.x + 1) / gridDim.x;
+  const u64 *Rv = R + (size_t)v * ld;
+  for (int64_t w = a + threadIdx.x; w < b; w += IT) {
+    const u64 r = Rv[w];
+    if (!r) continue;
+    const u64 u = U[w];
+    u64 nw = u & r;  // clauses newly covered by v
+    if (!nw) continue;
+    U[w] = u & ~r;
+    while (nw) {
+      const int64_t c = w * 64 + (__ffsll((long long)nw) - 1);
+      nw &= nw - 1;
+      for (int64_t e = off[c]; e < off[c + 1]; e++) atomicAdd(&hist[(int)var[e]], 1u);
+    }
+  }
+  __syncthreads();
+  for (int u = threadIdx.x; u < m; u += IT)
+    if (hist[u]) atomicSub(&counts[u], hist[u]);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&ctrl->ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    pick_argmax(counts, m, ctrl, picks);
+    if (threadIdx.x == 0) {
+      ctrl->ticket = 0;
+      ctrl->steps += 1;
+    }
   }
 }
 
@@ -413,12 +518,55 @@ __global__ void pack_vm_kernel(int m, int64_t n, const int64_t *off, const V *va
         if (bad) atomicOr(bad, 1);
         continue;
       }
-      if (varmajor)
-        atomicOr((unsigned long long *)&bits[(size_t)v * ld + (c >> 6)], 1ull << (c & 63));
-      else
-        atomicOr((unsigned long long *)&bits[(size_t)c * mw + (v >> 6)], 1ull << (v & 63));
+      unsigned long long old, bit;
+      if (varmajor) {
+        bit = 1ull << (c & 63);
+        old = atomicOr((unsigned long long *)&bits[(size_t)v * ld + (c >> 6)], bit);
+      } else {
+        bit = 1ull << (v & 63);
+        old = atomicOr((unsigned long long *)&bits[(size_t)c * mw + (v >> 6)], bit);
+      }
+      if ((old & bit) && bad) atomicOr(bad, 4);  // the clause lists v twice
     }
   }
+}
+
+// Tiled var-major pack (m <= 4096): a CTA owns 256 clause columns (4 words of
+// every row), builds them in shared memory with shared atomics, and writes
+// each row's 32-byte segment once -- every word of the matrix is written
+// (zeros included), so the caller need not clear it.
+constexpr int PK_T = 256;
+template <typename V>
+__global__ void __launch_bounds__(PK_T) pack_vm_tiled_kernel(int m, int64_t n, const int64_t *off,
+                                                            const V *var, u64 *bits, int64_t ld,
+                                                            int32_t *bad) {
+  extern __shared__ unsigned long long tile[];  // [m][4]
+  const int64_t ngroups = ld / 4;
+  int flags = 0;
+  for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
+    for (int q = threadIdx.x; q < m * 4; q += PK_T) tile[q] = 0;
+    __syncthreads();
+    const int64_t c = g * 256 + threadIdx.x;
+    if (c < n) {
+      const int64_t e0 = off[c], e1 = off[c + 1];
+      if (e1 <= e0) flags |= 2;
+      const int wq = threadIdx.x >> 6;
+      const unsigned long long bit = 1ull << (threadIdx.x & 63);
+      for (int64_t e = e0; e < e1; e++) {
+        const int v = (int)var[e];
+        if (v < 0 || v >= m) { flags |= 1; continue; }
+        if (atomicOr(&tile[v * 4 + wq], bit) & bit) flags |= 4;
+      }
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < m; r += PK_T) {
+      ulonglong2 *dst = (ulonglong2 *)(bits + (size_t)r * ld + g * 4);
+      dst[0] = make_ulonglong2(tile[r * 4], tile[r * 4 + 1]);
+      dst[1] = make_ulonglong2(tile[r * 4 + 2], tile[r * 4 + 3]);
+    }
+    __syncthreads();
+  }
+  if (bad && flags) atomicOr(bad, flags);
 }
 
 std::mutex g_mu;
@@ -430,6 +578,9 @@ int count_grid() {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaFuncSetAttribute(count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)COUNT_SMEM_V2);
+  for (auto f : {(const void *)incr_step_kernel<int16_t>, (const void *)incr_step_kernel<int32_t>,
+                 (const void *)csr_hist_kernel<int16_t>, (const void *)csr_hist_kernel<int32_t>})
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   g_count_grid = sms;
   return g_count_grid;
 }
@@ -438,6 +589,10 @@ int validate_matrix(const gr_bitmatrix *in) {
   if (!in || !in->bits) { gr_set_error("null matrix"); return GR_EINVAL; }
   if (in->m < 1 || in->n_pos < 0 || in->n_neg < 0 || (in->n_neg > 0 && !in->neg)) {
     gr_set_error("bad matrix sizes");
+    return GR_EINVAL;
+  }
+  if (in->pos_off && in->pos_var && in->var_bytes != 2 && in->var_bytes != 4) {
+    gr_set_error("var_bytes must be 2 or 4");
     return GR_EINVAL;
   }
   if (in->ld < (in->n_pos + 63) / 64 || in->ld % 64 != 0 || in->ld < 64) {
@@ -470,6 +625,22 @@ extern "C" int gr_pack_varmajor(int32_t m, int64_t n, const int64_t *off, const 
     return GR_EINVAL;
   }
   if (n == 0) return GR_OK;
+  cudaStream_t st = (cudaStream_t)s;
+  if (m <= 4096 && ld % 4 == 0) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(pack_vm_tiled_kernel<int16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 32);
+      cudaFuncSetAttribute(pack_vm_tiled_kernel<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 32);
+      attr = true;
+    }
+    const size_t sm = (size_t)m * 32;
+    const int grid = (int)std::min<int64_t>(ld / 4, 148 * 4);
+    if (var_bytes == 2)
+      GR_LAUNCH("pack_vm_tiled_kernel", st, pack_vm_tiled_kernel<int16_t><<<grid, PK_T, sm, st>>>(m, n, off, (const int16_t *)var, bits, ld, d_bad));
+    else
+      GR_LAUNCH("pack_vm_tiled_kernel", st, pack_vm_tiled_kernel<int32_t><<<grid, PK_T, sm, st>>>(m, n, off, (const int32_t *)var, bits, ld, d_bad));
+    return GR_OK;
+  }
   const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
   if (var_bytes == 2)
     GR_LAUNCH("pack_vm_kernel", (cudaStream_t)s, pack_vm_kernel<int16_t><<<grid, 256, 0, (cudaStream_t)s>>>(m, n, off, (const int16_t *)var, bits, ld, d_bad, 1));
@@ -534,21 +705,57 @@ extern "C" int gr_mhs_greedy_matrix(const gr_bitmatrix *in, uint64_t *assign, in
   const int grid = count_grid();
   int *h = pinned_ctrl();
   if (!h) { gr_set_error("cudaMallocHost failed"); return GR_ECUDA; }
-  // pass t reads U[t & 1] and writes U[(t & 1) ^ 1]; parity is host-known
-  // because every pass (even a no-op after done) flips it in argmax_kernel.
   const int CHUNK = 8;
   int t = 0;
-  for (;;) {
-    for (int j = 0; j < CHUNK; j++, t++) {
-      CountParams p{in->bits, ld, in->m, ntiles, U + (size_t)(t & 1) * ld,
-                    U + (size_t)((t & 1) ^ 1) * ld, counts, ctrl, 1};
-      GR_LAUNCH("count_kernel", (cudaStream_t)s, count_kernel<<<grid, CT, COUNT_SMEM_V2, st>>>(p));
-      GR_LAUNCH("argmax_kernel", (cudaStream_t)s, argmax_kernel<<<1, AT, 0, st>>>(counts, in->m, ctrl, wpicks));
+  bool eager = in->pos_off == nullptr || in->pos_var == nullptr || in->m > 50000 ||
+               getenv("GR_GREEDY_EAGER") != nullptr;
+  if (!eager) {
+    // incremental greedy: CSR histogram, then one cover-and-decrement step per pick
+    const int hgrid = (int)std::min<int64_t>((in->n_pos * 9 + 255) / 256, 148 * 8);
+    const size_t hs = sizeof(u32) * (size_t)in->m;
+    if (in->var_bytes == 2)
+      GR_LAUNCH("csr_hist_kernel", st, csr_hist_kernel<int16_t><<<std::max(hgrid, 1), 256, hs, st>>>(
+                                          in->n_pos, in->pos_off, (const int16_t *)in->pos_var, in->m, counts));
+    else
+      GR_LAUNCH("csr_hist_kernel", st, csr_hist_kernel<int32_t><<<std::max(hgrid, 1), 256, hs, st>>>(
+                                          in->n_pos, in->pos_off, (const int32_t *)in->pos_var, in->m, counts));
+    GR_LAUNCH("first_pick_kernel", st, first_pick_kernel<<<1, IT, 0, st>>>(counts, in->m, ctrl, wpicks));
+    const int STEPS = 32;
+    for (int round = 0;; round++) {
+      for (int j = 0; j < STEPS; j++) {
+        if (in->var_bytes == 2)
+          GR_LAUNCH("incr_step_kernel", st, incr_step_kernel<int16_t><<<grid, IT, hs, st>>>(
+                                                in->bits, ld, in->m, U, counts, in->pos_off,
+                                                (const int16_t *)in->pos_var, ctrl, wpicks));
+        else
+          GR_LAUNCH("incr_step_kernel", st, incr_step_kernel<int32_t><<<grid, IT, hs, st>>>(
+                                                in->bits, ld, in->m, U, counts, in->pos_off,
+                                                (const int32_t *)in->pos_var, ctrl, wpicks));
+      }
+      GR_CUDA(cudaMemcpyAsync(h, ctrl, sizeof(GCtrl), cudaMemcpyDeviceToHost, st));
+      GR_CUDA(cudaStreamSynchronize(st));
+      if (((GCtrl *)h)->done) break;
+      if ((long long)round * STEPS > (long long)in->m + 2 * STEPS) {
+        gr_set_error("greedy did not terminate");
+        return GR_ECUDA;
+      }
     }
-    GR_CUDA(cudaMemcpyAsync(h, ctrl, sizeof(GCtrl), cudaMemcpyDeviceToHost, st));
-    GR_CUDA(cudaStreamSynchronize(st));
-    if (((GCtrl *)h)->done) break;
-    if (t > in->m + 2 * CHUNK) { gr_set_error("greedy did not terminate"); return GR_ECUDA; }
+  }
+  if (eager) {
+    // pass t reads U[t & 1] and writes U[(t & 1) ^ 1]; parity is host-known
+    // because every pass (even a no-op after done) flips it in argmax_kernel.
+    for (;;) {
+      for (int j = 0; j < CHUNK; j++, t++) {
+        CountParams p{in->bits, ld, in->m, ntiles, U + (size_t)(t & 1) * ld,
+                      U + (size_t)((t & 1) ^ 1) * ld, counts, ctrl, 1};
+        GR_LAUNCH("count_kernel", (cudaStream_t)s, count_kernel<<<grid, CT, COUNT_SMEM_V2, st>>>(p));
+        GR_LAUNCH("argmax_kernel", (cudaStream_t)s, argmax_kernel<<<1, AT, 0, st>>>(counts, in->m, ctrl, wpicks));
+      }
+      GR_CUDA(cudaMemcpyAsync(h, ctrl, sizeof(GCtrl), cudaMemcpyDeviceToHost, st));
+      GR_CUDA(cudaStreamSynchronize(st));
+      if (((GCtrl *)h)->done) break;
+      if (t > 2 * in->m + 2 * CHUNK) { gr_set_error("greedy did not terminate"); return GR_ECUDA; }
+    }
   }
   const int np = ((GCtrl *)h)->npicks;
   if (n_picks) *n_picks = np;

@@ -239,11 +239,11 @@ def csr_from_lists(cls):
     return off, var
 
 
-def check_matrix(m, pos, neg):
+def check_matrix(m, pos, neg, keep_csr=True):
     po, pv = csr_from_lists(pos)
     no, nv = csr_from_lists(neg)
     o = oracle.greedy_csr(m, po, pv, no, nv)
-    bm = gr.pack_bitmatrix(m, po, pv, no, nv)
+    bm = gr.pack_bitmatrix(m, po, pv, no, nv, keep_csr=keep_csr)
     assert bm.bad == 0
     r = gr.mhs_greedy_matrix(bm)
     torch.cuda.synchronize()
@@ -255,20 +255,32 @@ def check_matrix(m, pos, neg):
     assert int(r.status.item()) == o.status
 
 
-@pytest.mark.parametrize("seed", range(3))
-def test_greedy_matrix_random(seed):
+@pytest.mark.parametrize("seed", range(4))
+@pytest.mark.parametrize("keep_csr", [True, False])  # incremental (f3) / recounting passes
+def test_greedy_matrix_random(seed, keep_csr):
     rng = random.Random(seed)
-    m = rng.choice([7, 64, 65, 300])
-    n = rng.choice([1, 100, 5000, 40000])
+    m = [7, 64, 300, 5000][seed]  # 5000 > 4096: the atomic (untiled) pack
+    n = [1, 5000, 40000, 20000][seed]
     pos = [sorted(rng.sample(range(m), rng.randint(1, min(m, 6)))) for _ in range(n)]
     neg = [sorted(rng.sample(range(m), min(m, 2))) for _ in range(5)]
-    check_matrix(m, pos, neg)
+    check_matrix(m, pos, neg, keep_csr)
 
 
-def test_greedy_matrix_c5_shape_reduced():
+def test_pack_flags():
+    """d_bad: 1 = id out of range, 2 = empty clause, 4 = repeated id."""
+    for m in (100, 5000):
+        for cls, want in (([[0, 1], [m]], 1), ([[0, 1], []], 2), ([[3, 3]], 4)):
+            po, pv = csr_from_lists(cls)
+            bm = gr.pack_bitmatrix(m, po, pv, np.zeros(1, np.int64), np.zeros(0, np.int32))
+            assert bm.bad == want, (m, cls, bm.bad)
+
+
+@pytest.mark.parametrize("keep_csr", [True, False])
+def test_greedy_matrix_c5_shape_reduced(keep_csr):
     csr, H = synth.c5_clauses(m=4096, n=1 << 18)
     o = oracle.greedy_csr(csr.m, csr.pos_off, csr.pos_var.astype(np.int32), csr.neg_off, csr.neg_var)
-    bm = gr.pack_bitmatrix(csr.m, csr.pos_off, csr.pos_var, csr.neg_off, csr.neg_var)
+    bm = gr.pack_bitmatrix(csr.m, csr.pos_off, csr.pos_var, csr.neg_off, csr.neg_var,
+                           keep_csr=keep_csr)
     r = gr.mhs_greedy_matrix(bm)
     torch.cuda.synchronize()
     assert r.picks.cpu().numpy()[: r.n_picks].tolist() == o.picks.tolist()
