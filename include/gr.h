@@ -96,6 +96,13 @@ typedef struct {
   const uint32_t *w;        /* [B][wstride] weight w_i >= 1 of soft clause (not b_i), i < m[b];
                                NULL = unit weights (PMS).  Read by gr_solve_pms only. */
   int32_t wstride;          /* host: row stride of w in elements (>= max m) */
+  const int32_t *k_start;   /* [B] or NULL (incremental Solve): unit-weight
+                               exact solvers enumerate levels k >= k_start[b] only.  The caller
+                               guarantees that no feasible set has fewer than k_start[b]
+                               elements -- e.g. phi grew by clauses since a solve whose optimum
+                               had k_start[b] elements (phi := phi U {c} only
+                               shrinks the feasible sets).  decided counts enumerated levels.
+                               Ignored by WPMS (a lighter optimum may use fewer elements). */
 } gr_batch;
 
 /* Per-instance results (device buffers, written by the library). */

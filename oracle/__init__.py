@@ -51,6 +51,9 @@ def lib():
         L.or_num_threads.restype = C.c_int
         L.or_set_threads.argtypes = [C.c_int]
         L.or_pms.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, p, p, C.c_int, p, p, p, p]
+        L.or_pms_kstart.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, p, C.c_int, C.c_int, p, p,
+                                    p, p]
+        L.or_pms_kstart.restype = C.c_int
         L.or_pms_brute.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, p, p, p, p, p]
         L.or_mhs.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, p, C.c_int, p, p, p, p]
         L.or_greedy.argtypes = [C.c_int, C.c_int64, p, p, C.c_int64, p, p, p, p, p, p, p]
@@ -105,6 +108,18 @@ def pms(m: int, n_pos: int, masks, w=None, reduce: int = 1, W: int = 1) -> Resul
                       _ptr(a), _ptr(c), _ptr(s), _ptr(d))
     if rc:
         raise RuntimeError(f"or_pms failed: {rc}")
+    return Result(int(s[0]), _join(a), int(c[0]), int(d[0]))
+
+
+def pms_kstart(m: int, n_pos: int, masks, kstart: int, reduce: int = 1, W: int = 1) -> Result:
+    """Unit-weight PMS enumerating levels >= kstart only (incremental Solve, f2)."""
+    mk = _inst(masks, W)
+    a, c, s, d = (np.zeros(W, np.uint64), np.zeros(1, np.uint64), np.zeros(1, np.int32),
+                  np.zeros(1, np.uint64))
+    rc = lib().or_pms_kstart(m, W, n_pos, mk.shape[0] - n_pos, _ptr(mk), reduce, kstart,
+                             _ptr(a), _ptr(c), _ptr(s), _ptr(d))
+    if rc:
+        raise RuntimeError(f"or_pms_kstart failed: {rc}")
     return Result(int(s[0]), _join(a), int(c[0]), int(d[0]))
 
 

@@ -157,8 +157,25 @@ static int validate(int m, int W, int n, const uint64_t *masks, const uint32_t *
  * Outputs: assign (1 word, 0 if UNSAT), cost (UINT64_MAX if UNSAT), status,
  *   decided = number of candidate subsets whose feasibility was tested.
  */
+static int or_pms_from(int m, int W, int n_pos, int n_neg, const uint64_t *masks,
+                       const uint32_t *w, int reduce, int kstart, uint64_t *assign,
+                       uint64_t *cost, int32_t *status, uint64_t *decided);
+
 int or_pms(int m, int W, int n_pos, int n_neg, const uint64_t *masks, const uint32_t *w,
            int reduce, uint64_t *assign, uint64_t *cost, int32_t *status, uint64_t *decided) {
+  return or_pms_from(m, W, n_pos, n_neg, masks, w, reduce, 0, assign, cost, status, decided);
+}
+
+/* Incremental Solve: unit weights, levels below kstart are
+ * not enumerated (the caller knows they hold no feasible set). */
+int or_pms_kstart(int m, int W, int n_pos, int n_neg, const uint64_t *masks, int reduce, int kstart,
+                  uint64_t *assign, uint64_t *cost, int32_t *status, uint64_t *decided) {
+  return or_pms_from(m, W, n_pos, n_neg, masks, NULL, reduce, kstart, assign, cost, status, decided);
+}
+
+static int or_pms_from(int m, int W, int n_pos, int n_neg, const uint64_t *masks,
+                       const uint32_t *w, int reduce, int kstart, uint64_t *assign,
+                       uint64_t *cost, int32_t *status, uint64_t *decided) {
   if (m < 0 || W < 1 || W > 2 || n_pos < 0 || n_neg < 0) return OR_EINVAL;
   for (int t = 0; t < W; t++) assign[t] = 0;
   *cost = UINT64_MAX; *decided = 0;
@@ -204,6 +221,7 @@ int or_pms(int m, int W, int n_pos, int n_neg, const uint64_t *masks, const uint
   for (int k = 0; k <= kmax; k++) {
     if (k > 0) Sk += ws[k - 1];
     if (w && found && Sk >= best_W) break;
+    if (!w && k > 0 && k < kstart) continue;  /* level 0 is always tested */
     uint64_t cnt = binom(me, k);
     uint64_t x = (k == 64) ? ~0ull : ((1ull << k) - 1);
     int lvl_found = 0; uint64_t lvl_x = 0, lvl_W = UINT64_MAX;

@@ -37,7 +37,7 @@ class GrBatch(C.Structure):
         ("B", C.c_int32), ("W", C.c_int32), ("total_clauses", C.c_int64),
         ("max_clauses", C.c_int32), ("flags", C.c_uint32),
         ("m", C.c_void_p), ("off", C.c_void_p), ("n_pos", C.c_void_p), ("masks", C.c_void_p),
-        ("w", C.c_void_p), ("wstride", C.c_int32),
+        ("w", C.c_void_p), ("wstride", C.c_int32), ("k_start", C.c_void_p),
     ]
 
 
@@ -148,6 +148,7 @@ class DeviceBatch:
     max_clauses: int
     wstride: int = 0
     flags: int = 0
+    k_start: "object" = None  # optional int32 [B] start levels (incremental Solve, f2)
 
     @staticmethod
     def from_host(cb, device="cuda", flags: int = 0, weighted: bool = True,
@@ -177,7 +178,8 @@ class DeviceBatch:
     def struct(self, weighted: bool = True) -> GrBatch:
         return GrBatch(self.B, self.W, self.total_clauses, self.max_clauses, self.flags,
                        _ptr(self.m), _ptr(self.off), _ptr(self.n_pos), _ptr(self.masks),
-                       _ptr(self.w) if weighted else None, self.wstride if weighted else 0)
+                       _ptr(self.w) if weighted else None, self.wstride if weighted else 0,
+                       _ptr(self.k_start))
 
 
 @dataclass

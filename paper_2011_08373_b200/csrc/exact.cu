@@ -43,14 +43,14 @@ constexpr int MAXC = 4096;       // max clauses per instance (exact solvers)
 struct Ctrl {
   u64 next_chunk;     // atomic chunk counter of the running level
   u64 total_chunks;   // chunks of the running level
-  int n_active;       // active instances
-  int pad0;
+  int n_active;       // instances listed for the running level
+  int n_remaining;    // instances not finished (listed or waiting for their start level)
   u64 lane_cands;     // candidates per lane per chunk (L)
   u64 pad1[4];
 };
 
 struct Layout {
-  size_t ctrl, meff, npr, nnr, kmax, done, rb, sup, decided, bestx, bestw, wtot, lvlkey, sk, wr,
+  size_t ctrl, meff, npr, nnr, kmax, ks, done, rb, sup, decided, bestx, bestw, wtot, lvlkey, sk, wr,
       active, chunk_base, pk, hrec, total;
 };
 
@@ -63,6 +63,7 @@ Layout layout_of(const gr_batch *in) {
   L.npr = take(4 * B);
   L.nnr = take(4 * B);
   L.kmax = take(4 * B);
+  L.ks = take(4 * B);
   L.done = take(4 * B);
   L.rb = take(4 * B);
   L.sup = take(16 * B);
@@ -83,7 +84,7 @@ Layout layout_of(const gr_batch *in) {
 
 struct WS {
   Ctrl *ctrl;
-  int *meff, *npr, *nnr, *kmax, *done, *rb;
+  int *meff, *npr, *nnr, *kmax, *ks, *done, *rb;
   u64 *sup, *decided, *bestx, *bestw, *wtot;
   i64 *lvlkey;
   u64 *sk;
@@ -102,6 +103,7 @@ WS ws_of(const gr_batch *in, void *base) {
   w.npr = (int *)(p + L.npr);
   w.nnr = (int *)(p + L.nnr);
   w.kmax = (int *)(p + L.kmax);
+  w.ks = (int *)(p + L.ks);
   w.done = (int *)(p + L.done);
   w.rb = (int *)(p + L.rb);
   w.sup = (u64 *)(p + L.sup);
@@ -128,6 +130,7 @@ struct In {
   const uint32_t *w;
   const int32_t *sel;  // optional: solve only instances with sel[b] == sel_val (others untouched)
   int sel_val;
+  const int32_t *kstart;  // optional (unit weights): first level to enumerate (f2)
 };
 struct Out {
   uint64_t *assign, *cost, *decided;
@@ -138,8 +141,9 @@ thread_local const int32_t *t_sel = nullptr;  // set by gr_solve around its fall
 thread_local int t_sel_val = 0;
 
 In in_of(const gr_batch *b, int which) {
+  const bool unit = which != 0 || b->w == nullptr;
   In r{b->B, b->W, b->max_clauses, b->wstride, b->m, b->off, b->n_pos, b->masks,
-       which == 0 ? b->w : nullptr, t_sel, t_sel_val};
+       which == 0 ? b->w : nullptr, t_sel, t_sel_val, unit ? b->k_start : nullptr};
   return r;
 }
 Out out_of(const gr_result *o) { return Out{o->assign, o->cost, o->decided, o->status}; }
@@ -322,6 +326,10 @@ __global__ void __launch_bounds__(PT) pack_kernel(In in, Out out, WS ws, int whi
     ws.npr[b] = npr;
     ws.nnr[b] = nnr;
     ws.kmax[b] = me < npr ? me : npr;
+    // f2: the caller guarantees no feasible set below k_start[b] (e.g. the
+    // previous optimum level of a sub-formula): those levels are skipped
+    const int ks = in.kstart ? (in.kstart[b] > 1 ? in.kstart[b] : 1) : 1;
+    ws.ks[b] = ks;
     ws.sup[2 * b] = sup0;
     ws.sup[2 * b + 1] = sup1;
     ws.wtot[b] = acc;
@@ -334,6 +342,9 @@ __global__ void __launch_bounds__(PT) pack_kernel(In in, Out out, WS ws, int whi
       // negative clause and is optimal
       ws.done[b] = 1;
       write_result(in, out, b, GR_SAT, 0, sup0, sup1, 0, 1, which);
+    } else if (ks > (me < npr ? me : npr)) {  // nothing left to enumerate (R13)
+      ws.done[b] = 1;
+      write_result(in, out, b, GR_UNSAT, 0, sup0, sup1, 0, 1, which);
     } else {
       ws.done[b] = 0;
     }
@@ -705,7 +716,7 @@ __global__ void __launch_bounds__(FT) finish_kernel(In in, Out out, WS ws, int w
   typedef cub::BlockScan<u64, FT> Scan;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ u64 s_carry;
-  __shared__ int s_cnt;
+  __shared__ int s_cnt, s_wait;
   const int t = threadIdx.x;
   const bool weighted = in.w != nullptr;
   const int nact_in = k == 0 ? in.B : ws.ctrl->n_active;
@@ -756,14 +767,22 @@ __global__ void __launch_bounds__(FT) finish_kernel(In in, Out out, WS ws, int w
     __syncthreads();
   }
   // phase 2: compact the still-active instances and plan level k+1
-  if (t == 0) { s_carry = 0; s_cnt = 0; }
+  // (with start levels, every unfinished instance is revisited: those whose
+  // start level is above k+1 wait, counted in n_remaining)
+  const bool all = k == 0 || in.kstart != nullptr;
+  const int n2 = all ? in.B : nact_in;
+  if (t == 0) { s_carry = 0; s_cnt = 0; s_wait = 0; }
   __syncthreads();
-  for (int base = 0; base < nact_in; base += FT) {
+  for (int base = 0; base < n2; base += FT) {
     const int i = base + t;
     int b = -1;
-    if (i < nact_in) {
-      b = k == 0 ? i : cur[i];
+    if (i < n2) {
+      b = all ? i : cur[i];
       if (ws.done[b]) b = -1;
+      else if (k + 1 < ws.ks[b]) {
+        atomicAdd(&s_wait, 1);
+        b = -1;
+      }
     }
     u64 csz = 0;
     if (b >= 0) {
@@ -823,6 +842,7 @@ __global__ void __launch_bounds__(FT) finish_kernel(In in, Out out, WS ws, int w
   if (t == 0) {
     ws.chunk_base[nact] = s_carry;
     ws.ctrl->n_active = nact;
+    ws.ctrl->n_remaining = nact + s_wait;
     ws.ctrl->total_chunks = s_carry;
     ws.ctrl->next_chunk = 0;
     ws.ctrl->lane_cands = L;
@@ -937,7 +957,7 @@ extern "C" int gr_exact_prepare(const gr_batch *in, int which, gr_result *out, v
   if (n_active) {
     int *h = pinned_i32();
     if (!h) { gr_set_error("cudaMallocHost failed"); return GR_ECUDA; }
-    GR_CUDA(cudaMemcpyAsync(h, &w.ctrl->n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
+    GR_CUDA(cudaMemcpyAsync(h, &w.ctrl->n_remaining, sizeof(int), cudaMemcpyDeviceToHost, st));
     GR_CUDA(cudaStreamSynchronize(st));
     *n_active = *h;
   }
@@ -991,7 +1011,7 @@ extern "C" int gr_exact_finish(const gr_batch *in, int which, int k, gr_result *
   if (n_active) {
     int *h = pinned_i32();
     if (!h) { gr_set_error("cudaMallocHost failed"); return GR_ECUDA; }
-    GR_CUDA(cudaMemcpyAsync(h, &w.ctrl->n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
+    GR_CUDA(cudaMemcpyAsync(h, &w.ctrl->n_remaining, sizeof(int), cudaMemcpyDeviceToHost, st));
     GR_CUDA(cudaStreamSynchronize(st));
     *n_active = *h;
   }

@@ -50,19 +50,19 @@ def test_version_and_host_validation():
     assert L.gr_mhs_greedy(None, None, None, 0, None) == N.GR_EINVAL
     assert L.gr_mhs_greedy_matrix(None, None, None, None, None, None, 0, None) == N.GR_EINVAL
     assert L.gr_last_error()
-    b = N.GrBatch(0, 1, 0, 0, 0, None, None, None, None, None, 0)
+    b = N.GrBatch(0, 1, 0, 0, 0, None, None, None, None, None, 0, None)
     assert L.gr_workspace_bytes(C.byref(b), 0) == 0  # B < 1
-    b = N.GrBatch(4, 3, 0, 0, 0, 1, 1, 1, 1, None, 0)
+    b = N.GrBatch(4, 3, 0, 0, 0, 1, 1, 1, 1, None, 0, None)
     assert L.gr_workspace_bytes(C.byref(b), 0) == 0  # W = 3
-    b = N.GrBatch(4, 1, 100, 10, 0, 1, 1, 1, 1, None, 0)
+    b = N.GrBatch(4, 1, 100, 10, 0, 1, 1, 1, 1, None, 0, None)
     assert L.gr_workspace_bytes(C.byref(b), 0) > 0
     assert L.gr_workspace_bytes(C.byref(b), 2) > 0
     # max_clauses beyond the exact solvers' limit is a call-level error
-    b = N.GrBatch(4, 1, 100, 5000, 0, 1, 1, 1, 1, None, 0)
+    b = N.GrBatch(4, 1, 100, 5000, 0, 1, 1, 1, 1, None, 0, None)
     r = N.GrResult(1, 1, 1, None)
     assert L.gr_solve_pms(C.byref(b), C.byref(r), 1, 1 << 40, None) == N.GR_ETOOBIG
     # workspace too small
-    b = N.GrBatch(4, 1, 100, 10, 0, 1, 1, 1, 1, None, 0)
+    b = N.GrBatch(4, 1, 100, 10, 0, 1, 1, 1, 1, None, 0, None)
     assert L.gr_solve_pms(C.byref(b), C.byref(r), 1, 8, None) == N.GR_EWORKSPACE
     assert N.bitmatrix_ld(1) == 64
     assert N.bitmatrix_ld(64 * 64) == 64

@@ -453,3 +453,27 @@ def test_composite_solve_properties():
     assert (fb == (g.status == NEGV)).all()
     assert (s.assign[fb] == p.assign[fb]).all() and (s.assign[~fb] == g.assign[~fb]).all()
     assert (s.status != NEGV).all()
+
+
+# ------------------------------------------------------- incremental Solve (f2)
+def test_incremental_kstart_monotone():
+    """phi := phi U {c}.  A feasible set of phi U {c} is feasible
+    for phi, so no feasible set lies below phi's optimum level: enumerating
+    from k* gives exactly the full answer with fewer candidates."""
+    rng = random.Random(31)
+    for _ in range(150):
+        m = rng.randint(2, 12)
+        pos, neg, _ = rand_instance(rng, m, rng.randint(1, 10))
+        r0 = oracle.pms(m, len(pos), masks_of(pos, neg))
+        if r0.status != SAT:
+            continue
+        c = sorted(rng.sample(range(1, m + 1), rng.randint(1, min(3, m))))
+        if rng.random() < 0.5:
+            pos2, neg2 = pos + [c], neg
+        else:
+            pos2, neg2 = pos, neg + [c]
+        full = oracle.pms(m, len(pos2), masks_of(pos2, neg2))
+        inc = oracle.pms_kstart(m, len(pos2), masks_of(pos2, neg2), r0.cost)
+        assert (inc.status, inc.assign, inc.cost) == (full.status, full.assign, full.cost)
+        assert inc.decided <= full.decided
+        assert full.cost >= r0.cost or full.status == UNSAT  # the optimum never decreases

@@ -435,3 +435,30 @@ def test_composite_solve(weighted):
     m = gr.solve(db, gr.GR_STRATEGY_MAXSAT).to_host()
     p = oracle.batch("pms", cb)
     assert (m["status"] == p.status).all() and (m["assign"] == p.assign).all()
+
+
+def test_incremental_kstart():
+    """f2: start levels from the previous solve of a sub-formula give the full
+    answer; decided equals the oracle's with the same start level."""
+    rng = random.Random(8)
+    base, grown = [], []
+    for _ in range(150):
+        m = rng.randint(10, 24)
+        inst = planted_instance(rng, m, rng.randint(3, 20), rng.randint(0, 6), rng.randint(1, 5))
+        base.append(inst)
+        c = sorted(rng.sample(range(1, m + 1), rng.randint(1, 3)))
+        grown.append((m, inst[1] + [c], inst[2]) if rng.random() < 0.6 else (m, inst[1], inst[2] + [c]))
+    cb0 = synth.batch_from_lists(base, W=1)
+    cb1 = synth.batch_from_lists(grown, W=1)
+    r0 = gpu_solve(cb0, "pms")
+    ks = np.where(r0["status"] == 0, r0["cost"].astype(np.int64), 1).astype(np.int32)
+    db = gr.DeviceBatch.from_host(cb1)
+    db.k_start = torch.from_numpy(ks).cuda()
+    got = gr.solve_pms(db).to_host()
+    full = oracle.batch("pms", cb1)
+    assert (got["status"] == full.status).all() and (got["assign"] == full.assign).all()
+    for b in range(cb1.B):
+        m, npos, mk, _ = cb1.instance(b)
+        o = oracle.pms_kstart(m, npos, mk, int(ks[b]))
+        if o.status == 0:
+            assert int(got["decided"][b]) == o.decided, b
