@@ -76,9 +76,13 @@ enum {
 
 /* flags of gr_batch.flags */
 enum {
-  GR_FLAG_EXHAUSTIVE = 1     /* exact unit-weight solvers: enumerate the witness level
+  GR_FLAG_EXHAUSTIVE = 1,    /* exact unit-weight solvers: enumerate the witness level
                                 completely (deterministic work; benchmarking mode).
                                 Results are identical. */
+  GR_FLAG_WEIGHTED_GREEDY = 2 /* gr_mhs_greedy / gr_solve(MHS) with w != NULL: the weighted
+                                mhs -- pick the variable
+                                maximising uncovered-hits / weight (exact cross-multiplied
+                                comparison, lowest index on ties, reading R20); cost = weight */
 };
 
 /* A batch of independent Solve-step instances. */
@@ -137,7 +141,8 @@ int gr_mhs_exact(const gr_batch *in, gr_result *out, void *ws, size_t ws_bytes, 
  * R11), then reverse-delete in reverse pick order to a minimal hitting set
  * (R12); GR_SAT_NEG_VIOLATED if the set contains some N of phi- (PAPER.md:26).
  * One warp per instance; m <= 128 (W <= 2); duplicates are counted as given (R9).
- * cost = |S|; decided is not written. */
+ * cost = |S| (with GR_FLAG_WEIGHTED_GREEDY: the weighted greedy, cost = weight);
+ * decided is not written. */
 int gr_mhs_greedy(const gr_batch *in, gr_result *out, void *ws, size_t ws_bytes, gr_stream_t s);
 
 /* ---- the composite Solve (Alg. 1 line `solve`) -------------

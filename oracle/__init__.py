@@ -58,6 +58,8 @@ def lib():
         L.or_mhs.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, p, C.c_int, p, p, p, p]
         L.or_greedy.argtypes = [C.c_int, C.c_int64, p, p, C.c_int64, p, p, p, p, p, p, p]
         L.or_greedy_masks.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, p, p, p, p, p]
+        L.or_greedy_masks_w.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, p, p, p, p, p, p]
+        L.or_greedy_masks_w.restype = C.c_int
         L.or_batch.argtypes = [C.c_int, C.c_int, C.c_int, p, p, p, p, p, C.c_int, C.c_int,
                                p, p, p, p]
         L.or_min_feasible_product.argtypes = [C.c_int, p, p, C.c_int, C.c_int, p, p]
@@ -170,14 +172,16 @@ def greedy_csr(m, pos_off, pos_var, neg_off, neg_var) -> GreedyResult:
     return GreedyResult(int(st[0]), picks[: int(nu[0])].copy(), inS[:m].copy(), int(nf[0]))
 
 
-def greedy(m: int, n_pos: int, masks, W: int = 1):
-    """Greedy mhs over mask-encoded clauses -> (status, assign words, picks)."""
+def greedy(m: int, n_pos: int, masks, W: int = 1, w=None):
+    """Greedy mhs over mask-encoded clauses -> (status, assign words, picks);
+    with weights w the weighted (ratio) greedy (f4)."""
     mk = _inst(masks, W)
     a = np.zeros(W, np.uint64)
     picks = np.zeros(max(m, 1), np.int32)
     nu, st = np.zeros(1, np.int32), np.zeros(1, np.int32)
-    rc = lib().or_greedy_masks(m, W, n_pos, mk.shape[0] - n_pos, _ptr(mk), _ptr(a), _ptr(picks),
-                               _ptr(nu), _ptr(st))
+    wa = None if w is None else np.ascontiguousarray(np.asarray(w, np.uint32))
+    rc = lib().or_greedy_masks_w(m, W, n_pos, mk.shape[0] - n_pos, _ptr(mk), _ptr(wa), _ptr(a),
+                                 _ptr(picks), _ptr(nu), _ptr(st))
     if rc:
         raise RuntimeError(f"or_greedy_masks failed: {rc}")
     return int(st[0]), a, picks[: int(nu[0])].copy()
@@ -195,7 +199,7 @@ def batch(which: str, cb, reduce: int = 1, weighted: bool = True) -> BatchResult
     """Solve every instance of a synth.ClauseBatch: which in {pms, mhs, greedy, solve}
     (solve = composite mhs strategy with MaxSAT fallback; its ``decided`` holds
     the fallback flag)."""
-    code = {"pms": 0, "mhs": 1, "greedy": 2, "solve": 3}[which]
+    code = {"pms": 0, "mhs": 1, "greedy": 2, "solve": 3, "greedy_w": 4, "solve_w": 5}[which]
     W = cb.W
     B = cb.B
     assign = np.zeros((B, W), np.uint64)
@@ -208,7 +212,7 @@ def batch(which: str, cb, reduce: int = 1, weighted: bool = True) -> BatchResult
     masks = np.ascontiguousarray(cb.masks, np.uint64)
     w = None
     ws = 0
-    if weighted and cb.w is not None and which in ("pms", "solve"):
+    if weighted and cb.w is not None and which in ("pms", "solve", "greedy_w", "solve_w"):
         w = np.ascontiguousarray(cb.w, np.uint32)
         ws = w.shape[1]
     rc = lib().or_batch(code, B, W, _ptr(m), _ptr(off), _ptr(npos), _ptr(masks), _ptr(w), ws,

@@ -315,10 +315,36 @@ int or_mhs(int m, int W, int n_pos, int n_neg, const uint64_t *masks, int reduce
  *   in_S[m] = final (pruned) set as 0/1 bytes; n_final = |S| after pruning.
  * Counting over clause ranges is parallel (per-thread counts then summed).
  */
+static int greedy_core(int m, int64_t n_pos, const int64_t *pos_off, const int32_t *pos_var,
+                       int64_t n_neg, const int64_t *neg_off, const int32_t *neg_var,
+                       const uint32_t *w, int32_t *picks, int32_t *n_unpruned, uint8_t *in_S,
+                       int32_t *n_final, int32_t *status);
+
 int or_greedy(int m, int64_t n_pos, const int64_t *pos_off, const int32_t *pos_var,
               int64_t n_neg, const int64_t *neg_off, const int32_t *neg_var,
               int32_t *picks, int32_t *n_unpruned, uint8_t *in_S, int32_t *n_final,
               int32_t *status) {
+  return greedy_core(m, n_pos, pos_off, pos_var, n_neg, neg_off, neg_var, NULL, picks,
+                     n_unpruned, in_S, n_final, status);
+}
+
+/* Weighted mhs ("weighted mhs"; SPEC.md:248 ratio rule, reading
+ * R20): each step picks the v maximising c[v] / w[v] (the uncovered clauses
+ * it hits per unit weight; Chvatal 1979), compared exactly as
+ * c[a] * w[b] > c[b] * w[a], lowest index on ties; then the same
+ * reverse-delete and phi- check. */
+int or_greedy_w(int m, int64_t n_pos, const int64_t *pos_off, const int32_t *pos_var,
+                int64_t n_neg, const int64_t *neg_off, const int32_t *neg_var, const uint32_t *w,
+                int32_t *picks, int32_t *n_unpruned, uint8_t *in_S, int32_t *n_final,
+                int32_t *status) {
+  return greedy_core(m, n_pos, pos_off, pos_var, n_neg, neg_off, neg_var, w, picks, n_unpruned,
+                     in_S, n_final, status);
+}
+
+static int greedy_core(int m, int64_t n_pos, const int64_t *pos_off, const int32_t *pos_var,
+                       int64_t n_neg, const int64_t *neg_off, const int32_t *neg_var,
+                       const uint32_t *w, int32_t *picks, int32_t *n_unpruned, uint8_t *in_S,
+                       int32_t *n_final, int32_t *status) {
   *n_unpruned = 0; *n_final = 0;
   if (m < 0 || n_pos < 0 || n_neg < 0) return OR_EINVAL;
   memset(in_S, 0, (size_t)m);
@@ -348,7 +374,11 @@ int or_greedy(int m, int64_t n_pos, const int64_t *pos_off, const int32_t *pos_v
     }
     for (int v = 0; v < m; v++) { int64_t s = 0; for (int t = 0; t < nt; t++) s += cnt_all[(size_t)t * (m + 1) + v]; cnt[v] = s; }
     int best = -1;
-    for (int v = 0; v < m; v++) if (best < 0 || cnt[v] > cnt[best]) best = v;
+    for (int v = 0; v < m; v++) {
+      if (best < 0) { best = v; continue; }
+      if (!w) { if (cnt[v] > cnt[best]) best = v; }
+      else if ((unsigned __int128)cnt[v] * w[best] > (unsigned __int128)cnt[best] * w[v]) best = v;
+    }
     if (best < 0 || cnt[best] == 0) break; /* U is empty */
     picks[nS++] = best;
     in_S[best] = 1;
@@ -387,12 +417,20 @@ int or_greedy(int m, int64_t n_pos, const int64_t *pos_off, const int32_t *pos_v
 
 /* greedy over mask-encoded clauses (W words each): unpack to variable lists
  * and run or_greedy.  assign: W words out. picks: capacity m. */
+int or_greedy_masks_w(int m, int W, int n_pos, int n_neg, const uint64_t *masks,
+                      const uint32_t *w, uint64_t *assign, int32_t *picks, int32_t *n_unpruned,
+                      int32_t *status);
 int or_greedy_masks(int m, int W, int n_pos, int n_neg, const uint64_t *masks,
                     uint64_t *assign, int32_t *picks, int32_t *n_unpruned, int32_t *status) {
+  return or_greedy_masks_w(m, W, n_pos, n_neg, masks, NULL, assign, picks, n_unpruned, status);
+}
+int or_greedy_masks_w(int m, int W, int n_pos, int n_neg, const uint64_t *masks,
+                      const uint32_t *w, uint64_t *assign, int32_t *picks, int32_t *n_unpruned,
+                      int32_t *status) {
   int n = n_pos + n_neg;
   for (int t = 0; t < W; t++) assign[t] = 0;
   *n_unpruned = 0;
-  if (bad_input(m, W, n, masks, NULL)) { *status = OR_BADINPUT; return OR_OK; }
+  if (bad_input(m, W, n, masks, w)) { *status = OR_BADINPUT; return OR_OK; }
   int64_t *off = malloc(sizeof(int64_t) * (n + 2));
   int32_t *var = malloc(sizeof(int32_t) * ((size_t)n * 64 * W + 1));
   uint8_t *inS = malloc((size_t)m + 1);
@@ -404,7 +442,7 @@ int or_greedy_masks(int m, int W, int n_pos, int n_neg, const uint64_t *masks,
     off[j + 1] = e;
   }
   int32_t nf;
-  int rc = or_greedy(m, n_pos, off, var, n_neg, off + n_pos, var, picks, n_unpruned, inS, &nf, status);
+  int rc = greedy_core(m, n_pos, off, var, n_neg, off + n_pos, var, w, picks, n_unpruned, inS, &nf, status);
   if (rc == OR_OK && *status != OR_UNSAT && *status != OR_BADINPUT)
     for (int i = 0; i < m; i++) if (inS[i]) assign[i / 64] |= 1ull << (i % 64);
   free(off); free(var); free(inS);
@@ -415,10 +453,11 @@ int or_greedy_masks(int m, int W, int n_pos, int n_neg, const uint64_t *masks,
  * the greedy set breaks phi- ("results in unsatisfiability"), fall back to
  * the MaxSAT solver (or_pms).  cost: weight (or size) of the returned set. */
 int or_solve_mhs(int m, int W, int n_pos, int n_neg, const uint64_t *masks, const uint32_t *w,
-                 int reduce, uint64_t *assign, uint64_t *cost, int32_t *status, uint64_t *decided,
-                 int32_t *fell_back) {
+                 int reduce, int weighted_greedy, uint64_t *assign, uint64_t *cost,
+                 int32_t *status, uint64_t *decided, int32_t *fell_back) {
   int32_t *pk = malloc(sizeof(int32_t) * (m + 1)), nu;
-  int rc = or_greedy_masks(m, W, n_pos, n_neg, masks, assign, pk, &nu, status);
+  int rc = or_greedy_masks_w(m, W, n_pos, n_neg, masks, weighted_greedy ? w : NULL, assign, pk,
+                             &nu, status);
   free(pk);
   *decided = 0;
   *fell_back = 0;
@@ -437,7 +476,8 @@ int or_solve_mhs(int m, int W, int n_pos, int n_neg, const uint64_t *masks, cons
 /* ---- batch drivers: independent instances in parallel ------------------ */
 /* which: 0 = PMS/WPMS (w may be NULL), 1 = MHS (weights ignored), 2 = greedy,
  * 3 = composite Solve, mhs strategy with MaxSAT fallback (decided[b] = 1 where
- * the fallback ran, else 0 -- the fallback flag, not a candidate count) */
+ * the fallback ran, else 0 -- the fallback flag, not a candidate count),
+ * 4 = weighted greedy (w), 5 = composite Solve with the weighted greedy */
 int or_batch(int which, int B, int W, const int32_t *m, const int64_t *off, const int32_t *n_pos,
              const uint64_t *masks, const uint32_t *w, int wstride, int reduce,
              uint64_t *assign /*[B][W]*/, uint64_t *cost, int32_t *status, uint64_t *decided) {
@@ -452,15 +492,19 @@ int or_batch(int which, int B, int W, const int32_t *m, const int64_t *off, cons
     for (int t = 0; t < W; t++) a[t] = 0;
     if (which == 0) rc = or_pms(m[b], W, np, nn, mk, w ? w + (size_t)b * wstride : NULL, reduce, a, &c, &s, &d);
     else if (which == 1) rc = or_mhs(m[b], W, np, nn, mk, reduce, a, &c, &s, &d);
-    else if (which == 3) {
+    else if (which == 3 || which == 5) {
       int32_t fb = 0;
-      rc = or_solve_mhs(m[b], W, np, nn, mk, w ? w + (size_t)b * wstride : NULL, reduce, a, &c, &s, &d, &fb);
+      rc = or_solve_mhs(m[b], W, np, nn, mk, w ? w + (size_t)b * wstride : NULL, reduce, which == 5,
+                        a, &c, &s, &d, &fb);
       d = (uint64_t)fb;
     }
     else {
+      const uint32_t *wb = (which == 4 && w) ? w + (size_t)b * wstride : NULL;
       int32_t *pk = malloc(sizeof(int32_t) * (m[b] + 1)); int32_t nu;
-      rc = or_greedy_masks(m[b], W, np, nn, mk, assign + (size_t)b * W, pk, &nu, &s);
-      c = 0; for (int t = 0; t < W; t++) c += (uint64_t)popc64(assign[(size_t)b * W + t]);
+      rc = or_greedy_masks_w(m[b], W, np, nn, mk, wb, assign + (size_t)b * W, pk, &nu, &s);
+      c = 0;
+      for (int t = 0; t < W; t++) c += wb ? cost_of(assign[(size_t)b * W + t], wb + 64 * t)
+                                         : (uint64_t)popc64(assign[(size_t)b * W + t]);
       if (s == OR_UNSAT || s == OR_BADINPUT) c = UINT64_MAX;
       free(pk);
     }

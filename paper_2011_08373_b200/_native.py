@@ -20,6 +20,7 @@ LIB_PATH = os.environ.get("GRSOLVE_LIB") or os.path.join(HERE, "libgrsolve.so") 
 GR_OK, GR_EINVAL, GR_ETOOBIG, GR_ECUDA, GR_ENOMEM, GR_EWORKSPACE = 0, -1, -2, -3, -4, -5
 GR_SAT, GR_UNSAT, GR_SAT_NEG_VIOLATED, GR_BADINPUT, GR_UNSUPPORTED = 0, 1, 2, 3, 4
 GR_FLAG_EXHAUSTIVE = 1
+GR_FLAG_WEIGHTED_GREEDY = 2
 PMS, MHS, GREEDY = 0, 1, 2
 
 EXPORTED = [
@@ -252,8 +253,17 @@ def mhs_exact(db: DeviceBatch, out: Optional[DeviceResult] = None, stream=None) 
 
 
 def mhs_greedy(db: DeviceBatch, out: Optional[DeviceResult] = None, stream=None) -> DeviceResult:
-    """(c) greedy mhs of phi+ (gr_mhs_greedy)."""
-    return _solve("gr_mhs_greedy", GREEDY, db, out, stream)
+    """(c) greedy mhs of phi+ (gr_mhs_greedy); weighted when db.flags has
+    GR_FLAG_WEIGHTED_GREEDY and db.w is set (f4)."""
+    L = lib()
+    b = db.struct(True)
+    ws = workspace(256, db.m.device, tag="greedy")
+    if out is None:
+        out = DeviceResult.empty(db.B, db.W, db.m.device)
+    r = out.struct()
+    _check(L.gr_mhs_greedy(C.byref(b), C.byref(r), _ptr(ws), ws.numel(), _stream(stream)),
+           "gr_mhs_greedy")
+    return out
 
 
 def solve(db: DeviceBatch, strategy: int = GR_STRATEGY_MHS, out: Optional[DeviceResult] = None,

@@ -10,6 +10,11 @@
 // set U is a bitmap in shared memory whose 32-bit words are owned round-robin
 // by the lanes when marking; argmax = warp max-reduction of the packed key
 // (count << 8 | 255 - v).
+//
+// Weighted mhs (GR_FLAG_WEIGHTED_GREEDY): the
+// pick maximises count[v] / w[v], compared exactly as c_a * w_b > c_b * w_a
+// with the lowest index on ties (reading R20); warp reduction over
+// (count, weight, v) triples.
 #include "common.cuh"
 
 namespace {
@@ -23,6 +28,8 @@ __global__ void __launch_bounds__(32) greedy_small_kernel(gr_batch in, gr_result
   __shared__ int s_picks[128];
   const int64_t lo = in.off[b], n64 = in.off[b + 1] - lo;
   const int m = in.m[b], np = in.n_pos[b], W = in.W;
+  const bool wgt = (in.flags & GR_FLAG_WEIGHTED_GREEDY) && in.w;
+  const uint32_t *wb = wgt ? in.w + (size_t)b * in.wstride : nullptr;
   int status = GR_SAT;
   u64 S0 = 0, S1 = 0;
   if (n64 < 0 || n64 > in.max_clauses || np < 0 || np > n64 || m < 0 || m > 64 * W) {
@@ -45,6 +52,8 @@ __global__ void __launch_bounds__(32) greedy_small_kernel(gr_batch in, gr_result
       U[q] = rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
     }
     __syncwarp();
+    if (wgt)
+      for (int i = lane; i < m; i += 32) bad |= wb[i] == 0;  // R4
     bad = __any_sync(0xffffffffu, bad);
     empty = __any_sync(0xffffffffu, empty);
     if (bad) status = GR_BADINPUT;
@@ -66,20 +75,44 @@ __global__ void __launch_bounds__(32) greedy_small_kernel(gr_batch in, gr_result
             cnt[3] += (int)((x1 >> (lane + 32)) & 1);
           }
         }
-        u32 key = 0;
-        for (int q = 0; q < 4; q++) {
-          const int v = lane + 32 * q;
-          if (v < m && cnt[q] > 0) {
-            const u32 kq = ((u32)cnt[q] << 8) | (u32)(255 - v);
-            key = kq > key ? kq : key;
+        int v = -1;
+        if (!wgt) {
+          u32 key = 0;
+          for (int q = 0; q < 4; q++) {
+            const int vq = lane + 32 * q;
+            if (vq < m && cnt[q] > 0) {
+              const u32 kq = ((u32)cnt[q] << 8) | (u32)(255 - vq);
+              key = kq > key ? kq : key;
+            }
           }
+          for (int o = 16; o; o >>= 1) {
+            const u32 o2 = __shfl_xor_sync(0xffffffffu, key, o);
+            key = o2 > key ? o2 : key;
+          }
+          if (!key) break;  // U is empty
+          v = 255 - (int)(key & 0xff);
+        } else {
+          // best (count, weight, index) of the lane, then of the warp
+          u32 bc = 0, bw = 1;
+          int bv = 0x7fffffff;
+          for (int q = 0; q < 4; q++) {
+            const int vq = lane + 32 * q;
+            if (vq < m && cnt[q] > 0) {
+              const u32 wq = wb[vq];
+              const u64 l = (u64)cnt[q] * bw, r = (u64)bc * wq;
+              if (l > r || (l == r && vq < bv)) { bc = (u32)cnt[q]; bw = wq; bv = vq; }
+            }
+          }
+          for (int o = 16; o; o >>= 1) {
+            const u32 oc = __shfl_xor_sync(0xffffffffu, bc, o);
+            const u32 ow = __shfl_xor_sync(0xffffffffu, bw, o);
+            const int ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            const u64 l = (u64)oc * bw, r = (u64)bc * ow;
+            if (l > r || (l == r && ov < bv)) { bc = oc; bw = ow; bv = ov; }
+          }
+          if (!bc) break;  // U is empty
+          v = bv;
         }
-        for (int o = 16; o; o >>= 1) {
-          const u32 o2 = __shfl_xor_sync(0xffffffffu, key, o);
-          key = o2 > key ? o2 : key;
-        }
-        if (!key) break;  // U is empty
-        const int v = 255 - (int)(key & 0xff);
         if (lane == 0) s_picks[npk] = v;
         npk++;
         if (v < 64) S0 |= 1ull << v; else S1 |= 1ull << (v - 64);
@@ -117,7 +150,13 @@ __global__ void __launch_bounds__(32) greedy_small_kernel(gr_batch in, gr_result
     const bool ok = status == GR_SAT || status == GR_SAT_NEG_VIOLATED;
     out.assign[(size_t)b * W] = ok ? S0 : 0;
     if (W > 1) out.assign[(size_t)b * W + 1] = ok ? S1 : 0;
-    out.cost[b] = ok ? (u64)(__popcll(S0) + __popcll(S1)) : ~0ull;
+    u64 cost = (u64)(__popcll(S0) + __popcll(S1));
+    if (wgt) {
+      cost = 0;
+      for (u64 a = S0; a; a &= a - 1) cost += wb[__ffsll((long long)a) - 1];
+      for (u64 a = S1; a; a &= a - 1) cost += wb[64 + __ffsll((long long)a) - 1];
+    }
+    out.cost[b] = ok ? cost : ~0ull;
     out.status[b] = status;
   }
 }

@@ -477,3 +477,49 @@ def test_incremental_kstart_monotone():
         assert (inc.status, inc.assign, inc.cost) == (full.status, full.assign, full.cost)
         assert inc.decided <= full.decided
         assert full.cost >= r0.cost or full.status == UNSAT  # the optimum never decreases
+
+
+# ------------------------------------------------------- weighted mhs (f4)
+def test_weighted_greedy_pins():
+    # phi+ = {b1 v b2}, w(b1) = 100, w(b2) = 1 -> only b2 true
+    st, a, picks = oracle.greedy(2, 1, masks_of([[1, 2]], []), w=[100, 1])
+    assert synth.mask_to_vars(a) == [2] and picks.tolist() == [1]
+    # unit (or constant) weights reduce to the unweighted greedy
+    rng = random.Random(41)
+    for _ in range(60):
+        m = rng.randint(2, 12)
+        pos, neg, _ = rand_instance(rng, m, rng.randint(1, 14))
+        mk = masks_of(pos, neg)
+        ref = oracle.greedy(m, len(pos), mk)
+        for c in (1, 7):
+            got = oracle.greedy(m, len(pos), mk, w=[c] * m)
+            assert got[0] == ref[0] and (got[1] == ref[1]).all() and (got[2] == ref[2]).all()
+
+
+def test_weighted_greedy_chvatal_bound_and_scaling():
+    """Chvatal 1979: the ratio greedy costs at most H(Delta+) x the weighted
+    optimum (here: WPMS over phi+ alone); scaling all weights changes nothing."""
+    rng = random.Random(43)
+    for _ in range(120):
+        m = rng.randint(2, 10)
+        pos, _, _ = rand_instance(rng, m, rng.randint(1, 12), p_neg=0.0)
+        if not pos:
+            continue
+        w = [rng.randint(1, 30) for _ in range(m)]
+        mk = masks_of(pos, [])
+        st, a, picks = oracle.greedy(m, len(pos), mk, w=w)
+        chosen = synth.mask_to_vars(a)
+        check_greedy_invariants_weighted(pos, chosen)
+        cost = sum(w[v - 1] for v in chosen)
+        opt = oracle.pms(m, len(pos), mk, w=w).cost
+        delta = max(sum(1 for c in pos if v in c) for v in range(1, m + 1))
+        assert opt <= cost <= sum(Fraction(1, i) for i in range(1, delta + 1)) * opt
+        st3, a3, p3 = oracle.greedy(m, len(pos), mk, w=[3 * x for x in w])
+        assert (a3 == a).all() and p3.tolist() == picks.tolist()
+
+
+def check_greedy_invariants_weighted(pos, chosen):
+    S = set(chosen)
+    assert all(set(c) & S for c in pos)
+    for x in S:
+        assert any(set(c) & S == {x} for c in pos)

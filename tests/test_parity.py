@@ -462,3 +462,24 @@ def test_incremental_kstart():
         o = oracle.pms_kstart(m, npos, mk, int(ks[b]))
         if o.status == 0:
             assert int(got["decided"][b]) == o.decided, b
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_weighted_greedy_and_solve(seed):
+    """f4: the weighted mhs (ratio greedy) and the composite Solve built on it."""
+    cb = rand_batch(500 + seed, 300, 30 if seed < 2 else 100, 16, weighted=True,
+                    W=1 if seed < 2 else 2)
+    db = gr.DeviceBatch.from_host(cb, flags=gr.GR_FLAG_WEIGHTED_GREEDY)
+    g = gr.mhs_greedy(db).to_host()
+    o = oracle.batch("greedy_w", cb)
+    assert (g["status"] == o.status).all()
+    assert (g["assign"] == o.assign).all()
+    assert (g["cost"] == o.cost).all()
+    if seed < 2:  # the exact fallback needs support <= 64
+        fb = torch.zeros(cb.B, dtype=torch.int32, device="cuda")
+        s = gr.solve(db, gr.GR_STRATEGY_MHS, fell_back=fb).to_host()
+        so = oracle.batch("solve_w", cb)
+        keep = so.status != -1
+        assert (s["status"][keep] == so.status[keep]).all()
+        assert (s["assign"][keep] == so.assign[keep]).all()
+        assert (s["cost"][keep] == so.cost[keep]).all()
