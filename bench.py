@@ -234,9 +234,8 @@ def main():
         if sharded:  # rank-range sharding of each level, NCCL all-reduce MIN per level
             multigpu.solve_exact_sharded(dbx, gr.PMS, rank, world, out=o[0])
             multigpu.solve_exact_sharded(dbx, gr.MHS, rank, world, out=o[1])
-        else:
-            gr.solve_pms(dbx, o[0])
-            gr.mhs_exact(dbx, o[1])
+        else:  # PMS and MHS level loops interleaved on two streams
+            gr.solve_pms_mhs(dbx, o[0], o[1])
         gr.mhs_greedy(dbx, o[2])
 
     for _ in range(a.warmup):
@@ -266,9 +265,22 @@ def main():
         cands_rank = cands / world  # every rank holds the full result
     else:
         cands_rank = cands
-    # ---------------- work counters (untimed, counting instantiation) ------
+    # ---------------- roofline pass (untimed): the solves serialised so launch
+    # durations are not shared between streams, then the counting instantiation
+    def serial_step(dbx, o):
+        if sharded:
+            step(dbx, o)
+        else:
+            gr.solve_pms(dbx, o[0])
+            gr.mhs_exact(dbx, o[1])
+            gr.mhs_greedy(dbx, o[2])
+
+    flush.fill_(1)
+    rprof = gr.profiler(1).start()
+    serial_step(db, outs)
+    kern_serial = rprof.stop()
     wprof = gr.profiler(2).start()
-    step(db, outs)
+    serial_step(db, outs)
     wk = wprof.stop()
     # ---------------- e2e through the public API from pinned host buffers --
     e2e_ms, h2d, d2h = None, 0, 0
@@ -300,7 +312,7 @@ def main():
     value = cands_all * a.steps / sec
     # ---------------- roofline of the dominant kernel (enum_kernel) ---------
     pk = peaks()
-    ek = kern.get("enum_kernel", {"launches": 0, "ms": 0.0})
+    ek = kern_serial.get("enum_kernel", {"launches": 0, "ms": 0.0})
     ew = wk.get("enum_kernel", {"launches": 0, "work": [0, 0, 0, 0]})
     tests, blocks, wcands, tests64 = ew["work"]
     wide = int((cb.m > 32).sum()) > cb.B // 2
@@ -324,7 +336,9 @@ def main():
                                f"{pk['sm_max_mhz']:.0f} MHz ({pk['source']})",
                 "clause_test_frac": test_ops / ew["launches"] / per_launch_s / 1e12 / peak_tops,
                 "ncu": ncu_evidence("enum_kernel"),
-                "share_of_step": ek["ms"] / total_ms if total_ms else None}
+                "launch_timing": "untimed serialised pass (the timed step overlaps PMS and MHS on two streams)",
+                "share_of_step": kern.get("enum_kernel", {"ms": 0.0})["ms"] / total_ms if total_ms else None,
+                "share_note": "summed enum_kernel event time / step time; > 1 when the two streams overlap"}
     line = {
         "metric": METRIC, "value": value, "unit": "candidates/s", "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": total_ms / a.steps,

@@ -28,7 +28,7 @@ EXPORTED = [
     "gr_exact_level", "gr_exact_level_keys", "gr_exact_finish", "gr_bitmatrix_ld",
     "gr_pack_varmajor", "gr_pack_clausemajor", "gr_greedy_matrix_workspace_bytes",
     "gr_mhs_greedy_matrix", "gr_greedy_count_shard", "gr_last_error", "gr_version",
-    "gr_profile", "gr_profile_read", "gr_launch_count", "gr_solve",
+    "gr_profile", "gr_profile_read", "gr_launch_count", "gr_solve", "gr_solve_pms_mhs",
 ]
 GR_STRATEGY_MHS, GR_STRATEGY_MAXSAT = 0, 1
 
@@ -77,6 +77,8 @@ def lib():
             f.restype = C.c_int
         L.gr_exact_prepare.argtypes = [vp, C.c_int, vp, vp, sz, vp, vp]
         L.gr_solve.argtypes = [vp, C.c_int, vp, vp, vp, sz, vp]
+        L.gr_solve_pms_mhs.argtypes = [vp, vp, vp, vp, sz, vp, vp]
+        L.gr_solve_pms_mhs.restype = C.c_int
         L.gr_solve.restype = C.c_int
         L.gr_profile.argtypes = [C.c_int]
         L.gr_profile.restype = C.c_int
@@ -250,6 +252,36 @@ def solve_pms(db: DeviceBatch, out: Optional[DeviceResult] = None, stream=None) 
 def mhs_exact(db: DeviceBatch, out: Optional[DeviceResult] = None, stream=None) -> DeviceResult:
     """(b) exact MHS of phi+ (gr_mhs_exact)."""
     return _solve("gr_mhs_exact", MHS, db, out, stream)
+
+
+_side_streams = {}
+
+
+def solve_pms_mhs(db: DeviceBatch, out_pms: Optional[DeviceResult] = None,
+                  out_mhs: Optional[DeviceResult] = None, stream=None):
+    """(a) + (b) at once (gr_solve_pms_mhs): PMS on the current stream, MHS on a
+    side stream of the same device; the current stream waits for both."""
+    torch = _torch()
+    L = lib()
+    b = db.struct(True)
+    nbytes = L.gr_workspace_bytes(C.byref(b), PMS)
+    if nbytes == 0:
+        raise GrError("gr_workspace_bytes rejected the batch")
+    half = (nbytes + 255) // 256 * 256
+    ws = workspace(2 * half, db.m.device, tag="pair")
+    dev = db.m.device
+    out_pms = out_pms if out_pms is not None else DeviceResult.empty(db.B, db.W, dev)
+    out_mhs = out_mhs if out_mhs is not None else DeviceResult.empty(db.B, db.W, dev)
+    s1 = stream if stream is not None else torch.cuda.current_stream(dev)
+    s2 = _side_streams.get(str(dev))
+    if s2 is None:
+        s2 = _side_streams[str(dev)] = torch.cuda.Stream(device=dev)
+    s2.wait_stream(s1)  # inputs produced on the current stream
+    r1, r2 = out_pms.struct(), out_mhs.struct()
+    _check(L.gr_solve_pms_mhs(C.byref(b), C.byref(r1), C.byref(r2), _ptr(ws), ws.numel(),
+                              int(s1.cuda_stream), int(s2.cuda_stream)), "gr_solve_pms_mhs")
+    s1.wait_stream(s2)
+    return out_pms, out_mhs
 
 
 def mhs_greedy(db: DeviceBatch, out: Optional[DeviceResult] = None, stream=None) -> DeviceResult:

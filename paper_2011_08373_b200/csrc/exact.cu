@@ -1052,6 +1052,51 @@ extern "C" int gr_solve_pms(const gr_batch *in, gr_result *out, void *ws, size_t
   return solve_exact(in, out, ws, ws_bytes, s, 0);
 }
 
+// PMS and MHS of one batch with their level loops interleaved on two streams
+// (the small levels and level tails of one overlap the other's work).
+extern "C" int gr_solve_pms_mhs(const gr_batch *in, gr_result *out_pms, gr_result *out_mhs,
+                                void *ws, size_t ws_bytes, gr_stream_t s_pms, gr_stream_t s_mhs) {
+  int rc = validate_batch(in, 0);
+  if (rc) return rc;
+  const size_t half = align256(layout_of(in).total);
+  if (!ws || ws_bytes < 2 * half) { gr_set_error("workspace too small (2 x gr_workspace_bytes)"); return GR_EWORKSPACE; }
+  void *ws1 = ws, *ws2 = (char *)ws + half;
+  int32_t n1 = 0, n2 = 0;
+  rc = gr_exact_prepare(in, 0, out_pms, ws1, half, s_pms, nullptr);
+  if (rc) return rc;
+  rc = gr_exact_prepare(in, 1, out_mhs, ws2, half, s_mhs, nullptr);
+  if (rc) return rc;
+  int *h = pinned_i32();
+  if (!h) { gr_set_error("cudaMallocHost failed"); return GR_ECUDA; }
+  cudaStream_t st1 = (cudaStream_t)s_pms, st2 = (cudaStream_t)s_mhs;
+  WS w1 = ws_of(in, ws1), w2 = ws_of(in, ws2);
+  GR_CUDA(cudaMemcpyAsync(h, &w1.ctrl->n_remaining, sizeof(int), cudaMemcpyDeviceToHost, st1));
+  GR_CUDA(cudaMemcpyAsync(h + 1, &w2.ctrl->n_remaining, sizeof(int), cudaMemcpyDeviceToHost, st2));
+  GR_CUDA(cudaStreamSynchronize(st1));
+  GR_CUDA(cudaStreamSynchronize(st2));
+  n1 = h[0];
+  n2 = h[1];
+  const int SPEC = 4;
+  for (int k = 1; (n1 > 0 || n2 > 0) && k <= 64;) {
+    const bool a1 = n1 > 0, a2 = n2 > 0;
+    for (int i = 0; i < SPEC && k <= 64; i++, k++) {
+      if (a1) {
+        if ((rc = gr_exact_level(in, 0, k, 0, 1, ws1, half, s_pms))) return rc;
+        if ((rc = gr_exact_finish(in, 0, k, out_pms, ws1, half, s_pms, nullptr))) return rc;
+      }
+      if (a2) {
+        if ((rc = gr_exact_level(in, 1, k, 0, 1, ws2, half, s_mhs))) return rc;
+        if ((rc = gr_exact_finish(in, 1, k, out_mhs, ws2, half, s_mhs, nullptr))) return rc;
+      }
+    }
+    if (a1) GR_CUDA(cudaMemcpyAsync(h, &w1.ctrl->n_remaining, sizeof(int), cudaMemcpyDeviceToHost, st1));
+    if (a2) GR_CUDA(cudaMemcpyAsync(h + 1, &w2.ctrl->n_remaining, sizeof(int), cudaMemcpyDeviceToHost, st2));
+    if (a1) { GR_CUDA(cudaStreamSynchronize(st1)); n1 = h[0]; }
+    if (a2) { GR_CUDA(cudaStreamSynchronize(st2)); n2 = h[1]; }
+  }
+  return GR_OK;
+}
+
 extern "C" int gr_mhs_exact(const gr_batch *in, gr_result *out, void *ws, size_t ws_bytes,
                             gr_stream_t s) {
   return solve_exact(in, out, ws, ws_bytes, s, 1);

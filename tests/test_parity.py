@@ -483,3 +483,16 @@ def test_weighted_greedy_and_solve(seed):
         assert (s["status"][keep] == so.status[keep]).all()
         assert (s["assign"][keep] == so.assign[keep]).all()
         assert (s["cost"][keep] == so.cost[keep]).all()
+
+
+def test_pms_mhs_pair_on_two_streams():
+    cb = synth.c2_batch()
+    db = gr.DeviceBatch.from_host(cb)
+    p, h = gr.solve_pms_mhs(db)
+    p, h = p.to_host(), h.to_host()
+    e = np.load(os.path.join(GOLDEN, "expected_c2.npz"))
+    for f in ("status", "assign", "cost"):
+        assert (p[f].reshape(cb.B, -1) == e[f"pms_{f}"].reshape(cb.B, -1)).all()
+        assert (h[f].reshape(cb.B, -1) == e[f"mhs_{f}"].reshape(cb.B, -1)).all()
+    rp, rh = gr.solve_pms(db).to_host(), gr.mhs_exact(db).to_host()
+    assert (p["decided"] == rp["decided"]).all() and (h["decided"] == rh["decided"]).all()
