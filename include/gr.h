@@ -209,6 +209,9 @@ typedef struct {
   const int64_t *pos_off; /* [n_pos+1] or NULL */
   const void *pos_var;    /* [pos_off[n_pos]] int16 / int32 variable ids, or NULL */
   int32_t var_bytes;      /* 2 or 4 when pos_var is given; m <= 50000 (shared histogram) */
+  const uint32_t *w;      /* [m] weights >= 1 or NULL: the weighted mhs (SURVEY §8(f) f4,
+                             reading R20) -- pick the variable maximising uncovered hits /
+                             weight, exact cross-multiplied comparison, lowest index on ties */
 } gr_bitmatrix;
 
 /* Row stride (words) the library uses for n_pos clauses: a multiple of 64. */
@@ -216,9 +219,9 @@ int64_t gr_bitmatrix_ld(int64_t n_pos);
 
 /* Pack CSR variable lists into the variable-major bit matrix (clause packing
  * step a1).  off [n+1] int64, var [off[n]] int16 (var_bytes = 2) or int32
- * (var_bytes = 4), 0-based variable ids.  For m <= 4096 every word of
- * bits [m][ld] is written (shared-memory tiles, no need to clear it); for
- * larger m bits must be zeroed by the caller.  *d_bad (device int32, may be NULL) gets bit 1 if some id is outside
+ * (var_bytes = 4), 0-based variable ids.  Every word of bits [m][ld] is
+ * written (shared-memory tiles; ld a multiple of 16, as gr_bitmatrix_ld
+ * gives), so it need not be cleared.  *d_bad (device int32, may be NULL) gets bit 1 if some id is outside
  * [0, m), bit 2 if some clause is empty (phi is then UNSAT, R6), bit 4 if a
  * clause lists a variable twice. */
 int gr_pack_varmajor(int32_t m, int64_t n, const int64_t *off, const void *var, int var_bytes,

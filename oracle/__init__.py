@@ -57,6 +57,8 @@ def lib():
         L.or_pms_brute.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, p, p, p, p, p]
         L.or_mhs.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, p, C.c_int, p, p, p, p]
         L.or_greedy.argtypes = [C.c_int, C.c_int64, p, p, C.c_int64, p, p, p, p, p, p, p]
+        L.or_greedy_w.argtypes = [C.c_int, C.c_int64, p, p, C.c_int64, p, p, p, p, p, p, p, p]
+        L.or_greedy_w.restype = C.c_int
         L.or_greedy_masks.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, p, p, p, p, p]
         L.or_greedy_masks_w.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, p, p, p, p, p, p]
         L.or_greedy_masks_w.restype = C.c_int
@@ -156,7 +158,8 @@ class GreedyResult:
     n_final: int
 
 
-def greedy_csr(m, pos_off, pos_var, neg_off, neg_var) -> GreedyResult:
+def greedy_csr(m, pos_off, pos_var, neg_off, neg_var, w=None) -> GreedyResult:
+    """Greedy over CSR clause lists; with weights w the weighted (ratio) greedy."""
     pos_off = np.ascontiguousarray(pos_off, np.int64)
     pos_var = np.ascontiguousarray(pos_var, np.int32)
     neg_off = np.ascontiguousarray(neg_off, np.int64)
@@ -164,9 +167,15 @@ def greedy_csr(m, pos_off, pos_var, neg_off, neg_var) -> GreedyResult:
     picks = np.zeros(max(m, 1), np.int32)
     inS = np.zeros(max(m, 1), np.uint8)
     nu, nf, st = np.zeros(1, np.int32), np.zeros(1, np.int32), np.zeros(1, np.int32)
-    rc = lib().or_greedy(m, pos_off.shape[0] - 1, _ptr(pos_off), _ptr(pos_var),
-                         neg_off.shape[0] - 1, _ptr(neg_off), _ptr(neg_var), _ptr(picks),
-                         _ptr(nu), _ptr(inS), _ptr(nf), _ptr(st))
+    if w is None:
+        rc = lib().or_greedy(m, pos_off.shape[0] - 1, _ptr(pos_off), _ptr(pos_var),
+                             neg_off.shape[0] - 1, _ptr(neg_off), _ptr(neg_var), _ptr(picks),
+                             _ptr(nu), _ptr(inS), _ptr(nf), _ptr(st))
+    else:
+        wa = np.ascontiguousarray(np.asarray(w, np.uint32))
+        rc = lib().or_greedy_w(m, pos_off.shape[0] - 1, _ptr(pos_off), _ptr(pos_var),
+                               neg_off.shape[0] - 1, _ptr(neg_off), _ptr(neg_var), _ptr(wa),
+                               _ptr(picks), _ptr(nu), _ptr(inS), _ptr(nf), _ptr(st))
     if rc:
         raise RuntimeError(f"or_greedy failed: {rc}")
     return GreedyResult(int(st[0]), picks[: int(nu[0])].copy(), inS[:m].copy(), int(nf[0]))

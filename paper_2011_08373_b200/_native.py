@@ -55,7 +55,7 @@ class GrKernelStat(C.Structure):
 class GrBitmatrix(C.Structure):
     _fields_ = [("m", C.c_int32), ("n_pos", C.c_int64), ("ld", C.c_int64), ("bits", C.c_void_p),
                 ("n_neg", C.c_int32), ("neg", C.c_void_p), ("pos_off", C.c_void_p),
-                ("pos_var", C.c_void_p), ("var_bytes", C.c_int32)]
+                ("pos_var", C.c_void_p), ("var_bytes", C.c_int32), ("w", C.c_void_p)]
 
 
 _lib = None
@@ -377,11 +377,13 @@ class DeviceBitMatrix:
     bad: int = 0  # 1: id out of range, 2: empty positive clause, 4: repeated id in a clause
     pos_off: "object" = None  # device CSR of phi+ (enables the incremental greedy)
     pos_var: "object" = None
+    w: "object" = None  # optional int32 view of uint32 weights [m] (weighted mhs, f4)
 
     def struct(self) -> GrBitmatrix:
         vb = 0 if self.pos_var is None else self.pos_var.element_size()
         return GrBitmatrix(self.m, self.n_pos, self.ld, _ptr(self.bits), self.n_neg,
-                           _ptr(self.neg), _ptr(self.pos_off), _ptr(self.pos_var), vb)
+                           _ptr(self.neg), _ptr(self.pos_off), _ptr(self.pos_var), vb,
+                           _ptr(self.w))
 
 
 def pack_bitmatrix(m, pos_off, pos_var, neg_off, neg_var, device="cuda", stream=None,
@@ -401,8 +403,8 @@ def pack_bitmatrix(m, pos_off, pos_var, neg_off, neg_var, device="cuda", stream=
     no, nv = dev(neg_off, np.int64), dev(neg_var, None)
     n_pos, n_neg = int(po.numel() - 1), int(no.numel() - 1)
     ld = bitmatrix_ld(n_pos)
-    # m <= 4096: the tiled device pack writes every word (no clearing pass)
-    bits = (torch.empty if m <= 4096 else torch.zeros)((m, ld), dtype=torch.int64, device=device)
+    # the tiled device pack writes every word (no clearing pass)
+    bits = torch.empty((m, ld), dtype=torch.int64, device=device)
     mw = (m + 63) // 64
     neg = torch.zeros((max(n_neg, 1), mw), dtype=torch.int64, device=device)
     bad = torch.zeros(1, dtype=torch.int32, device=device)

@@ -265,31 +265,42 @@ __global__ void __launch_bounds__(CT, 1) count_kernel(CountParams p) {
 }
 
 // ---- argmax + bookkeeping (one CTA) ------------------------------------------
+// The pick maximises count[v] / w[v] (w = 1 without weights: the plain
+// argmax), compared exactly as c_a * w_b > c_b * w_a, lowest index on ties
+// (readings R11, R20).
+struct Cand {
+  u32 c, w;
+  int v;
+};
+struct CandBetter {
+  __device__ __forceinline__ Cand operator()(const Cand &a, const Cand &b) const {
+    const u64 l = (u64)a.c * b.w, r = (u64)b.c * a.w;
+    return (l > r || (l == r && a.v < b.v)) ? a : b;
+  }
+};
 constexpr int AT = 1024;
-__global__ void __launch_bounds__(AT) argmax_kernel(u32 *counts, int m, GCtrl *ctrl, int *picks) {
-  typedef cub::BlockReduce<u64, AT> Red;
+__global__ void __launch_bounds__(AT) argmax_kernel(u32 *counts, int m, const u32 *w, GCtrl *ctrl,
+                                                    int *picks) {
+  typedef cub::BlockReduce<Cand, AT> Red;
   __shared__ typename Red::TempStorage tmp;
   if (*(volatile int *)&ctrl->done) return;
-  u64 best = 0;
+  Cand best{0u, 1u, 0x7fffffff};
   for (int v = threadIdx.x; v < m; v += AT) {
-    const u32 c = counts[v];
+    const Cand cv{counts[v], w ? w[v] : 1u, v};
     counts[v] = 0;  // ready for the next pass
-    const u64 key = ((u64)c << 32) | (u64)(0xffffffffu - (u32)v);
-    best = key > best ? key : best;
+    best = CandBetter()(cv, best);
   }
-  best = Red(tmp).Reduce(best, cub::Max());
+  best = Red(tmp).Reduce(best, CandBetter());
   if (threadIdx.x == 0) {
-    const u32 c = (u32)(best >> 32);
-    ctrl->maxcount = c;
+    ctrl->maxcount = best.c;
     ctrl->upar ^= 1;  // the pass just run wrote U[upar ^ 1]
-    if (c == 0) {
+    if (best.c == 0) {
       ctrl->done = 1;
       ctrl->vprev = -1;
     } else {
-      const int v = (int)(0xffffffffu - (u32)(best & 0xffffffffu));
-      picks[ctrl->npicks] = v;
+      picks[ctrl->npicks] = best.v;
       ctrl->npicks += 1;
-      ctrl->vprev = v;
+      ctrl->vprev = best.v;
     }
   }
 }
@@ -344,31 +355,29 @@ __global__ void csr_hist_kernel(int64_t n, const int64_t *off, const V *var, int
 
 constexpr int IT = 512;
 // the argmax of the counts (lowest index on ties) -> ctrl (pick or done)
-__device__ __forceinline__ void pick_argmax(const u32 *counts, int m, GCtrl *ctrl, int *picks) {
-  typedef cub::BlockReduce<u64, IT> Red;
+__device__ __forceinline__ void pick_argmax(const u32 *counts, int m, const u32 *w, GCtrl *ctrl,
+                                            int *picks) {
+  typedef cub::BlockReduce<Cand, IT> Red;
   __shared__ typename Red::TempStorage tmp;
-  u64 key = 0;
-  for (int v = threadIdx.x; v < m; v += IT) {
-    const u64 k = ((u64)__ldcg(&counts[v]) << 32) | (u64)(0xffffffffu - (u32)v);
-    key = k > key ? k : key;
-  }
-  key = Red(tmp).Reduce(key, cub::Max());
+  Cand best{0u, 1u, 0x7fffffff};
+  for (int v = threadIdx.x; v < m; v += IT)
+    best = CandBetter()(Cand{__ldcg(&counts[v]), w ? w[v] : 1u, v}, best);
+  best = Red(tmp).Reduce(best, CandBetter());
   if (threadIdx.x == 0) {
-    if ((key >> 32) == 0) {  // every count is 0: U is empty
+    if (best.c == 0) {  // every count is 0: U is empty
       ctrl->done = 1;
       ctrl->pending = -1;
     } else {
-      const int v = (int)(0xffffffffu - (u32)(key & 0xffffffffu));
-      picks[ctrl->npicks] = v;
+      picks[ctrl->npicks] = best.v;
       ctrl->npicks += 1;
-      ctrl->pending = v;
+      ctrl->pending = best.v;
     }
   }
 }
 
-__global__ void __launch_bounds__(IT) first_pick_kernel(const u32 *counts, int m, GCtrl *ctrl,
-                                                       int *picks) {
-  pick_argmax(counts, m, ctrl, picks);
+__global__ void __launch_bounds__(IT) first_pick_kernel(const u32 *counts, int m, const u32 *w,
+                                                       GCtrl *ctrl, int *picks) {
+  pick_argmax(counts, m, w, ctrl, picks);
 }
 
 // one pick: apply the pending pick v (cover its clauses, decrement counts),
@@ -376,7 +385,8 @@ __global__ void __launch_bounds__(IT) first_pick_kernel(const u32 *counts, int m
 template <typename V>
 __global__ void __launch_bounds__(IT) incr_step_kernel(const u64 *R, int64_t ld, int m, u64 *U,
                                                       u32 *counts, const int64_t *off,
-                                                      const V *var, GCtrl *ctrl, int *picks) {
+                                                      const V *var, const u32 *w, GCtrl *ctrl,
+                                                      int *picks) {
   extern __shared__ u32 hist[];
   __shared__ int s_last;
   if (*(volatile int *)&ctrl->done) return;
@@ -407,7 +417,7 @@ __global__ void __launch_bounds__(IT) incr_step_kernel(const u64 *R, int64_t ld,
   __syncthreads();
   if (s_last) {
     __threadfence();
-    pick_argmax(counts, m, ctrl, picks);
+    pick_argmax(counts, m, w, ctrl, picks);
     if (threadIdx.x == 0) {
       ctrl->ticket = 0;
       ctrl->steps += 1;
@@ -531,38 +541,52 @@ __global__ void pack_vm_kernel(int m, int64_t n, const int64_t *off, const V *va
   }
 }
 
-// Tiled var-major pack (m <= 4096): a CTA owns 256 clause columns (4 words of
-// every row), builds them in shared memory with shared atomics, and writes
-// each row's 32-byte segment once -- every word of the matrix is written
-// (zeros included), so the caller need not clear it.
-constexpr int PK_T = 256;
+// Tiled var-major pack: a CTA owns a tile of PK_R rows x PK_C clauses (16
+// words = one 128-byte line per row), builds it in shared memory with shared
+// atomics (flagging out-of-range / empty / repeated ids) and writes every
+// row's line once -- every word of the matrix is written (zeros included), so
+// the caller need not clear it.  Each clause list is read once per row block.
+constexpr int PK_T = 512;
+constexpr int PK_R = 1024;            // rows per tile
+constexpr int PK_W = 16;              // words per tile row (1024 clauses)
+constexpr size_t PK_SMEM = (size_t)PK_R * PK_W * 8;  // 128 KB
 template <typename V>
 __global__ void __launch_bounds__(PK_T) pack_vm_tiled_kernel(int m, int64_t n, const int64_t *off,
                                                             const V *var, u64 *bits, int64_t ld,
                                                             int32_t *bad) {
-  extern __shared__ unsigned long long tile[];  // [m][4]
-  const int64_t ngroups = ld / 4;
+  extern __shared__ unsigned long long tile[];  // [PK_R][PK_W]
+  const int nrb = (m + PK_R - 1) / PK_R;
+  const int64_t ncb = ld / PK_W;
   int flags = 0;
-  for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
-    for (int q = threadIdx.x; q < m * 4; q += PK_T) tile[q] = 0;
+  for (int64_t g = blockIdx.x; g < (int64_t)nrb * ncb; g += gridDim.x) {
+    const int rb = (int)(g % nrb);
+    const int64_t cb = g / nrb;
+    const int r0 = rb * PK_R;
+    const int nr = min(PK_R, m - r0);
+    for (int q = threadIdx.x; q < PK_R * PK_W; q += PK_T) tile[q] = 0;
     __syncthreads();
-    const int64_t c = g * 256 + threadIdx.x;
-    if (c < n) {
+    for (int cc = threadIdx.x; cc < PK_W * 64; cc += PK_T) {
+      const int64_t c = cb * (PK_W * 64) + cc;
+      if (c >= n) break;
       const int64_t e0 = off[c], e1 = off[c + 1];
-      if (e1 <= e0) flags |= 2;
-      const int wq = threadIdx.x >> 6;
-      const unsigned long long bit = 1ull << (threadIdx.x & 63);
+      if (rb == 0 && e1 <= e0) flags |= 2;
+      const unsigned long long bit = 1ull << (cc & 63);
       for (int64_t e = e0; e < e1; e++) {
         const int v = (int)var[e];
-        if (v < 0 || v >= m) { flags |= 1; continue; }
-        if (atomicOr(&tile[v * 4 + wq], bit) & bit) flags |= 4;
+        if (v < 0 || v >= m) {
+          if (rb == 0) flags |= 1;
+          continue;
+        }
+        if (v < r0 || v >= r0 + nr) continue;
+        if (atomicOr(&tile[(v - r0) * PK_W + (cc >> 6)], bit) & bit) flags |= 4;
       }
     }
     __syncthreads();
-    for (int r = threadIdx.x; r < m; r += PK_T) {
-      ulonglong2 *dst = (ulonglong2 *)(bits + (size_t)r * ld + g * 4);
-      dst[0] = make_ulonglong2(tile[r * 4], tile[r * 4 + 1]);
-      dst[1] = make_ulonglong2(tile[r * 4 + 2], tile[r * 4 + 3]);
+    // write: 8 threads per row, 16 bytes each -> one 128-byte line per row
+    for (int q = threadIdx.x; q < nr * (PK_W / 2); q += PK_T) {
+      const int r = q / (PK_W / 2), h = q % (PK_W / 2);
+      ulonglong2 *dst = (ulonglong2 *)(bits + (size_t)(r0 + r) * ld + cb * PK_W) + h;
+      *dst = make_ulonglong2(tile[r * PK_W + 2 * h], tile[r * PK_W + 2 * h + 1]);
     }
     __syncthreads();
   }
@@ -626,19 +650,18 @@ extern "C" int gr_pack_varmajor(int32_t m, int64_t n, const int64_t *off, const 
   }
   if (n == 0) return GR_OK;
   cudaStream_t st = (cudaStream_t)s;
-  if (m <= 4096 && ld % 4 == 0) {
+  if (ld % PK_W == 0) {
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(pack_vm_tiled_kernel<int16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 32);
-      cudaFuncSetAttribute(pack_vm_tiled_kernel<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 32);
+      cudaFuncSetAttribute(pack_vm_tiled_kernel<int16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PK_SMEM);
+      cudaFuncSetAttribute(pack_vm_tiled_kernel<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PK_SMEM);
       attr = true;
     }
-    const size_t sm = (size_t)m * 32;
-    const int grid = (int)std::min<int64_t>(ld / 4, 148 * 4);
+    const int grid = 148;
     if (var_bytes == 2)
-      GR_LAUNCH("pack_vm_tiled_kernel", st, pack_vm_tiled_kernel<int16_t><<<grid, PK_T, sm, st>>>(m, n, off, (const int16_t *)var, bits, ld, d_bad));
+      GR_LAUNCH("pack_vm_tiled_kernel", st, pack_vm_tiled_kernel<int16_t><<<grid, PK_T, PK_SMEM, st>>>(m, n, off, (const int16_t *)var, bits, ld, d_bad));
     else
-      GR_LAUNCH("pack_vm_tiled_kernel", st, pack_vm_tiled_kernel<int32_t><<<grid, PK_T, sm, st>>>(m, n, off, (const int32_t *)var, bits, ld, d_bad));
+      GR_LAUNCH("pack_vm_tiled_kernel", st, pack_vm_tiled_kernel<int32_t><<<grid, PK_T, PK_SMEM, st>>>(m, n, off, (const int32_t *)var, bits, ld, d_bad));
     return GR_OK;
   }
   const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
@@ -719,18 +742,18 @@ extern "C" int gr_mhs_greedy_matrix(const gr_bitmatrix *in, uint64_t *assign, in
     else
       GR_LAUNCH("csr_hist_kernel", st, csr_hist_kernel<int32_t><<<std::max(hgrid, 1), 256, hs, st>>>(
                                           in->n_pos, in->pos_off, (const int32_t *)in->pos_var, in->m, counts));
-    GR_LAUNCH("first_pick_kernel", st, first_pick_kernel<<<1, IT, 0, st>>>(counts, in->m, ctrl, wpicks));
+    GR_LAUNCH("first_pick_kernel", st, first_pick_kernel<<<1, IT, 0, st>>>(counts, in->m, in->w, ctrl, wpicks));
     const int STEPS = 32;
     for (int round = 0;; round++) {
       for (int j = 0; j < STEPS; j++) {
         if (in->var_bytes == 2)
           GR_LAUNCH("incr_step_kernel", st, incr_step_kernel<int16_t><<<grid, IT, hs, st>>>(
                                                 in->bits, ld, in->m, U, counts, in->pos_off,
-                                                (const int16_t *)in->pos_var, ctrl, wpicks));
+                                                (const int16_t *)in->pos_var, in->w, ctrl, wpicks));
         else
           GR_LAUNCH("incr_step_kernel", st, incr_step_kernel<int32_t><<<grid, IT, hs, st>>>(
                                                 in->bits, ld, in->m, U, counts, in->pos_off,
-                                                (const int32_t *)in->pos_var, ctrl, wpicks));
+                                                (const int32_t *)in->pos_var, in->w, ctrl, wpicks));
       }
       GR_CUDA(cudaMemcpyAsync(h, ctrl, sizeof(GCtrl), cudaMemcpyDeviceToHost, st));
       GR_CUDA(cudaStreamSynchronize(st));
@@ -749,7 +772,7 @@ extern "C" int gr_mhs_greedy_matrix(const gr_bitmatrix *in, uint64_t *assign, in
         CountParams p{in->bits, ld, in->m, ntiles, U + (size_t)(t & 1) * ld,
                       U + (size_t)((t & 1) ^ 1) * ld, counts, ctrl, 1};
         GR_LAUNCH("count_kernel", (cudaStream_t)s, count_kernel<<<grid, CT, COUNT_SMEM_V2, st>>>(p));
-        GR_LAUNCH("argmax_kernel", (cudaStream_t)s, argmax_kernel<<<1, AT, 0, st>>>(counts, in->m, ctrl, wpicks));
+        GR_LAUNCH("argmax_kernel", (cudaStream_t)s, argmax_kernel<<<1, AT, 0, st>>>(counts, in->m, in->w, ctrl, wpicks));
       }
       GR_CUDA(cudaMemcpyAsync(h, ctrl, sizeof(GCtrl), cudaMemcpyDeviceToHost, st));
       GR_CUDA(cudaStreamSynchronize(st));

@@ -239,11 +239,13 @@ def csr_from_lists(cls):
     return off, var
 
 
-def check_matrix(m, pos, neg, keep_csr=True):
+def check_matrix(m, pos, neg, keep_csr=True, w=None):
     po, pv = csr_from_lists(pos)
     no, nv = csr_from_lists(neg)
-    o = oracle.greedy_csr(m, po, pv, no, nv)
+    o = oracle.greedy_csr(m, po, pv, no, nv, w=w)
     bm = gr.pack_bitmatrix(m, po, pv, no, nv, keep_csr=keep_csr)
+    if w is not None:
+        bm.w = torch.from_numpy(np.asarray(w, np.uint32).view(np.int32)).cuda()
     assert bm.bad == 0
     r = gr.mhs_greedy_matrix(bm)
     torch.cuda.synchronize()
@@ -264,6 +266,17 @@ def test_greedy_matrix_random(seed, keep_csr):
     pos = [sorted(rng.sample(range(m), rng.randint(1, min(m, 6)))) for _ in range(n)]
     neg = [sorted(rng.sample(range(m), min(m, 2))) for _ in range(5)]
     check_matrix(m, pos, neg, keep_csr)
+
+
+@pytest.mark.parametrize("keep_csr", [True, False])
+def test_weighted_greedy_matrix(keep_csr):
+    """f4 on the bit-matrix path (both the incremental and the recounting greedy)."""
+    rng = random.Random(17)
+    m, n = 300, 20000
+    pos = [sorted(rng.sample(range(m), rng.randint(1, 6))) for _ in range(n)]
+    neg = [sorted(rng.sample(range(m), 2)) for _ in range(5)]
+    w = [rng.randint(1, 40) for _ in range(m)]
+    check_matrix(m, pos, neg, keep_csr, w=w)
 
 
 def test_pack_flags():
