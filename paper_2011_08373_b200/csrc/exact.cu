@@ -77,7 +77,7 @@ Layout layout_of(const gr_batch *in) {
   L.active = take(4 * 2 * B);
   L.chunk_base = take(8 * (B + 1));
   L.pk = take(8 * (size_t)std::max<int64_t>(in->total_clauses, 1));
-  L.hrec = take(8 * 5 * (size_t)std::max<int64_t>(in->total_clauses, 1));
+  L.hrec = take(16 * 5 * (size_t)std::max<int64_t>(in->total_clauses, 1));
   L.total = o;
   return L;
 }
@@ -173,7 +173,11 @@ __device__ void write_result(const In &in, const Out &out, int b, int status, u6
   if (out.decided) out.decided[b] = decided;
 }
 
-__device__ u64 hitting(int j, u64 p);
+// A sub-block's candidate mask: up to 128 candidates in two words.
+struct F2 {
+  u64 lo, hi;
+};
+__device__ F2 hitting(int j, u64 p);
 
 // ---------------------------------------------------------------------------
 // pack: one CTA per instance
@@ -287,7 +291,7 @@ __global__ void __launch_bounds__(PT) pack_kernel(In in, Out out, WS ws, int whi
     const int64_t dst = lo + (j < np ? 0 : npr) + d;
     ws.pk[dst] = R[j];
     if (j < np)
-      for (int jj = 1; jj <= 5; jj++) ws.hrec[dst * 5 + jj - 1] = hitting(jj, R[j]);
+      for (int jj = 1; jj <= 5; jj++) ((F2 *)ws.hrec)[dst * 5 + jj - 1] = hitting(jj, R[j]);
   }
   // weights of the support variables (relabelled order) and S_k
   if (t < 64) {
@@ -375,19 +379,35 @@ __global__ void __launch_bounds__(PT) pack_kernel(In in, Out out, WS ws, int whi
 constexpr int JMAX = 5;
 constexpr int HREC = 5;  // per-clause record: H_1 (= P), H_2, H_3, H_4, H_5
 
+__device__ __forceinline__ F2 f2_and(F2 a, F2 b) { return F2{a.lo & b.lo, a.hi & b.hi}; }
+__device__ __forceinline__ F2 f2_andnot(F2 a, F2 b) { return F2{a.lo & ~b.lo, a.hi & ~b.hi}; }
+__device__ __forceinline__ bool f2_any(F2 a) { return (a.lo | a.hi) != 0; }
+__device__ __forceinline__ F2 f2_nbits(u64 n) {  // the n lowest bits, n <= 128
+  return n >= 128 ? F2{~0ull, ~0ull}
+                  : (n >= 64 ? F2{~0ull, (1ull << (n - 64)) - 1ull} : F2{(1ull << n) - 1ull, 0ull});
+}
+__device__ __forceinline__ int f2_ctz(F2 a) {
+  return a.lo ? __ffsll((long long)a.lo) - 1 : 64 + __ffsll((long long)a.hi) - 1;
+}
+__device__ __forceinline__ int f2_popc(F2 a) { return __popcll(a.lo) + __popcll(a.hi); }
+
+// R_j = the largest region with C(R_j, j) <= 128 (j = 1: every variable)
 __host__ __device__ constexpr int region_of(int j) {
-  return (int)((0x0807080B40ull >> (8 * (j - 1))) & 0xffull);  // 64, 11, 8, 7, 8
+  return (int)((0x09090A1040ull >> (8 * (j - 1))) & 0xffull);  // 64, 16, 10, 9, 9
 }
 __device__ __forceinline__ u64 nbits(u64 n) { return n >= 64 ? ~0ull : ((1ull << n) - 1ull); }
 
 // H_j(p): bit i set iff the i-th j-subset of [0, R_j) (colex order) meets p
-__device__ u64 hitting(int j, u64 p) {
-  if (j == 1) return p;
+__device__ F2 hitting(int j, u64 p) {
+  if (j == 1) return F2{p, 0ull};
   const int R = region_of(j);
   const u64 n = binom(R, j);
-  u64 x = (1ull << j) - 1, r = 0;
+  u64 x = (1ull << j) - 1;
+  F2 r{0ull, 0ull};
   for (u64 i = 0; i < n; i++) {
-    if (x & p) r |= 1ull << i;
+    if (x & p) {
+      if (i < 64) r.lo |= 1ull << i; else r.hi |= 1ull << (i - 64);
+    }
     const u64 c = x & (~x + 1), y = x + c;  // Gosper: next j-subset
     x = y | (((y ^ x) >> 2) >> (__ffsll((long long)c) - 1));
   }
@@ -403,43 +423,43 @@ struct Work {
 template <typename M>
 struct Clauses {
   const M *P;       // [np + nn] positives then negatives (uniform reads)
-  const u64 *H;     // [np][HREC] H_j(P) at H[q * HREC + j - 1]
-  const u64 *hitx;  // [6][64] HIT_j({x}) (0 when x >= R_j), shared memory
+  const F2 *H;      // [np][HREC] H_j(P) at H[q * HREC + j - 1]
+  const F2 *hitx;   // [6][64] HIT_j({x}) (0 when x >= R_j), shared memory
   const u32 *cs;    // [65][8] C(n, j) for j <= 5 (fits 32 bits), shared memory
   int np, nn;
 };
 
 template <typename M, bool COUNT>
-__device__ __forceinline__ u64 test_sub(int j, M U, int e, u64 F, const Clauses<M> &c, Work &wk) {
+__device__ __forceinline__ F2 test_sub(int j, M U, int e, F2 F, const Clauses<M> &c, Work &wk) {
   const int np = c.np;
-  const u64 *H = c.H + (j - 1);
+  const F2 *H = c.H + (j - 1);
   int q = 0;
   for (; q + 4 <= np; q += 4) {
     const M p0 = c.P[q], p1 = c.P[q + 1], p2 = c.P[q + 2], p3 = c.P[q + 3];
-    const u64 h0 = H[HREC * q], h1 = H[HREC * (q + 1)], h2 = H[HREC * (q + 2)],
-              h3 = H[HREC * (q + 3)];
-    if (!(U & p0)) F &= h0;
-    if (!(U & p1)) F &= h1;
-    if (!(U & p2)) F &= h2;
-    if (!(U & p3)) F &= h3;
+    const F2 h0 = H[HREC * q], h1 = H[HREC * (q + 1)], h2 = H[HREC * (q + 2)],
+             h3 = H[HREC * (q + 3)];
+    if (!(U & p0)) F = f2_and(F, h0);
+    if (!(U & p1)) F = f2_and(F, h1);
+    if (!(U & p2)) F = f2_and(F, h2);
+    if (!(U & p3)) F = f2_and(F, h3);
     if (COUNT) wk.tests += 4;
-    if (!F) return 0;
+    if (!f2_any(F)) return F;
   }
   for (; q < np; q++) {
-    if (!(U & c.P[q])) F &= H[HREC * q];
+    if (!(U & c.P[q])) F = f2_and(F, H[HREC * q]);
     if (COUNT) wk.tests += 1;
   }
-  if (!F) return 0;
+  if (!f2_any(F)) return F;
   const M lowm = (M)nbits((u64)e);
-  const u64 *hx = c.hitx + 64 * j;
+  const F2 *hx = c.hitx + 64 * j;
   for (int t = 0; t < c.nn; t++) {
     M rest = c.P[np + t] & ~U;
     if (COUNT) wk.tests += 1;
     if ((rest & ~lowm) || popc(rest) > j) continue;  // some variable of N stays false
-    u64 kill = ~0ull;
-    for (; rest; rest &= rest - 1) kill &= hx[ctz(rest)];
-    F &= ~kill;  // the S holding every variable of N outside U
-    if (!F) return 0;
+    F2 kill{~0ull, ~0ull};
+    for (; rest; rest &= rest - 1) kill = f2_and(kill, hx[ctz(rest)]);
+    F = f2_andnot(F, kill);  // the S holding every variable of N outside U
+    if (!f2_any(F)) return F;
   }
   return F;
 }
@@ -507,20 +527,21 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
     if (base >= r_hi) return best;
     const u64 n = CS(ea, j);
     if (n && base + n > r_lo) {
-      u64 F = nbits(n);
-      if (r_lo > base) F &= ~nbits(r_lo - base);
-      if (r_hi < base + n) F &= nbits(r_hi - base);
-      if (COUNT) { wk.blocks++; wk.cands += (u64)__popcll(F); }
+      F2 F = f2_nbits(n);
+      if (r_lo > base) F = f2_andnot(F, f2_nbits(r_lo - base));
+      if (r_hi < base + n) F = f2_and(F, f2_nbits(r_hi - base));
+      if (COUNT) { wk.blocks++; wk.cands += (u64)f2_popc(F); }
       F = test_sub<M, COUNT>(j, U, ea, F, c, wk);
-      if (F) {
+      if (f2_any(F)) {
         if (MODE == 2) {
-          for (u64 f = F; f; f &= f - 1) {
-            const u64 idx = (u64)(__ffsll((long long)f) - 1);
-            const i64 key = (i64)((weight_of<M>(j, idx, U, w) << rb) | (base + idx));
-            best = key < best ? key : best;
-          }
+          for (int h = 0; h < 2; h++)
+            for (u64 f = h ? F.hi : F.lo; f; f &= f - 1) {
+              const u64 idx = (u64)(64 * h + __ffsll((long long)f) - 1);
+              const i64 key = (i64)((weight_of<M>(j, idx, U, w) << rb) | (base + idx));
+              best = key < best ? key : best;
+            }
         } else {
-          if (best == GR_KEY_NONE) best = (i64)(base + (u64)(__ffsll((long long)F) - 1));
+          if (best == GR_KEY_NONE) best = (i64)(base + (u64)f2_ctz(F));
           if (MODE == 0) return best;
         }
       }
@@ -595,8 +616,8 @@ __device__ i64 run_lane(const EnumParams &p, u64 r_lo, u64 cnt, int me, const Cl
 __device__ unsigned long long g_work[4];  // counting instantiation totals
 
 constexpr int SMC = 512;  // clauses staged in shared memory (larger instances read L1/L2)
-constexpr size_t TAB_SMEM = 6 * 64 * 8 + 65 * 8 * 4;  // HIT table + small binomials
-constexpr size_t ENUM_SMEM = TAB_SMEM + (size_t)SMC * (8 * HREC + 8);
+constexpr size_t TAB_SMEM = 6 * 64 * 16 + 65 * 8 * 4 + 32;  // HIT table + small binomials
+constexpr size_t ENUM_SMEM = TAB_SMEM + (size_t)SMC * (16 * HREC + 8);
 
 template <bool COUNT>
 __global__ void __launch_bounds__(NT) enum_kernel(EnumParams p) {
@@ -608,11 +629,11 @@ __global__ void __launch_bounds__(NT) enum_kernel(EnumParams p) {
   __shared__ i64 s_wmin[NT / 32];
   const int t = threadIdx.x;
   if (t == 0) s_cur = -1;
-  u64 *hitx = cls;                     // [6][64] HIT_j({x}): j-subsets of [0, R_j) containing x
-  u32 *cs = (u32 *)(cls + 6 * 64);     // [65][8] C(n, j), j <= 5
+  F2 *hitx = (F2 *)cls;                 // [6][64] HIT_j({x}): j-subsets of [0, R_j) containing x
+  u32 *cs = (u32 *)(cls + 2 * 6 * 64);   // [65][8] C(n, j), j <= 5
   for (int q = t; q < 6 * 64; q += NT) {
     const int jj = q / 64, x = q % 64;
-    hitx[q] = (jj >= 1 && x < region_of(jj)) ? hitting(jj, 1ull << x) : 0ull;
+    hitx[q] = (jj >= 1 && x < region_of(jj)) ? hitting(jj, 1ull << x) : F2{0ull, 0ull};
   }
   for (int q = t; q < 65 * 8; q += NT) cs[q] = (q % 8) <= 5 ? (u32)binom(q / 8, q % 8) : 0u;
   u64 *stage = cls + TAB_SMEM / 8;  // staged clause records
@@ -654,11 +675,11 @@ __global__ void __launch_bounds__(NT) enum_kernel(EnumParams p) {
     const int64_t lo = p.off[b];
     const bool staged = np + nn <= SMC;
     const bool narrow = staged && me <= 32;
-    u64 *sH = stage;                       // [np][HREC]
-    u64 *sP = stage + (size_t)HREC * np;   // [np + nn] as u32 or u64
+    F2 *sH = (F2 *)stage;                       // [np][HREC]
+    u64 *sP = stage + (size_t)2 * HREC * np;     // [np + nn] as u32 or u64
     if (b != s_cur) {
       if (staged) {
-        for (int q = t; q < np * HREC; q += NT) sH[q] = p.ws.hrec[lo * HREC + q];
+        for (int q = t; q < np * HREC; q += NT) sH[q] = ((const F2 *)p.ws.hrec)[lo * HREC + q];
         if (narrow) {
           u32 *c32 = (u32 *)sP;
           for (int q = t; q < np + nn; q += NT) c32[q] = (u32)p.ws.pk[lo + q];
@@ -684,7 +705,7 @@ __global__ void __launch_bounds__(NT) enum_kernel(EnumParams p) {
         Clauses<u64> c{sP, sH, hitx, cs, np, nn};
         key = run_lane<u64, COUNT>(p, r_lo, cnt, me, c, s_w, rb, wk);
       } else {
-        Clauses<u64> c{p.ws.pk + lo, p.ws.hrec + lo * HREC, hitx, cs, np, nn};
+        Clauses<u64> c{p.ws.pk + lo, (const F2 *)p.ws.hrec + lo * HREC, hitx, cs, np, nn};
         key = run_lane<u64, COUNT>(p, r_lo, cnt, me, c, s_w, rb, wk);
       }
     }
