@@ -49,6 +49,12 @@ struct Ctrl {
   u64 pad1[4];
 };
 
+#ifndef GR_JMAX
+#define GR_JMAX 8
+#endif
+constexpr int JMAX = GR_JMAX;  // S = the J = min(k, JMAX) lowest elements of a candidate
+constexpr int HREC = JMAX;     // per-clause record: H_1 (= P), H_2, ..., H_JMAX
+
 struct Layout {
   size_t ctrl, meff, npr, nnr, kmax, ks, done, rb, sup, decided, bestx, bestw, wtot, lvlkey, sk, wr,
       active, chunk_base, pk, hrec, total;
@@ -77,7 +83,7 @@ Layout layout_of(const gr_batch *in) {
   L.active = take(4 * 2 * B);
   L.chunk_base = take(8 * (B + 1));
   L.pk = take(8 * (size_t)std::max<int64_t>(in->total_clauses, 1));
-  L.hrec = take(16 * 5 * (size_t)std::max<int64_t>(in->total_clauses, 1));
+  L.hrec = take(16 * HREC * (size_t)std::max<int64_t>(in->total_clauses, 1));
   L.total = o;
   return L;
 }
@@ -291,7 +297,7 @@ __global__ void __launch_bounds__(PT) pack_kernel(In in, Out out, WS ws, int whi
     const int64_t dst = lo + (j < np ? 0 : npr) + d;
     ws.pk[dst] = R[j];
     if (j < np)
-      for (int jj = 1; jj <= 5; jj++) ((F2 *)ws.hrec)[dst * 5 + jj - 1] = hitting(jj, R[j]);
+      for (int jj = 1; jj <= HREC; jj++) ((F2 *)ws.hrec)[dst * HREC + jj - 1] = hitting(jj, R[j]);
   }
   // weights of the support variables (relabelled order) and S_k
   if (t < 64) {
@@ -376,8 +382,6 @@ __global__ void __launch_bounds__(PT) pack_kernel(In in, Out out, WS ws, int whi
 // N's region part.  Each lane visits one sub-block per loop iteration (a flat
 // depth-first iterator over the node tree), so the lanes of a warp run the
 // same clause-test code in lock step.
-constexpr int JMAX = 5;
-constexpr int HREC = 5;  // per-clause record: H_1 (= P), H_2, H_3, H_4, H_5
 
 __device__ __forceinline__ F2 f2_and(F2 a, F2 b) { return F2{a.lo & b.lo, a.hi & b.hi}; }
 __device__ __forceinline__ F2 f2_andnot(F2 a, F2 b) { return F2{a.lo & ~b.lo, a.hi & ~b.hi}; }
@@ -393,7 +397,7 @@ __device__ __forceinline__ int f2_popc(F2 a) { return __popcll(a.lo) + __popcll(
 
 // R_j = the largest region with C(R_j, j) <= 128 (j = 1: every variable)
 __host__ __device__ constexpr int region_of(int j) {
-  return (int)((0x09090A1040ull >> (8 * (j - 1))) & 0xffull);  // 64, 16, 10, 9, 9
+  return (int)((0x0A0A0909090A1040ull >> (8 * (j - 1))) & 0xffull);  // 64 16 10 9 9 9 10 10
 }
 __device__ __forceinline__ u64 nbits(u64 n) { return n >= 64 ? ~0ull : ((1ull << n) - 1ull); }
 
@@ -425,7 +429,7 @@ struct Clauses {
   const M *P;       // [np + nn] positives then negatives (uniform reads)
   const F2 *H;      // [np][HREC] H_j(P) at H[q * HREC + j - 1]
   const F2 *hitx;   // [6][64] HIT_j({x}) (0 when x >= R_j), shared memory
-  const u32 *cs;    // [65][8] C(n, j) for j <= 5 (fits 32 bits), shared memory
+  const u32 *cs;    // [65][16] C(n, j) for j <= 8 (saturated at 2^32 - 1), shared memory
   int np, nn;
 };
 
@@ -487,8 +491,8 @@ template <typename M, int MODE, bool COUNT>
 __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const u32 *w, int rb,
                     Work &wk) {
   const int J = k < JMAX ? k : JMAX;
-  const u32 *cs = c.cs;  // C(n, j), j <= 5
-#define CS(n, j) ((u64)cs[(n) * 8 + (j)])
+  const u32 *cs = c.cs;  // C(n, j), j <= 8; only C(64, 8) saturates and is never used
+#define CS(n, j) ((u64)cs[(n) * 16 + (j)])
   const u64 r_hi = r_lo + cnt;
   i64 best = GR_KEY_NONE;
   // ---- position the iterator on the sub-block that holds rank r_lo
@@ -508,12 +512,12 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
   M U = Utop;
   u64 base = base_top;
   int d = 0;
-  u32 tp = 0;  // t_0 .. t_{d-1}, 6 bits each
+  u64 tp = 0;  // t_0 .. t_{d-1}, 6 bits each
   for (;;) {
     const int j = J - d;
     if (j < 2 || s[j - 1] < region_of(j)) break;
     const int t = s[j - 1];
-    tp |= (u32)t << (6 * d);
+    tp |= (u64)t << (6 * d);
     U |= (M)1 << t;
     base += CS(t, j);
     d++;
@@ -548,7 +552,7 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
     }
     // ---- advance: first child of this node, else next sibling up the path
     if (j >= 2 && R < e) {
-      tp |= (u32)R << (6 * d);
+      tp |= (u64)R << (6 * d);
       U |= (M)1 << R;
       base += CS(R, j);
       d++;
@@ -560,9 +564,9 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
       const int t = (int)((tp >> sh) & 63u);
       const int jp = J - (d - 1);
       const int ep = d == 1 ? e_top : (int)((tp >> (sh - 6)) & 63u);
-      tp &= ~(63u << sh);
+      tp &= ~(63ull << sh);
       if (t + 1 < ep) {  // next sibling: t -> t + 1
-        tp |= (u32)(t + 1) << sh;
+        tp |= (u64)(t + 1) << sh;
         U ^= (M)3 << t;
         base += CS(t + 1, jp) - CS(t, jp);
         moved = true;
@@ -574,8 +578,9 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
     }
     if (moved) continue;
     // ---- next top-level U (Gosper on the (k-J)-subsets of [J, me))
+    if (!Utop) return best;
     base_top += CS(e_top, J);
-    if (base_top >= r_hi || !Utop) return best;
+    if (base_top >= r_hi) return best;
     M S = Utop >> J;
     const M lb = lowbit(S);
     const M r = S + lb;
@@ -615,8 +620,8 @@ __device__ i64 run_lane(const EnumParams &p, u64 r_lo, u64 cnt, int me, const Cl
 
 __device__ unsigned long long g_work[4];  // counting instantiation totals
 
-constexpr int SMC = 512;  // clauses staged in shared memory (larger instances read L1/L2)
-constexpr size_t TAB_SMEM = 6 * 64 * 16 + 65 * 8 * 4 + 32;  // HIT table + small binomials
+constexpr int SMC = HREC > 5 ? 256 : 512;  // clauses staged in shared memory (larger: L1/L2)
+constexpr size_t TAB_SMEM = (JMAX + 1) * 64 * 16 + 65 * 16 * 4 + 32;  // HIT table + binomials
 constexpr size_t ENUM_SMEM = TAB_SMEM + (size_t)SMC * (16 * HREC + 8);
 
 template <bool COUNT>
@@ -629,13 +634,16 @@ __global__ void __launch_bounds__(NT) enum_kernel(EnumParams p) {
   __shared__ i64 s_wmin[NT / 32];
   const int t = threadIdx.x;
   if (t == 0) s_cur = -1;
-  F2 *hitx = (F2 *)cls;                 // [6][64] HIT_j({x}): j-subsets of [0, R_j) containing x
-  u32 *cs = (u32 *)(cls + 2 * 6 * 64);   // [65][8] C(n, j), j <= 5
-  for (int q = t; q < 6 * 64; q += NT) {
+  F2 *hitx = (F2 *)cls;  // [JMAX + 1][64] HIT_j({x}): j-subsets of [0, R_j) containing x
+  u32 *cs = (u32 *)(cls + 2 * (JMAX + 1) * 64);  // [65][16] C(n, j), j <= JMAX
+  for (int q = t; q < (JMAX + 1) * 64; q += NT) {
     const int jj = q / 64, x = q % 64;
     hitx[q] = (jj >= 1 && x < region_of(jj)) ? hitting(jj, 1ull << x) : F2{0ull, 0ull};
   }
-  for (int q = t; q < 65 * 8; q += NT) cs[q] = (q % 8) <= 5 ? (u32)binom(q / 8, q % 8) : 0u;
+  for (int q = t; q < 65 * 16; q += NT) {
+    const u64 v = (q % 16) <= JMAX ? binom(q / 16, q % 16) : 0ull;
+    cs[q] = v > 0xffffffffull ? 0xffffffffu : (u32)v;
+  }
   u64 *stage = cls + TAB_SMEM / 8;  // staged clause records
   const u64 Lc = p.ws.ctrl->lane_cands;
   const u64 CH = Lc * NT;
