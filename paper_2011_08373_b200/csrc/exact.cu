@@ -50,7 +50,7 @@ struct Ctrl {
 };
 
 #ifndef GR_JMAX
-#define GR_JMAX 8
+#define GR_JMAX 10
 #endif
 constexpr int JMAX = GR_JMAX;  // S = the J = min(k, JMAX) lowest elements of a candidate
 constexpr int HREC = JMAX;     // per-clause record: H_1 (= P), H_2, ..., H_JMAX
@@ -397,7 +397,8 @@ __device__ __forceinline__ int f2_popc(F2 a) { return __popcll(a.lo) + __popcll(
 
 // R_j = the largest region with C(R_j, j) <= 128 (j = 1: every variable)
 __host__ __device__ constexpr int region_of(int j) {
-  return (int)((0x0A0A0909090A1040ull >> (8 * (j - 1))) & 0xffull);  // 64 16 10 9 9 9 10 10
+  return j <= 8 ? (int)((0x0A0A0909090A1040ull >> (8 * (j - 1))) & 0xffull)  // 64 16 10 9 9 9 10 10
+                : (j == 9 ? 11 : 12);                                           // 11 12
 }
 __device__ __forceinline__ u64 nbits(u64 n) { return n >= 64 ? ~0ull : ((1ull << n) - 1ull); }
 
@@ -429,7 +430,7 @@ struct Clauses {
   const M *P;       // [np + nn] positives then negatives (uniform reads)
   const F2 *H;      // [np][HREC] H_j(P) at H[q * HREC + j - 1]
   const F2 *hitx;   // [6][64] HIT_j({x}) (0 when x >= R_j), shared memory
-  const u32 *cs;    // [65][16] C(n, j) for j <= 8 (saturated at 2^32 - 1), shared memory
+  const u64 *cs;    // [65][JMAX + 1] C(n, j) for j <= JMAX, shared memory
   int np, nn;
 };
 
@@ -491,8 +492,8 @@ template <typename M, int MODE, bool COUNT>
 __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const u32 *w, int rb,
                     Work &wk) {
   const int J = k < JMAX ? k : JMAX;
-  const u32 *cs = c.cs;  // C(n, j), j <= 8; only C(64, 8) saturates and is never used
-#define CS(n, j) ((u64)cs[(n) * 16 + (j)])
+  const u64 *cs = c.cs;  // C(n, j), j <= JMAX
+#define CS(n, j) (cs[(n) * (JMAX + 1) + (j)])
   const u64 r_hi = r_lo + cnt;
   i64 best = GR_KEY_NONE;
   // ---- position the iterator on the sub-block that holds rank r_lo
@@ -620,8 +621,9 @@ __device__ i64 run_lane(const EnumParams &p, u64 r_lo, u64 cnt, int me, const Cl
 
 __device__ unsigned long long g_work[4];  // counting instantiation totals
 
-constexpr int SMC = HREC > 5 ? 256 : 512;  // clauses staged in shared memory (larger: L1/L2)
-constexpr size_t TAB_SMEM = (JMAX + 1) * 64 * 16 + 65 * 16 * 4 + 32;  // HIT table + binomials
+constexpr size_t TAB_SMEM = (JMAX + 1) * 64 * 16 + 65 * (JMAX + 1) * 8;  // HIT table + binomials
+// clauses staged in shared memory (larger instances read L1/L2), sized for 4 CTAs per SM
+constexpr int SMC = (int)((54000 - TAB_SMEM) / (16 * HREC + 8)) / 32 * 32;
 constexpr size_t ENUM_SMEM = TAB_SMEM + (size_t)SMC * (16 * HREC + 8);
 
 template <bool COUNT>
@@ -635,15 +637,12 @@ __global__ void __launch_bounds__(NT) enum_kernel(EnumParams p) {
   const int t = threadIdx.x;
   if (t == 0) s_cur = -1;
   F2 *hitx = (F2 *)cls;  // [JMAX + 1][64] HIT_j({x}): j-subsets of [0, R_j) containing x
-  u32 *cs = (u32 *)(cls + 2 * (JMAX + 1) * 64);  // [65][16] C(n, j), j <= JMAX
+  u64 *cs = cls + 2 * (JMAX + 1) * 64;  // [65][JMAX + 1] C(n, j), j <= JMAX
   for (int q = t; q < (JMAX + 1) * 64; q += NT) {
     const int jj = q / 64, x = q % 64;
     hitx[q] = (jj >= 1 && x < region_of(jj)) ? hitting(jj, 1ull << x) : F2{0ull, 0ull};
   }
-  for (int q = t; q < 65 * 16; q += NT) {
-    const u64 v = (q % 16) <= JMAX ? binom(q / 16, q % 16) : 0ull;
-    cs[q] = v > 0xffffffffull ? 0xffffffffu : (u32)v;
-  }
+  for (int q = t; q < 65 * (JMAX + 1); q += NT) cs[q] = binom(q / (JMAX + 1), q % (JMAX + 1));
   u64 *stage = cls + TAB_SMEM / 8;  // staged clause records
   const u64 Lc = p.ws.ctrl->lane_cands;
   const u64 CH = Lc * NT;
