@@ -13,14 +13,17 @@
 //   enum_kernel     persistent CTAs (grid = SMs x occupancy) pull fixed-size
 //                   chunks of the current level's colex rank range from a
 //                   global atomic counter; each lane walks a contiguous
-//                   sub-range.  The walk fixes the k-1 upper elements T (the
-//                   "prefix") and decides all candidates T | {a}, a < min(T),
-//                   at once: their feasible set is a bit mask A, narrowed by
-//                   every positive clause T misses (A &= P) and every negative
-//                   clause with |N \ T| <= 1.  Clause masks are staged in
-//                   shared memory (broadcast reads).  Canonical minimum:
-//                   per-lane first witness -> warp shuffle-min -> CTA min ->
-//                   one 64-bit atomicMin per chunk.
+//                   sub-range.  A candidate is x = U | S with S its J =
+//                   min(k, JMAX) lowest elements; the walk visits sub-blocks
+//                   (fixed U, S ranging over the j-subsets of a small region
+//                   [0, R_j), at most 128 candidates = one two-word mask F) in
+//                   rank order.  A positive clause P that U misses narrows F by
+//                   its precomputed record H_j(P); a negative clause with at
+//                   most j variables outside U removes the S that hold them
+//                   all.  Clause records are staged in shared memory
+//                   (broadcast reads).  Canonical minimum: per-lane first
+//                   witness -> warp shuffle-min -> CTA min -> one 64-bit
+//                   atomicMin per chunk.
 //   finish_kernel   one CTA: commits level k for every active instance
 //                   (decode, weighted incumbent, S_k stop rule, k_max), writes
 //                   finished results, compacts the active list and plans the
@@ -97,7 +100,7 @@ struct WS {
   u32 *wr;
   int *active;
   u64 *chunk_base;
-  u64 *pk, *hrec;  // packed clause masks; [clause][5] H_j(P) records of the positives
+  u64 *pk, *hrec;  // packed clause masks; [clause][HREC] two-word H_j(P) records of the positives
 };
 
 WS ws_of(const gr_batch *in, void *base) {
@@ -402,19 +405,38 @@ __host__ __device__ constexpr int region_of(int j) {
 }
 __device__ __forceinline__ u64 nbits(u64 n) { return n >= 64 ? ~0ull : ((1ull << n) - 1ull); }
 
-// H_j(p): bit i set iff the i-th j-subset of [0, R_j) (colex order) meets p
-__device__ F2 hitting(int j, u64 p) {
-  if (j == 1) return F2{p, 0ull};
-  const int R = region_of(j);
-  const u64 n = binom(R, j);
-  u64 x = (1ull << j) - 1;
-  F2 r{0ull, 0ull};
-  for (u64 i = 0; i < n; i++) {
-    if (x & p) {
-      if (i < 64) r.lo |= 1ull << i; else r.hi |= 1ull << (i - 64);
+// HIT_j({x}) for j <= JMAX, x < 64 (0 when x >= R_j), built at compile time:
+// bit i set iff the i-th j-subset of [0, R_j) in colex order contains x.
+struct HitTable {
+  u64 lo[(JMAX + 1) * 64], hi[(JMAX + 1) * 64];
+  constexpr HitTable() : lo(), hi() {
+    for (int v = 0; v < 64; v++) lo[64 + v] = 1ull << v;  // j = 1: R_1 = 64, HIT = {x}
+    for (int j = 2; j <= JMAX; j++) {
+      const int R = region_of(j);
+      u64 x = (1ull << j) - 1;
+      for (int i = 0; x < (1ull << R); i++) {  // j-subsets of [0, R) in colex order
+        for (int v = 0; v < R; v++)
+          if (x >> v & 1ull) {
+            if (i < 64) lo[64 * j + v] |= 1ull << i; else hi[64 * j + v] |= 1ull << (i - 64);
+          }
+        u64 c = x & (~x + 1), y = x + c;  // Gosper: next j-subset
+        int tz = 0;
+        while (!(c >> tz & 1ull)) tz++;
+        x = y | (((y ^ x) >> 2) >> tz);
+      }
     }
-    const u64 c = x & (~x + 1), y = x + c;  // Gosper: next j-subset
-    x = y | (((y ^ x) >> 2) >> (__ffsll((long long)c) - 1));
+  }
+};
+static __device__ const HitTable g_hit = HitTable();
+
+// H_j(p): bit i set iff the i-th j-subset of [0, R_j) (colex order) meets p,
+// i.e. the union of HIT_j({x}) over the elements x of p
+__device__ F2 hitting(int j, u64 p) {
+  F2 r{0ull, 0ull};
+  for (; p; p &= p - 1) {
+    const int x = __ffsll((long long)p) - 1;
+    r.lo |= g_hit.lo[64 * j + x];
+    r.hi |= g_hit.hi[64 * j + x];
   }
   return r;
 }
@@ -638,10 +660,7 @@ __global__ void __launch_bounds__(NT) enum_kernel(EnumParams p) {
   if (t == 0) s_cur = -1;
   F2 *hitx = (F2 *)cls;  // [JMAX + 1][64] HIT_j({x}): j-subsets of [0, R_j) containing x
   u64 *cs = cls + 2 * (JMAX + 1) * 64;  // [65][JMAX + 1] C(n, j), j <= JMAX
-  for (int q = t; q < (JMAX + 1) * 64; q += NT) {
-    const int jj = q / 64, x = q % 64;
-    hitx[q] = (jj >= 1 && x < region_of(jj)) ? hitting(jj, 1ull << x) : F2{0ull, 0ull};
-  }
+  for (int q = t; q < (JMAX + 1) * 64; q += NT) hitx[q] = F2{g_hit.lo[q], g_hit.hi[q]};
   for (int q = t; q < 65 * (JMAX + 1); q += NT) cs[q] = binom(q / (JMAX + 1), q % (JMAX + 1));
   u64 *stage = cls + TAB_SMEM / 8;  // staged clause records
   const u64 Lc = p.ws.ctrl->lane_cands;
