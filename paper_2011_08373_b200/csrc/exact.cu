@@ -518,17 +518,34 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
 #define CS(n, j) (cs[(n) * (JMAX + 1) + (j)])
   const u64 r_hi = r_lo + cnt;
   i64 best = GR_KEY_NONE;
-  // ---- position the iterator on the sub-block that holds rank r_lo
-  const u64 x = unrank_colex(r_lo, k, me);
+  // ---- position the iterator on the sub-block that holds rank r_lo: colex
+  // unrank of r_lo (element i is the largest c with C(c, i) <= the remaining
+  // rank); the top k - J elements (binary search) form Utop, the J lowest go
+  // to s[] (downward scan over the shared binomial table)
   int s[JMAX];  // the J lowest elements of x, ascending
-  u64 Ux = x, off = 0;
-  for (int i = 0; i < J; i++) {
-    s[i] = __ffsll((long long)Ux) - 1;
-    Ux &= Ux - 1;
-    off += CS(s[i], i + 1);
+  M Utop = 0;
+  u64 rr = r_lo, base_top;
+  {
+    int cc = me - 1;
+    for (int i = k; i > J; i--) {  // binary search in [i - 1, cc]
+      int lo = i - 1, h = cc;
+      while (lo < h) {
+        const int mid = (lo + h + 1) >> 1;
+        if (binom(mid, i) <= rr) lo = mid; else h = mid - 1;
+      }
+      Utop |= (M)1 << lo;
+      rr -= binom(lo, i);
+      cc = lo - 1;
+    }
+    base_top = r_lo - rr;  // rank of (Utop, the J lowest elements of [0, min Utop))
+    for (int i = J; i >= 1; i--) {
+      u64 v;
+      while ((v = CS(cc, i)) > rr) cc--;
+      s[i - 1] = cc;
+      rr -= v;
+      cc--;
+    }
   }
-  M Utop = (M)Ux;
-  u64 base_top = r_lo - off;
   int e_top = Utop ? ctz(Utop) : me;
   // descend: at depth d (node j = J - d) x lies in part B iff its j-th lowest
   // element s[j-1] >= R_j; then t_d = s[j-1]
@@ -554,6 +571,7 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
     if (base >= r_hi) return best;
     const u64 n = CS(ea, j);
     if (n && base + n > r_lo) {
+      // candidates [a, b) of this sub-block lie in the lane's window
       F2 F = f2_nbits(n);
       if (r_lo > base) F = f2_andnot(F, f2_nbits(r_lo - base));
       if (r_hi < base + n) F = f2_and(F, f2_nbits(r_hi - base));
