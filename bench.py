@@ -101,16 +101,50 @@ def traffic_of(kernel: str):
 
 # ---------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + clock-event (throttle) reasons DURING the timed region.
 
+    The fields of the recipe's `nvidia-smi --query-gpu=clocks.sm,clocks.max.sm,
+    clocks_event_reasons.*` line, read through NVML (the library nvidia-smi
+    queries) every 2 ms so that short timed regions still get samples; only
+    the samples between start() and stop() count.  Falls back to nvidia-smi
+    -lms 100 when NVML is unavailable."""
+
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
-        self.index, self.rows, self.proc = index, [], None
+        self.index, self.rows, self.proc, self.nvml = index, [], None, None
+        self.t0 = self.t1 = None
+        self.stop_evt = threading.Event()
+        self.max_mhz = None
+
+    def _handle(self):
+        import pynvml as nv
+
+        nv.nvmlInit()
+        try:
+            p = torch.cuda.get_device_properties(self.index)
+            bus = "%08X:%02X:%02X.0" % (p.pci_domain_id, p.pci_bus_id, p.pci_device_id)
+            return nv, nv.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return nv, nv.nvmlDeviceGetHandleByIndex(self.index)
 
     def __enter__(self):
+        try:
+            nv, h = self._handle()
+            self.nvml = (nv, h)
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
@@ -123,37 +157,70 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def _poll(self):
+        nv, h = self.nvml
+        getr = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self.stop_evt.is_set():
+            try:
+                mhz = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                bits = int(getr(h))
+            except Exception:
+                break
+            self.rows.append((time.perf_counter(), mhz, bits))
+            time.sleep(0.002)
+
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            r = [x.strip() for x in line.split(",")]
+            if len(r) > 8:
+                try:
+                    mhz, mx = float(r[1]), float(r[2])
+                except ValueError:
+                    continue
+                self.max_mhz = mx
+                bits = sum(1 << i for i in range(4) if r[5 + i].lower().startswith("active"))
+                self.rows.append((time.perf_counter(), mhz, -1 - bits))
+
+    def start(self):
+        self.t0 = time.perf_counter()
+
+    def stop(self):
+        self.t1 = time.perf_counter()
 
     def __exit__(self, *a):
+        self.stop_evt.set()
         if self.proc:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=2)
             except Exception:
                 self.proc.kill()
+        if self.nvml:
+            self.t.join(timeout=1)
 
     def summary(self):
-        def num(x):
-            try:
-                return float(x)
-            except ValueError:
-                return None
-
-        rows = [r for r in self.rows if len(r) > 8]
-        sm = [num(r[1]) for r in rows if num(r[1])]
-        mx = [num(r[2]) for r in rows if num(r[2])]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        t0 = self.t0 if self.t0 is not None else -1e30
+        t1 = self.t1 if self.t1 is not None else 1e30
+        rows = [r for r in list(self.rows) if t0 <= r[0] <= t1]
         reasons = set()
-        for r in rows:
-            for i, n in enumerate(names):
-                if r[5 + i].lower().startswith("active"):
-                    reasons.add(n)
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        for _, _, bits in rows:
+            if bits >= 0 and self.nvml:
+                nv = self.nvml[0]
+                for name, const in self.REASONS:
+                    if bits & int(getattr(nv, const, 0)):
+                        reasons.add(name)
+            elif bits < 0:
+                b = -1 - bits
+                for i, name in enumerate(("hw_slowdown", "hw_thermal_slowdown",
+                                          "sw_thermal_slowdown", "sw_power_cap")):
+                    if b >> i & 1:
+                        reasons.add(name)
+        sm = [r[1] for r in rows]
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(reasons), "samples": len(sm),
+                "source": "NVML every 2 ms in the timed region" if self.nvml
+                else "nvidia-smi -lms 100 in the timed region"}
 
 
 # ---------------------------------------------------------------- workloads
@@ -248,6 +315,7 @@ def main():
     l0 = gr.launch_count()
     total_ms = 0.0
     with ClockSampler(local) as clk:
+        clk.start()
         for _ in range(a.steps):
             flush.fill_(1)  # L2 flush between timed iterations (untimed)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -256,6 +324,7 @@ def main():
             e1.record(stream)
             e1.synchronize()
             total_ms += e0.elapsed_time(e1)
+        clk.stop()
     launches = gr.launch_count() - l0
     kern = prof.stop()
     torch.cuda.synchronize()
@@ -395,6 +464,7 @@ def run_c5(a, rank, world, local, dev):
         l0 = gr.launch_count()
         ms = 0.0
         with ClockSampler(local) as clk:
+            clk.start()
             for _ in range(steps):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
@@ -404,6 +474,7 @@ def run_c5(a, rank, world, local, dev):
                 ms += e0.elapsed_time(e1)
                 ld = bm.ld
                 del bm
+            clk.stop()
         return ms, r, ld, prof.stop(), gr.launch_count() - l0, clk.summary()
 
     # primary: the north-star design -- recounting passes streaming the 8 GiB
@@ -421,6 +492,34 @@ def run_c5(a, rank, world, local, dev):
     a_ = r.assign.cpu().numpy().view(np.uint64)
     size = int(sum(bin(int(x)).count("1") for x in a_))
     n = csr.n_pos
+    # e2e through the public API: pinned host CSR -> device, pack + greedy,
+    # result (assignment, picks, status) -> host, every step
+    e2e = None
+    if not a.no_e2e:
+        hp = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory()
+              for k, v in (("po", csr.pos_off), ("pv", csr.pos_var), ("no", csr.neg_off),
+                           ("nv", csr.neg_var))}
+        h2d = sum(int(t.numel() * t.element_size()) for t in hp.values())
+        ems, d2h = 0.0, 0
+        for s_ in range(max(1, min(a.warmup, 2)) + a.steps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            dd = {k: v.to(dev, non_blocking=True) for k, v in hp.items()}
+            bm = gr.pack_bitmatrix(csr.m, dd["po"], dd["pv"], dd["no"], dd["nv"], device=dev,
+                                   check=False, keep_csr=False)
+            rr = gr.mhs_greedy_matrix(bm)
+            host = [rr.assign.cpu(), rr.picks.cpu(), rr.status.cpu()]
+            e1.record(stream)
+            e1.synchronize()
+            del bm, dd
+            if s_ >= max(1, min(a.warmup, 2)):
+                ems += e0.elapsed_time(e1)
+        d2h = sum(int(x.numel() * x.element_size()) for x in host)
+        e2e = {"value": n * a.steps / (ems / 1e3), "unit": "clauses/s (greedy)",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ems / a.steps}
+    cpu = None
+    if rank == 0 and not a.no_cpu_baseline:
+        cpu = cpu_baseline_c5(rank)
     line = {
         "metric": METRIC, "value": n * a.steps / (total_ms / 1e3), "unit": "clauses/s (greedy)",
         "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": total_ms / a.steps,
@@ -436,14 +535,46 @@ def run_c5(a, rank, world, local, dev):
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": ach / pk["hbm_gbs"], "traffic": traffic_of("count_kernel_c5"),
+                     "traffic_source": "profiles/traffic.json (ncu --set full, scripts/prof_c5.py --full)",
                      "kernel": "count_kernel", "share_of_step": ck["ms"] / total_ms,
                      "per_launch": {"bytes": bytes_per_launch, "ms": ck["ms"] / eff},
                      "ncu": ncu_evidence("count_kernel")},
         "clocks": clocks,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
         "kernels": {k: {"launches": v["launches"], "ms_per_step": v["ms"] / a.steps} for k, v in kern.items()},
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+C5_SAMPLE_N = 1 << 21
+
+
+def c5_oracle_once(csr):
+    import oracle
+
+    t0 = time.perf_counter()
+    g = oracle.greedy_csr(csr.m, csr.pos_off, csr.pos_var, csr.neg_off, csr.neg_var)
+    return time.perf_counter() - t0, g
+
+
+def cpu_baseline_c5(rank):
+    """The oracle's textbook greedy (recount per pick) on a C5-recipe instance
+    with 1/8 of the clauses, repeated for >= 10 s."""
+    import oracle
+    from paper_2011_08373_b200 import synth
+
+    csr, _ = synth.c5_clauses(seed=synth.seed_for(5, rank), n=C5_SAMPLE_N)
+    sec, reps = 0.0, 0
+    while sec < 10.0 and reps < 20:
+        dt, _ = c5_oracle_once(csr)
+        sec += dt
+        reps += 1
+    return {"value": C5_SAMPLE_N * reps / sec, "unit": "clauses/s (greedy)",
+            "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"{reps} greedy solve(s) of a C5-recipe instance with n = 2^21 clauses "
+                      f"(1/8 of C5), m = 4096", "seconds": sec}
 
 
 # ---------------------------------------------------------------- CPU oracle legs
@@ -494,6 +625,29 @@ def run_reference(a, rank, world):
         return
     import oracle
 
+    if a.config == "c5":
+        from paper_2011_08373_b200 import synth
+
+        csr, _ = synth.c5_clauses(seed=synth.seed_for(5, 0), n=C5_SAMPLE_N)
+        ts = []
+        for s in range(a.warmup + a.steps):
+            dt, _ = c5_oracle_once(csr)
+            if s >= a.warmup:
+                ts.append(dt)
+        sec = float(np.sum(ts))
+        v = C5_SAMPLE_N * a.steps / sec
+        sdesc = "greedy over a C5-recipe instance with n = 2^21 clauses (1/8 of C5), m = 4096"
+        print(json.dumps({
+            "impl": "reference", "metric": METRIC, "value": v, "unit": "clauses/s (greedy)",
+            "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * sec / a.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic", "config": {"workload": "C5 sample: " + sdesc},
+            "cpu_baseline": {"value": v, "unit": "clauses/s (greedy)", "cores": oracle.num_threads(),
+                             "kind": "oracle", "sample": sdesc},
+            "e2e": {"value": v, "unit": "clauses/s (greedy)", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+        }), flush=True)
+        return
     cfg = a.config if a.config in ("c1", "c2", "c4") else "c2"
     cb, desc = make_workload(cfg, 0)
     sub, sdesc = oracle_sample(cfg, cb)
