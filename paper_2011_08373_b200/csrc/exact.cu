@@ -547,31 +547,37 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
     }
   }
   int e_top = Utop ? ctz(Utop) : me;
-  // descend: at depth d (node j = J - d) x lies in part B iff its j-th lowest
-  // element s[j-1] >= R_j; then t_d = s[j-1]
+  // Iterator state: the path t_0 > t_1 > ... > t_{d-1} of part-B choices
+  // below Utop; the current node is (j = J - d, U, e = t_{d-1} or e_top) with
+  // region R = R_j, first rank base, and ep = the parent's e (t_{d-2} or
+  // e_top).  tp keeps the ancestors t_0 .. t_{d-2} (6 bits each); the current
+  // e and ep live in registers, so moving to a sibling does not touch tp.
   M U = Utop;
   u64 base = base_top;
-  int d = 0;
-  u64 tp = 0;  // t_0 .. t_{d-1}, 6 bits each
-  for (;;) {
-    const int j = J - d;
-    if (j < 2 || s[j - 1] < region_of(j)) break;
+  int d = 0, j = J, e = e_top, ep = e_top;
+  u64 tp = 0;
+  // descend: at node j, x lies in part B iff its j-th lowest element
+  // s[j-1] >= R_j; then the child is t = s[j-1]
+  while (j >= 2 && s[j - 1] >= region_of(j)) {
     const int t = s[j - 1];
-    tp |= (u64)t << (6 * d);
+    if (d > 0) {
+      const int sh = 6 * (d - 1);
+      tp = (tp & ~(63ull << sh)) | ((u64)e << sh);
+    }
+    ep = e;
+    e = t;
     U |= (M)1 << t;
     base += CS(t, j);
     d++;
+    j--;
   }
+  int R = region_of(j);
   // ---- iterate over sub-blocks in rank order
   for (;;) {
-    const int j = J - d;
-    const int e = d == 0 ? e_top : (int)((tp >> (6 * (d - 1))) & 63u);
-    const int R = region_of(j);
     const int ea = e < R ? e : R;
     if (base >= r_hi) return best;
     const u64 n = CS(ea, j);
     if (n && base + n > r_lo) {
-      // candidates [a, b) of this sub-block lie in the lane's window
       F2 F = f2_nbits(n);
       if (r_lo > base) F = f2_andnot(F, f2_nbits(r_lo - base));
       if (r_hi < base + n) F = f2_and(F, f2_nbits(r_hi - base));
@@ -591,33 +597,44 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
         }
       }
     }
-    // ---- advance: first child of this node, else next sibling up the path
+    // ---- advance: first child t = R of this node, else the next sibling up
+    // the path
     if (j >= 2 && R < e) {
-      tp |= (u64)R << (6 * d);
+      if (d > 0) {
+        const int sh = 6 * (d - 1);
+        tp = (tp & ~(63ull << sh)) | ((u64)e << sh);
+      }
+      ep = e;
+      e = R;
       U |= (M)1 << R;
       base += CS(R, j);
       d++;
+      j--;
+      R = region_of(j);
       continue;
     }
     bool moved = false;
     while (d > 0) {
-      const int sh = 6 * (d - 1);
-      const int t = (int)((tp >> sh) & 63u);
-      const int jp = J - (d - 1);
-      const int ep = d == 1 ? e_top : (int)((tp >> (sh - 6)) & 63u);
-      tp &= ~(63ull << sh);
-      if (t + 1 < ep) {  // next sibling: t -> t + 1
-        tp |= (u64)(t + 1) << sh;
-        U ^= (M)3 << t;
-        base += CS(t + 1, jp) - CS(t, jp);
+      const int jp = j + 1;  // the parent's level
+      if (e + 1 < ep) {      // next sibling: t -> t + 1
+        U ^= (M)3 << e;
+        base += CS(e + 1, jp) - CS(e, jp);
+        e++;
         moved = true;
         break;
       }
-      U &= ~((M)1 << t);
-      base -= CS(t, jp);
+      U &= ~((M)1 << e);
+      base -= CS(e, jp);
       d--;
+      j = jp;
+      e = ep;
+      ep = d >= 2 ? (int)((tp >> (6 * (d - 2))) & 63u) : e_top;
     }
-    if (moved) continue;
+    if (moved) {
+      R = region_of(j);
+      continue;
+    }
+    R = region_of(j);
     // ---- next top-level U (Gosper on the (k-J)-subsets of [J, me))
     if (!Utop) return best;
     base_top += CS(e_top, J);
@@ -630,8 +647,7 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
     e_top = ctz(Utop);
     U = Utop;
     base = base_top;
-    d = 0;
-    tp = 0;
+    e = ep = e_top;
   }
 #undef CS
 }
