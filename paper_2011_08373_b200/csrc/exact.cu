@@ -57,6 +57,7 @@ struct Ctrl {
 #endif
 constexpr int JMAX = GR_JMAX;  // S = the J = min(k, JMAX) lowest elements of a candidate
 constexpr int HREC = JMAX;     // per-clause record: H_1 (= P), H_2, ..., H_JMAX
+constexpr int HX = 16;         // HIT_j({x}) is 0 for x >= R_j, and R_j <= 16 for j >= 2
 
 struct Layout {
   size_t ctrl, meff, npr, nnr, kmax, ks, done, rb, sup, decided, bestx, bestw, wtot, lvlkey, sk, wr,
@@ -451,7 +452,8 @@ template <typename M>
 struct Clauses {
   const M *P;       // [np + nn] positives then negatives (uniform reads)
   const F2 *H;      // [np][HREC] H_j(P) at H[q * HREC + j - 1]
-  const F2 *hitx;   // [6][64] HIT_j({x}) (0 when x >= R_j), shared memory
+  const F2 *hitx;   // [JMAX + 1][HX] HIT_j({x}) for j >= 2 (0 when x >= R_j), shared memory
+  const F2 *lowb;   // [129] the n lowest bits, shared memory
   const u64 *cs;    // [65][JMAX + 1] C(n, j) for j <= JMAX, shared memory
   int np, nn;
 };
@@ -478,13 +480,17 @@ __device__ __forceinline__ F2 test_sub(int j, M U, int e, F2 F, const Clauses<M>
   }
   if (!f2_any(F)) return F;
   const M lowm = (M)nbits((u64)e);
-  const F2 *hx = c.hitx + 64 * j;
+  const F2 *hx = c.hitx + HX * j;
   for (int t = 0; t < c.nn; t++) {
     M rest = c.P[np + t] & ~U;
     if (COUNT) wk.tests += 1;
     if ((rest & ~lowm) || popc(rest) > j) continue;  // some variable of N stays false
     F2 kill{~0ull, ~0ull};
-    for (; rest; rest &= rest - 1) kill = f2_and(kill, hx[ctz(rest)]);
+    if (j == 1) {  // HIT_1({x}) = bit x
+      if (rest) kill = F2{(u64)rest, 0ull};
+    } else {
+      for (; rest; rest &= rest - 1) kill = f2_and(kill, hx[ctz(rest)]);
+    }
     F = f2_andnot(F, kill);  // the S holding every variable of N outside U
     if (!f2_any(F)) return F;
   }
@@ -578,9 +584,9 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
     if (base >= r_hi) return best;
     const u64 n = CS(ea, j);
     if (n && base + n > r_lo) {
-      F2 F = f2_nbits(n);
-      if (r_lo > base) F = f2_andnot(F, f2_nbits(r_lo - base));
-      if (r_hi < base + n) F = f2_and(F, f2_nbits(r_hi - base));
+      F2 F = c.lowb[n];
+      if (r_lo > base) F = f2_andnot(F, c.lowb[r_lo - base]);
+      if (r_hi < base + n) F = f2_and(F, c.lowb[r_hi - base]);
       if (COUNT) { wk.blocks++; wk.cands += (u64)f2_popc(F); }
       F = test_sub<M, COUNT>(j, U, ea, F, c, wk);
       if (f2_any(F)) {
@@ -677,7 +683,8 @@ __device__ i64 run_lane(const EnumParams &p, u64 r_lo, u64 cnt, int me, const Cl
 
 __device__ unsigned long long g_work[4];  // counting instantiation totals
 
-constexpr size_t TAB_SMEM = (JMAX + 1) * 64 * 16 + 65 * (JMAX + 1) * 8;  // HIT table + binomials
+constexpr size_t TAB_SMEM =
+    (JMAX + 1) * HX * 16 + 65 * (JMAX + 1) * 8 + 129 * 16;  // HIT table, binomials, low masks
 // clauses staged in shared memory (larger instances read L1/L2), sized for 4 CTAs per SM
 constexpr int SMC = (int)((54000 - TAB_SMEM) / (16 * HREC + 8)) / 32 * 32;
 constexpr size_t ENUM_SMEM = TAB_SMEM + (size_t)SMC * (16 * HREC + 8);
@@ -692,10 +699,13 @@ __global__ void __launch_bounds__(NT) enum_kernel(EnumParams p) {
   __shared__ i64 s_wmin[NT / 32];
   const int t = threadIdx.x;
   if (t == 0) s_cur = -1;
-  F2 *hitx = (F2 *)cls;  // [JMAX + 1][64] HIT_j({x}): j-subsets of [0, R_j) containing x
-  u64 *cs = cls + 2 * (JMAX + 1) * 64;  // [65][JMAX + 1] C(n, j), j <= JMAX
-  for (int q = t; q < (JMAX + 1) * 64; q += NT) hitx[q] = F2{g_hit.lo[q], g_hit.hi[q]};
+  F2 *hitx = (F2 *)cls;  // [JMAX + 1][HX] HIT_j({x}): j-subsets of [0, R_j) containing x
+  u64 *cs = cls + 2 * (JMAX + 1) * HX;  // [65][JMAX + 1] C(n, j), j <= JMAX
+  F2 *lowb = (F2 *)(cs + 65 * (JMAX + 1));  // [129] the n lowest bits
+  for (int q = t; q < (JMAX + 1) * HX; q += NT)
+    hitx[q] = F2{g_hit.lo[64 * (q / HX) + q % HX], g_hit.hi[64 * (q / HX) + q % HX]};
   for (int q = t; q < 65 * (JMAX + 1); q += NT) cs[q] = binom(q / (JMAX + 1), q % (JMAX + 1));
+  for (int q = t; q < 129; q += NT) lowb[q] = f2_nbits((u64)q);
   u64 *stage = cls + TAB_SMEM / 8;  // staged clause records
   const u64 Lc = p.ws.ctrl->lane_cands;
   const u64 CH = Lc * NT;
@@ -759,13 +769,13 @@ __global__ void __launch_bounds__(NT) enum_kernel(EnumParams p) {
       const u64 cnt = (ck - r_lo) < Lc ? (ck - r_lo) : Lc;
       const int rb = p.ws.rb[b];
       if (narrow) {
-        Clauses<u32> c{(const u32 *)sP, sH, hitx, cs, np, nn};
+        Clauses<u32> c{(const u32 *)sP, sH, hitx, lowb, cs, np, nn};
         key = run_lane<u32, COUNT>(p, r_lo, cnt, me, c, s_w, rb, wk);
       } else if (staged) {
-        Clauses<u64> c{sP, sH, hitx, cs, np, nn};
+        Clauses<u64> c{sP, sH, hitx, lowb, cs, np, nn};
         key = run_lane<u64, COUNT>(p, r_lo, cnt, me, c, s_w, rb, wk);
       } else {
-        Clauses<u64> c{p.ws.pk + lo, (const F2 *)p.ws.hrec + lo * HREC, hitx, cs, np, nn};
+        Clauses<u64> c{p.ws.pk + lo, (const F2 *)p.ws.hrec + lo * HREC, hitx, lowb, cs, np, nn};
         key = run_lane<u64, COUNT>(p, r_lo, cnt, me, c, s_w, rb, wk);
       }
     }
