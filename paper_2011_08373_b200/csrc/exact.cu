@@ -454,6 +454,7 @@ struct Clauses {
   const F2 *H;      // [np][HREC] H_j(P) at H[q * HREC + j - 1]
   const F2 *hitx;   // [JMAX + 1][HX] HIT_j({x}) for j >= 2 (0 when x >= R_j), shared memory
   const F2 *lowb;   // [129] the n lowest bits, shared memory
+  const int *reg;   // [JMAX + 1] R_j, shared memory
   const u64 *cs;    // [65][JMAX + 1] C(n, j) for j <= JMAX, shared memory
   int np, nn;
 };
@@ -577,7 +578,7 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
     d++;
     j--;
   }
-  int R = region_of(j);
+  int R = c.reg[j];
   // ---- iterate over sub-blocks in rank order
   for (;;) {
     const int ea = e < R ? e : R;
@@ -616,31 +617,26 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
       base += CS(R, j);
       d++;
       j--;
-      R = region_of(j);
+      R = c.reg[j];
       continue;
     }
-    bool moved = false;
-    while (d > 0) {
-      const int jp = j + 1;  // the parent's level
-      if (e + 1 < ep) {      // next sibling: t -> t + 1
-        U ^= (M)3 << e;
-        base += CS(e + 1, jp) - CS(e, jp);
-        e++;
-        moved = true;
-        break;
-      }
-      U &= ~((M)1 << e);
-      base -= CS(e, jp);
-      d--;
-      j = jp;
-      e = ep;
-      ep = d >= 2 ? (int)((tp >> (6 * (d - 2))) & 63u) : e_top;
+    if (d > 0 && e + 1 >= ep) {  // no next sibling here: pop until there is one
+      do {
+        U &= ~((M)1 << e);
+        base -= CS(e, j + 1);
+        d--;
+        j++;
+        e = ep;
+        ep = d >= 2 ? (int)((tp >> (6 * (d - 2))) & 63u) : e_top;
+      } while (d > 0 && e + 1 >= ep);
+      R = c.reg[j];
     }
-    if (moved) {
-      R = region_of(j);
+    if (d > 0) {  // next sibling: t -> t + 1 (children of the parent at level j + 1)
+      U ^= (M)3 << e;
+      base += CS(e + 1, j + 1) - CS(e, j + 1);
+      e++;
       continue;
     }
-    R = region_of(j);
     // ---- next top-level U (Gosper on the (k-J)-subsets of [J, me))
     if (!Utop) return best;
     base_top += CS(e_top, J);
@@ -684,7 +680,7 @@ __device__ i64 run_lane(const EnumParams &p, u64 r_lo, u64 cnt, int me, const Cl
 __device__ unsigned long long g_work[4];  // counting instantiation totals
 
 constexpr size_t TAB_SMEM =
-    (JMAX + 1) * HX * 16 + 65 * (JMAX + 1) * 8 + 129 * 16;  // HIT table, binomials, low masks
+    (JMAX + 1) * HX * 16 + 65 * (JMAX + 1) * 8 + 129 * 16 + 64;  // HIT table, binomials, low masks, R_j
 // clauses staged in shared memory (larger instances read L1/L2), sized for 4 CTAs per SM
 constexpr int SMC = (int)((54000 - TAB_SMEM) / (16 * HREC + 8)) / 32 * 32;
 constexpr size_t ENUM_SMEM = TAB_SMEM + (size_t)SMC * (16 * HREC + 8);
@@ -706,6 +702,8 @@ __global__ void __launch_bounds__(NT) enum_kernel(EnumParams p) {
     hitx[q] = F2{g_hit.lo[64 * (q / HX) + q % HX], g_hit.hi[64 * (q / HX) + q % HX]};
   for (int q = t; q < 65 * (JMAX + 1); q += NT) cs[q] = binom(q / (JMAX + 1), q % (JMAX + 1));
   for (int q = t; q < 129; q += NT) lowb[q] = f2_nbits((u64)q);
+  int *reg = (int *)(lowb + 129);  // [JMAX + 1] R_j
+  if (t <= JMAX) reg[t] = t ? region_of(t) : 0;
   u64 *stage = cls + TAB_SMEM / 8;  // staged clause records
   const u64 Lc = p.ws.ctrl->lane_cands;
   const u64 CH = Lc * NT;
@@ -769,13 +767,13 @@ __global__ void __launch_bounds__(NT) enum_kernel(EnumParams p) {
       const u64 cnt = (ck - r_lo) < Lc ? (ck - r_lo) : Lc;
       const int rb = p.ws.rb[b];
       if (narrow) {
-        Clauses<u32> c{(const u32 *)sP, sH, hitx, lowb, cs, np, nn};
+        Clauses<u32> c{(const u32 *)sP, sH, hitx, lowb, reg, cs, np, nn};
         key = run_lane<u32, COUNT>(p, r_lo, cnt, me, c, s_w, rb, wk);
       } else if (staged) {
-        Clauses<u64> c{sP, sH, hitx, lowb, cs, np, nn};
+        Clauses<u64> c{sP, sH, hitx, lowb, reg, cs, np, nn};
         key = run_lane<u64, COUNT>(p, r_lo, cnt, me, c, s_w, rb, wk);
       } else {
-        Clauses<u64> c{p.ws.pk + lo, (const F2 *)p.ws.hrec + lo * HREC, hitx, lowb, cs, np, nn};
+        Clauses<u64> c{p.ws.pk + lo, (const F2 *)p.ws.hrec + lo * HREC, hitx, lowb, reg, cs, np, nn};
         key = run_lane<u64, COUNT>(p, r_lo, cnt, me, c, s_w, rb, wk);
       }
     }
