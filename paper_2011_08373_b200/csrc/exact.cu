@@ -801,7 +801,8 @@ __device__ __forceinline__ int bitlen(u64 x) { return x ? 64 - __clzll((long lon
 
 __global__ void __launch_bounds__(FT) finish_kernel(In in, Out out, WS ws, int which, int k,
                                                     int exhaustive, int enum_lanes,
-                                                    u64 fixed_lane, int windows_per_lane) {
+                                                    u64 fixed_lane, int windows_per_lane,
+                                                    u64 lane_max, u64 lane_max_w) {
   typedef cub::BlockScan<u64, FT> Scan;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ u64 s_carry;
@@ -906,9 +907,12 @@ __global__ void __launch_bounds__(FT) finish_kernel(In in, Out out, WS ws, int w
     __syncthreads();
   }
   // lane window L: about 4 windows per lane of the enumeration grid, a power
-  // of two in [256, 4096]
+  // of two in [256, 16384] (weighted levels: [256, lane_max_w]; their feasible
+  // candidates cluster, and long windows leave one lane with most of the
+  // weight decoding)
+  const u64 Lmax = weighted ? lane_max_w : lane_max;
   u64 L = s_carry / ((u64)enum_lanes * (u64)windows_per_lane);
-  L = L < 256 ? 256 : (L > 4096 ? 4096 : L);
+  L = L < 256 ? 256 : (L > Lmax ? Lmax : L);
   L = 1ull << (63 - __clzll((long long)L));
   if (fixed_lane) L = fixed_lane;  // GR_LANE_CANDIDATES override
   const u64 CH = L * NT;
@@ -990,6 +994,17 @@ int windows_per_lane() {  // adaptive lane window: windows per lane per level
   }
   return v;
 }
+u64 lane_max(bool weighted) {  // the adaptive lane window's upper bound
+  static u64 v[2] = {0, 0};     // GR_LANE_MAX / GR_LANE_MAX_W override
+  const int i = weighted ? 1 : 0;
+  if (!v[i]) {
+    const char *e = getenv(weighted ? "GR_LANE_MAX_W" : "GR_LANE_MAX");
+    const u64 dflt = weighted ? 4096ull : 16384ull;
+    v[i] = e ? strtoull(e, nullptr, 10) : dflt;
+    if (v[i] < 256) v[i] = dflt;
+  }
+  return v[i];
+}
 u64 lane_cands() {  // 0 = adaptive (GR_LANE_CANDIDATES overrides)
   const u64 v = lane_cands_raw();
   return v == ~0ull ? 0ull : v;
@@ -1042,7 +1057,8 @@ extern "C" int gr_exact_prepare(const gr_batch *in, int which, gr_result *out, v
   }
   GR_LAUNCH("pack_kernel", (cudaStream_t)s, pack_kernel<<<in->B, PT, smem, st>>>(in_of(in, which), out_of(out), w, which));
   GR_LAUNCH("finish_kernel", (cudaStream_t)s, finish_kernel<<<1, FT, 0, st>>>(in_of(in, which), out_of(out), w, which, 0,
-                                   (in->flags & GR_FLAG_EXHAUSTIVE) ? 1 : 0, enum_grid() * NT, lane_cands(), windows_per_lane()));
+                                   (in->flags & GR_FLAG_EXHAUSTIVE) ? 1 : 0, enum_grid() * NT, lane_cands(), windows_per_lane(),
+                                   lane_max(false), lane_max(true)));
   if (n_active) {
     int *h = pinned_i32();
     if (!h) { gr_set_error("cudaMallocHost failed"); return GR_ECUDA; }
@@ -1096,7 +1112,8 @@ extern "C" int gr_exact_finish(const gr_batch *in, int which, int k, gr_result *
   WS w = ws_of(in, ws);
   cudaStream_t st = (cudaStream_t)s;
   GR_LAUNCH("finish_kernel", (cudaStream_t)s, finish_kernel<<<1, FT, 0, st>>>(in_of(in, which), out_of(out), w, which, k,
-                                   (in->flags & GR_FLAG_EXHAUSTIVE) ? 1 : 0, enum_grid() * NT, lane_cands(), windows_per_lane()));
+                                   (in->flags & GR_FLAG_EXHAUSTIVE) ? 1 : 0, enum_grid() * NT, lane_cands(), windows_per_lane(),
+                                   lane_max(false), lane_max(true)));
   if (n_active) {
     int *h = pinned_i32();
     if (!h) { gr_set_error("cudaMallocHost failed"); return GR_ECUDA; }
