@@ -498,16 +498,17 @@ __device__ __forceinline__ F2 test_sub(int j, M U, int e, F2 F, const Clauses<M>
   return F;
 }
 
-// weighted: W(U) + the weights of the j low elements encoded by bit idx
-template <typename M>
-__device__ __forceinline__ u64 weight_of(int j, u64 idx, M U, const u32 *w) {
+// weighted: the weights of the j low elements encoded by bit idx (colex
+// unrank of idx within [0, ea), downward scan over the shared binomials)
+__device__ __forceinline__ u64 weight_low(int j, u64 idx, int ea, const u32 *w, const u64 *cs) {
   u64 W = 0;
-  for (M t = U; t; t &= t - 1) W += w[ctz(t)];
-  for (int i = j; i >= 1; i--) {  // colex unrank of idx within [0, R_j)
-    int c = i - 1;
-    while (binom(c + 1, i) <= idx) c++;
+  int c = ea - 1;
+  for (int i = j; i >= 1; i--) {
+    u64 v;
+    while ((v = cs[c * (JMAX + 1) + i]) > idx) c--;
     W += w[c];
-    idx -= binom(c, i);
+    idx -= v;
+    c--;
   }
   return W;
 }
@@ -592,10 +593,13 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
       F = test_sub<M, COUNT>(j, U, ea, F, c, wk);
       if (f2_any(F)) {
         if (MODE == 2) {
+          u64 WU = 0;  // W(U), once per sub-block
+          for (M t = U; t; t &= t - 1) WU += w[ctz(t)];
           for (int h = 0; h < 2; h++)
             for (u64 f = h ? F.hi : F.lo; f; f &= f - 1) {
               const u64 idx = (u64)(64 * h + __ffsll((long long)f) - 1);
-              const i64 key = (i64)((weight_of<M>(j, idx, U, w) << rb) | (base + idx));
+              const i64 key =
+                  (i64)(((WU + weight_low(j, idx, ea, w, cs)) << rb) | (base + idx));
               best = key < best ? key : best;
             }
         } else {
