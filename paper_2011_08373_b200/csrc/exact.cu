@@ -557,9 +557,10 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
   int e_top = Utop ? ctz(Utop) : me;
   // Iterator state: the path t_0 > t_1 > ... > t_{d-1} of part-B choices
   // below Utop; the current node is (j = J - d, U, e = t_{d-1} or e_top) with
-  // region R = R_j, first rank base, and ep = the parent's e (t_{d-2} or
-  // e_top).  tp keeps the ancestors t_0 .. t_{d-2} (6 bits each); the current
-  // e and ep live in registers, so moving to a sibling does not touch tp.
+  // region R = R_j and ep = the parent's e (t_{d-2} or e_top).  tp is a stack
+  // of the older ancestors (6 bits each, most recent lowest).  Sub-blocks
+  // partition the level in rank order, so the next sub-block starts where
+  // this one ends: base += n.
   M U = Utop;
   u64 base = base_top;
   int d = 0, j = J, e = e_top, ep = e_top;
@@ -568,10 +569,7 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
   // s[j-1] >= R_j; then the child is t = s[j-1]
   while (j >= 2 && s[j - 1] >= region_of(j)) {
     const int t = s[j - 1];
-    if (d > 0) {
-      const int sh = 6 * (d - 1);
-      tp = (tp & ~(63ull << sh)) | ((u64)e << sh);
-    }
+    tp = (tp << 6) | (u64)ep;
     ep = e;
     e = t;
     U |= (M)1 << t;
@@ -608,17 +606,14 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
         }
       }
     }
+    base += n;
     // ---- advance: first child t = R of this node, else the next sibling up
     // the path
     if (j >= 2 && R < e) {
-      if (d > 0) {
-        const int sh = 6 * (d - 1);
-        tp = (tp & ~(63ull << sh)) | ((u64)e << sh);
-      }
+      tp = (tp << 6) | (u64)ep;
       ep = e;
       e = R;
       U |= (M)1 << R;
-      base += CS(R, j);
       d++;
       j--;
       R = c.reg[j];
@@ -627,24 +622,21 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
     if (d > 0 && e + 1 >= ep) {  // no next sibling here: pop until there is one
       do {
         U &= ~((M)1 << e);
-        base -= CS(e, j + 1);
         d--;
         j++;
         e = ep;
-        ep = d >= 2 ? (int)((tp >> (6 * (d - 2))) & 63u) : e_top;
+        ep = (int)(tp & 63u);
+        tp >>= 6;
       } while (d > 0 && e + 1 >= ep);
       R = c.reg[j];
     }
-    if (d > 0) {  // next sibling: t -> t + 1 (children of the parent at level j + 1)
+    if (d > 0) {  // next sibling: t -> t + 1
       U ^= (M)3 << e;
-      base += CS(e + 1, j + 1) - CS(e, j + 1);
       e++;
       continue;
     }
     // ---- next top-level U (Gosper on the (k-J)-subsets of [J, me))
     if (!Utop) return best;
-    base_top += CS(e_top, J);
-    if (base_top >= r_hi) return best;
     M S = Utop >> J;
     const M lb = lowbit(S);
     const M r = S + lb;
@@ -652,7 +644,6 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
     Utop = (M)(S << J);
     e_top = ctz(Utop);
     U = Utop;
-    base = base_top;
     e = ep = e_top;
   }
 #undef CS
