@@ -455,6 +455,7 @@ struct Clauses {
   const F2 *hitx;   // [JMAX + 1][HX] HIT_j({x}) for j >= 2 (0 when x >= R_j), shared memory
   const F2 *lowb;   // [129] the n lowest bits, shared memory
   const int *reg;   // [JMAX + 1] R_j, shared memory
+  const unsigned char *nb;  // [JMAX + 1][65] C(min(e, R_j), j), the sub-block sizes
   const u64 *cs;    // [65][JMAX + 1] C(n, j) for j <= JMAX, shared memory
   int np, nn;
 };
@@ -524,7 +525,6 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
   const int J = k < JMAX ? k : JMAX;
   const u64 *cs = c.cs;  // C(n, j), j <= JMAX
 #define CS(n, j) (cs[(n) * (JMAX + 1) + (j)])
-  const u64 r_hi = r_lo + cnt;
   i64 best = GR_KEY_NONE;
   // ---- position the iterator on the sub-block that holds rank r_lo: colex
   // unrank of r_lo (element i is the largest c with C(c, i) <= the remaining
@@ -578,16 +578,19 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
     j--;
   }
   int R = c.reg[j];
+  // positions relative to r_lo fit 32 bits (windows hold <= 2^14 candidates)
+  int pos = (int)((i64)base - (i64)r_lo);
+  const int cnt32 = (int)cnt;
   // ---- iterate over sub-blocks in rank order
   for (;;) {
-    const int ea = e < R ? e : R;
-    if (base >= r_hi) return best;
-    const u64 n = CS(ea, j);
-    if (n && base + n > r_lo) {
+    if (pos >= cnt32) return best;
+    const int n = c.nb[j * 65 + e];  // C(min(e, R_j), j)
+    if (n && pos + n > 0) {
       F2 F = c.lowb[n];
-      if (r_lo > base) F = f2_andnot(F, c.lowb[r_lo - base]);
-      if (r_hi < base + n) F = f2_and(F, c.lowb[r_hi - base]);
+      if (pos < 0) F = f2_andnot(F, c.lowb[-pos]);
+      if (cnt32 - pos < n) F = f2_and(F, c.lowb[cnt32 - pos]);
       if (COUNT) { wk.blocks++; wk.cands += (u64)f2_popc(F); }
+      const int ea = e < R ? e : R;
       F = test_sub<M, COUNT>(j, U, ea, F, c, wk);
       if (f2_any(F)) {
         if (MODE == 2) {
@@ -596,17 +599,17 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
           for (int h = 0; h < 2; h++)
             for (u64 f = h ? F.hi : F.lo; f; f &= f - 1) {
               const u64 idx = (u64)(64 * h + __ffsll((long long)f) - 1);
-              const i64 key =
-                  (i64)(((WU + weight_low(j, idx, ea, w, cs)) << rb) | (base + idx));
+              const i64 key = (i64)(((WU + weight_low(j, idx, ea, w, cs)) << rb) |
+                                    (r_lo + (u64)((i64)pos + (i64)idx)));
               best = key < best ? key : best;
             }
         } else {
-          if (best == GR_KEY_NONE) best = (i64)(base + (u64)f2_ctz(F));
+          if (best == GR_KEY_NONE) best = (i64)(r_lo + (u64)(pos + f2_ctz(F)));
           if (MODE == 0) return best;
         }
       }
     }
-    base += n;
+    pos += n;
     // ---- advance: first child t = R of this node, else the next sibling up
     // the path
     if (j >= 2 && R < e) {
@@ -675,7 +678,8 @@ __device__ i64 run_lane(const EnumParams &p, u64 r_lo, u64 cnt, int me, const Cl
 __device__ unsigned long long g_work[4];  // counting instantiation totals
 
 constexpr size_t TAB_SMEM =
-    (JMAX + 1) * HX * 16 + 65 * (JMAX + 1) * 8 + 129 * 16 + 64;  // HIT table, binomials, low masks, R_j
+    (JMAX + 1) * HX * 16 + 65 * (JMAX + 1) * 8 + 129 * 16 + 64 +
+    ((JMAX + 1) * 65 + 15) / 16 * 16;  // HIT table, binomials, low masks, R_j, sub-block sizes
 // clauses staged in shared memory (larger instances read L1/L2), sized for 4 CTAs per SM
 constexpr int SMC = (int)((54000 - TAB_SMEM) / (16 * HREC + 8)) / 32 * 32;
 constexpr size_t ENUM_SMEM = TAB_SMEM + (size_t)SMC * (16 * HREC + 8);
@@ -699,6 +703,11 @@ __global__ void __launch_bounds__(NT) enum_kernel(EnumParams p) {
   for (int q = t; q < 129; q += NT) lowb[q] = f2_nbits((u64)q);
   int *reg = (int *)(lowb + 129);  // [JMAX + 1] R_j
   if (t <= JMAX) reg[t] = t ? region_of(t) : 0;
+  unsigned char *nb = (unsigned char *)(reg + 16);  // [JMAX + 1][65] sub-block sizes
+  for (int q = t; q < (JMAX + 1) * 65; q += NT) {
+    const int jj = q / 65, ee = q % 65;
+    nb[q] = jj ? (unsigned char)binom(ee < region_of(jj) ? ee : region_of(jj), jj) : 0;
+  }
   u64 *stage = cls + TAB_SMEM / 8;  // staged clause records
   const u64 Lc = p.ws.ctrl->lane_cands;
   const u64 CH = Lc * NT;
@@ -762,13 +771,13 @@ __global__ void __launch_bounds__(NT) enum_kernel(EnumParams p) {
       const u64 cnt = (ck - r_lo) < Lc ? (ck - r_lo) : Lc;
       const int rb = p.ws.rb[b];
       if (narrow) {
-        Clauses<u32> c{(const u32 *)sP, sH, hitx, lowb, reg, cs, np, nn};
+        Clauses<u32> c{(const u32 *)sP, sH, hitx, lowb, reg, nb, cs, np, nn};
         key = run_lane<u32, COUNT>(p, r_lo, cnt, me, c, s_w, rb, wk);
       } else if (staged) {
-        Clauses<u64> c{sP, sH, hitx, lowb, reg, cs, np, nn};
+        Clauses<u64> c{sP, sH, hitx, lowb, reg, nb, cs, np, nn};
         key = run_lane<u64, COUNT>(p, r_lo, cnt, me, c, s_w, rb, wk);
       } else {
-        Clauses<u64> c{p.ws.pk + lo, (const F2 *)p.ws.hrec + lo * HREC, hitx, lowb, reg, cs, np, nn};
+        Clauses<u64> c{p.ws.pk + lo, (const F2 *)p.ws.hrec + lo * HREC, hitx, lowb, reg, nb, cs, np, nn};
         key = run_lane<u64, COUNT>(p, r_lo, cnt, me, c, s_w, rb, wk);
       }
     }
@@ -976,6 +985,7 @@ u64 lane_cands_raw() {
   if (!v) {
     const char *e = getenv("GR_LANE_CANDIDATES");
     v = e ? strtoull(e, nullptr, 10) : 0ull;  // 0: adaptive per level
+    if (v > (1ull << 20)) v = 1ull << 20;      // the walk keeps window positions in 32 bits
     if (!e) v = ~0ull;
   }
   return v;
