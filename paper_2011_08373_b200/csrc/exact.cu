@@ -910,7 +910,7 @@ __global__ void __launch_bounds__(FT) finish_kernel(In in, Out out, WS ws, int w
     }
     __syncthreads();
   }
-  // lane window L: about 4 windows per lane of the enumeration grid, a power
+  // lane window L: about 2 windows per lane of the enumeration grid, a power
   // of two in [256, 16384] (weighted levels: [256, lane_max_w]; their feasible
   // candidates cluster, and long windows leave one lane with most of the
   // weight decoding)
@@ -994,8 +994,8 @@ int windows_per_lane() {  // adaptive lane window: windows per lane per level
   static int v = 0;
   if (!v) {
     const char *e = getenv("GR_WINDOWS_PER_LANE");
-    v = e ? atoi(e) : 4;
-    if (v < 1) v = 4;
+    v = e ? atoi(e) : 2;
+    if (v < 1) v = 2;
   }
   return v;
 }
