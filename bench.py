@@ -445,15 +445,32 @@ def run_c5(a, rank, world, local, dev):
     import paper_2011_08373_b200 as gr
     from paper_2011_08373_b200 import synth
 
-    csr, H = synth.c5_clauses(seed=synth.seed_for(5, rank))
-    d = {"po": torch.from_numpy(csr.pos_off).to(dev), "pv": torch.from_numpy(csr.pos_var).to(dev),
+    from paper_2011_08373_b200 import multigpu
+
+    # N > 1: one C5 phi+ split by clause columns across the ranks (SURVEY.md
+    # §8(e) C5): each rank packs and streams its own column range, one NCCL
+    # all-reduce (SUM) of the 4096 counts per pick -- strong scaling
+    sharded = world > 1
+    csr, H = synth.c5_clauses(seed=synth.seed_for(5, 0 if sharded else rank))
+    po, pv = csr.pos_off, csr.pos_var
+    if sharded:
+        c0, c1 = multigpu.column_range(csr.n_pos, rank, world)
+        po, pv = (po[c0:c1 + 1] - po[c0]).astype(np.int64), pv[po[c0]:po[c1]]
+    d = {"po": torch.from_numpy(po).to(dev), "pv": torch.from_numpy(pv).to(dev),
          "no": torch.from_numpy(csr.neg_off).to(dev), "nv": torch.from_numpy(csr.neg_var).to(dev)}
     stream = torch.cuda.current_stream()
 
-    def step(keep_csr):
-        bm = gr.pack_bitmatrix(csr.m, d["po"], d["pv"], d["no"], d["nv"], device=dev, check=False,
-                               keep_csr=keep_csr)
-        return bm, gr.mhs_greedy_matrix(bm)
+    def solve(bm):
+        if sharded:
+            assign, status, picks, npk = multigpu.greedy_matrix_sharded(bm, rank, world)
+            return gr.GreedyMatrixResult(assign, status, picks, npk)
+        return gr.mhs_greedy_matrix(bm)
+
+    def step(keep_csr, dd=None):
+        dd = dd or d
+        bm = gr.pack_bitmatrix(csr.m, dd["po"], dd["pv"], dd["no"], dd["nv"], device=dev,
+                               check=False, keep_csr=keep_csr)
+        return bm, solve(bm)
 
     def timed(keep_csr, steps):
         for _ in range(max(1, min(a.warmup, 2))):
@@ -481,6 +498,12 @@ def run_c5(a, rank, world, local, dev):
     # bit matrix (count_kernel, HBM roofline); then the f3 incremental greedy
     total_ms, r, ld, kern, launches, clocks = timed(False, a.steps)
     inc_ms, r2, _, kern2, _, _ = timed(True, a.steps)
+    if world > 1:  # device time, max over ranks
+        import torch.distributed as dist
+
+        t = torch.tensor([total_ms, inc_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, inc_ms = t.tolist()
     same = (r2.picks.cpu() == r.picks.cpu()).all().item() and r2.n_picks == r.n_picks
     pk = peaks()
     ck = kern["count_kernel"]
@@ -491,23 +514,21 @@ def run_c5(a, rank, world, local, dev):
     ach = bytes_per_launch / (ck["ms"] / eff / 1e3) / 1e9
     a_ = r.assign.cpu().numpy().view(np.uint64)
     size = int(sum(bin(int(x)).count("1") for x in a_))
-    n = csr.n_pos
+    # whole-job clauses per step: the one split phi+ (sharded) or one per rank
+    n = csr.n_pos if sharded else csr.n_pos * world
     # e2e through the public API: pinned host CSR -> device, pack + greedy,
     # result (assignment, picks, status) -> host, every step
     e2e = None
     if not a.no_e2e:
         hp = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory()
-              for k, v in (("po", csr.pos_off), ("pv", csr.pos_var), ("no", csr.neg_off),
-                           ("nv", csr.neg_var))}
+              for k, v in (("po", po), ("pv", pv), ("no", csr.neg_off), ("nv", csr.neg_var))}
         h2d = sum(int(t.numel() * t.element_size()) for t in hp.values())
         ems, d2h = 0.0, 0
         for s_ in range(max(1, min(a.warmup, 2)) + a.steps):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             dd = {k: v.to(dev, non_blocking=True) for k, v in hp.items()}
-            bm = gr.pack_bitmatrix(csr.m, dd["po"], dd["pv"], dd["no"], dd["nv"], device=dev,
-                                   check=False, keep_csr=False)
-            rr = gr.mhs_greedy_matrix(bm)
+            bm, rr = step(False, dd)
             host = [rr.assign.cpu(), rr.picks.cpu(), rr.status.cpu()]
             e1.record(stream)
             e1.synchronize()
@@ -515,6 +536,12 @@ def run_c5(a, rank, world, local, dev):
             if s_ >= max(1, min(a.warmup, 2)):
                 ems += e0.elapsed_time(e1)
         d2h = sum(int(x.numel() * x.element_size()) for x in host)
+        if world > 1:
+            import torch.distributed as dist
+
+            t = torch.tensor([ems], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
         e2e = {"value": n * a.steps / (ems / 1e3), "unit": "clauses/s (greedy)",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ems / a.steps}
     cpu = None
@@ -523,9 +550,12 @@ def run_c5(a, rank, world, local, dev):
     line = {
         "metric": METRIC, "value": n * a.steps / (total_ms / 1e3), "unit": "clauses/s (greedy)",
         "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": total_ms / a.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "higher_is_better": True, "scaling": "strong" if sharded else "weak", "vs_baseline": None,
+        "dtype": "u64",
         "data": "synthetic", "config": {"workload": "C5: greedy mhs, m=4096, n=2^24 positive clauses (8 GiB bit matrix); step = device pack + greedy + prune",
-                                        "l2": "inputs (8 GiB) larger than L2"},
+                                        "l2": "inputs (8 GiB) larger than L2",
+                                        "parallelism": (f"clause columns sharded x{world} (NCCL allreduce SUM of the counts per pick)"
+                                                        if sharded else "single GPU")},
         "greedy": {"picks": r.n_picks, "size": size, "status": int(r.status.item()), "planted": 256,
                    "passes": ck["launches"] / a.steps},
         "f3_incremental": {"ms_per_step": inc_ms / a.steps, "speedup": total_ms / inc_ms,

@@ -245,6 +245,51 @@ int gr_mhs_greedy_matrix(const gr_bitmatrix *in, uint64_t *assign, int32_t *stat
 int gr_greedy_count_shard(const gr_bitmatrix *shard, const uint64_t *d_U, uint32_t *d_counts,
                           gr_stream_t s);
 
+/* ---- column-sharded greedy (PAPER.md:24 greedy mhs) ---
+ * Each rank owns a contiguous range of phi+'s clause columns as its own
+ * gr_bitmatrix (same m, its own n_pos / ld / bits and, optionally, the CSR of
+ * its clauses; phi- replicated).  The greedy's counts are sums over clauses,
+ * so the caller all-reduces (SUM) the per-rank counts between steps and every
+ * rank takes the same pick (ratio rule with weights, lowest index on ties,
+ * readings R11/R20) -- picks identical to gr_mhs_greedy_matrix over the
+ * whole matrix.  Protocol, all on stream s, one workspace per shard
+ * (gr_greedy_shard_workspace_bytes, caller-owned device memory):
+ *
+ *   gr_greedy_shard_begin(sh, counts)        counts := this shard's counts
+ *   repeat: all_reduce_sum(counts); gr_greedy_shard_step(sh, counts)
+ *           (counts in: global counts; out: this shard's counts after the
+ *            pick; a step after the last pick is a no-op)
+ *   gr_greedy_shard_state(...)               n_picks, done (synchronises s)
+ *   prune (reverse-delete, R12):
+ *     gr_greedy_shard_private(sh, -1, flags) flags[j] |= pick j is the sole
+ *                                            hitter of a clause of this shard
+ *     all_reduce_max(flags); for j = n_picks-1 .. 0 with flags[j] == 0:
+ *       flags[j] := 0; gr_greedy_shard_private(sh, j, flags);
+ *       all_reduce_max(flags[j]); if still 0: removed[j] := 1 and
+ *       gr_greedy_shard_remove(sh, j)
+ *   gr_greedy_shard_finalize(sh, removed, assign, status)
+ *
+ * counts: device uint32 [m].  flags, removed: device int32 [m].  assign:
+ * device [ceil(m/64)] words; status: device int32 (GR_SAT or
+ * GR_SAT_NEG_VIOLATED).  Errors: GR_EINVAL (null pointer, bad matrix, j out
+ * of range), GR_EWORKSPACE (workspace too small). */
+size_t gr_greedy_shard_workspace_bytes(const gr_bitmatrix *shard);
+int gr_greedy_shard_begin(const gr_bitmatrix *shard, uint32_t *d_counts, void *ws,
+                          size_t ws_bytes, gr_stream_t s);
+int gr_greedy_shard_step(const gr_bitmatrix *shard, uint32_t *d_counts, void *ws, size_t ws_bytes,
+                         gr_stream_t s);
+/* n_picks, done: host int32 (may be NULL); d_picks: device int32 [m] (may be
+ * NULL) receives the pick order padded with -1. */
+int gr_greedy_shard_state(const gr_bitmatrix *shard, const void *ws, size_t ws_bytes,
+                          int32_t *n_picks, int32_t *done, int32_t *d_picks, gr_stream_t s);
+int gr_greedy_shard_private(const gr_bitmatrix *shard, int32_t only, int32_t *d_flags, void *ws,
+                            size_t ws_bytes, gr_stream_t s);
+int gr_greedy_shard_remove(const gr_bitmatrix *shard, int32_t j, void *ws, size_t ws_bytes,
+                           gr_stream_t s);
+int gr_greedy_shard_finalize(const gr_bitmatrix *shard, const int32_t *d_removed,
+                             uint64_t *assign, int32_t *status, void *ws, size_t ws_bytes,
+                             gr_stream_t s);
+
 /* ---- launch accounting and profiling ------------------------------------
  * Every kernel launch of the library is counted (gr_launch_count).  With
  * gr_profile(1) each launch is bracketed by CUDA events recorded on the

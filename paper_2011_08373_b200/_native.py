@@ -29,6 +29,9 @@ EXPORTED = [
     "gr_pack_varmajor", "gr_pack_clausemajor", "gr_greedy_matrix_workspace_bytes",
     "gr_mhs_greedy_matrix", "gr_greedy_count_shard", "gr_last_error", "gr_version",
     "gr_profile", "gr_profile_read", "gr_launch_count", "gr_solve", "gr_solve_pms_mhs",
+    "gr_greedy_shard_workspace_bytes", "gr_greedy_shard_begin", "gr_greedy_shard_step",
+    "gr_greedy_shard_state", "gr_greedy_shard_private", "gr_greedy_shard_remove",
+    "gr_greedy_shard_finalize",
 ]
 GR_STRATEGY_MHS, GR_STRATEGY_MAXSAT = 0, 1
 
@@ -97,6 +100,17 @@ def lib():
         L.gr_greedy_matrix_workspace_bytes.restype = sz
         L.gr_mhs_greedy_matrix.argtypes = [vp, vp, vp, vp, vp, vp, sz, vp]
         L.gr_greedy_count_shard.argtypes = [vp, vp, vp, vp]
+        L.gr_greedy_shard_workspace_bytes.argtypes = [vp]
+        L.gr_greedy_shard_workspace_bytes.restype = sz
+        L.gr_greedy_shard_begin.argtypes = [vp, vp, vp, sz, vp]
+        L.gr_greedy_shard_step.argtypes = [vp, vp, vp, sz, vp]
+        L.gr_greedy_shard_state.argtypes = [vp, vp, sz, vp, vp, vp, vp]
+        L.gr_greedy_shard_private.argtypes = [vp, i32, vp, vp, sz, vp]
+        L.gr_greedy_shard_remove.argtypes = [vp, i32, vp, sz, vp]
+        L.gr_greedy_shard_finalize.argtypes = [vp, vp, vp, vp, vp, sz, vp]
+        for f in (L.gr_greedy_shard_begin, L.gr_greedy_shard_step, L.gr_greedy_shard_state,
+                  L.gr_greedy_shard_private, L.gr_greedy_shard_remove, L.gr_greedy_shard_finalize):
+            f.restype = C.c_int
         L.gr_last_error.restype = C.c_char_p
         L.gr_version.restype = C.c_char_p
         for f in (L.gr_exact_prepare, L.gr_exact_level, L.gr_exact_finish, L.gr_pack_varmajor,
@@ -457,6 +471,57 @@ def greedy_count_shard(bm: DeviceBitMatrix, U, counts, stream=None):
     s = bm.struct()
     _check(lib().gr_greedy_count_shard(C.byref(s), _ptr(U), _ptr(counts), _stream(stream)),
            "gr_greedy_count_shard")
+
+
+class GreedyShard:
+    """One rank's column shard of the greedy (gr_greedy_shard_*, SURVEY.md
+    §8(e) C5).  Argument marshalling only: begin/step/state/private/remove/
+    finalize map one-to-one onto the C-ABI; the exchange between steps is the
+    caller's (multigpu.greedy_matrix_sharded)."""
+
+    def __init__(self, bm: DeviceBitMatrix, stream=None):
+        torch = _torch()
+        self.L, self.bm, self.stream = lib(), bm, stream
+        self.s = bm.struct()
+        nbytes = self.L.gr_greedy_shard_workspace_bytes(C.byref(self.s))
+        if nbytes == 0:
+            raise GrError("gr_greedy_shard_workspace_bytes rejected the shard")
+        dev = bm.bits.device
+        self.ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        self.counts = torch.zeros(bm.m, dtype=torch.int32, device=dev)  # uint32 counts
+
+    def begin(self):
+        _check(self.L.gr_greedy_shard_begin(C.byref(self.s), _ptr(self.counts), _ptr(self.ws),
+                                            self.ws.numel(), _stream(self.stream)),
+               "gr_greedy_shard_begin")
+
+    def step(self):
+        _check(self.L.gr_greedy_shard_step(C.byref(self.s), _ptr(self.counts), _ptr(self.ws),
+                                           self.ws.numel(), _stream(self.stream)),
+               "gr_greedy_shard_step")
+
+    def state(self, picks=None):
+        n, d = C.c_int32(0), C.c_int32(0)
+        _check(self.L.gr_greedy_shard_state(C.byref(self.s), _ptr(self.ws), self.ws.numel(),
+                                            C.byref(n), C.byref(d),
+                                            _ptr(picks) if picks is not None else None,
+                                            _stream(self.stream)), "gr_greedy_shard_state")
+        return int(n.value), bool(d.value)
+
+    def private(self, only, flags):
+        _check(self.L.gr_greedy_shard_private(C.byref(self.s), int(only), _ptr(flags),
+                                              _ptr(self.ws), self.ws.numel(),
+                                              _stream(self.stream)), "gr_greedy_shard_private")
+
+    def remove(self, j):
+        _check(self.L.gr_greedy_shard_remove(C.byref(self.s), int(j), _ptr(self.ws),
+                                             self.ws.numel(), _stream(self.stream)),
+               "gr_greedy_shard_remove")
+
+    def finalize(self, removed, assign, status):
+        _check(self.L.gr_greedy_shard_finalize(C.byref(self.s), _ptr(removed), _ptr(assign),
+                                               _ptr(status), _ptr(self.ws), self.ws.numel(),
+                                               _stream(self.stream)), "gr_greedy_shard_finalize")
 
 
 def version() -> str:

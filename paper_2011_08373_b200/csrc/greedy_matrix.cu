@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(IT) first_pick_kernel(const u32 *counts, int m
 
 // one pick: apply the pending pick v (cover its clauses, decrement counts),
 // then the last CTA chooses the next pick
-template <typename V>
+template <typename V, bool PICK = true>
 __global__ void __launch_bounds__(IT) incr_step_kernel(const u64 *R, int64_t ld, int m, u64 *U,
                                                       u32 *counts, const int64_t *off,
                                                       const V *var, const u32 *w, GCtrl *ctrl,
@@ -411,6 +411,7 @@ __global__ void __launch_bounds__(IT) incr_step_kernel(const u64 *R, int64_t ld,
   __syncthreads();
   for (int u = threadIdx.x; u < m; u += IT)
     if (hist[u]) atomicSub(&counts[u], hist[u]);
+  if (!PICK) return;  // sharded greedy: the next pick needs the all-reduced counts
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) s_last = atomicAdd(&ctrl->ticket, 1u) == gridDim.x - 1;
@@ -423,6 +424,47 @@ __global__ void __launch_bounds__(IT) incr_step_kernel(const u64 *R, int64_t ld,
       ctrl->steps += 1;
     }
   }
+}
+
+// ---- column-sharded greedy ----------------------------------
+// Each rank owns a range of clause columns; the host all-reduces (SUM) the
+// per-rank counts between steps, so every rank takes the same pick from the
+// same global counts.  One step: pick from the global counts, then cover this
+// shard's clauses of the pick and bring the local counts up to date
+// (incremental decrement, or mark + recount pass).
+__global__ void __launch_bounds__(IT) shard_pick_kernel(const u32 *gcounts, int m, const u32 *w,
+                                                       GCtrl *ctrl, int *picks, u32 *counts,
+                                                       int zero_counts) {
+  typedef cub::BlockReduce<Cand, IT> Red;
+  __shared__ typename Red::TempStorage tmp;
+  if (*(volatile int *)&ctrl->done) return;
+  Cand best{0u, 1u, 0x7fffffff};
+  for (int v = threadIdx.x; v < m; v += IT) {
+    best = CandBetter()(Cand{gcounts[v], w ? w[v] : 1u, v}, best);
+    if (zero_counts) counts[v] = 0;  // the recount pass accumulates into them
+  }
+  best = Red(tmp).Reduce(best, CandBetter());
+  if (threadIdx.x == 0) {
+    ctrl->maxcount = best.c;
+    if (best.c == 0) {  // no uncovered clause anywhere
+      ctrl->done = 1;
+      ctrl->pending = ctrl->vprev = -1;
+    } else {
+      picks[ctrl->npicks] = best.v;
+      ctrl->npicks += 1;
+      ctrl->pending = ctrl->vprev = best.v;
+    }
+  }
+}
+
+// U &= ~R[v*] on this shard (recounting steps)
+__global__ void shard_mark_kernel(const u64 *R, int64_t ld, u64 *U, const GCtrl *ctrl) {
+  if (*(volatile const int *)&ctrl->done) return;
+  const int v = ctrl->vprev;
+  const u64 *Rv = R + (size_t)v * ld;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < ld;
+       w += (int64_t)gridDim.x * blockDim.x)
+    U[w] &= ~Rv[w];
 }
 
 // ---- prune: bit-sliced hit counters over the picks ----------------------------
@@ -820,5 +862,163 @@ extern "C" int gr_mhs_greedy_matrix(const gr_bitmatrix *in, uint64_t *assign, in
                                      status, smask));
   if (picks) GR_CUDA(cudaMemcpyAsync(picks, wpicks, sizeof(int) * in->m, cudaMemcpyDeviceToDevice, st));
   GR_CUDA(cudaStreamSynchronize(st));
+  return GR_OK;
+}
+
+// ---- column-sharded greedy ------------------------------------
+namespace {
+struct ShardWS {
+  GCtrl *ctrl;
+  u64 *U, *planes, *smask;
+  u32 *counts;
+  int *picks, *flags;
+  GLayout L;
+};
+int shard_ws(const gr_bitmatrix *in, void *ws, size_t ws_bytes, ShardWS &o) {
+  int rc = validate_matrix(in);
+  if (rc) return rc;
+  o.L = glayout(in);
+  if (!ws || ws_bytes < o.L.total) { gr_set_error("workspace too small"); return GR_EWORKSPACE; }
+  char *base = (char *)ws;
+  o.ctrl = (GCtrl *)(base + o.L.ctrl);
+  o.U = (u64 *)(base + o.L.U);
+  o.counts = (u32 *)(base + o.L.counts);
+  o.picks = (int *)(base + o.L.picks);
+  o.planes = (u64 *)(base + o.L.planes);
+  o.flags = (int *)(base + o.L.flags);
+  o.smask = (u64 *)(base + o.L.smask);
+  return GR_OK;
+}
+bool shard_incremental(const gr_bitmatrix *in) {
+  return in->pos_off != nullptr && in->pos_var != nullptr && in->m <= 50000 &&
+         getenv("GR_GREEDY_EAGER") == nullptr;
+}
+}  // namespace
+
+extern "C" size_t gr_greedy_shard_workspace_bytes(const gr_bitmatrix *shard) {
+  return gr_greedy_matrix_workspace_bytes(shard);
+}
+
+extern "C" int gr_greedy_shard_begin(const gr_bitmatrix *shard, uint32_t *d_counts, void *ws,
+                                     size_t ws_bytes, gr_stream_t s) {
+  ShardWS w;
+  int rc = shard_ws(shard, ws, ws_bytes, w);
+  if (rc) return rc;
+  if (!d_counts) { gr_set_error("null counts"); return GR_EINVAL; }
+  cudaStream_t st = (cudaStream_t)s;
+  const int64_t ld = shard->ld;
+  GR_LAUNCH("init_kernel", st, init_kernel<<<592, 256, 0, st>>>(w.U, ld, shard->n_pos, w.ctrl, w.counts, shard->m, w.picks));
+  count_grid();
+  if (shard_incremental(shard)) {
+    const int hgrid = (int)std::min<int64_t>((shard->n_pos * 9 + 255) / 256, 148 * 8);
+    const size_t hs = sizeof(u32) * (size_t)shard->m;
+    if (shard->var_bytes == 2)
+      GR_LAUNCH("csr_hist_kernel", st, csr_hist_kernel<int16_t><<<std::max(hgrid, 1), 256, hs, st>>>(
+                                          shard->n_pos, shard->pos_off, (const int16_t *)shard->pos_var, shard->m, w.counts));
+    else
+      GR_LAUNCH("csr_hist_kernel", st, csr_hist_kernel<int32_t><<<std::max(hgrid, 1), 256, hs, st>>>(
+                                          shard->n_pos, shard->pos_off, (const int32_t *)shard->pos_var, shard->m, w.counts));
+  } else {
+    CountParams p{shard->bits, ld, shard->m, (int)((ld + TW - 1) / TW), w.U, nullptr, w.counts,
+                  nullptr, 0};
+    GR_LAUNCH("count_kernel", st, count_kernel<<<count_grid(), CT, COUNT_SMEM_V2, st>>>(p));
+  }
+  GR_CUDA(cudaMemcpyAsync(d_counts, w.counts, sizeof(u32) * shard->m, cudaMemcpyDeviceToDevice, st));
+  return GR_OK;
+}
+
+extern "C" int gr_greedy_shard_step(const gr_bitmatrix *shard, uint32_t *d_counts, void *ws,
+                                    size_t ws_bytes, gr_stream_t s) {
+  ShardWS w;
+  int rc = shard_ws(shard, ws, ws_bytes, w);
+  if (rc) return rc;
+  if (!d_counts) { gr_set_error("null counts"); return GR_EINVAL; }
+  cudaStream_t st = (cudaStream_t)s;
+  const int64_t ld = shard->ld;
+  const bool inc = shard_incremental(shard);
+  GR_LAUNCH("shard_pick_kernel", st, shard_pick_kernel<<<1, IT, 0, st>>>(d_counts, shard->m, shard->w, w.ctrl, w.picks, w.counts, inc ? 0 : 1));
+  if (inc) {
+    const size_t hs = sizeof(u32) * (size_t)shard->m;
+    if (shard->var_bytes == 2)
+      GR_LAUNCH("incr_step_kernel", st, (incr_step_kernel<int16_t, false><<<count_grid(), IT, hs, st>>>(
+                                            shard->bits, ld, shard->m, w.U, w.counts, shard->pos_off,
+                                            (const int16_t *)shard->pos_var, shard->w, w.ctrl, w.picks)));
+    else
+      GR_LAUNCH("incr_step_kernel", st, (incr_step_kernel<int32_t, false><<<count_grid(), IT, hs, st>>>(
+                                            shard->bits, ld, shard->m, w.U, w.counts, shard->pos_off,
+                                            (const int32_t *)shard->pos_var, shard->w, w.ctrl, w.picks)));
+  } else {
+    const int egrid = (int)std::min<int64_t>((ld + 255) / 256, 148 * 8);
+    GR_LAUNCH("shard_mark_kernel", st, shard_mark_kernel<<<egrid, 256, 0, st>>>(shard->bits, ld, w.U, w.ctrl));
+    CountParams p{shard->bits, ld, shard->m, (int)((ld + TW - 1) / TW), w.U, nullptr, w.counts,
+                  w.ctrl, 0};
+    GR_LAUNCH("count_kernel", st, count_kernel<<<count_grid(), CT, COUNT_SMEM_V2, st>>>(p));
+  }
+  GR_CUDA(cudaMemcpyAsync(d_counts, w.counts, sizeof(u32) * shard->m, cudaMemcpyDeviceToDevice, st));
+  return GR_OK;
+}
+
+extern "C" int gr_greedy_shard_state(const gr_bitmatrix *shard, const void *ws, size_t ws_bytes,
+                                     int32_t *n_picks, int32_t *done, int32_t *d_picks,
+                                     gr_stream_t s) {
+  ShardWS w;
+  int rc = shard_ws(shard, (void *)ws, ws_bytes, w);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)s;
+  int *h = pinned_ctrl();
+  if (!h) { gr_set_error("cudaMallocHost failed"); return GR_ECUDA; }
+  GR_CUDA(cudaMemcpyAsync(h, w.ctrl, sizeof(GCtrl), cudaMemcpyDeviceToHost, st));
+  if (d_picks)
+    GR_CUDA(cudaMemcpyAsync(d_picks, w.picks, sizeof(int) * shard->m, cudaMemcpyDeviceToDevice, st));
+  GR_CUDA(cudaStreamSynchronize(st));
+  if (n_picks) *n_picks = ((GCtrl *)h)->npicks;
+  if (done) *done = ((GCtrl *)h)->done;
+  return GR_OK;
+}
+
+extern "C" int gr_greedy_shard_private(const gr_bitmatrix *shard, int32_t only, int32_t *d_flags,
+                                       void *ws, size_t ws_bytes, gr_stream_t s) {
+  ShardWS w;
+  int rc = shard_ws(shard, ws, ws_bytes, w);
+  if (rc) return rc;
+  if (!d_flags) { gr_set_error("null flags"); return GR_EINVAL; }
+  cudaStream_t st = (cudaStream_t)s;
+  const int64_t ld = shard->ld;
+  const int egrid = (int)std::min<int64_t>((ld + 255) / 256, 148 * 8);
+  u64 *one = w.U + ld;  // the second U buffer is free after the greedy loop
+  if (only < 0) {
+    GR_LAUNCH("planes_build_kernel", st, planes_build_kernel<<<egrid, 256, 0, st>>>(shard->bits, ld, w.picks, w.ctrl, w.planes, w.L.nplanes));
+    GR_LAUNCH("one_kernel", st, one_kernel<<<egrid, 256, 0, st>>>(w.planes, w.L.nplanes, ld, one));
+  }
+  GR_LAUNCH("private_kernel", st, private_kernel<<<148 * 4, 256, 0, st>>>(shard->bits, ld, w.picks, w.ctrl, one, d_flags, only));
+  return GR_OK;
+}
+
+extern "C" int gr_greedy_shard_remove(const gr_bitmatrix *shard, int32_t j, void *ws,
+                                      size_t ws_bytes, gr_stream_t s) {
+  ShardWS w;
+  int rc = shard_ws(shard, ws, ws_bytes, w);
+  if (rc) return rc;
+  if (j < 0 || j >= shard->m) { gr_set_error("pick index out of range"); return GR_EINVAL; }
+  cudaStream_t st = (cudaStream_t)s;
+  const int64_t ld = shard->ld;
+  const int egrid = (int)std::min<int64_t>((ld + 255) / 256, 148 * 8);
+  int v = -1;
+  GR_CUDA(cudaMemcpyAsync(&v, w.picks + j, sizeof(int), cudaMemcpyDeviceToHost, st));
+  GR_CUDA(cudaStreamSynchronize(st));
+  if (v < 0 || v >= shard->m) { gr_set_error("no such pick"); return GR_EINVAL; }
+  GR_LAUNCH("remove_kernel", st, remove_kernel<<<egrid, 256, 0, st>>>(shard->bits, ld, v, w.planes, w.L.nplanes, w.U + ld));
+  return GR_OK;
+}
+
+extern "C" int gr_greedy_shard_finalize(const gr_bitmatrix *shard, const int32_t *d_removed,
+                                        uint64_t *assign, int32_t *status, void *ws,
+                                        size_t ws_bytes, gr_stream_t s) {
+  ShardWS w;
+  int rc = shard_ws(shard, ws, ws_bytes, w);
+  if (rc) return rc;
+  if (!d_removed || !assign || !status) { gr_set_error("null removed / assign / status"); return GR_EINVAL; }
+  cudaStream_t st = (cudaStream_t)s;
+  GR_LAUNCH("finalize_kernel", st, finalize_kernel<<<1, 256, 0, st>>>(w.picks, w.ctrl, d_removed, shard->m, shard->neg, shard->n_neg, assign, status, w.smask));
   return GR_OK;
 }

@@ -11,7 +11,11 @@ Two ways the Solve step shards:
   c % G (``gr_exact_level(.., shard=r, nshard=G)``); after each level the
   per-instance minimum key is all-reduced (MIN, int64; 8 bytes per instance)
   so every rank commits the same level (``run_levels_sharded``).  This is the
-  method's only real exchange step: one 8-byte all-reduce per level.
+  exact solvers' only real exchange step: one 8-byte all-reduce per level.
+* column sharding of one huge phi+ for the greedy (config C5): each rank owns
+  a contiguous range of clause columns; the counts are sums over clauses, so
+  one all-reduce (SUM) of the m counts per pick gives every rank the same
+  pick (``run_greedy_sharded`` over the gr_greedy_shard_* protocol).
 """
 from __future__ import annotations
 
@@ -77,3 +81,82 @@ def solve_exact_sharded(db, which: int, rank: int, world: int, group=None, out=N
     levels = run_levels_sharded(s, rank, world,
                                 nccl_allreduce_min(group) if world > 1 else (lambda t: None))
     return s.out, levels
+
+
+# ---- column-sharded greedy (C5) ------------------------------------------------
+def run_greedy_sharded(shard, allreduce_sum: Callable[[object], None],
+                       allreduce_max: Callable[[object], None], steps_per_check: int = 32):
+    """Greedy mhs over phi+ split by clause columns across ranks (SURVEY.md
+    §8(e) C5).  ``shard`` offers the gr_greedy_shard_* protocol (a
+    GreedyShard on the GPU): ``counts`` (int32 tensor [m]), begin(), step(),
+    state(picks=None) -> (n_picks, done), private(only, flags), remove(j),
+    finalize(removed, assign, status).  The exchanges are one all-reduce (SUM)
+    of the m counts per pick and, in the prune, one all-reduce (MAX) of the
+    private flags plus one single-flag all-reduce per re-checked pick.
+    Returns (assign, status, picks, n_picks), identical on every rank."""
+    import torch
+
+    counts = shard.counts
+    dev, m = counts.device, counts.numel()
+    shard.begin()
+    steps = 0
+    while True:
+        for _ in range(steps_per_check):
+            allreduce_sum(counts)
+            shard.step()
+        steps += steps_per_check
+        n, done = shard.state()
+        if done:
+            break
+        if steps > m + 2 * steps_per_check:
+            raise RuntimeError("sharded greedy did not terminate")
+    picks = torch.full((m,), -1, dtype=torch.int32, device=dev)
+    n, _ = shard.state(picks)
+    # prune (R12): picks that are the sole hitter of a clause on some rank stay
+    flags = torch.zeros(m, dtype=torch.int32, device=dev)
+    shard.private(-1, flags)
+    allreduce_max(flags)
+    keep = flags[:n].cpu().tolist()
+    removed = torch.zeros(m, dtype=torch.int32, device=dev)
+    for j in range(n - 1, -1, -1):  # the others in reverse pick order
+        if keep[j]:
+            continue
+        fj = flags[j:j + 1]
+        fj.zero_()
+        shard.private(j, flags)
+        allreduce_max(fj)
+        if int(fj.item()) == 0:
+            removed[j] = 1
+            shard.remove(j)
+    assign = torch.zeros((m + 63) // 64, dtype=torch.int64, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    shard.finalize(removed, assign, status)
+    return assign, status, picks, n
+
+
+def nccl_allreduce(op: str, group=None):
+    import torch.distributed as dist
+
+    red = {"sum": dist.ReduceOp.SUM, "max": dist.ReduceOp.MAX, "min": dist.ReduceOp.MIN}[op]
+
+    def f(t):
+        dist.all_reduce(t, op=red, group=group)
+
+    return f
+
+
+def column_range(n_pos: int, rank: int, world: int):
+    """Clause columns [c0, c1) of ``rank``: equal contiguous slices."""
+    return n_pos * rank // world, n_pos * (rank + 1) // world
+
+
+def greedy_matrix_sharded(bm_shard, rank: int, world: int, group=None, stream=None):
+    """Greedy mhs of a C5-style phi+ whose clause columns are split across
+    the ranks of ``group`` (each rank passes its own DeviceBitMatrix shard);
+    every rank returns the same (assign, status, picks, n_picks)."""
+    from . import _native as N
+
+    sh = N.GreedyShard(bm_shard, stream=stream)
+    if world > 1:
+        return run_greedy_sharded(sh, nccl_allreduce("sum", group), nccl_allreduce("max", group))
+    return run_greedy_sharded(sh, lambda t: None, lambda t: None)

@@ -125,3 +125,126 @@ def test_shard_instances_balanced_and_complete():
         assert allidx == list(range(748))
         loads = [costs[p].sum() for p in parts]
         assert max(loads) <= 2.0 * (sum(loads) / world) + costs.max()
+
+
+# ---- column-sharded greedy (C5 protocol) ------------------------------------------
+class FakeGreedyShard:
+    """CPU stand-in of one rank's gr_greedy_shard_* calls: this rank's clauses
+    (lists of variable ids) and the replicated negatives."""
+
+    def __init__(self, m, clauses, neg):
+        self.m, self.cl, self.neg = m, [set(c) for c in clauses], [set(c) for c in neg]
+        self.counts = torch.zeros(m, dtype=torch.int32)
+
+    def _local_counts(self):
+        c = np.zeros(self.m, np.int64)
+        for i, cl in enumerate(self.cl):
+            if self.unc[i]:
+                for v in cl:
+                    c[v] += 1
+        self.counts.copy_(torch.from_numpy(c.astype(np.int32)))
+
+    def begin(self):
+        self.unc = [True] * len(self.cl)
+        self.picks, self.done = [], False
+        self._local_counts()
+
+    def step(self):  # counts hold the all-reduced global counts
+        if not self.done:
+            g = self.counts.numpy()
+            if g.max() == 0:
+                self.done = True
+            else:
+                v = int(np.argmax(g))  # first maximum = lowest index on ties
+                self.picks.append(v)
+                for i, cl in enumerate(self.cl):
+                    if v in cl:
+                        self.unc[i] = False
+        self._local_counts()
+
+    def state(self, picks=None):
+        if picks is not None:
+            picks[:len(self.picks)] = torch.tensor(self.picks, dtype=torch.int32)
+        self.removed = set()
+        return len(self.picks), self.done
+
+    def private(self, only, flags):
+        live = [p for j, p in enumerate(self.picks) if j not in self.removed]
+        js = range(len(self.picks)) if only < 0 else [only]
+        for j in js:
+            v = self.picks[j]
+            for cl in self.cl:
+                if v in cl and sum(1 for p in live if p in cl) == 1:
+                    flags[j] = 1
+                    break
+
+    def remove(self, j):
+        self.removed.add(j)
+
+    def finalize(self, removed, assign, status):
+        S = {p for j, p in enumerate(self.picks) if not int(removed[j])}
+        for v in S:
+            assign[v // 64] |= 1 << (v % 64) if v % 64 < 63 else -(1 << 63)
+        status[0] = 2 if any(n <= S for n in self.neg) else 0
+
+
+def greedy_instance(seed):
+    rng = np.random.default_rng(seed)
+    m, n = 40, 120
+    H = rng.choice(m, size=6, replace=False)
+    cl = []
+    for _ in range(n):
+        s = int(rng.integers(2, 6))
+        c = {int(rng.choice(H))} | set(rng.choice(m, size=s - 1, replace=False).tolist())
+        cl.append(sorted(c))
+    neg = [sorted(rng.choice(m, size=2, replace=False).tolist()) for _ in range(4)]
+    return m, cl, neg
+
+
+def _greedy_worker(rank, world, port, seed, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2011_08373_b200.multigpu import column_range, run_greedy_sharded
+
+    m, cl, neg = greedy_instance(seed)
+    c0, c1 = column_range(len(cl), rank, world)
+    sh = FakeGreedyShard(m, cl[c0:c1], neg)
+
+    def red(op):
+        return lambda t: dist.all_reduce(t, op=op)
+
+    assign, status, picks, n = run_greedy_sharded(sh, red(dist.ReduceOp.SUM), red(dist.ReduceOp.MAX),
+                                                  steps_per_check=4)
+    q.put((rank, assign.tolist(), int(status[0]), picks[:n].tolist()))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_greedy_column_sharding_gloo_world2(seed):
+    """The sharded protocol over two gloo ranks gives the textbook greedy of
+    the whole phi+ (the oracle): same pick order, same pruned set, same phi-
+    verdict."""
+    import oracle
+
+    m, cl, neg = greedy_instance(seed)
+    off = np.cumsum([0] + [len(c) for c in cl]).astype(np.int64)
+    var = np.concatenate([np.array(c, np.int32) for c in cl])
+    noff = np.cumsum([0] + [len(c) for c in neg]).astype(np.int64)
+    nvar = np.concatenate([np.array(c, np.int32) for c in neg])
+    ref = oracle.greedy_csr(m, off, var, noff, nvar)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_greedy_worker, args=(r, 2, port, seed, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ref_set = sorted(np.nonzero(ref.in_S)[0].tolist())
+    for rank, assign, status, picks in got:
+        assert picks == ref.picks.tolist()
+        got_set = [v for v in range(m) if (assign[v // 64] >> (v % 64)) & 1]
+        assert got_set == ref_set
+        assert status == (2 if ref.status == oracle.SAT_NEG_VIOLATED else 0)

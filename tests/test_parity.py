@@ -509,3 +509,76 @@ def test_pms_mhs_pair_on_two_streams():
         assert (h[f].reshape(cb.B, -1) == e[f"mhs_{f}"].reshape(cb.B, -1)).all()
     rp, rh = gr.solve_pms(db).to_host(), gr.mhs_exact(db).to_host()
     assert (p["decided"] == rp["decided"]).all() and (h["decided"] == rh["decided"]).all()
+
+
+# ------------------------------------------------------------------ column-sharded greedy
+class _ThreadGroup:
+    """In-process stand-in for the NCCL all-reduces of G ranks: one host
+    thread per shard, all on this GPU; the exchange happens on the host between
+    kernel launches (no kernel waits on another shard)."""
+
+    def __init__(self, n):
+        import threading
+
+        self.n, self.bar, self.buf, self.res = n, threading.Barrier(n), [None] * n, None
+
+    def allreduce(self, rank, op):
+        def f(t):
+            self.buf[rank] = t
+            self.bar.wait()
+            if rank == 0:
+                acc = self.buf[0].clone()
+                for x in self.buf[1:]:
+                    acc = acc + x if op == "sum" else torch.maximum(acc, x)
+                self.res = acc
+            self.bar.wait()
+            t.copy_(self.res)
+            self.bar.wait()
+
+        return f
+
+
+def _shard_csr(po, pv, c0, c1):
+    off = po[c0:c1 + 1] - po[c0]
+    return off.astype(np.int64), pv[po[c0]:po[c1]]
+
+
+@pytest.mark.parametrize("keep_csr", [True, False])  # incremental / recounting steps
+@pytest.mark.parametrize("world", [1, 3])
+def test_greedy_column_sharded(world, keep_csr):
+    """gr_greedy_shard_* over G clause-column shards (G host threads on one
+    GPU standing in for the ranks) = the oracle's greedy of the whole phi+."""
+    import threading
+
+    from paper_2011_08373_b200.multigpu import column_range, run_greedy_sharded
+
+    rng = random.Random(5 + world)
+    m, n = 300, 30000
+    pos = [sorted(rng.sample(range(m), rng.randint(1, 6))) for _ in range(n)]
+    neg = [sorted(rng.sample(range(m), 2)) for _ in range(6)]
+    po, pv = csr_from_lists(pos)
+    no, nv = csr_from_lists(neg)
+    o = oracle.greedy_csr(m, po, pv, no, nv)
+    grp = _ThreadGroup(world)
+    out = [None] * world
+
+    def run(r):
+        c0, c1 = column_range(n, r, world)
+        so, sv = _shard_csr(po, pv, c0, c1)
+        bm = gr.pack_bitmatrix(m, so, sv, no, nv, keep_csr=keep_csr)
+        sh = gr.GreedyShard(bm)
+        out[r] = run_greedy_sharded(sh, grp.allreduce(r, "sum"), grp.allreduce(r, "max"),
+                                    steps_per_check=8)
+        torch.cuda.synchronize()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    for assign, status, picks, npk in out:
+        assert picks.cpu().numpy()[:npk].tolist() == o.picks.tolist()
+        a = assign.cpu().numpy().view(np.uint64)
+        got = [i for i in range(m) if (int(a[i // 64]) >> (i % 64)) & 1]
+        assert got == np.nonzero(o.in_S)[0].tolist()
+        assert int(status.item()) == o.status
