@@ -681,11 +681,15 @@ constexpr size_t TAB_SMEM =
     (JMAX + 1) * HX * 16 + 65 * (JMAX + 1) * 8 + 129 * 16 + 64 +
     ((JMAX + 1) * 65 + 15) / 16 * 16;  // HIT table, binomials, low masks, R_j, sub-block sizes
 // clauses staged in shared memory (larger instances read L1/L2), sized for 4 CTAs per SM
-constexpr int SMC = (int)((54000 - TAB_SMEM) / (16 * HREC + 8)) / 32 * 32;
+#ifndef GR_ENUM_CTAS
+#define GR_ENUM_CTAS 4
+#endif
+constexpr int ENUM_CTAS = GR_ENUM_CTAS;  // resident enumeration CTAs per SM (registers, smem)
+constexpr int SMC = (int)(((227 * 1024) / ENUM_CTAS - 1024 - 400 - TAB_SMEM) / (16 * HREC + 8)) / 32 * 32;
 constexpr size_t ENUM_SMEM = TAB_SMEM + (size_t)SMC * (16 * HREC + 8);
 
 template <bool COUNT>
-__global__ void __launch_bounds__(NT) enum_kernel(EnumParams p) {
+__global__ void __launch_bounds__(NT, COUNT ? 1 : ENUM_CTAS) enum_kernel(EnumParams p) {
   extern __shared__ u64 cls[];  // [np][HREC] H records, [np + nn] P (u32 or u64)
   __shared__ u64 s_chunk;
   __shared__ int s_b, s_cur, s_skip;
