@@ -460,8 +460,14 @@ struct Clauses {
   int np, nn;
 };
 
+// Test one sub-block: F (its candidates in the lane's window) narrowed by
+// every clause.  dead := some clause rules out the node's whole subtree, i.e.
+// every x = U | S with S a j-subset of [0, e_node) (cover = U | [0, e_node)):
+// a positive clause inside the complement of cover, or a negative clause
+// inside U.  Checked on the clause group that empties F.
 template <typename M, bool COUNT>
-__device__ __forceinline__ F2 test_sub(int j, M U, int e, F2 F, const Clauses<M> &c, Work &wk) {
+__device__ __forceinline__ F2 test_sub(int j, M U, M cover, int e, F2 F, const Clauses<M> &c,
+                                       Work &wk, bool &dead) {
   const int np = c.np;
   const F2 *H = c.H + (j - 1);
   int q = 0;
@@ -474,7 +480,10 @@ __device__ __forceinline__ F2 test_sub(int j, M U, int e, F2 F, const Clauses<M>
     if (!(U & p2)) F = f2_and(F, h2);
     if (!(U & p3)) F = f2_and(F, h3);
     if (COUNT) wk.tests += 4;
-    if (!f2_any(F)) return F;
+    if (!f2_any(F)) {
+      dead = !(cover & p0) || !(cover & p1) || !(cover & p2) || !(cover & p3);
+      return F;
+    }
   }
   for (; q < np; q++) {
     if (!(U & c.P[q])) F = f2_and(F, H[HREC * q]);
@@ -486,6 +495,10 @@ __device__ __forceinline__ F2 test_sub(int j, M U, int e, F2 F, const Clauses<M>
   for (int t = 0; t < c.nn; t++) {
     M rest = c.P[np + t] & ~U;
     if (COUNT) wk.tests += 1;
+    if (!rest) {  // N inside U: every candidate of the subtree holds N
+      dead = true;
+      return F2{0ull, 0ull};
+    }
     if ((rest & ~lowm) || popc(rest) > j) continue;  // some variable of N stays false
     F2 kill{~0ull, ~0ull};
     if (j == 1) {  // HIT_1({x}) = bit x
@@ -585,13 +598,14 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
   for (;;) {
     if (pos >= cnt32) return best;
     const int n = c.nb[j * 65 + e];  // C(min(e, R_j), j)
+    bool dead = false;
     if (n && pos + n > 0) {
       F2 F = c.lowb[n];
       if (pos < 0) F = f2_andnot(F, c.lowb[-pos]);
       if (cnt32 - pos < n) F = f2_and(F, c.lowb[cnt32 - pos]);
       if (COUNT) { wk.blocks++; wk.cands += (u64)f2_popc(F); }
       const int ea = e < R ? e : R;
-      F = test_sub<M, COUNT>(j, U, ea, F, c, wk);
+      F = test_sub<M, COUNT>(j, U, U | (M)nbits((u64)e), ea, F, c, wk, dead);
       if (f2_any(F)) {
         if (MODE == 2) {
           u64 WU = 0;  // W(U), once per sub-block
@@ -609,10 +623,15 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
         }
       }
     }
-    pos += n;
+    if (dead) {  // skip the whole subtree: its C(e, j) candidates are infeasible
+      const u64 sz = CS(e, j);
+      pos = sz >= (u64)(cnt32 - pos) ? cnt32 : pos + (int)sz;
+    } else {
+      pos += n;
+    }
     // ---- advance: first child t = R of this node, else the next sibling up
     // the path
-    if (j >= 2 && R < e) {
+    if (!dead && j >= 2 && R < e) {
       tp = (tp << 6) | (u64)ep;
       ep = e;
       e = R;
