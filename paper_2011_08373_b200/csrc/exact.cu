@@ -461,13 +461,9 @@ struct Clauses {
 };
 
 // Test one sub-block: F (its candidates in the lane's window) narrowed by
-// every clause.  dead := some clause rules out the node's whole subtree, i.e.
-// every x = U | S with S a j-subset of [0, e_node) (cover = U | [0, e_node)):
-// a positive clause inside the complement of cover, or a negative clause
-// inside U.  Checked on the clause group that empties F.
+// every clause.
 template <typename M, bool COUNT>
-__device__ __forceinline__ F2 test_sub(int j, M U, M cover, int e, F2 F, const Clauses<M> &c,
-                                       Work &wk, bool &dead) {
+__device__ __forceinline__ F2 test_sub(int j, M U, int e, F2 F, const Clauses<M> &c, Work &wk) {
   const int np = c.np;
   const F2 *H = c.H + (j - 1);
   int q = 0;
@@ -480,10 +476,7 @@ __device__ __forceinline__ F2 test_sub(int j, M U, M cover, int e, F2 F, const C
     if (!(U & p2)) F = f2_and(F, h2);
     if (!(U & p3)) F = f2_and(F, h3);
     if (COUNT) wk.tests += 4;
-    if (!f2_any(F)) {
-      dead = !(cover & p0) || !(cover & p1) || !(cover & p2) || !(cover & p3);
-      return F;
-    }
+    if (!f2_any(F)) return F;
   }
   for (; q < np; q++) {
     if (!(U & c.P[q])) F = f2_and(F, H[HREC * q]);
@@ -495,10 +488,6 @@ __device__ __forceinline__ F2 test_sub(int j, M U, M cover, int e, F2 F, const C
   for (int t = 0; t < c.nn; t++) {
     M rest = c.P[np + t] & ~U;
     if (COUNT) wk.tests += 1;
-    if (!rest) {  // N inside U: every candidate of the subtree holds N
-      dead = true;
-      return F2{0ull, 0ull};
-    }
     if ((rest & ~lowm) || popc(rest) > j) continue;  // some variable of N stays false
     F2 kill{~0ull, ~0ull};
     if (j == 1) {  // HIT_1({x}) = bit x
@@ -598,14 +587,28 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
   for (;;) {
     if (pos >= cnt32) return best;
     const int n = c.nb[j * 65 + e];  // C(min(e, R_j), j)
+    // An inner node (one with children) first asks whether a single clause
+    // rules out its whole subtree -- every x = U | S, S a j-subset of [0, e):
+    // a positive clause missing U and [0, e), or a negative clause inside U.
+    // Then all C(e, j) candidates of the subtree are decided at once.
     bool dead = false;
-    if (n && pos + n > 0) {
+    if (j >= 2 && R < e) {
+      const M cover = U | (M)nbits((u64)e);
+      int r = 0;
+      for (; r < c.np; r++)
+        if (!(cover & c.P[r])) { dead = true; break; }
+      if (!dead)
+        for (int q = 0; q < c.nn; q++)
+          if (!(c.P[c.np + q] & ~U)) { dead = true; break; }
+      if (COUNT) wk.tests += (u64)r;
+    }
+    if (!dead && n && pos + n > 0) {
       F2 F = c.lowb[n];
       if (pos < 0) F = f2_andnot(F, c.lowb[-pos]);
       if (cnt32 - pos < n) F = f2_and(F, c.lowb[cnt32 - pos]);
       if (COUNT) { wk.blocks++; wk.cands += (u64)f2_popc(F); }
       const int ea = e < R ? e : R;
-      F = test_sub<M, COUNT>(j, U, U | (M)nbits((u64)e), ea, F, c, wk, dead);
+      F = test_sub<M, COUNT>(j, U, ea, F, c, wk);
       if (f2_any(F)) {
         if (MODE == 2) {
           u64 WU = 0;  // W(U), once per sub-block
