@@ -587,16 +587,30 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
   for (;;) {
     if (pos >= cnt32) return best;
     const int n = c.nb[j * 65 + e];  // C(min(e, R_j), j)
-    // An inner node (one with children) first asks whether a single clause
-    // rules out its whole subtree -- every x = U | S, S a j-subset of [0, e):
-    // a positive clause missing U and [0, e), or a negative clause inside U.
-    // Then all C(e, j) candidates of the subtree are decided at once.
+    // An inner node (one with children) first asks whether its whole subtree
+    // -- every x = U | S, S a j-subset of [0, e) -- is infeasible: a positive
+    // clause missing U and [0, e), more than j pairwise disjoint positive
+    // clauses missing U (restricted to [0, e)), or a negative clause inside
+    // U.  Then all C(e, j) candidates of the subtree are decided at once.
     bool dead = false;
     if (j >= 2 && R < e) {
-      const M cover = U | (M)nbits((u64)e);
       int r = 0;
-      for (; r < c.np; r++)
-        if (!(cover & c.P[r])) { dead = true; break; }
+      // lower bound: clauses missing U, restricted to [0, e), pairwise
+      // disjoint (greedy packing in clause order) -- S needs one element of
+      // each, so more than j of them (or an empty one) refute the subtree
+      const M lowe = (M)nbits((u64)e);
+      M used = 0;
+      int pk = 0;
+      for (; r < c.np; r++) {
+        const M pr = c.P[r];
+        if (pr & U) continue;
+        const M q = pr & lowe;
+        if (!q) { dead = true; break; }
+        if (!(q & used)) {
+          used |= q;
+          if (++pk > j) { dead = true; break; }
+        }
+      }
       if (!dead)
         for (int q = 0; q < c.nn; q++)
           if (!(c.P[c.np + q] & ~U)) { dead = true; break; }
