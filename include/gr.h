@@ -79,10 +79,13 @@ enum {
   GR_FLAG_EXHAUSTIVE = 1,    /* exact unit-weight solvers: enumerate the witness level
                                 completely (deterministic work; benchmarking mode).
                                 Results are identical. */
-  GR_FLAG_WEIGHTED_GREEDY = 2 /* gr_mhs_greedy / gr_solve(MHS) with w != NULL: the weighted
+  GR_FLAG_WEIGHTED_GREEDY = 2, /* gr_mhs_greedy / gr_solve(MHS) with w != NULL: the weighted
                                 mhs -- pick the variable
                                 maximising uncovered-hits / weight (exact cross-multiplied
                                 comparison, lowest index on ties, reading R20); cost = weight */
+  GR_FLAG_NO_PRUNE = 4       /* exact solvers: decide every sub-block by its clause tests,
+                                without refuting whole subtrees first (measurement mode;
+                                results and decided counts are identical) */
 };
 
 /* A batch of independent Solve-step instances. */

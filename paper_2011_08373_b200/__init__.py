@@ -10,7 +10,7 @@ Public API (thin marshalling over libgrsolve.so, include/gr.h):
 Seeded synthetic workloads: paper_2011_08373_b200.synth.
 """
 from ._native import (  # noqa: F401
-    GR_BADINPUT, GR_FLAG_EXHAUSTIVE, GR_FLAG_WEIGHTED_GREEDY, GR_SAT, GR_SAT_NEG_VIOLATED, GR_UNSAT, GR_UNSUPPORTED, MHS,
+    GR_BADINPUT, GR_FLAG_EXHAUSTIVE, GR_FLAG_WEIGHTED_GREEDY, GR_FLAG_NO_PRUNE, GR_SAT, GR_SAT_NEG_VIOLATED, GR_UNSAT, GR_UNSUPPORTED, MHS,
     PMS, GREEDY, DeviceBatch, DeviceBitMatrix, DeviceResult, ExactSession, GrError,
     bitmatrix_ld, greedy_count_shard, lib, mhs_exact, mhs_greedy, mhs_greedy_matrix,
     pack_bitmatrix, solve_pms, version, launch_count, profiler, Profiler, solve,

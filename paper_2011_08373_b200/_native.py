@@ -21,6 +21,7 @@ GR_OK, GR_EINVAL, GR_ETOOBIG, GR_ECUDA, GR_ENOMEM, GR_EWORKSPACE = 0, -1, -2, -3
 GR_SAT, GR_UNSAT, GR_SAT_NEG_VIOLATED, GR_BADINPUT, GR_UNSUPPORTED = 0, 1, 2, 3, 4
 GR_FLAG_EXHAUSTIVE = 1
 GR_FLAG_WEIGHTED_GREEDY = 2
+GR_FLAG_NO_PRUNE = 4
 PMS, MHS, GREEDY = 0, 1, 2
 
 EXPORTED = [

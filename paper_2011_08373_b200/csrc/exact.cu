@@ -523,7 +523,7 @@ __device__ __forceinline__ u64 weight_low(int j, u64 idx, int ea, const u32 *w, 
 // each in tp), the current U and the current sub-block's first rank base.
 template <typename M, int MODE, bool COUNT>
 __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const u32 *w, int rb,
-                    Work &wk) {
+                    int prune, Work &wk) {
   const int J = k < JMAX ? k : JMAX;
   const u64 *cs = c.cs;  // C(n, j), j <= JMAX
 #define CS(n, j) (cs[(n) * (JMAX + 1) + (j)])
@@ -593,7 +593,7 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
     // clauses missing U (restricted to [0, e)), or a negative clause inside
     // U.  Then all C(e, j) candidates of the subtree are decided at once.
     bool dead = false;
-    if (j >= 2 && R < e) {
+    if (prune && j >= 2 && R < e) {
       int r = 0;
       // lower bound: clauses missing U, restricted to [0, e), pairwise
       // disjoint (greedy packing in clause order) -- S needs one element of
@@ -700,15 +700,15 @@ __device__ __forceinline__ i64 warp_min(i64 v) {
 struct EnumParams {
   WS ws;
   const int64_t *off;
-  int k, weighted, exhaustive, shard, nshard;
+  int k, weighted, exhaustive, shard, nshard, prune;
 };
 
 template <typename M, bool COUNT>
 __device__ i64 run_lane(const EnumParams &p, u64 r_lo, u64 cnt, int me, const Clauses<M> &c,
                         const u32 *w, int rb, Work &wk) {
-  if (p.weighted) return walk<M, 2, COUNT>(p.k, me, r_lo, cnt, c, w, rb, wk);
-  if (p.exhaustive) return walk<M, 1, COUNT>(p.k, me, r_lo, cnt, c, w, rb, wk);
-  return walk<M, 0, COUNT>(p.k, me, r_lo, cnt, c, w, rb, wk);
+  if (p.weighted) return walk<M, 2, COUNT>(p.k, me, r_lo, cnt, c, w, rb, p.prune, wk);
+  if (p.exhaustive) return walk<M, 1, COUNT>(p.k, me, r_lo, cnt, c, w, rb, p.prune, wk);
+  return walk<M, 0, COUNT>(p.k, me, r_lo, cnt, c, w, rb, p.prune, wk);
 }
 
 __device__ unsigned long long g_work[4];  // counting instantiation totals
@@ -951,7 +951,7 @@ __global__ void __launch_bounds__(FT) finish_kernel(In in, Out out, WS ws, int w
     __syncthreads();
   }
   // lane window L: about 2 windows per lane of the enumeration grid, a power
-  // of two in [256, 16384] (weighted levels: [256, lane_max_w]; their feasible
+  // of two in [256, 2^18] (weighted levels: [256, 4096]; their feasible
   // candidates cluster, and long windows leave one lane with most of the
   // weight decoding)
   const u64 Lmax = weighted ? lane_max_w : lane_max;
@@ -1044,8 +1044,9 @@ u64 lane_max(bool weighted) {  // the adaptive lane window's upper bound
   const int i = weighted ? 1 : 0;
   if (!v[i]) {
     const char *e = getenv(weighted ? "GR_LANE_MAX_W" : "GR_LANE_MAX");
-    const u64 dflt = weighted ? 4096ull : 16384ull;
+    const u64 dflt = weighted ? 4096ull : 262144ull;
     v[i] = e ? strtoull(e, nullptr, 10) : dflt;
+    if (v[i] > (1ull << 24)) v[i] = 1ull << 24;
     if (v[i] < 256) v[i] = dflt;
   }
   return v[i];
@@ -1130,6 +1131,7 @@ extern "C" int gr_exact_level(const gr_batch *in, int which, int k, int shard, i
   p.k = k;
   p.weighted = (which == 0 && in->w) ? 1 : 0;
   p.exhaustive = (in->flags & GR_FLAG_EXHAUSTIVE) ? 1 : 0;
+  p.prune = (in->flags & GR_FLAG_NO_PRUNE) ? 0 : 1;
   p.shard = shard;
   p.nshard = nshard;
   int grid = enum_grid();

@@ -349,6 +349,20 @@ def test_c2_exhaustive_flag_same_results():
             assert (r[f].reshape(cb.B, -1) == e[f"{prefix}_{f}"].reshape(cb.B, -1)).all(), (which, f)
 
 
+@pytest.mark.parametrize("extra", [0, gr.GR_FLAG_EXHAUSTIVE])
+def test_no_prune_flag_same_results(extra):
+    """GR_FLAG_NO_PRUNE (every sub-block decided by its own clause tests, no
+    subtree refutation) gives the same statuses, assignments, costs and decided
+    counts on C2, C4-shaped weighted instances and C3."""
+    cases = [synth.c2_batch(), synth.c4_batch(B=300), synth.c3_instance()[0]]
+    for cb in cases:
+        for which in ("pms", "mhs"):
+            a = gpu_solve(cb, which, flags=extra)
+            b = gpu_solve(cb, which, flags=extra | gr.GR_FLAG_NO_PRUNE)
+            for f in ("status", "assign", "cost", "decided"):
+                assert (a[f] == b[f]).all(), (which, f)
+
+
 def test_batch_shard_emulation():
     """Rank-range sharding of every level of a whole batch (G = 3 sequential
     shards, host MIN of the level keys) equals the single-GPU solve."""
