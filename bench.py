@@ -142,6 +142,9 @@ class ClockSampler:
             self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
             self.t = threading.Thread(target=self._poll, daemon=True)
             self.t.start()
+            t_end = time.perf_counter() + 2.0  # the poller is live before the timed region
+            while not self.rows and time.perf_counter() < t_end:
+                time.sleep(0.001)
             return self
         except Exception:
             self.nvml = None
@@ -218,7 +221,8 @@ class ClockSampler:
                         reasons.add(name)
         sm = [r[1] for r in rows]
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(reasons), "samples": len(sm),
+                "reasons": sorted(reasons), "samples": len(sm), "samples_all": len(self.rows),
+                "window_s": (t1 - t0) if self.t0 is not None and self.t1 is not None else None,
                 "source": "NVML every 2 ms in the timed region" if self.nvml
                 else "nvidia-smi -lms 100 in the timed region"}
 

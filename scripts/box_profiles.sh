@@ -10,6 +10,7 @@ for c in c2 c3 c4 c5; do
   timeout 900 python bench.py --config $c > $O/${R}_bench_$c.json 2> $O/${R}_bench_$c.err || echo "bench $c failed"
 done
 timeout 900 python bench.py --impl reference > $O/${R}_bench_reference.json 2> $O/${R}_bench_reference.err
+timeout 900 python bench.py --impl reference --config c5 > $O/${R}_bench_reference_c5.json 2>> $O/${R}_bench_reference.err
 # launch list of the bench command (cold-cache, serialised: shares only)
 if timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > $O/launch_run.json 2>&1; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \

@@ -20,7 +20,7 @@ SRC = os.path.join("gpurun_out", "prof")
 DST = "profiles"
 NCU = "/usr/local/cuda/bin/ncu"
 
-for cfg in ("c2", "c3", "c4", "c5", "reference"):
+for cfg in ("c2", "c3", "c4", "c5", "reference", "reference_c5"):
     p = os.path.join(SRC, f"{R}_bench_{cfg}.json")
     if os.path.exists(p) and os.path.getsize(p) > 0:
         line = open(p).read().strip().splitlines()[-1]
