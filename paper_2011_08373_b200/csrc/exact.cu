@@ -523,7 +523,7 @@ __device__ __forceinline__ u64 weight_low(int j, u64 idx, int ea, const u32 *w, 
 // each in tp), the current U and the current sub-block's first rank base.
 template <typename M, int MODE, bool COUNT>
 __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const u32 *w, int rb,
-                    int prune, Work &wk) {
+                    int prune, Work &wk, const u64 *skj = nullptr, u64 wstar = ~0ull) {
   const int J = k < JMAX ? k : JMAX;
   const u64 *cs = c.cs;  // C(n, j), j <= JMAX
 #define CS(n, j) (cs[(n) * (JMAX + 1) + (j)])
@@ -593,7 +593,20 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
     // clauses missing U (restricted to [0, e)), or a negative clause inside
     // U.  Then all C(e, j) candidates of the subtree are decided at once.
     bool dead = false;
-    if (prune && j >= 2 && R < e) {
+    u64 WU = 0;  // weighted: W(U), and a bound on the whole subtree -- every x
+                 // in it weighs >= W(U) + S_j (the j smallest weights); it can
+                 // only matter below the incumbent of earlier levels (W*,
+                 // strictly, R3) and below this lane's best so far (ties lose
+                 // on rank: the walk is in rank order)
+    if (MODE == 2) {
+      for (M tt = U; tt; tt &= tt - 1) WU += w[ctz(tt)];
+      if (prune) {
+        const u64 lb = (u64)best >> rb;
+        const u64 lim = best == GR_KEY_NONE ? wstar : (lb < wstar ? lb : wstar);
+        if (WU + skj[j] >= lim) dead = true;
+      }
+    }
+    if (!dead && prune && j >= 2 && R < e) {
       int r = 0;
       // lower bound: clauses missing U, restricted to [0, e), pairwise
       // disjoint (greedy packing in clause order) -- S needs one element of
@@ -625,8 +638,6 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
       F = test_sub<M, COUNT>(j, U, ea, F, c, wk);
       if (f2_any(F)) {
         if (MODE == 2) {
-          u64 WU = 0;  // W(U), once per sub-block
-          for (M t = U; t; t &= t - 1) WU += w[ctz(t)];
           for (int h = 0; h < 2; h++)
             for (u64 f = h ? F.hi : F.lo; f; f &= f - 1) {
               const u64 idx = (u64)(64 * h + __ffsll((long long)f) - 1);
@@ -705,8 +716,8 @@ struct EnumParams {
 
 template <typename M, bool COUNT>
 __device__ i64 run_lane(const EnumParams &p, u64 r_lo, u64 cnt, int me, const Clauses<M> &c,
-                        const u32 *w, int rb, Work &wk) {
-  if (p.weighted) return walk<M, 2, COUNT>(p.k, me, r_lo, cnt, c, w, rb, p.prune, wk);
+                        const u32 *w, int rb, Work &wk, const u64 *skj, u64 wstar) {
+  if (p.weighted) return walk<M, 2, COUNT>(p.k, me, r_lo, cnt, c, w, rb, p.prune, wk, skj, wstar);
   if (p.exhaustive) return walk<M, 1, COUNT>(p.k, me, r_lo, cnt, c, w, rb, p.prune, wk);
   return walk<M, 0, COUNT>(p.k, me, r_lo, cnt, c, w, rb, p.prune, wk);
 }
@@ -730,6 +741,7 @@ __global__ void __launch_bounds__(NT, COUNT ? 1 : ENUM_CTAS) enum_kernel(EnumPar
   __shared__ u64 s_chunk;
   __shared__ int s_b, s_cur, s_skip;
   __shared__ u64 s_r0, s_ck;
+  __shared__ u64 s_skj[JMAX + 1], s_wstar;  // weighted: S_j and the incumbent W*
   __shared__ u32 s_w[64];
   __shared__ i64 s_wmin[NT / 32];
   const int t = threadIdx.x;
@@ -800,6 +812,8 @@ __global__ void __launch_bounds__(NT, COUNT ? 1 : ENUM_CTAS) enum_kernel(EnumPar
         }
       }
       if (t < 64) s_w[t] = p.ws.wr[(size_t)b * 64 + t];
+      if (p.weighted && t <= JMAX) s_skj[t] = p.ws.sk[(size_t)b * 65 + t];
+      if (p.weighted && t == 0) s_wstar = p.ws.bestw[b];
       __syncthreads();
       if (t == 0) s_cur = b;
     }
@@ -812,13 +826,13 @@ __global__ void __launch_bounds__(NT, COUNT ? 1 : ENUM_CTAS) enum_kernel(EnumPar
       const int rb = p.ws.rb[b];
       if (narrow) {
         Clauses<u32> c{(const u32 *)sP, sH, hitx, lowb, reg, nb, cs, np, nn};
-        key = run_lane<u32, COUNT>(p, r_lo, cnt, me, c, s_w, rb, wk);
+        key = run_lane<u32, COUNT>(p, r_lo, cnt, me, c, s_w, rb, wk, s_skj, s_wstar);
       } else if (staged) {
         Clauses<u64> c{sP, sH, hitx, lowb, reg, nb, cs, np, nn};
-        key = run_lane<u64, COUNT>(p, r_lo, cnt, me, c, s_w, rb, wk);
+        key = run_lane<u64, COUNT>(p, r_lo, cnt, me, c, s_w, rb, wk, s_skj, s_wstar);
       } else {
         Clauses<u64> c{p.ws.pk + lo, (const F2 *)p.ws.hrec + lo * HREC, hitx, lowb, reg, nb, cs, np, nn};
-        key = run_lane<u64, COUNT>(p, r_lo, cnt, me, c, s_w, rb, wk);
+        key = run_lane<u64, COUNT>(p, r_lo, cnt, me, c, s_w, rb, wk, s_skj, s_wstar);
       }
     }
     if (COUNT) {
