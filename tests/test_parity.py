@@ -596,3 +596,37 @@ def test_greedy_column_sharded(world, keep_csr):
         got = [i for i in range(m) if (int(a[i // 64]) >> (i % 64)) & 1]
         assert got == np.nonzero(o.in_S)[0].tolist()
         assert int(status.item()) == o.status
+
+
+# ------------------------------------------------------------------ subtree refutation
+def refutation_batch(seed, B, mlo, mhi, weighted=False):
+    """Shapes that exercise the subtree refutation: many 1-3 variable positive
+    clauses (empty restrictions, disjoint packings) and negative clauses that
+    make dense levels UNSAT (negatives inside U); weights in a narrow band so
+    the weight bound prunes (C4-like) or a wide one (it rarely does)."""
+    rng = random.Random(seed)
+    insts, ws = [], []
+    for _ in range(B):
+        m = rng.randint(mlo, mhi)
+        pos, neg = set(), set()
+        for _ in range(rng.randint(4, 30)):
+            s = rng.choice([1, 2, 2, 3, 3, rng.randint(2, max(2, m // 3))])
+            pos.add(tuple(sorted(rng.sample(range(1, m + 1), min(s, m)))))
+        for _ in range(rng.randint(0, 14)):
+            neg.add(tuple(sorted(rng.sample(range(1, m + 1), rng.choice([1, 2, 2, 3])))))
+        insts.append((m, [list(c) for c in sorted(pos)], [list(c) for c in sorted(neg)]))
+        lo = rng.choice([1, 50, 90])
+        ws.append([rng.randint(lo, 100) for _ in range(m)])
+    return synth.batch_from_lists(insts, weights=ws if weighted else None, W=1)
+
+
+@pytest.mark.parametrize("seed", range(3))
+@pytest.mark.parametrize("weighted", [False, True])
+def test_refutation_shapes_vs_oracle(seed, weighted):
+    cb = refutation_batch(100 + seed, 160, 10, 26, weighted)
+    check_batch(cb)
+    for which in ("pms", "mhs"):  # and the unpruned walk agrees
+        a = gpu_solve(cb, which)
+        b = gpu_solve(cb, which, flags=gr.GR_FLAG_NO_PRUNE)
+        for f in ("status", "assign", "cost", "decided"):
+            assert (a[f] == b[f]).all(), (which, f)
