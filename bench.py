@@ -642,8 +642,30 @@ def cpu_baseline_c5(rank):
 
 
 # ---------------------------------------------------------------- CPU oracle legs
+def c3_oracle_batch(n):
+    """n C3-recipe instances scaled to m = 33 (11 groups of 3, k* = 11; clause
+    counts scaled by 33/48), one seed each: the oracle (one thread per
+    instance) finishes each in ~2.5 s where C3 itself would take hours."""
+    from paper_2011_08373_b200 import synth
+
+    insts = []
+    for i in range(n):
+        cb, _, _ = synth.c3_instance(seed=synth.seed_for(3) + 1000 + i, m=33, groups=11,
+                                     n_rand_pos=124 * 33 // 48, n_neg=60 * 33 // 48)
+        m, npos, mk, _ = cb.instance(0)
+        cl = [synth.mask_to_vars(mk[j]) for j in range(mk.shape[0])]
+        insts.append((m, cl[:npos], cl[npos:]))
+    return synth.batch_from_lists(insts, W=1)
+
+
 def oracle_sample(cfg, cb):
     """Bounded sample of the workload for the CPU oracle (about 10-30 s)."""
+    if cfg == "c3":
+        import oracle
+
+        n = oracle.num_threads()
+        return (c3_oracle_batch(n),
+                f"{n} C3-recipe instances at m = 33 (11 groups, k* = 11), PMS + MHS, first witness")
     if cfg == "c2":
         idx = [b for b in range(cb.B) if cb.m[b] <= 26]
         return cb.subset(idx), f"{len(idx)} of {cb.B} C2 instances (those with m <= 26), PMS+MHS+greedy"
@@ -669,9 +691,6 @@ def run_oracle_once(cfg, sub):
 def cpu_baseline(cfg, cb):
     import oracle
 
-    if cfg == "c3":
-        return {"value": None, "unit": "candidates/s", "cores": oracle.num_threads(), "kind": "oracle",
-                "sample": "not run: 4.1e12 candidates (~hours on the host); see DESIGN.md §7"}
     sub, desc = oracle_sample(cfg, cb)
     sec, cands, reps = 0.0, 0.0, 0
     while sec < 10.0 and reps < 50:
@@ -712,7 +731,7 @@ def run_reference(a, rank, world):
                     "d2h_bytes_per_step": 0},
         }), flush=True)
         return
-    cfg = a.config if a.config in ("c1", "c2", "c4") else "c2"
+    cfg = a.config if a.config in ("c1", "c2", "c3", "c4") else "c2"
     cb, desc = make_workload(cfg, 0)
     sub, sdesc = oracle_sample(cfg, cb)
     ts, cands = [], 0.0
