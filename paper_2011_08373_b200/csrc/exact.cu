@@ -521,6 +521,34 @@ __device__ __forceinline__ u64 weight_low(int j, u64 idx, int ea, const u32 *w, 
 // Iterator state: the top-level U (k - J elements) with its first rank
 // base_top, the path t_0 > t_1 > ... of part-B choices below it (6 bits
 // each in tp), the current U and the current sub-block's first rank base.
+// Is the whole subtree of node (j, U, e) -- every x = U | S, S a j-subset of
+// [0, e) -- infeasible?  A positive clause missing U and [0, e), more than j
+// pairwise disjoint positive clauses missing U (restricted to [0, e), greedy
+// packing in clause order: S needs one element of each), or a negative
+// clause inside U.
+template <typename M, bool COUNT>
+__device__ __forceinline__ bool refuted(int j, M U, int e, const Clauses<M> &c, Work &wk) {
+  const M lowe = (M)nbits((u64)e);
+  M used = 0;
+  int pk = 0, r = 0;
+  bool dead = false;
+  for (; r < c.np; r++) {
+    const M pr = c.P[r];
+    if (pr & U) continue;
+    const M q = pr & lowe;
+    if (!q) { dead = true; break; }
+    if (!(q & used)) {
+      used |= q;
+      if (++pk > j) { dead = true; break; }
+    }
+  }
+  if (!dead)
+    for (int q = 0; q < c.nn; q++)
+      if (!(c.P[c.np + q] & ~U)) { dead = true; break; }
+  if (COUNT) wk.tests += (u64)r;
+  return dead;
+}
+
 template <typename M, int MODE, bool COUNT>
 __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const u32 *w, int rb,
                     int prune, Work &wk, const u64 *skj = nullptr, u64 wstar = ~0ull) {
@@ -568,8 +596,16 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
   int d = 0, j = J, e = e_top, ep = e_top;
   u64 tp = 0;
   // descend: at node j, x lies in part B iff its j-th lowest element
-  // s[j-1] >= R_j; then the child is t = s[j-1]
+  // s[j-1] >= R_j; then the child is t = s[j-1].  An ancestor whose whole
+  // subtree is refuted stops the descent: the walk resumes after it (without
+  // this a window starting deep inside a refuted subtree would refute each
+  // remaining sibling on the path one by one).
+  bool dead0 = false;
   while (j >= 2 && s[j - 1] >= region_of(j)) {
+    if (prune && refuted<M, COUNT>(j, U, e, c, wk)) {
+      dead0 = true;
+      break;
+    }
     const int t = s[j - 1];
     tp = (tp << 6) | (u64)ep;
     ep = e;
@@ -592,7 +628,8 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
     // clause missing U and [0, e), more than j pairwise disjoint positive
     // clauses missing U (restricted to [0, e)), or a negative clause inside
     // U.  Then all C(e, j) candidates of the subtree are decided at once.
-    bool dead = false;
+    bool dead = dead0;
+    dead0 = false;
     u64 WU = 0;  // weighted: W(U), and a bound on the whole subtree -- every x
                  // in it weighs >= W(U) + S_j (the j smallest weights); it can
                  // only matter below the incumbent of earlier levels (W*,
@@ -600,35 +637,13 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
                  // on rank: the walk is in rank order)
     if (MODE == 2) {
       for (M tt = U; tt; tt &= tt - 1) WU += w[ctz(tt)];
-      if (prune) {
+      if (prune && !dead) {
         const u64 lb = (u64)best >> rb;
         const u64 lim = best == GR_KEY_NONE ? wstar : (lb < wstar ? lb : wstar);
         if (WU + skj[j] >= lim) dead = true;
       }
     }
-    if (!dead && prune && j >= 2 && R < e) {
-      int r = 0;
-      // lower bound: clauses missing U, restricted to [0, e), pairwise
-      // disjoint (greedy packing in clause order) -- S needs one element of
-      // each, so more than j of them (or an empty one) refute the subtree
-      const M lowe = (M)nbits((u64)e);
-      M used = 0;
-      int pk = 0;
-      for (; r < c.np; r++) {
-        const M pr = c.P[r];
-        if (pr & U) continue;
-        const M q = pr & lowe;
-        if (!q) { dead = true; break; }
-        if (!(q & used)) {
-          used |= q;
-          if (++pk > j) { dead = true; break; }
-        }
-      }
-      if (!dead)
-        for (int q = 0; q < c.nn; q++)
-          if (!(c.P[c.np + q] & ~U)) { dead = true; break; }
-      if (COUNT) wk.tests += (u64)r;
-    }
+    if (!dead && prune && j >= 2 && R < e) dead = refuted<M, COUNT>(j, U, e, c, wk);
     if (!dead && n && pos + n > 0) {
       F2 F = c.lowb[n];
       if (pos < 0) F = f2_andnot(F, c.lowb[-pos]);
