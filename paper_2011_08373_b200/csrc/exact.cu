@@ -979,12 +979,13 @@ __global__ void __launch_bounds__(FT) finish_kernel(In in, Out out, WS ws, int w
     }
     __syncthreads();
   }
-  // lane window L: about 2 windows per lane of the enumeration grid, a power
-  // of two in [256, 2^18] (weighted levels: [256, 4096]; their feasible
-  // candidates cluster, and long windows leave one lane with most of the
-  // weight decoding)
+  // lane window L: about 3 windows per lane of the enumeration grid, a power
+  // of two in [256, 2^18] (weighted levels: 4 windows, at most 2^16)
   const u64 Lmax = weighted ? lane_max_w : lane_max;
-  u64 L = s_carry / ((u64)enum_lanes * (u64)windows_per_lane);
+  // windows per lane: the host's value for unit weights, its high 16 bits
+  // for weighted levels
+  const u64 wpl = weighted ? (u64)(windows_per_lane >> 16) : (u64)(windows_per_lane & 0xffff);
+  u64 L = s_carry / ((u64)enum_lanes * (wpl ? wpl : 2));
   L = L < 256 ? 256 : (L > Lmax ? Lmax : L);
   L = 1ull << (63 - __clzll((long long)L));
   if (fixed_lane) L = fixed_lane;  // GR_LANE_CANDIDATES override
@@ -1059,21 +1060,23 @@ u64 lane_cands_raw() {
   }
   return v;
 }
-int windows_per_lane() {  // adaptive lane window: windows per lane per level
-  static int v = 0;
-  if (!v) {
-    const char *e = getenv("GR_WINDOWS_PER_LANE");
-    v = e ? atoi(e) : 2;
-    if (v < 1) v = 2;
+int windows_per_lane(bool weighted) {  // adaptive lane window: windows per lane per level
+  static int v[2] = {0, 0};              // GR_WINDOWS_PER_LANE / _W override
+  const int i = weighted ? 1 : 0;
+  if (!v[i]) {
+    const char *e = getenv(weighted ? "GR_WINDOWS_PER_LANE_W" : "GR_WINDOWS_PER_LANE");
+    const int dflt = weighted ? 4 : 3;
+    v[i] = e ? atoi(e) : dflt;
+    if (v[i] < 1 || v[i] > 0xffff) v[i] = dflt;
   }
-  return v;
+  return v[i];
 }
 u64 lane_max(bool weighted) {  // the adaptive lane window's upper bound
   static u64 v[2] = {0, 0};     // GR_LANE_MAX / GR_LANE_MAX_W override
   const int i = weighted ? 1 : 0;
   if (!v[i]) {
     const char *e = getenv(weighted ? "GR_LANE_MAX_W" : "GR_LANE_MAX");
-    const u64 dflt = weighted ? 4096ull : 262144ull;
+    const u64 dflt = weighted ? 65536ull : 262144ull;
     v[i] = e ? strtoull(e, nullptr, 10) : dflt;
     if (v[i] > (1ull << 24)) v[i] = 1ull << 24;
     if (v[i] < 256) v[i] = dflt;
@@ -1132,7 +1135,7 @@ extern "C" int gr_exact_prepare(const gr_batch *in, int which, gr_result *out, v
   }
   GR_LAUNCH("pack_kernel", (cudaStream_t)s, pack_kernel<<<in->B, PT, smem, st>>>(in_of(in, which), out_of(out), w, which));
   GR_LAUNCH("finish_kernel", (cudaStream_t)s, finish_kernel<<<1, FT, 0, st>>>(in_of(in, which), out_of(out), w, which, 0,
-                                   (in->flags & GR_FLAG_EXHAUSTIVE) ? 1 : 0, enum_grid() * NT, lane_cands(), windows_per_lane(),
+                                   (in->flags & GR_FLAG_EXHAUSTIVE) ? 1 : 0, enum_grid() * NT, lane_cands(), windows_per_lane(false) | (windows_per_lane(true) << 16),
                                    lane_max(false), lane_max(true)));
   if (n_active) {
     int *h = pinned_i32();
@@ -1188,7 +1191,7 @@ extern "C" int gr_exact_finish(const gr_batch *in, int which, int k, gr_result *
   WS w = ws_of(in, ws);
   cudaStream_t st = (cudaStream_t)s;
   GR_LAUNCH("finish_kernel", (cudaStream_t)s, finish_kernel<<<1, FT, 0, st>>>(in_of(in, which), out_of(out), w, which, k,
-                                   (in->flags & GR_FLAG_EXHAUSTIVE) ? 1 : 0, enum_grid() * NT, lane_cands(), windows_per_lane(),
+                                   (in->flags & GR_FLAG_EXHAUSTIVE) ? 1 : 0, enum_grid() * NT, lane_cands(), windows_per_lane(false) | (windows_per_lane(true) << 16),
                                    lane_max(false), lane_max(true)));
   if (n_active) {
     int *h = pinned_i32();
