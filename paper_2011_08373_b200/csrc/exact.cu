@@ -1167,7 +1167,9 @@ extern "C" int gr_exact_level(const gr_batch *in, int which, int k, int shard, i
   p.shard = shard;
   p.nshard = nshard;
   int grid = enum_grid();
-  GR_CUDA(cudaMemsetAsync(&w.ctrl->next_chunk, 0, sizeof(u64), (cudaStream_t)s));
+  // the finish kernel leaves next_chunk at 0; several shards of one level on
+  // one device (multi-shard emulation) need it reset between them
+  if (nshard > 1) GR_CUDA(cudaMemsetAsync(&w.ctrl->next_chunk, 0, sizeof(u64), (cudaStream_t)s));
   if (gr_prof_mode() == 2)
     GR_LAUNCH("enum_kernel", (cudaStream_t)s, enum_kernel<true><<<grid, NT, ENUM_SMEM, (cudaStream_t)s>>>(p));
   else
