@@ -1205,6 +1205,17 @@ extern "C" int gr_exact_finish(const gr_batch *in, int which, int k, gr_result *
   return GR_OK;
 }
 
+// levels queued per host read-back of n_active (GR_SPEC_LEVELS)
+static int spec_levels() {
+  static int v = 0;
+  if (!v) {
+    const char *e = getenv("GR_SPEC_LEVELS");
+    v = e ? atoi(e) : 4;
+    if (v < 1 || v > 64) v = 4;
+  }
+  return v;
+}
+
 static int solve_exact(const gr_batch *in, gr_result *out, void *ws, size_t ws_bytes, gr_stream_t s,
                        int which) {
   int32_t n = 0;  // level 0 is handled by the pack; instances active for level 1
@@ -1212,7 +1223,7 @@ static int solve_exact(const gr_batch *in, gr_result *out, void *ws, size_t ws_b
   if (rc) return rc;
   // levels are queued SPEC at a time and n_active is read back once per batch;
   // levels past the last active one are no-ops (empty active list)
-  const int SPEC = 4;
+  const int SPEC = spec_levels();
   for (int k = 1; n > 0 && k <= 64;) {
     for (int i = 0; i < SPEC && k <= 64; i++, k++) {
       rc = gr_exact_level(in, which, k, 0, 1, ws, ws_bytes, s);
@@ -1263,7 +1274,7 @@ extern "C" int gr_solve_pms_mhs(const gr_batch *in, gr_result *out_pms, gr_resul
   GR_CUDA(cudaStreamSynchronize(st2));
   n1 = h[0];
   n2 = h[1];
-  const int SPEC = 4;
+  const int SPEC = spec_levels();
   for (int k = 1; (n1 > 0 || n2 > 0) && k <= 64;) {
     const bool a1 = n1 > 0, a2 = n2 > 0;
     for (int i = 0; i < SPEC && k <= 64; i++, k++) {
