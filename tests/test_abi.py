@@ -49,6 +49,14 @@ def test_version_and_host_validation():
     assert L.gr_mhs_exact(None, None, None, 0, None) == N.GR_EINVAL
     assert L.gr_mhs_greedy(None, None, None, 0, None) == N.GR_EINVAL
     assert L.gr_mhs_greedy_matrix(None, None, None, None, None, None, 0, None) == N.GR_EINVAL
+    # the column-sharded greedy protocol rejects a missing shard
+    assert L.gr_greedy_shard_workspace_bytes(None) == 0
+    assert L.gr_greedy_shard_begin(None, None, None, 0, None) == N.GR_EINVAL
+    assert L.gr_greedy_shard_step(None, None, None, 0, None) == N.GR_EINVAL
+    assert L.gr_greedy_shard_state(None, None, 0, None, None, None, None) == N.GR_EINVAL
+    assert L.gr_greedy_shard_private(None, -1, None, None, 0, None) == N.GR_EINVAL
+    assert L.gr_greedy_shard_remove(None, 0, None, 0, None) == N.GR_EINVAL
+    assert L.gr_greedy_shard_finalize(None, None, None, None, None, 0, None) == N.GR_EINVAL
     assert L.gr_last_error()
     b = N.GrBatch(0, 1, 0, 0, 0, None, None, None, None, None, 0, None)
     assert L.gr_workspace_bytes(C.byref(b), 0) == 0  # B < 1
