@@ -160,3 +160,56 @@ def greedy_matrix_sharded(bm_shard, rank: int, world: int, group=None, stream=No
     if world > 1:
         return run_greedy_sharded(sh, nccl_allreduce("sum", group), nccl_allreduce("max", group))
     return run_greedy_sharded(sh, lambda t: None, lambda t: None)
+
+
+# ---- batch sharding with result collection (C2 / C4) -------------------------------
+def solve_batch_sharded(cb, rank: int, world: int, solve_fn: Callable, allgather: Callable):
+    """Solve a host ClauseBatch split across ranks: instances are dealt by
+    estimated cost (``shard_instances``), each rank solves its slice with
+    ``solve_fn(sub_batch) -> dict`` (status int32 [n], assign uint64 [n, W],
+    cost uint64 [n], decided uint64 [n]; e.g. a gr.solve_pms on this rank's
+    GPU), and one all-gather of (index, status, cost, decided, assign) rows
+    gives every rank the whole batch's results in input order.  The gather is
+    result collection after the solve, not part of the data path.
+    ``allgather(t) -> list of tensors`` (one per rank, same shape as t)."""
+    import torch
+
+    parts = shard_instances(estimate_costs(cb.m, cb.n_pos), world)
+    mine = parts[rank]
+    W = cb.W
+    width = 4 + W
+    maxn = max(len(p) for p in parts)
+    rows = torch.full((max(maxn, 1), width), -1, dtype=torch.int64)
+    if mine:
+        r = solve_fn(cb.subset(mine))
+        n = len(mine)
+        rows[:n, 0] = torch.tensor(mine, dtype=torch.int64)
+        rows[:n, 1] = torch.from_numpy(np.asarray(r["status"], np.int64))
+        rows[:n, 2] = torch.from_numpy(np.asarray(r["cost"], np.uint64).view(np.int64))
+        rows[:n, 3] = torch.from_numpy(np.asarray(r["decided"], np.uint64).view(np.int64))
+        rows[:n, 4:] = torch.from_numpy(np.asarray(r["assign"], np.uint64).reshape(n, W).view(np.int64))
+    got = allgather(rows)
+    out = {"status": np.zeros(cb.B, np.int32), "cost": np.zeros(cb.B, np.uint64),
+           "decided": np.zeros(cb.B, np.uint64), "assign": np.zeros((cb.B, W), np.uint64)}
+    for g in got:
+        g = g.cpu().numpy()
+        g = g[g[:, 0] >= 0]
+        idx = g[:, 0]
+        out["status"][idx] = g[:, 1].astype(np.int32)
+        out["cost"][idx] = g[:, 2].view(np.uint64)
+        out["decided"][idx] = g[:, 3].view(np.uint64)
+        out["assign"][idx] = g[:, 4:].view(np.uint64)
+    return out
+
+
+def nccl_allgather(group=None, device=None):
+    import torch
+    import torch.distributed as dist
+
+    def f(t):
+        t = t.to(device) if device is not None else t
+        outs = [torch.empty_like(t) for _ in range(dist.get_world_size(group))]
+        dist.all_gather(outs, t, group=group)
+        return outs
+
+    return f

@@ -248,3 +248,54 @@ def test_greedy_column_sharding_gloo_world2(seed):
         got_set = [v for v in range(m) if (assign[v // 64] >> (v % 64)) & 1]
         assert got_set == ref_set
         assert status == (2 if ref.status == oracle.SAT_NEG_VIOLATED else 0)
+
+
+# ---- batch sharding with result collection ---------------------------------------
+def _batch_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    from paper_2011_08373_b200 import synth
+    from paper_2011_08373_b200.multigpu import solve_batch_sharded
+
+    cb = synth.c2_batch()
+    cb = cb.subset([b for b in range(cb.B) if cb.m[b] <= 14])
+
+    def solve(sub):  # CPU stand-in for this rank's GPU solve
+        r = oracle.batch("pms", sub)
+        return {"status": r.status, "assign": r.assign, "cost": r.cost, "decided": r.decided}
+
+    def allgather(t):
+        outs = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(outs, t)
+        return outs
+
+    out = solve_batch_sharded(cb, rank, world, solve, allgather)
+    q.put((rank, {k: v.tolist() for k, v in out.items()}))
+    dist.destroy_process_group()
+
+
+def test_batch_sharding_allgather_gloo_world2():
+    """Instances dealt by cost over two ranks + one all-gather = the
+    single-rank results, in input order, on every rank."""
+    import oracle
+    from paper_2011_08373_b200 import synth
+
+    cb = synth.c2_batch()
+    cb = cb.subset([b for b in range(cb.B) if cb.m[b] <= 14])
+    ref = oracle.batch("pms", cb)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_batch_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, out in got:
+        assert out["status"] == ref.status.tolist()
+        assert np.array_equal(np.asarray(out["assign"], np.uint64).reshape(-1),
+                              np.asarray(ref.assign, np.uint64).reshape(-1))
+        assert out["decided"] == np.asarray(ref.decided, np.uint64).tolist()

@@ -630,3 +630,41 @@ def test_refutation_shapes_vs_oracle(seed, weighted):
         b = gpu_solve(cb, which, flags=gr.GR_FLAG_NO_PRUNE)
         for f in ("status", "assign", "cost", "decided"):
             assert (a[f] == b[f]).all(), (which, f)
+
+
+def test_batch_sharded_solve_threads():
+    """solve_batch_sharded with G = 3 shards (host threads on this GPU, a host
+    all-gather between them) = the single-GPU PMS of the whole batch."""
+    import threading
+
+    from paper_2011_08373_b200.multigpu import solve_batch_sharded
+
+    cb = synth.c2_batch()
+    ref = gpu_solve(cb, "pms")
+    G = 3
+    bar, buf, out = threading.Barrier(G), [None] * G, [None] * G
+    lock = threading.Lock()  # one process per GPU has its own workspace; threads share one
+
+    def run(r):
+        def gather(t):
+            buf[r] = t.clone()
+            bar.wait()
+            res = [x.clone() for x in buf]
+            bar.wait()
+            return res
+
+        def solve(sub):
+            with lock:
+                return gr.solve_pms(gr.DeviceBatch.from_host(sub)).to_host()
+
+        out[r] = solve_batch_sharded(cb, r, G, solve, gather)
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(G)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    for o in out:
+        for f in ("status", "cost", "decided"):
+            assert (o[f] == ref[f]).all(), f
+        assert (o["assign"].reshape(cb.B, -1) == ref["assign"].reshape(cb.B, -1)).all()
