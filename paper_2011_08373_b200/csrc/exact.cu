@@ -245,12 +245,15 @@ __global__ void __launch_bounds__(PT) pack_kernel(In in, Out out, WS ws, int whi
   if (s_bad) status = GR_BADINPUT;
   else if (s_unsat || (which == 0 && s_negempty)) status = GR_UNSAT;
   else if (me > 64) status = GR_UNSUPPORTED;
-  if (status >= 0) {
+  // an empty negative clause decides the PMS (UNSAT) but not the MHS: the
+  // clauses are still packed, for a fused PMS + MHS walk (gr_solve_pms_mhs)
+  const bool decided_here = status >= 0;
+  if (decided_here) {
     if (t == 0) {
       ws.done[b] = 1;
       write_result(in, out, b, status, 0, 0, 0, 0, 0, which);
     }
-    return;
+    if (!(status == GR_UNSAT && !s_unsat)) return;
   }
   // relabel onto the support; negatives that touch a non-support variable are
   // always satisfied by an optimum (those variables are false) -> dropped (R13)
@@ -351,7 +354,9 @@ __global__ void __launch_bounds__(PT) pack_kernel(In in, Out out, WS ws, int whi
     ws.bestx[b] = 0;
     ws.lvlkey[b] = GR_KEY_NONE;
     ws.decided[b] = 1;  // level 0: the empty assignment
-    if (npr == 0) {
+    if (decided_here) {
+      // done at pack (see above); the packed clauses serve a fused MHS only
+    } else if (npr == 0) {
       // phi+ empty: the all-false assignment satisfies every (non-empty)
       // negative clause and is optimal
       ws.done[b] = 1;
@@ -461,9 +466,9 @@ struct Clauses {
 };
 
 // Test one sub-block: F (its candidates in the lane's window) narrowed by
-// every clause.
+// every positive clause (test_pos), then by every negative clause (test_neg).
 template <typename M, bool COUNT>
-__device__ __forceinline__ F2 test_sub(int j, M U, int e, F2 F, const Clauses<M> &c, Work &wk) {
+__device__ __forceinline__ F2 test_pos(int j, M U, F2 F, const Clauses<M> &c, Work &wk) {
   const int np = c.np;
   const F2 *H = c.H + (j - 1);
   int q = 0;
@@ -482,7 +487,12 @@ __device__ __forceinline__ F2 test_sub(int j, M U, int e, F2 F, const Clauses<M>
     if (!(U & c.P[q])) F = f2_and(F, H[HREC * q]);
     if (COUNT) wk.tests += 1;
   }
-  if (!f2_any(F)) return F;
+  return F;
+}
+
+template <typename M, bool COUNT>
+__device__ __forceinline__ F2 test_neg(int j, M U, int e, F2 F, const Clauses<M> &c, Work &wk) {
+  const int np = c.np;
   const M lowm = (M)nbits((u64)e);
   const F2 *hx = c.hitx + HX * j;
   for (int t = 0; t < c.nn; t++) {
@@ -499,6 +509,13 @@ __device__ __forceinline__ F2 test_sub(int j, M U, int e, F2 F, const Clauses<M>
     if (!f2_any(F)) return F;
   }
   return F;
+}
+
+template <typename M, bool COUNT>
+__device__ __forceinline__ F2 test_sub(int j, M U, int e, F2 F, const Clauses<M> &c, Work &wk) {
+  F = test_pos<M, COUNT>(j, U, F, c, wk);
+  if (!f2_any(F)) return F;
+  return test_neg<M, COUNT>(j, U, e, F, c, wk);
 }
 
 // weighted: the weights of the j low elements encoded by bit idx (colex
@@ -526,8 +543,10 @@ __device__ __forceinline__ u64 weight_low(int j, u64 idx, int ea, const u32 *w, 
 // pairwise disjoint positive clauses missing U (restricted to [0, e), greedy
 // packing in clause order: S needs one element of each), or a negative
 // clause inside U.
+// 0: not refuted; 1: refuted by the positive clauses (for the MHS too);
+// 2: only by a negative clause inside U
 template <typename M, bool COUNT>
-__device__ __forceinline__ bool refuted(int j, M U, int e, const Clauses<M> &c, Work &wk) {
+__device__ __forceinline__ int refuted_by(int j, M U, int e, const Clauses<M> &c, Work &wk) {
   const M lowe = (M)nbits((u64)e);
   M used = 0;
   int pk = 0, r = 0;
@@ -542,16 +561,27 @@ __device__ __forceinline__ bool refuted(int j, M U, int e, const Clauses<M> &c, 
       if (++pk > j) { dead = true; break; }
     }
   }
+  int kind = dead ? 1 : 0;
   if (!dead)
     for (int q = 0; q < c.nn; q++)
-      if (!(c.P[c.np + q] & ~U)) { dead = true; break; }
+      if (!(c.P[c.np + q] & ~U)) { kind = 2; break; }
   if (COUNT) wk.tests += (u64)r;
-  return dead;
+  return kind;
+}
+template <typename M, bool COUNT>
+__device__ __forceinline__ bool refuted(int j, M U, int e, const Clauses<M> &c, Work &wk) {
+  return refuted_by<M, COUNT>(j, U, e, c, wk) != 0;
 }
 
 template <typename M, int MODE, bool COUNT>
 __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const u32 *w, int rb,
-                    int prune, Work &wk, const u64 *skj = nullptr, u64 wstar = ~0ull) {
+                    int prune, Work &wk, const u64 *skj = nullptr, u64 wstar = ~0ull,
+                    int need_p = 1, int need_m = 0, i64 *best_m = nullptr) {
+  // MODE 3 (PMS and MHS of one instance in one walk): the first witness of
+  // phi (returned) and of phi+ alone (*best_m), each only while needed
+  i64 dummy = GR_KEY_NONE;
+  i64 &bm = MODE == 3 ? *best_m : dummy;
+  bool wp = MODE != 3 || need_p, wm = MODE == 3 && need_m;
   const int J = k < JMAX ? k : JMAX;
   const u64 *cs = c.cs;  // C(n, j), j <= JMAX
 #define CS(n, j) (cs[(n) * (JMAX + 1) + (j)])
@@ -602,9 +632,12 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
   // remaining sibling on the path one by one).
   bool dead0 = false;
   while (j >= 2 && s[j - 1] >= region_of(j)) {
-    if (prune && refuted<M, COUNT>(j, U, e, c, wk)) {
-      dead0 = true;
-      break;
+    if (prune) {
+      const int kind = refuted_by<M, COUNT>(j, U, e, c, wk);
+      if (kind == 1 || (kind == 2 && !wm)) {
+        dead0 = true;
+        break;
+      }
     }
     const int t = s[j - 1];
     tp = (tp << 6) | (u64)ep;
@@ -643,14 +676,34 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
         if (WU + skj[j] >= lim) dead = true;
       }
     }
-    if (!dead && prune && j >= 2 && R < e) dead = refuted<M, COUNT>(j, U, e, c, wk);
+    if (!dead && prune && j >= 2 && R < e) {
+      const int kind = refuted_by<M, COUNT>(j, U, e, c, wk);
+      dead = kind == 1 || (kind == 2 && !wm);  // the MHS ignores phi-
+    }
     if (!dead && n && pos + n > 0) {
       F2 F = c.lowb[n];
       if (pos < 0) F = f2_andnot(F, c.lowb[-pos]);
       if (cnt32 - pos < n) F = f2_and(F, c.lowb[cnt32 - pos]);
       if (COUNT) { wk.blocks++; wk.cands += (u64)f2_popc(F); }
       const int ea = e < R ? e : R;
-      F = test_sub<M, COUNT>(j, U, ea, F, c, wk);
+      if (MODE == 3) {
+        F = test_pos<M, COUNT>(j, U, F, c, wk);
+        if (wm && f2_any(F)) {
+          bm = (i64)(r_lo + (u64)(pos + f2_ctz(F)));
+          wm = false;
+        }
+        if (wp && f2_any(F)) {
+          F = test_neg<M, COUNT>(j, U, ea, F, c, wk);
+          if (f2_any(F)) {
+            best = (i64)(r_lo + (u64)(pos + f2_ctz(F)));
+            wp = false;
+          }
+        }
+        if (!wp && !wm) return best;
+        F = F2{0ull, 0ull};
+      } else {
+        F = test_sub<M, COUNT>(j, U, ea, F, c, wk);
+      }
       if (f2_any(F)) {
         if (MODE == 2) {
           for (int h = 0; h < 2; h++)
@@ -727,6 +780,10 @@ struct EnumParams {
   WS ws;
   const int64_t *off;
   int k, weighted, exhaustive, shard, nshard, prune;
+  // fused: the MHS of the same batch (its own workspace ws2) is decided in
+  // the PMS walk (MODE 3); the chunk plan is the PMS workspace's
+  int fused;
+  WS ws2;
 };
 
 template <typename M, bool COUNT>
@@ -754,11 +811,11 @@ template <bool COUNT>
 __global__ void __launch_bounds__(NT, COUNT ? 1 : ENUM_CTAS) enum_kernel(EnumParams p) {
   extern __shared__ u64 cls[];  // [np][HREC] H records, [np + nn] P (u32 or u64)
   __shared__ u64 s_chunk;
-  __shared__ int s_b, s_cur, s_skip;
+  __shared__ int s_b, s_cur, s_skip, s_needp, s_needm;
   __shared__ u64 s_r0, s_ck;
   __shared__ u64 s_skj[JMAX + 1], s_wstar;  // weighted: S_j and the incumbent W*
   __shared__ u32 s_w[64];
-  __shared__ i64 s_wmin[NT / 32];
+  __shared__ i64 s_wmin[NT / 32], s_wmin2[NT / 32];
   const int t = threadIdx.x;
   if (t == 0) s_cur = -1;
   F2 *hitx = (F2 *)cls;  // [JMAX + 1][HX] HIT_j({x}): j-subsets of [0, R_j) containing x
@@ -804,6 +861,15 @@ __global__ void __launch_bounds__(NT, COUNT ? 1 : ENUM_CTAS) enum_kernel(EnumPar
           const i64 cur = *(volatile i64 *)&p.ws.lvlkey[b];
           if (cur != GR_KEY_NONE && (u64)cur < r0) s_skip = 1;  // a lower witness exists
         }
+        if (p.fused) {  // each solve is needed unless done or already below r0
+          const i64 c1 = *(volatile i64 *)&p.ws.lvlkey[b];
+          const i64 c2 = *(volatile i64 *)&p.ws2.lvlkey[b];
+          const int np_ = !p.ws.done[b] && !(c1 != GR_KEY_NONE && (u64)c1 < r0 && !p.exhaustive);
+          const int nm_ = !p.ws2.done[b] && !(c2 != GR_KEY_NONE && (u64)c2 < r0 && !p.exhaustive);
+          s_needp = np_;
+          s_needm = nm_;
+          s_skip = !np_ && !nm_;
+        }
       }
     }
     __syncthreads();
@@ -834,12 +900,27 @@ __global__ void __launch_bounds__(NT, COUNT ? 1 : ENUM_CTAS) enum_kernel(EnumPar
     }
     const u64 r_lo = s_r0 + (u64)t * Lc;
     const u64 ck = s_ck;
-    i64 key = GR_KEY_NONE;
+    i64 key = GR_KEY_NONE, key_m = GR_KEY_NONE;
     Work wk;
     if (r_lo < ck) {
       const u64 cnt = (ck - r_lo) < Lc ? (ck - r_lo) : Lc;
       const int rb = p.ws.rb[b];
-      if (narrow) {
+      if (p.fused) {
+        const int nq = s_needp, nm = s_needm;
+        if (narrow) {
+          Clauses<u32> c{(const u32 *)sP, sH, hitx, lowb, reg, nb, cs, np, nn};
+          key = walk<u32, 3, COUNT>(p.k, me, r_lo, cnt, c, s_w, rb, p.prune, wk, nullptr, ~0ull,
+                                    nq, nm, &key_m);
+        } else if (staged) {
+          Clauses<u64> c{sP, sH, hitx, lowb, reg, nb, cs, np, nn};
+          key = walk<u64, 3, COUNT>(p.k, me, r_lo, cnt, c, s_w, rb, p.prune, wk, nullptr, ~0ull,
+                                    nq, nm, &key_m);
+        } else {
+          Clauses<u64> c{p.ws.pk + lo, (const F2 *)p.ws.hrec + lo * HREC, hitx, lowb, reg, nb, cs, np, nn};
+          key = walk<u64, 3, COUNT>(p.k, me, r_lo, cnt, c, s_w, rb, p.prune, wk, nullptr, ~0ull,
+                                    nq, nm, &key_m);
+        }
+      } else if (narrow) {
         Clauses<u32> c{(const u32 *)sP, sH, hitx, lowb, reg, nb, cs, np, nn};
         key = run_lane<u32, COUNT>(p, r_lo, cnt, me, c, s_w, rb, wk, s_skj, s_wstar);
       } else if (staged) {
@@ -857,12 +938,20 @@ __global__ void __launch_bounds__(NT, COUNT ? 1 : ENUM_CTAS) enum_kernel(EnumPar
       if (!narrow) atomicAdd(&g_work[3], (unsigned long long)wk.tests);
     }
     key = warp_min(key);
-    if ((t & 31) == 0) s_wmin[t >> 5] = key;
+    if (p.fused) key_m = warp_min(key_m);
+    if ((t & 31) == 0) {
+      s_wmin[t >> 5] = key;
+      s_wmin2[t >> 5] = key_m;
+    }
     __syncthreads();
     if (t == 0) {
-      i64 v = s_wmin[0];
-      for (int i = 1; i < NT / 32; i++) v = s_wmin[i] < v ? s_wmin[i] : v;
+      i64 v = s_wmin[0], v2 = s_wmin2[0];
+      for (int i = 1; i < NT / 32; i++) {
+        v = s_wmin[i] < v ? s_wmin[i] : v;
+        v2 = s_wmin2[i] < v2 ? s_wmin2[i] : v2;
+      }
       if (v != GR_KEY_NONE) atomicMin((long long *)&p.ws.lvlkey[b], (long long)v);
+      if (p.fused && v2 != GR_KEY_NONE) atomicMin((long long *)&p.ws2.lvlkey[b], (long long)v2);
     }
   }
 }
@@ -875,7 +964,10 @@ __device__ __forceinline__ int bitlen(u64 x) { return x ? 64 - __clzll((long lon
 __global__ void __launch_bounds__(FT) finish_kernel(In in, Out out, WS ws, int which, int k,
                                                     int exhaustive, int enum_lanes,
                                                     u64 fixed_lane, int windows_per_lane,
-                                                    u64 lane_max, u64 lane_max_w) {
+                                                    u64 lane_max, u64 lane_max_w,
+                                                    const int *done_other) {
+  // done_other (fused PMS + MHS): the MHS workspace's done flags -- an
+  // instance stays listed (and planned) while either solve still searches
   typedef cub::BlockScan<u64, FT> Scan;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ u64 s_carry;
@@ -889,6 +981,7 @@ __global__ void __launch_bounds__(FT) finish_kernel(In in, Out out, WS ws, int w
   if (k > 0) {
     for (int i = t; i < nact_in; i += FT) {
       const int b = cur[i];
+      if (ws.done[b]) continue;  // fused: listed for the other solve only
       const int me = ws.meff[b];
       const u64 ck = binom(me, k);
       const i64 key = ws.lvlkey[b];
@@ -941,7 +1034,7 @@ __global__ void __launch_bounds__(FT) finish_kernel(In in, Out out, WS ws, int w
     int b = -1;
     if (i < n2) {
       b = all ? i : cur[i];
-      if (ws.done[b]) b = -1;
+      if (ws.done[b] && (!done_other || done_other[b])) b = -1;
       else if (k + 1 < ws.ks[b]) {
         atomicAdd(&s_wait, 1);
         b = -1;
@@ -1114,6 +1207,29 @@ int *pinned_i32() {
 }
 }  // namespace
 
+namespace {
+int launch_finish(const gr_batch *in, int which, const gr_result *out, const WS &w, int k,
+                  cudaStream_t st, const int *done_other) {
+  GR_LAUNCH("finish_kernel", st, finish_kernel<<<1, FT, 0, st>>>(in_of(in, which), out_of(out), w, which, k,
+                                   (in->flags & GR_FLAG_EXHAUSTIVE) ? 1 : 0, enum_grid() * NT, lane_cands(), windows_per_lane(false) | (windows_per_lane(true) << 16),
+                                   lane_max(false), lane_max(true), done_other));
+  return GR_OK;
+}
+int launch_pack(const gr_batch *in, int which, const gr_result *out, const WS &w, cudaStream_t st) {
+  Ctrl c{};
+  c.lane_cands = lane_cands();
+  GR_CUDA(cudaMemcpyAsync(w.ctrl, &c, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
+  size_t smem = (size_t)std::max(in->max_clauses, 1) * 13 + 16;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MAXC * 13 + 16);
+    attr = true;
+  }
+  GR_LAUNCH("pack_kernel", st, pack_kernel<<<in->B, PT, smem, st>>>(in_of(in, which), out_of(out), w, which));
+  return GR_OK;
+}
+}  // namespace
+
 extern "C" int gr_exact_prepare(const gr_batch *in, int which, gr_result *out, void *ws,
                                 size_t ws_bytes, gr_stream_t s, int32_t *n_active) {
   int rc = validate_batch(in, which);
@@ -1124,19 +1240,8 @@ extern "C" int gr_exact_prepare(const gr_batch *in, int which, gr_result *out, v
   if (!ws || ws_bytes < L.total) { gr_set_error("workspace too small"); return GR_EWORKSPACE; }
   WS w = ws_of(in, ws);
   cudaStream_t st = (cudaStream_t)s;
-  Ctrl c{};
-  c.lane_cands = lane_cands();
-  GR_CUDA(cudaMemcpyAsync(w.ctrl, &c, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
-  size_t smem = (size_t)std::max(in->max_clauses, 1) * 13 + 16;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MAXC * 13 + 16);
-    attr = true;
-  }
-  GR_LAUNCH("pack_kernel", (cudaStream_t)s, pack_kernel<<<in->B, PT, smem, st>>>(in_of(in, which), out_of(out), w, which));
-  GR_LAUNCH("finish_kernel", (cudaStream_t)s, finish_kernel<<<1, FT, 0, st>>>(in_of(in, which), out_of(out), w, which, 0,
-                                   (in->flags & GR_FLAG_EXHAUSTIVE) ? 1 : 0, enum_grid() * NT, lane_cands(), windows_per_lane(false) | (windows_per_lane(true) << 16),
-                                   lane_max(false), lane_max(true)));
+  if ((rc = launch_pack(in, which, out, w, st))) return rc;
+  if ((rc = launch_finish(in, which, out, w, 0, st, nullptr))) return rc;
   if (n_active) {
     int *h = pinned_i32();
     if (!h) { gr_set_error("cudaMallocHost failed"); return GR_ECUDA; }
@@ -1166,6 +1271,8 @@ extern "C" int gr_exact_level(const gr_batch *in, int which, int k, int shard, i
   p.prune = (in->flags & GR_FLAG_NO_PRUNE) ? 0 : 1;
   p.shard = shard;
   p.nshard = nshard;
+  p.fused = 0;
+  p.ws2 = w;
   int grid = enum_grid();
   // the finish kernel leaves next_chunk at 0; several shards of one level on
   // one device (multi-shard emulation) need it reset between them
@@ -1194,7 +1301,7 @@ extern "C" int gr_exact_finish(const gr_batch *in, int which, int k, gr_result *
   cudaStream_t st = (cudaStream_t)s;
   GR_LAUNCH("finish_kernel", (cudaStream_t)s, finish_kernel<<<1, FT, 0, st>>>(in_of(in, which), out_of(out), w, which, k,
                                    (in->flags & GR_FLAG_EXHAUSTIVE) ? 1 : 0, enum_grid() * NT, lane_cands(), windows_per_lane(false) | (windows_per_lane(true) << 16),
-                                   lane_max(false), lane_max(true)));
+                                   lane_max(false), lane_max(true), nullptr));
   if (n_active) {
     int *h = pinned_i32();
     if (!h) { gr_set_error("cudaMallocHost failed"); return GR_ECUDA; }
@@ -1259,6 +1366,57 @@ extern "C" int gr_solve_pms_mhs(const gr_batch *in, gr_result *out_pms, gr_resul
   const size_t half = align256(layout_of(in).total);
   if (!ws || ws_bytes < 2 * half) { gr_set_error("workspace too small (2 x gr_workspace_bytes)"); return GR_EWORKSPACE; }
   void *ws1 = ws, *ws2 = (char *)ws + half;
+  if (!in->w && !in->k_start && !(in->flags & GR_FLAG_EXHAUSTIVE) && !getenv("GR_NO_FUSE")) {
+    // unit weights: one walk decides both -- the MHS is phi+'s part of the
+    // PMS test (MODE 3); the PMS workspace plans the union of both searches
+    if (!out_pms || !out_mhs) { gr_set_error("null result"); return GR_EINVAL; }
+    cudaStream_t st = (cudaStream_t)s_pms;
+    WS w1 = ws_of(in, ws1), w2 = ws_of(in, ws2);
+    if ((rc = launch_pack(in, 1, out_mhs, w2, st))) return rc;
+    if ((rc = launch_finish(in, 1, out_mhs, w2, 0, st, nullptr))) return rc;
+    if ((rc = launch_pack(in, 0, out_pms, w1, st))) return rc;
+    if ((rc = launch_finish(in, 0, out_pms, w1, 0, st, w2.done))) return rc;
+    int *h = pinned_i32();
+    if (!h) { gr_set_error("cudaMallocHost failed"); return GR_ECUDA; }
+    GR_CUDA(cudaMemcpyAsync(h, &w1.ctrl->n_remaining, sizeof(int), cudaMemcpyDeviceToHost, st));
+    GR_CUDA(cudaStreamSynchronize(st));
+    int n = h[0];
+    const int grid = enum_grid();
+    const int SPEC = spec_levels();
+    for (int k = 1; n > 0 && k <= 64;) {
+      for (int i = 0; i < SPEC && k <= 64; i++, k++) {
+        EnumParams p;
+        p.ws = w1;
+        p.ws.active = w1.active + (size_t)(k & 1) * in->B;
+        p.ws2 = w2;
+        p.off = in->off;
+        p.k = k;
+        p.weighted = 0;
+        p.exhaustive = 0;
+        p.prune = (in->flags & GR_FLAG_NO_PRUNE) ? 0 : 1;
+        p.shard = 0;
+        p.nshard = 1;
+        p.fused = 1;
+        if (gr_prof_mode() == 2)
+          GR_LAUNCH("enum_kernel", st, enum_kernel<true><<<grid, NT, ENUM_SMEM, st>>>(p));
+        else
+          GR_LAUNCH("enum_kernel", st, enum_kernel<false><<<grid, NT, ENUM_SMEM, st>>>(p));
+        if ((rc = launch_finish(in, 1, out_mhs, w2, k, st, nullptr))) return rc;   // MHS first: the PMS
+        if ((rc = launch_finish(in, 0, out_pms, w1, k, st, w2.done))) return rc;   // plan reads its done flags
+      }
+      GR_CUDA(cudaMemcpyAsync(h, &w1.ctrl->n_remaining, sizeof(int), cudaMemcpyDeviceToHost, st));
+      GR_CUDA(cudaStreamSynchronize(st));
+      n = h[0];
+    }
+    if (s_mhs != s_pms) {  // the MHS results are ordered on s_mhs too
+      cudaEvent_t ev;
+      GR_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      GR_CUDA(cudaEventRecord(ev, st));
+      GR_CUDA(cudaStreamWaitEvent((cudaStream_t)s_mhs, ev, 0));
+      GR_CUDA(cudaEventDestroy(ev));
+    }
+    return GR_OK;
+  }
   int32_t n1 = 0, n2 = 0;
   rc = gr_exact_prepare(in, 0, out_pms, ws1, half, s_pms, nullptr);
   if (rc) return rc;

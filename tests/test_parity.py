@@ -668,3 +668,30 @@ def test_batch_sharded_solve_threads():
         for f in ("status", "cost", "decided"):
             assert (o[f] == ref[f]).all(), f
         assert (o["assign"].reshape(cb.B, -1) == ref["assign"].reshape(cb.B, -1)).all()
+
+
+@pytest.mark.parametrize("case", ["fuzz", "refutation", "wide", "c3", "edge"])
+def test_pms_mhs_fused_matches_separate(case):
+    """gr_solve_pms_mhs (one walk deciding PMS and MHS, unit weights) gives
+    the separate solvers' statuses, assignments, costs and decided counts."""
+    if case == "fuzz":
+        cb = rand_batch(7, 300, 20, 24)
+    elif case == "refutation":
+        cb = refutation_batch(31, 200, 10, 28)
+    elif case == "wide":
+        cb = rand_batch(8, 60, 44, 14)
+    elif case == "c3":
+        cb = synth.c3_instance()[0]
+    else:  # empty negative clauses, empty phi+, duplicates (edge=True), m = 0
+        cb = rand_batch(9, 400, 10, 12, edge=True, p_neg=0.5)
+    db = gr.DeviceBatch.from_host(cb, weighted=False)
+    p, h = gr.solve_pms_mhs(db)
+    p, h = p.to_host(), h.to_host()
+    rp, rh = gpu_solve(cb, "pms"), gpu_solve(cb, "mhs")
+    for f in ("status", "assign", "cost", "decided"):
+        assert (p[f] == rp[f]).all(), ("pms", f)
+        assert (h[f] == rh[f]).all(), ("mhs", f)
+    if case in ("fuzz", "edge"):
+        o = oracle.batch("pms", cb)
+        keep = o.status != -1
+        assert (p["status"][keep] == o.status[keep]).all()
