@@ -961,24 +961,14 @@ __global__ void __launch_bounds__(NT, COUNT ? 1 : ENUM_CTAS) enum_kernel(EnumPar
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ int bitlen(u64 x) { return x ? 64 - __clzll((long long)x) : 0; }
 
-__global__ void __launch_bounds__(FT) finish_kernel(In in, Out out, WS ws, int which, int k,
-                                                    int exhaustive, int enum_lanes,
-                                                    u64 fixed_lane, int windows_per_lane,
-                                                    u64 lane_max, u64 lane_max_w,
-                                                    const int *done_other) {
-  // done_other (fused PMS + MHS): the MHS workspace's done flags -- an
-  // instance stays listed (and planned) while either solve still searches
-  typedef cub::BlockScan<u64, FT> Scan;
-  __shared__ typename Scan::TempStorage tmp;
-  __shared__ u64 s_carry;
-  __shared__ int s_cnt, s_wait;
+// phase 1 of the finish: commit level k of every listed instance
+__device__ void finish_commit(const In &in, const Out &out, const WS &ws, int which, int k,
+                              int exhaustive) {
   const int t = threadIdx.x;
   const bool weighted = in.w != nullptr;
   const int nact_in = k == 0 ? in.B : ws.ctrl->n_active;
-  int *cur = ws.active + (size_t)(k & 1) * in.B;        // list enumerated at level k
-  int *nxt = ws.active + (size_t)((k + 1) & 1) * in.B;  // list for level k+1
-  // phase 1: commit level k
-  if (k > 0) {
+  const int *cur = ws.active + (size_t)(k & 1) * in.B;  // list enumerated at level k
+  {
     for (int i = t; i < nact_in; i += FT) {
       const int b = cur[i];
       if (ws.done[b]) continue;  // fused: listed for the other solve only
@@ -1022,6 +1012,23 @@ __global__ void __launch_bounds__(FT) finish_kernel(In in, Out out, WS ws, int w
     }
     __syncthreads();
   }
+}
+
+// phase 2: compact the active list and plan level k+1.  done_other (fused
+// PMS + MHS): the MHS workspace's done flags -- an instance stays listed (and
+// planned) while either solve still searches
+__device__ void finish_plan(const In &in, const Out &out, const WS &ws, int which, int k,
+                            int enum_lanes, u64 fixed_lane, int windows_per_lane, u64 lane_max,
+                            u64 lane_max_w, const int *done_other) {
+  typedef cub::BlockScan<u64, FT> Scan;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ u64 s_carry;
+  __shared__ int s_cnt, s_wait;
+  const int t = threadIdx.x;
+  const bool weighted = in.w != nullptr;
+  const int nact_in = k == 0 ? in.B : ws.ctrl->n_active;
+  int *cur = ws.active + (size_t)(k & 1) * in.B;        // list enumerated at level k
+  int *nxt = ws.active + (size_t)((k + 1) & 1) * in.B;  // list for level k+1
   // phase 2: compact the still-active instances and plan level k+1
   // (with start levels, every unfinished instance is revisited: those whose
   // start level is above k+1 wait, counted in n_remaining)
@@ -1107,6 +1114,33 @@ __global__ void __launch_bounds__(FT) finish_kernel(In in, Out out, WS ws, int w
     ws.ctrl->next_chunk = 0;
     ws.ctrl->lane_cands = L;
   }
+}
+
+__global__ void __launch_bounds__(FT) finish_kernel(In in, Out out, WS ws, int which, int k,
+                                                    int exhaustive, int enum_lanes,
+                                                    u64 fixed_lane, int windows_per_lane,
+                                                    u64 lane_max, u64 lane_max_w,
+                                                    const int *done_other) {
+  if (k > 0) finish_commit(in, out, ws, which, k, exhaustive);
+  finish_plan(in, out, ws, which, k, enum_lanes, fixed_lane, windows_per_lane, lane_max, lane_max_w,
+              done_other);
+}
+
+// fused PMS (ws1) + MHS (ws2): both commits, then the MHS list, then the PMS
+// plan over the union -- one launch per level
+__global__ void __launch_bounds__(FT) finish_fused_kernel(In in1, Out out1, WS ws1, In in2, Out out2,
+                                                          WS ws2, int k, int enum_lanes,
+                                                          u64 fixed_lane, int windows_per_lane,
+                                                          u64 lane_max, u64 lane_max_w) {
+  if (k > 0) {
+    finish_commit(in2, out2, ws2, 1, k, 0);
+    finish_commit(in1, out1, ws1, 0, k, 0);
+  }
+  finish_plan(in2, out2, ws2, 1, k, enum_lanes, fixed_lane, windows_per_lane, lane_max, lane_max_w,
+              nullptr);
+  __syncthreads();
+  finish_plan(in1, out1, ws1, 0, k, enum_lanes, fixed_lane, windows_per_lane, lane_max, lane_max_w,
+              ws2.done);
 }
 
 // ---------------------------------------------------------------------------
@@ -1401,8 +1435,11 @@ extern "C" int gr_solve_pms_mhs(const gr_batch *in, gr_result *out_pms, gr_resul
           GR_LAUNCH("enum_kernel", st, enum_kernel<true><<<grid, NT, ENUM_SMEM, st>>>(p));
         else
           GR_LAUNCH("enum_kernel", st, enum_kernel<false><<<grid, NT, ENUM_SMEM, st>>>(p));
-        if ((rc = launch_finish(in, 1, out_mhs, w2, k, st, nullptr))) return rc;   // MHS first: the PMS
-        if ((rc = launch_finish(in, 0, out_pms, w1, k, st, w2.done))) return rc;   // plan reads its done flags
+        GR_LAUNCH("finish_kernel", st, finish_fused_kernel<<<1, FT, 0, st>>>(
+                                           in_of(in, 0), out_of(out_pms), w1, in_of(in, 1),
+                                           out_of(out_mhs), w2, k, enum_grid() * NT, lane_cands(),
+                                           windows_per_lane(false) | (windows_per_lane(true) << 16),
+                                           lane_max(false), lane_max(true)));
       }
       GR_CUDA(cudaMemcpyAsync(h, &w1.ctrl->n_remaining, sizeof(int), cudaMemcpyDeviceToHost, st));
       GR_CUDA(cudaStreamSynchronize(st));
