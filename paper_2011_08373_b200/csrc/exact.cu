@@ -1019,7 +1019,7 @@ __device__ void finish_commit(const In &in, const Out &out, const WS &ws, int wh
 // planned) while either solve still searches
 __device__ void finish_plan(const In &in, const Out &out, const WS &ws, int which, int k,
                             int enum_lanes, u64 fixed_lane, int windows_per_lane, u64 lane_max,
-                            u64 lane_max_w, const int *done_other) {
+                            u64 lane_max_w, const int *done_other, bool plan_chunks = true) {
   typedef cub::BlockScan<u64, FT> Scan;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ u64 s_carry;
@@ -1094,7 +1094,7 @@ __device__ void finish_plan(const In &in, const Out &out, const WS &ws, int whic
   __syncthreads();
   if (t == 0) s_carry = 0;
   __syncthreads();
-  for (int base = 0; base < nact; base += FT) {
+  for (int base = 0; plan_chunks && base < nact; base += FT) {
     const int i = base + t;
     u64 nch = 0;
     if (i < nact) nch = (binom(ws.meff[nxt[i]], k + 1) + CH - 1) / CH;
@@ -1137,7 +1137,7 @@ __global__ void __launch_bounds__(FT) finish_fused_kernel(In in1, Out out1, WS w
     finish_commit(in1, out1, ws1, 0, k, 0);
   }
   finish_plan(in2, out2, ws2, 1, k, enum_lanes, fixed_lane, windows_per_lane, lane_max, lane_max_w,
-              nullptr);
+              nullptr, false);  // its list only: the PMS workspace plans the chunks
   __syncthreads();
   finish_plan(in1, out1, ws1, 0, k, enum_lanes, fixed_lane, windows_per_lane, lane_max, lane_max_w,
               ws2.done);
