@@ -285,9 +285,18 @@ def main():
     import paper_2011_08373_b200 as gr
     from paper_2011_08373_b200 import multigpu
 
+    # functional check of the multi-rank code on one GPU (never a measurement):
+    # GR_BENCH_ONE_GPU=1 puts every rank on cuda:0 with the gloo backend --
+    # the ranks' kernels never wait on each other, only host collectives do
+    one_gpu = os.environ.get("GR_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     if a.config == "c5":
         return run_c5(a, rank, world, local, dev)
