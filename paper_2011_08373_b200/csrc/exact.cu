@@ -49,7 +49,9 @@ struct Ctrl {
   int n_active;       // instances listed for the running level
   int n_remaining;    // instances not finished (listed or waiting for their start level)
   u64 lane_cands;     // candidates per lane per chunk (L)
-  u64 pad1[4];
+  unsigned fin_ticket;  // finish: blocks done committing (the last one plans)
+  unsigned pad0;
+  u64 pad1[3];
 };
 
 #ifndef GR_JMAX
@@ -61,7 +63,7 @@ constexpr int HX = 16;         // HIT_j({x}) is 0 for x >= R_j, and R_j <= 16 fo
 
 struct Layout {
   size_t ctrl, meff, npr, nnr, kmax, ks, done, rb, sup, decided, bestx, bestw, wtot, lvlkey, sk, wr,
-      active, chunk_base, pk, hrec, total;
+      active, chunk_base, pk, hrec, ptmp, total;
 };
 
 Layout layout_of(const gr_batch *in) {
@@ -86,6 +88,7 @@ Layout layout_of(const gr_batch *in) {
   L.wr = take(4 * 64 * B);
   L.active = take(4 * 2 * B);
   L.chunk_base = take(8 * (B + 1));
+  L.ptmp = take(8 * B);
   L.pk = take(8 * (size_t)std::max<int64_t>(in->total_clauses, 1));
   L.hrec = take(16 * HREC * (size_t)std::max<int64_t>(in->total_clauses, 1));
   L.total = o;
@@ -101,6 +104,7 @@ struct WS {
   u32 *wr;
   int *active;
   u64 *chunk_base;
+  u64 *ptmp;       // finish scratch: level size per listed position (~0: not listed)
   u64 *pk, *hrec;  // packed clause masks; [clause][HREC] two-word H_j(P) records of the positives
 };
 
@@ -126,6 +130,7 @@ WS ws_of(const gr_batch *in, void *base) {
   w.wr = (u32 *)(p + L.wr);
   w.active = (int *)(p + L.active);
   w.chunk_base = (u64 *)(p + L.chunk_base);
+  w.ptmp = (u64 *)(p + L.ptmp);
   w.pk = (u64 *)(p + L.pk);
   w.hrec = (u64 *)(p + L.hrec);
   return w;
@@ -969,7 +974,7 @@ __device__ void finish_commit(const In &in, const Out &out, const WS &ws, int wh
   const int nact_in = k == 0 ? in.B : ws.ctrl->n_active;
   const int *cur = ws.active + (size_t)(k & 1) * in.B;  // list enumerated at level k
   {
-    for (int i = t; i < nact_in; i += FT) {
+    for (int i = blockIdx.x * FT + t; i < nact_in; i += gridDim.x * FT) {
       const int b = cur[i];
       if (ws.done[b]) continue;  // fused: listed for the other solve only
       const int me = ws.meff[b];
@@ -1034,51 +1039,67 @@ __device__ void finish_plan(const In &in, const Out &out, const WS &ws, int whic
   // start level is above k+1 wait, counted in n_remaining)
   const bool all = k == 0 || in.kstart != nullptr;
   const int n2 = all ? in.B : nact_in;
-  if (t == 0) { s_carry = 0; s_cnt = 0; s_wait = 0; }
-  __syncthreads();
-  for (int base = 0; base < n2; base += FT) {
-    const int i = base + t;
-    int b = -1;
-    if (i < n2) {
-      b = all ? i : cur[i];
-      if (ws.done[b] && (!done_other || done_other[b])) b = -1;
-      else if (k + 1 < ws.ks[b]) {
-        atomicAdd(&s_wait, 1);
-        b = -1;
-      }
-    }
-    u64 csz = 0;
-    if (b >= 0) {
+  // each thread takes a contiguous segment of the list (the loads of its
+  // instances are independent, one block scan for all): pass A decides and
+  // records each entry's level size (~0: not listed), pass B compacts
+  const u64 NOTL = ~0ull;
+  const int per = (n2 + FT - 1) / FT;
+  const int i0 = min(n2, t * per), i1 = min(n2, i0 + per);
+  u64 my_cnt = 0, my_sz = 0;
+  int my_wait = 0;
+  for (int i = i0; i < i1; i++) {
+    const int b = all ? i : cur[i];
+    u64 v = NOTL;
+    if (ws.done[b] && (!done_other || done_other[b])) {
+    } else if (k + 1 < ws.ks[b]) {
+      my_wait++;
+    } else {
       const int me = ws.meff[b];
       const u64 ck = binom(me, k + 1);
+      bool ok = true;
       if (weighted) {
         const int rb = bitlen(ck - 1);
         if (bitlen(ws.wtot[b]) + rb > 63) {  // key (W << rb | rank) would not fit
           ws.done[b] = 1;
           write_result(in, out, b, GR_UNSUPPORTED, 0, 0, 0, 0, ws.decided[b], which);
-          b = -1;
+          ok = false;
         } else {
           ws.rb[b] = rb;
         }
       }
-      if (b >= 0) {
+      if (ok) {
         ws.lvlkey[b] = GR_KEY_NONE;
-        csz = ck;
+        v = ck;
       }
     }
-    u64 flag = b >= 0 ? 1 : 0, pos, tot;
-    Scan(tmp).ExclusiveSum(flag, pos);
-    __syncthreads();
-    Scan(tmp).ExclusiveSum(csz, tot);
-    __syncthreads();
-    if (b >= 0) nxt[s_cnt + (int)pos] = b;
-    __syncthreads();
-    if (t == FT - 1) {
-      s_cnt += (int)(pos + flag);
-      s_carry += tot + csz;  // candidates of level k+1 (saturation is harmless: only sizes L)
+    ws.ptmp[i] = v;
+    if (v != NOTL) {
+      my_cnt++;
+      my_sz += v;  // candidates of level k+1 (wrap-around is harmless: only sizes L)
     }
-    __syncthreads();
   }
+  if (my_wait) atomicAdd(&s_wait, my_wait);
+  u64 pos, n_list;
+  Scan(tmp).ExclusiveSum(my_cnt, pos, n_list);
+  __syncthreads();
+  u64 szpos, sz_all;
+  Scan(tmp).ExclusiveSum(my_sz, szpos, sz_all);
+  __syncthreads();
+  {
+    u64 q = pos;
+    for (int i = i0; i < i1; i++) {
+      const u64 v = ws.ptmp[i];
+      if (v == NOTL) continue;
+      nxt[q] = all ? i : cur[i];
+      ws.chunk_base[q] = v;  // the level size; the plan below turns it into a prefix
+      q++;
+    }
+  }
+  if (t == 0) {
+    s_cnt = (int)n_list;
+    s_carry = sz_all;
+  }
+  __syncthreads();
   // lane window L: about 3 windows per lane of the enumeration grid, a power
   // of two in [256, 2^18] (weighted levels: 4 windows, at most 2^16)
   const u64 Lmax = weighted ? lane_max_w : lane_max;
@@ -1094,16 +1115,20 @@ __device__ void finish_plan(const In &in, const Out &out, const WS &ws, int whic
   __syncthreads();
   if (t == 0) s_carry = 0;
   __syncthreads();
-  for (int base = 0; plan_chunks && base < nact; base += FT) {
-    const int i = base + t;
-    u64 nch = 0;
-    if (i < nact) nch = (binom(ws.meff[nxt[i]], k + 1) + CH - 1) / CH;
-    u64 cpos;
-    Scan(tmp).ExclusiveSum(nch, cpos);
+  if (plan_chunks) {
+    const int per2 = (nact + FT - 1) / FT;
+    const int q0 = min(nact, t * per2), q1 = min(nact, q0 + per2);
+    u64 my_ch = 0;
+    for (int q = q0; q < q1; q++) my_ch += (ws.chunk_base[q] + CH - 1) / CH;
+    u64 cpos, ch_all;
+    Scan(tmp).ExclusiveSum(my_ch, cpos, ch_all);
     __syncthreads();
-    if (i < nact) ws.chunk_base[i] = s_carry + cpos;
-    __syncthreads();
-    if (t == FT - 1) s_carry += cpos + nch;
+    for (int q = q0; q < q1; q++) {
+      const u64 nch = (ws.chunk_base[q] + CH - 1) / CH;
+      ws.chunk_base[q] = cpos;
+      cpos += nch;
+    }
+    if (t == 0) s_carry = ch_all;
     __syncthreads();
   }
   if (t == 0) {
@@ -1116,19 +1141,31 @@ __device__ void finish_plan(const In &in, const Out &out, const WS &ws, int whic
   }
 }
 
-__global__ void __launch_bounds__(FT) finish_kernel(In in, Out out, WS ws, int which, int k,
+__global__ void __launch_bounds__(FT, 1) finish_kernel(In in, Out out, WS ws, int which, int k,
                                                     int exhaustive, int enum_lanes,
                                                     u64 fixed_lane, int windows_per_lane,
                                                     u64 lane_max, u64 lane_max_w,
                                                     const int *done_other) {
+  // the commit is per instance: every block takes a share; the last block to
+  // finish it plans the next level for all
   if (k > 0) finish_commit(in, out, ws, which, k, exhaustive);
+  if (gridDim.x > 1) {
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(&ws.ctrl->fin_ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (threadIdx.x == 0) ws.ctrl->fin_ticket = 0;
+  }
   finish_plan(in, out, ws, which, k, enum_lanes, fixed_lane, windows_per_lane, lane_max, lane_max_w,
               done_other);
 }
 
 // fused PMS (ws1) + MHS (ws2): both commits, then the MHS list, then the PMS
 // plan over the union -- one launch per level
-__global__ void __launch_bounds__(FT) finish_fused_kernel(In in1, Out out1, WS ws1, In in2, Out out2,
+__global__ void __launch_bounds__(FT, 1) finish_fused_kernel(In in1, Out out1, WS ws1, In in2, Out out2,
                                                           WS ws2, int k, int enum_lanes,
                                                           u64 fixed_lane, int windows_per_lane,
                                                           u64 lane_max, u64 lane_max_w) {
@@ -1244,7 +1281,8 @@ int *pinned_i32() {
 namespace {
 int launch_finish(const gr_batch *in, int which, const gr_result *out, const WS &w, int k,
                   cudaStream_t st, const int *done_other) {
-  GR_LAUNCH("finish_kernel", st, finish_kernel<<<1, FT, 0, st>>>(in_of(in, which), out_of(out), w, which, k,
+  const int fgrid = k > 0 ? std::max(1, std::min((in->B + FT - 1) / FT, 64)) : 1;
+  GR_LAUNCH("finish_kernel", st, finish_kernel<<<fgrid, FT, 0, st>>>(in_of(in, which), out_of(out), w, which, k,
                                    (in->flags & GR_FLAG_EXHAUSTIVE) ? 1 : 0, enum_grid() * NT, lane_cands(), windows_per_lane(false) | (windows_per_lane(true) << 16),
                                    lane_max(false), lane_max(true), done_other));
   return GR_OK;
@@ -1333,7 +1371,8 @@ extern "C" int gr_exact_finish(const gr_batch *in, int which, int k, gr_result *
   if (k < 1 || k > 64) { gr_set_error("bad level"); return GR_EINVAL; }
   WS w = ws_of(in, ws);
   cudaStream_t st = (cudaStream_t)s;
-  GR_LAUNCH("finish_kernel", (cudaStream_t)s, finish_kernel<<<1, FT, 0, st>>>(in_of(in, which), out_of(out), w, which, k,
+  const int fgrid = std::max(1, std::min((in->B + FT - 1) / FT, 64));
+  GR_LAUNCH("finish_kernel", (cudaStream_t)s, finish_kernel<<<fgrid, FT, 0, st>>>(in_of(in, which), out_of(out), w, which, k,
                                    (in->flags & GR_FLAG_EXHAUSTIVE) ? 1 : 0, enum_grid() * NT, lane_cands(), windows_per_lane(false) | (windows_per_lane(true) << 16),
                                    lane_max(false), lane_max(true), nullptr));
   if (n_active) {
