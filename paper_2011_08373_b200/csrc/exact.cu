@@ -968,13 +968,13 @@ __device__ __forceinline__ int bitlen(u64 x) { return x ? 64 - __clzll((long lon
 
 // phase 1 of the finish: commit level k of every listed instance
 __device__ void finish_commit(const In &in, const Out &out, const WS &ws, int which, int k,
-                              int exhaustive) {
+                              int exhaustive, int part, int nparts) {
   const int t = threadIdx.x;
   const bool weighted = in.w != nullptr;
   const int nact_in = k == 0 ? in.B : ws.ctrl->n_active;
   const int *cur = ws.active + (size_t)(k & 1) * in.B;  // list enumerated at level k
   {
-    for (int i = blockIdx.x * FT + t; i < nact_in; i += gridDim.x * FT) {
+    for (int i = part * FT + t; i < nact_in; i += nparts * FT) {
       const int b = cur[i];
       if (ws.done[b]) continue;  // fused: listed for the other solve only
       const int me = ws.meff[b];
@@ -1148,7 +1148,7 @@ __global__ void __launch_bounds__(FT, 1) finish_kernel(In in, Out out, WS ws, in
                                                     const int *done_other) {
   // the commit is per instance: every block takes a share; the last block to
   // finish it plans the next level for all
-  if (k > 0) finish_commit(in, out, ws, which, k, exhaustive);
+  if (k > 0) finish_commit(in, out, ws, which, k, exhaustive, blockIdx.x, gridDim.x);
   if (gridDim.x > 1) {
     __shared__ int s_last;
     __threadfence();
@@ -1169,9 +1169,21 @@ __global__ void __launch_bounds__(FT, 1) finish_fused_kernel(In in1, Out out1, W
                                                           WS ws2, int k, int enum_lanes,
                                                           u64 fixed_lane, int windows_per_lane,
                                                           u64 lane_max, u64 lane_max_w) {
+  // blocks [0, P) commit the PMS, [P, 2P) the MHS; the last block plans
+  const int P = gridDim.x / 2;
   if (k > 0) {
-    finish_commit(in2, out2, ws2, 1, k, 0);
-    finish_commit(in1, out1, ws1, 0, k, 0);
+    if ((int)blockIdx.x < P) finish_commit(in1, out1, ws1, 0, k, 0, blockIdx.x, P);
+    else finish_commit(in2, out2, ws2, 1, k, 0, blockIdx.x - P, P);
+  }
+  {
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(&ws1.ctrl->fin_ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (threadIdx.x == 0) ws1.ctrl->fin_ticket = 0;
   }
   finish_plan(in2, out2, ws2, 1, k, enum_lanes, fixed_lane, windows_per_lane, lane_max, lane_max_w,
               nullptr, false);  // its list only: the PMS workspace plans the chunks
@@ -1474,7 +1486,8 @@ extern "C" int gr_solve_pms_mhs(const gr_batch *in, gr_result *out_pms, gr_resul
           GR_LAUNCH("enum_kernel", st, enum_kernel<true><<<grid, NT, ENUM_SMEM, st>>>(p));
         else
           GR_LAUNCH("enum_kernel", st, enum_kernel<false><<<grid, NT, ENUM_SMEM, st>>>(p));
-        GR_LAUNCH("finish_kernel", st, finish_fused_kernel<<<1, FT, 0, st>>>(
+        const int P = std::max(1, std::min((in->B + FT - 1) / FT, 32));
+        GR_LAUNCH("finish_kernel", st, finish_fused_kernel<<<2 * P, FT, 0, st>>>(
                                            in_of(in, 0), out_of(out_pms), w1, in_of(in, 1),
                                            out_of(out_mhs), w2, k, enum_grid() * NT, lane_cands(),
                                            windows_per_lane(false) | (windows_per_lane(true) << 16),
