@@ -581,7 +581,7 @@ __device__ __forceinline__ bool refuted(int j, M U, int e, const Clauses<M> &c, 
 template <typename M, int MODE, bool COUNT>
 __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const u32 *w, int rb,
                     int prune, Work &wk, const u64 *skj = nullptr, u64 wstar = ~0ull,
-                    int need_p = 1, int need_m = 0, i64 *best_m = nullptr) {
+                    int need_p = 1, int need_m = 0, i64 *best_m = nullptr, bool exh = false) {
   // MODE 3 (PMS and MHS of one instance in one walk): the first witness of
   // phi (returned) and of phi+ alone (*best_m), each only while needed
   i64 dummy = GR_KEY_NONE;
@@ -704,7 +704,7 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
             wp = false;
           }
         }
-        if (!wp && !wm) return best;
+        if (!wp && !wm && !exh) return best;  // exhaustive: the level is walked in full
         F = F2{0ull, 0ull};
       } else {
         F = test_sub<M, COUNT>(j, U, ea, F, c, wk);
@@ -915,15 +915,15 @@ __global__ void __launch_bounds__(NT, COUNT ? 1 : ENUM_CTAS) enum_kernel(EnumPar
         if (narrow) {
           Clauses<u32> c{(const u32 *)sP, sH, hitx, lowb, reg, nb, cs, np, nn};
           key = walk<u32, 3, COUNT>(p.k, me, r_lo, cnt, c, s_w, rb, p.prune, wk, nullptr, ~0ull,
-                                    nq, nm, &key_m);
+                                    nq, nm, &key_m, p.exhaustive);
         } else if (staged) {
           Clauses<u64> c{sP, sH, hitx, lowb, reg, nb, cs, np, nn};
           key = walk<u64, 3, COUNT>(p.k, me, r_lo, cnt, c, s_w, rb, p.prune, wk, nullptr, ~0ull,
-                                    nq, nm, &key_m);
+                                    nq, nm, &key_m, p.exhaustive);
         } else {
           Clauses<u64> c{p.ws.pk + lo, (const F2 *)p.ws.hrec + lo * HREC, hitx, lowb, reg, nb, cs, np, nn};
           key = walk<u64, 3, COUNT>(p.k, me, r_lo, cnt, c, s_w, rb, p.prune, wk, nullptr, ~0ull,
-                                    nq, nm, &key_m);
+                                    nq, nm, &key_m, p.exhaustive);
         }
       } else if (narrow) {
         Clauses<u32> c{(const u32 *)sP, sH, hitx, lowb, reg, nb, cs, np, nn};
@@ -1166,14 +1166,14 @@ __global__ void __launch_bounds__(FT, 1) finish_kernel(In in, Out out, WS ws, in
 // fused PMS (ws1) + MHS (ws2): both commits, then the MHS list, then the PMS
 // plan over the union -- one launch per level
 __global__ void __launch_bounds__(FT, 1) finish_fused_kernel(In in1, Out out1, WS ws1, In in2, Out out2,
-                                                          WS ws2, int k, int enum_lanes,
+                                                          WS ws2, int k, int exhaustive, int enum_lanes,
                                                           u64 fixed_lane, int windows_per_lane,
                                                           u64 lane_max, u64 lane_max_w) {
   // blocks [0, P) commit the PMS, [P, 2P) the MHS; the last block plans
   const int P = gridDim.x / 2;
   if (k > 0) {
-    if ((int)blockIdx.x < P) finish_commit(in1, out1, ws1, 0, k, 0, blockIdx.x, P);
-    else finish_commit(in2, out2, ws2, 1, k, 0, blockIdx.x - P, P);
+    if ((int)blockIdx.x < P) finish_commit(in1, out1, ws1, 0, k, exhaustive, blockIdx.x, P);
+    else finish_commit(in2, out2, ws2, 1, k, exhaustive, blockIdx.x - P, P);
   }
   {
     __shared__ int s_last;
@@ -1451,7 +1451,7 @@ extern "C" int gr_solve_pms_mhs(const gr_batch *in, gr_result *out_pms, gr_resul
   const size_t half = align256(layout_of(in).total);
   if (!ws || ws_bytes < 2 * half) { gr_set_error("workspace too small (2 x gr_workspace_bytes)"); return GR_EWORKSPACE; }
   void *ws1 = ws, *ws2 = (char *)ws + half;
-  if (!in->w && !in->k_start && !(in->flags & GR_FLAG_EXHAUSTIVE) && !getenv("GR_NO_FUSE")) {
+  if (!in->w && !in->k_start && !getenv("GR_NO_FUSE")) {
     // unit weights: one walk decides both -- the MHS is phi+'s part of the
     // PMS test (MODE 3); the PMS workspace plans the union of both searches
     if (!out_pms || !out_mhs) { gr_set_error("null result"); return GR_EINVAL; }
@@ -1477,7 +1477,7 @@ extern "C" int gr_solve_pms_mhs(const gr_batch *in, gr_result *out_pms, gr_resul
         p.off = in->off;
         p.k = k;
         p.weighted = 0;
-        p.exhaustive = 0;
+        p.exhaustive = (in->flags & GR_FLAG_EXHAUSTIVE) ? 1 : 0;
         p.prune = (in->flags & GR_FLAG_NO_PRUNE) ? 0 : 1;
         p.shard = 0;
         p.nshard = 1;
@@ -1489,7 +1489,8 @@ extern "C" int gr_solve_pms_mhs(const gr_batch *in, gr_result *out_pms, gr_resul
         const int P = std::max(1, std::min((in->B + FT - 1) / FT, 32));
         GR_LAUNCH("finish_kernel", st, finish_fused_kernel<<<2 * P, FT, 0, st>>>(
                                            in_of(in, 0), out_of(out_pms), w1, in_of(in, 1),
-                                           out_of(out_mhs), w2, k, enum_grid() * NT, lane_cands(),
+                                           out_of(out_mhs), w2, k,
+                                           (in->flags & GR_FLAG_EXHAUSTIVE) ? 1 : 0, enum_grid() * NT, lane_cands(),
                                            windows_per_lane(false) | (windows_per_lane(true) << 16),
                                            lane_max(false), lane_max(true)));
       }

@@ -695,3 +695,19 @@ def test_pms_mhs_fused_matches_separate(case):
         o = oracle.batch("pms", cb)
         keep = o.status != -1
         assert (p["status"][keep] == o.status[keep]).all()
+
+
+@pytest.mark.parametrize("which_cb", ["c2", "c3", "fuzz"])
+def test_pms_mhs_fused_exhaustive(which_cb):
+    """The fused walk with GR_FLAG_EXHAUSTIVE (witness level walked in full)
+    = the separate exhaustive solvers, decided counts included."""
+    cb = {"c2": lambda: synth.c2_batch(), "c3": lambda: synth.c3_instance()[0],
+          "fuzz": lambda: rand_batch(11, 300, 20, 24)}[which_cb]()
+    db = gr.DeviceBatch.from_host(cb, weighted=False, flags=gr.GR_FLAG_EXHAUSTIVE)
+    p, h = gr.solve_pms_mhs(db)
+    p, h = p.to_host(), h.to_host()
+    rp = gpu_solve(cb, "pms", flags=gr.GR_FLAG_EXHAUSTIVE)
+    rh = gpu_solve(cb, "mhs", flags=gr.GR_FLAG_EXHAUSTIVE)
+    for f in ("status", "assign", "cost", "decided"):
+        assert (p[f] == rp[f]).all(), ("pms", f)
+        assert (h[f] == rh[f]).all(), ("mhs", f)
