@@ -397,7 +397,7 @@ def main():
             e0.record(stream)
             dbx = device_batch(hb, cb, dev, flags)
             step(dbx, outs)
-            host = [o.to_host() for o in outs]
+            host = gr.to_host_many(outs)
             e1.record(stream)
             e1.synchronize()
             if s >= a.warmup:

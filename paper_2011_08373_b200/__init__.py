@@ -14,5 +14,5 @@ from ._native import (  # noqa: F401
     PMS, GREEDY, DeviceBatch, DeviceBitMatrix, DeviceResult, ExactSession, GrError,
     bitmatrix_ld, greedy_count_shard, lib, mhs_exact, mhs_greedy, mhs_greedy_matrix,
     pack_bitmatrix, solve_pms, version, launch_count, profiler, Profiler, solve,
-    GR_STRATEGY_MHS, GR_STRATEGY_MAXSAT, solve_pms_mhs, GreedyShard, GreedyMatrixResult,
+    GR_STRATEGY_MHS, GR_STRATEGY_MAXSAT, solve_pms_mhs, GreedyShard, to_host_many, GreedyMatrixResult,
 )

@@ -221,12 +221,32 @@ class DeviceResult:
 
     def to_host(self):
         """-> dict of numpy arrays (assign/cost/decided as uint64)."""
-        return {
-            "assign": self.assign.cpu().numpy().view(np.uint64),
-            "cost": self.cost.cpu().numpy().view(np.uint64),
-            "status": self.status.cpu().numpy(),
-            "decided": self.decided.cpu().numpy().view(np.uint64),
-        }
+        return to_host_many([self])[0]
+
+
+def to_host_many(results):
+    """Several DeviceResults -> dicts of numpy arrays with one synchronisation:
+    every field is copied (non-blocking) into pinned host memory on the
+    current stream, then the stream is synchronised once."""
+    torch = _torch()
+    pend = []
+    for r in results:
+        d = {}
+        for k in ("assign", "cost", "status", "decided"):
+            t = getattr(r, k)
+            h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+            h.copy_(t, non_blocking=True)
+            d[k] = h
+        pend.append(d)
+    if results:
+        torch.cuda.current_stream(results[0].status.device).synchronize()
+    out = []
+    for d in pend:
+        out.append({"assign": d["assign"].numpy().view(np.uint64),
+                    "cost": d["cost"].numpy().view(np.uint64),
+                    "status": d["status"].numpy(),
+                    "decided": d["decided"].numpy().view(np.uint64)})
+    return out
 
 
 _ws_cache = {}
