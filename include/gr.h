@@ -139,10 +139,12 @@ int gr_solve_pms(const gr_batch *in, gr_result *out, void *ws, size_t ws_bytes, 
  * status GR_SAT_NEG_VIOLATED flags that the canonical MHS breaks phi-. */
 int gr_mhs_exact(const gr_batch *in, gr_result *out, void *ws, size_t ws_bytes, gr_stream_t s);
 
-/* (a) + (b) of one batch at once: the PMS and MHS level loops run interleaved
- * on two streams (their small levels and level tails overlap).  ws_bytes >=
- * 2 * gr_workspace_bytes(in, 0) (+256).  Synchronises both streams; results
- * are identical to gr_solve_pms / gr_mhs_exact. */
+/* (a) + (b) of one batch at once.  Unit weights (w == NULL, no k_start): one
+ * enumeration decides both -- the MHS is phi+'s part of the PMS clause test --
+ * on s_pms, and s_mhs waits for it.  Otherwise the PMS and MHS level loops
+ * run interleaved on the two streams.  ws_bytes >= 2 * gr_workspace_bytes(in,
+ * 0) (+256).  Results (status, assignment, cost, decided) are identical to
+ * gr_solve_pms / gr_mhs_exact. */
 int gr_solve_pms_mhs(const gr_batch *in, gr_result *out_pms, gr_result *out_mhs, void *ws,
                      size_t ws_bytes, gr_stream_t s_pms, gr_stream_t s_mhs);
 

@@ -383,19 +383,20 @@ __global__ void __launch_bounds__(PT) pack_kernel(In in, Out out, WS ws, int whi
 // elements.  All candidates sharing U form one contiguous rank block, S
 // ranging over the J-subsets of [0, min U) in colex order.  Recursively,
 //   node(j, U, e, base) = part A: the j-subsets of [0, min(e, R_j))   (one
-//                                 sub-block, <= 64 candidates)
+//                                 sub-block, <= 128 candidates)
 //                         part B: for t in [R_j, e): node(j-1, U | {t}, t,
 //                                 base + C(t, j))
-// where R_j is the largest R with C(R, j) <= 64 (R_1 = 64, R_2 = 11, R_3 = 8,
-// R_4 = 7, R_5 = 8).  A sub-block's candidates are the bits of one 64-bit
-// mask F whose bit index is the colex offset idx_j(S) = sum_i C(s_i, i), so
-// rank = base + bit.  A positive clause P missed by U keeps the candidates
+// where R_j is the largest R with C(R, j) <= 128 (R = 64, 16, 10, 9, 9, 9, 10,
+// 10, 11, 12 for j = 1..10).  A sub-block's candidates are the bits of one
+// two-word mask F whose bit index is the colex offset idx_j(S) = sum_i
+// C(s_i, i), so rank = base + bit.  A positive clause P missed by U keeps the candidates
 // that meet P: F &= H_j(P), H_j(P) = {j-subsets of [0, R_j) meeting P}
 // (precomputed per clause by the pack; H_1(P) = P).  A negative clause N
 // whose variables outside the region all lie in U kills the S that contain
 // N's region part.  Each lane visits one sub-block per loop iteration (a flat
 // depth-first iterator over the node tree), so the lanes of a warp run the
-// same clause-test code in lock step.
+// same clause-test code in lock step.  An inner node's whole subtree is
+// first checked for a refutation by one clause scan (refuted_by).
 
 __device__ __forceinline__ F2 f2_and(F2 a, F2 b) { return F2{a.lo & b.lo, a.hi & b.hi}; }
 __device__ __forceinline__ F2 f2_andnot(F2 a, F2 b) { return F2{a.lo & ~b.lo, a.hi & ~b.hi}; }
@@ -1442,8 +1443,9 @@ extern "C" int gr_solve_pms(const gr_batch *in, gr_result *out, void *ws, size_t
   return solve_exact(in, out, ws, ws_bytes, s, 0);
 }
 
-// PMS and MHS of one batch with their level loops interleaved on two streams
-// (the small levels and level tails of one overlap the other's work).
+// PMS and MHS of one batch: unit weights -> one fused walk (MODE 3) on s_pms;
+// otherwise their level loops interleaved on two streams (the small levels
+// and level tails of one overlap the other's work).
 extern "C" int gr_solve_pms_mhs(const gr_batch *in, gr_result *out_pms, gr_result *out_mhs,
                                 void *ws, size_t ws_bytes, gr_stream_t s_pms, gr_stream_t s_mhs) {
   int rc = validate_batch(in, 0);
