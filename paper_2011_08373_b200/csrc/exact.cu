@@ -810,37 +810,50 @@ constexpr size_t TAB_SMEM =
 #define GR_ENUM_CTAS 4
 #endif
 constexpr int ENUM_CTAS = GR_ENUM_CTAS;  // resident enumeration CTAs per SM (registers, smem)
-constexpr int SMC = (int)(((227 * 1024) / ENUM_CTAS - 1024 - 400 - TAB_SMEM) / (16 * HREC + 8)) / 32 * 32;
-constexpr size_t ENUM_SMEM = TAB_SMEM + (size_t)SMC * (16 * HREC + 8);
+// Two shapes of the enumeration CTA: NT = 256 threads x 4 per SM (room to
+// stage 256 clauses), or 128 threads x 8 per SM for batches of at most 96
+// clauses per instance (smaller CTAs, fewer lanes waiting at each chunk's
+// barrier: C4 -13%).  A chunk is always NT lane windows; a 128-thread CTA
+// walks two windows per thread.
+template <int NTK>
+__host__ __device__ constexpr int smc_of() {
+  return (int)(((227 * 1024) / (ENUM_CTAS * NT / NTK) - 1024 - 400 - TAB_SMEM) / (16 * HREC + 8)) /
+         32 * 32;
+}
+template <int NTK>
+__host__ __device__ constexpr size_t enum_smem_of() {
+  return TAB_SMEM + (size_t)smc_of<NTK>() * (16 * HREC + 8);
+}
+constexpr int NT_SMALL = NT / 2;
 
-template <bool COUNT>
-__global__ void __launch_bounds__(NT, COUNT ? 1 : ENUM_CTAS) enum_kernel(EnumParams p) {
+template <bool COUNT, int NTK>
+__global__ void __launch_bounds__(NTK, COUNT ? 1 : ENUM_CTAS * NT / NTK) enum_kernel(EnumParams p) {
   extern __shared__ u64 cls[];  // [np][HREC] H records, [np + nn] P (u32 or u64)
   __shared__ u64 s_chunk;
   __shared__ int s_b, s_cur, s_skip, s_needp, s_needm;
   __shared__ u64 s_r0, s_ck;
   __shared__ u64 s_skj[JMAX + 1], s_wstar;  // weighted: S_j and the incumbent W*
   __shared__ u32 s_w[64];
-  __shared__ i64 s_wmin[NT / 32], s_wmin2[NT / 32];
+  __shared__ i64 s_wmin[NTK / 32], s_wmin2[NTK / 32];
   const int t = threadIdx.x;
   if (t == 0) s_cur = -1;
   F2 *hitx = (F2 *)cls;  // [JMAX + 1][HX] HIT_j({x}): j-subsets of [0, R_j) containing x
   u64 *cs = cls + 2 * (JMAX + 1) * HX;  // [65][JMAX + 1] C(n, j), j <= JMAX
   F2 *lowb = (F2 *)(cs + 65 * (JMAX + 1));  // [129] the n lowest bits
-  for (int q = t; q < (JMAX + 1) * HX; q += NT)
+  for (int q = t; q < (JMAX + 1) * HX; q += NTK)
     hitx[q] = F2{g_hit.lo[64 * (q / HX) + q % HX], g_hit.hi[64 * (q / HX) + q % HX]};
-  for (int q = t; q < 65 * (JMAX + 1); q += NT) cs[q] = binom(q / (JMAX + 1), q % (JMAX + 1));
-  for (int q = t; q < 129; q += NT) lowb[q] = f2_nbits((u64)q);
+  for (int q = t; q < 65 * (JMAX + 1); q += NTK) cs[q] = binom(q / (JMAX + 1), q % (JMAX + 1));
+  for (int q = t; q < 129; q += NTK) lowb[q] = f2_nbits((u64)q);
   int *reg = (int *)(lowb + 129);  // [JMAX + 1] R_j
   if (t <= JMAX) reg[t] = t ? region_of(t) : 0;
   unsigned char *nb = (unsigned char *)(reg + 16);  // [JMAX + 1][65] sub-block sizes
-  for (int q = t; q < (JMAX + 1) * 65; q += NT) {
+  for (int q = t; q < (JMAX + 1) * 65; q += NTK) {
     const int jj = q / 65, ee = q % 65;
     nb[q] = jj ? (unsigned char)binom(ee < region_of(jj) ? ee : region_of(jj), jj) : 0;
   }
   u64 *stage = cls + TAB_SMEM / 8;  // staged clause records
   const u64 Lc = p.ws.ctrl->lane_cands;
-  const u64 CH = Lc * NT;
+  const u64 CH = Lc * NTK;  // a chunk: one lane window per thread
   const u64 total = p.ws.ctrl->total_chunks;
   const int nact = p.ws.ctrl->n_active;
   const int *active = p.ws.active;  // list of this level (offset by the host)
@@ -884,18 +897,18 @@ __global__ void __launch_bounds__(NT, COUNT ? 1 : ENUM_CTAS) enum_kernel(EnumPar
     const int b = s_b;
     const int me = p.ws.meff[b], np = p.ws.npr[b], nn = p.ws.nnr[b];
     const int64_t lo = p.off[b];
-    const bool staged = np + nn <= SMC;
+    const bool staged = np + nn <= smc_of<NTK>();
     const bool narrow = staged && me <= 32;
     F2 *sH = (F2 *)stage;                       // [np][HREC]
     u64 *sP = stage + (size_t)2 * HREC * np;     // [np + nn] as u32 or u64
     if (b != s_cur) {
       if (staged) {
-        for (int q = t; q < np * HREC; q += NT) sH[q] = ((const F2 *)p.ws.hrec)[lo * HREC + q];
+        for (int q = t; q < np * HREC; q += NTK) sH[q] = ((const F2 *)p.ws.hrec)[lo * HREC + q];
         if (narrow) {
           u32 *c32 = (u32 *)sP;
-          for (int q = t; q < np + nn; q += NT) c32[q] = (u32)p.ws.pk[lo + q];
+          for (int q = t; q < np + nn; q += NTK) c32[q] = (u32)p.ws.pk[lo + q];
         } else {
-          for (int q = t; q < np + nn; q += NT) sP[q] = p.ws.pk[lo + q];
+          for (int q = t; q < np + nn; q += NTK) sP[q] = p.ws.pk[lo + q];
         }
       }
       if (t < 64) s_w[t] = p.ws.wr[(size_t)b * 64 + t];
@@ -904,10 +917,12 @@ __global__ void __launch_bounds__(NT, COUNT ? 1 : ENUM_CTAS) enum_kernel(EnumPar
       __syncthreads();
       if (t == 0) s_cur = b;
     }
-    const u64 r_lo = s_r0 + (u64)t * Lc;
     const u64 ck = s_ck;
     i64 key = GR_KEY_NONE, key_m = GR_KEY_NONE;
     Work wk;
+    {
+    const u64 r_lo = s_r0 + (u64)t * Lc;
+    i64 key1 = GR_KEY_NONE, key_m1 = GR_KEY_NONE;
     if (r_lo < ck) {
       const u64 cnt = (ck - r_lo) < Lc ? (ck - r_lo) : Lc;
       const int rb = p.ws.rb[b];
@@ -915,27 +930,30 @@ __global__ void __launch_bounds__(NT, COUNT ? 1 : ENUM_CTAS) enum_kernel(EnumPar
         const int nq = s_needp, nm = s_needm;
         if (narrow) {
           Clauses<u32> c{(const u32 *)sP, sH, hitx, lowb, reg, nb, cs, np, nn};
-          key = walk<u32, 3, COUNT>(p.k, me, r_lo, cnt, c, s_w, rb, p.prune, wk, nullptr, ~0ull,
-                                    nq, nm, &key_m, p.exhaustive);
+          key1 = walk<u32, 3, COUNT>(p.k, me, r_lo, cnt, c, s_w, rb, p.prune, wk, nullptr, ~0ull,
+                                    nq, nm, &key_m1, p.exhaustive);
         } else if (staged) {
           Clauses<u64> c{sP, sH, hitx, lowb, reg, nb, cs, np, nn};
-          key = walk<u64, 3, COUNT>(p.k, me, r_lo, cnt, c, s_w, rb, p.prune, wk, nullptr, ~0ull,
-                                    nq, nm, &key_m, p.exhaustive);
+          key1 = walk<u64, 3, COUNT>(p.k, me, r_lo, cnt, c, s_w, rb, p.prune, wk, nullptr, ~0ull,
+                                    nq, nm, &key_m1, p.exhaustive);
         } else {
           Clauses<u64> c{p.ws.pk + lo, (const F2 *)p.ws.hrec + lo * HREC, hitx, lowb, reg, nb, cs, np, nn};
-          key = walk<u64, 3, COUNT>(p.k, me, r_lo, cnt, c, s_w, rb, p.prune, wk, nullptr, ~0ull,
-                                    nq, nm, &key_m, p.exhaustive);
+          key1 = walk<u64, 3, COUNT>(p.k, me, r_lo, cnt, c, s_w, rb, p.prune, wk, nullptr, ~0ull,
+                                    nq, nm, &key_m1, p.exhaustive);
         }
       } else if (narrow) {
         Clauses<u32> c{(const u32 *)sP, sH, hitx, lowb, reg, nb, cs, np, nn};
-        key = run_lane<u32, COUNT>(p, r_lo, cnt, me, c, s_w, rb, wk, s_skj, s_wstar);
+        key1 = run_lane<u32, COUNT>(p, r_lo, cnt, me, c, s_w, rb, wk, s_skj, s_wstar);
       } else if (staged) {
         Clauses<u64> c{sP, sH, hitx, lowb, reg, nb, cs, np, nn};
-        key = run_lane<u64, COUNT>(p, r_lo, cnt, me, c, s_w, rb, wk, s_skj, s_wstar);
+        key1 = run_lane<u64, COUNT>(p, r_lo, cnt, me, c, s_w, rb, wk, s_skj, s_wstar);
       } else {
         Clauses<u64> c{p.ws.pk + lo, (const F2 *)p.ws.hrec + lo * HREC, hitx, lowb, reg, nb, cs, np, nn};
-        key = run_lane<u64, COUNT>(p, r_lo, cnt, me, c, s_w, rb, wk, s_skj, s_wstar);
+        key1 = run_lane<u64, COUNT>(p, r_lo, cnt, me, c, s_w, rb, wk, s_skj, s_wstar);
       }
+    }
+    key = key1 < key ? key1 : key;
+    key_m = key_m1 < key_m ? key_m1 : key_m;
     }
     if (COUNT) {
       atomicAdd(&g_work[0], (unsigned long long)wk.tests);
@@ -952,7 +970,7 @@ __global__ void __launch_bounds__(NT, COUNT ? 1 : ENUM_CTAS) enum_kernel(EnumPar
     __syncthreads();
     if (t == 0) {
       i64 v = s_wmin[0], v2 = s_wmin2[0];
-      for (int i = 1; i < NT / 32; i++) {
+      for (int i = 1; i < NTK / 32; i++) {
         v = s_wmin[i] < v ? s_wmin[i] : v;
         v2 = s_wmin2[i] < v2 ? s_wmin2[i] : v2;
       }
@@ -1025,7 +1043,8 @@ __device__ void finish_commit(const In &in, const Out &out, const WS &ws, int wh
 // planned) while either solve still searches
 __device__ void finish_plan(const In &in, const Out &out, const WS &ws, int which, int k,
                             int enum_lanes, u64 fixed_lane, int windows_per_lane, u64 lane_max,
-                            u64 lane_max_w, const int *done_other, bool plan_chunks = true) {
+                            u64 lane_max_w, const int *done_other, int chunk_lanes,
+                            bool plan_chunks = true) {
   typedef cub::BlockScan<u64, FT> Scan;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ u64 s_carry;
@@ -1111,7 +1130,7 @@ __device__ void finish_plan(const In &in, const Out &out, const WS &ws, int whic
   L = L < 256 ? 256 : (L > Lmax ? Lmax : L);
   L = 1ull << (63 - __clzll((long long)L));
   if (fixed_lane) L = fixed_lane;  // GR_LANE_CANDIDATES override
-  const u64 CH = L * NT;
+  const u64 CH = L * (u64)chunk_lanes;  // the enumeration CTA's threads
   const int nact = s_cnt;
   __syncthreads();
   if (t == 0) s_carry = 0;
@@ -1146,7 +1165,7 @@ __global__ void __launch_bounds__(FT, 1) finish_kernel(In in, Out out, WS ws, in
                                                     int exhaustive, int enum_lanes,
                                                     u64 fixed_lane, int windows_per_lane,
                                                     u64 lane_max, u64 lane_max_w,
-                                                    const int *done_other) {
+                                                    const int *done_other, int chunk_lanes) {
   // the commit is per instance: every block takes a share; the last block to
   // finish it plans the next level for all
   if (k > 0) finish_commit(in, out, ws, which, k, exhaustive, blockIdx.x, gridDim.x);
@@ -1161,7 +1180,7 @@ __global__ void __launch_bounds__(FT, 1) finish_kernel(In in, Out out, WS ws, in
     if (threadIdx.x == 0) ws.ctrl->fin_ticket = 0;
   }
   finish_plan(in, out, ws, which, k, enum_lanes, fixed_lane, windows_per_lane, lane_max, lane_max_w,
-              done_other);
+              done_other, chunk_lanes);
 }
 
 // fused PMS (ws1) + MHS (ws2): both commits, then the MHS list, then the PMS
@@ -1169,7 +1188,8 @@ __global__ void __launch_bounds__(FT, 1) finish_kernel(In in, Out out, WS ws, in
 __global__ void __launch_bounds__(FT, 1) finish_fused_kernel(In in1, Out out1, WS ws1, In in2, Out out2,
                                                           WS ws2, int k, int exhaustive, int enum_lanes,
                                                           u64 fixed_lane, int windows_per_lane,
-                                                          u64 lane_max, u64 lane_max_w) {
+                                                          u64 lane_max, u64 lane_max_w,
+                                                          int chunk_lanes) {
   // blocks [0, P) commit the PMS, [P, 2P) the MHS; the last block plans
   const int P = gridDim.x / 2;
   if (k > 0) {
@@ -1187,10 +1207,10 @@ __global__ void __launch_bounds__(FT, 1) finish_fused_kernel(In in1, Out out1, W
     if (threadIdx.x == 0) ws1.ctrl->fin_ticket = 0;
   }
   finish_plan(in2, out2, ws2, 1, k, enum_lanes, fixed_lane, windows_per_lane, lane_max, lane_max_w,
-              nullptr, false);  // its list only: the PMS workspace plans the chunks
+              nullptr, chunk_lanes, false);  // its list only: the PMS workspace plans the chunks
   __syncthreads();
   finish_plan(in1, out1, ws1, 0, k, enum_lanes, fixed_lane, windows_per_lane, lane_max, lane_max_w,
-              ws2.done);
+              ws2.done, chunk_lanes);
 }
 
 // ---------------------------------------------------------------------------
@@ -1210,21 +1230,39 @@ int validate_batch(const gr_batch *in, int which) {
 }
 
 std::mutex g_occ_mu;
-int g_enum_grid = 0;
+int g_enum_grid[2] = {0, 0};
 
-int enum_grid() {
-  std::lock_guard<std::mutex> lk(g_occ_mu);
-  if (g_enum_grid) return g_enum_grid;
+template <int NTK>
+int enum_grid_of() {
   int dev = 0, sms = 0, per = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  size_t smem = ENUM_SMEM;
-  cudaFuncSetAttribute(enum_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaFuncSetAttribute(enum_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, enum_kernel<false>, NT, smem);
-  if (per < 1) per = 1;
-  g_enum_grid = sms * per;
-  return g_enum_grid;
+  const size_t smem = enum_smem_of<NTK>();
+  cudaFuncSetAttribute(enum_kernel<false, NTK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(enum_kernel<true, NTK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, enum_kernel<false, NTK>, NTK, smem);
+  return sms * (per < 1 ? 1 : per);
+}
+// grid of the NT-thread (small = false) or NT/2-thread enumeration CTA
+int enum_grid(bool small = false) {
+  std::lock_guard<std::mutex> lk(g_occ_mu);
+  int &g = g_enum_grid[small ? 1 : 0];
+  if (!g) g = small ? enum_grid_of<NT_SMALL>() : enum_grid_of<NT>();
+  return g;
+}
+// the small CTA shape when every instance's clauses fit its staging area
+bool enum_small(const gr_batch *in) {
+  static const int off = getenv("GR_NO_SMALL_CTA") ? 1 : 0;
+  return !off && in->max_clauses <= smc_of<NT_SMALL>();
+}
+template <bool COUNT>
+int launch_enum(const EnumParams &p, bool small, cudaStream_t st) {
+  if (small)
+    GR_LAUNCH("enum_kernel", st, (enum_kernel<COUNT, NT_SMALL><<<enum_grid(true), NT_SMALL,
+                                                               enum_smem_of<NT_SMALL>(), st>>>(p)));
+  else
+    GR_LAUNCH("enum_kernel", st, (enum_kernel<COUNT, NT><<<enum_grid(false), NT, enum_smem_of<NT>(), st>>>(p)));
+  return GR_OK;
 }
 
 u64 lane_cands_raw() {
@@ -1297,7 +1335,8 @@ int launch_finish(const gr_batch *in, int which, const gr_result *out, const WS 
   const int fgrid = k > 0 ? std::max(1, std::min((in->B + FT - 1) / FT, 64)) : 1;
   GR_LAUNCH("finish_kernel", st, finish_kernel<<<fgrid, FT, 0, st>>>(in_of(in, which), out_of(out), w, which, k,
                                    (in->flags & GR_FLAG_EXHAUSTIVE) ? 1 : 0, enum_grid() * NT, lane_cands(), windows_per_lane(false) | (windows_per_lane(true) << 16),
-                                   lane_max(false), lane_max(true), done_other));
+                                   lane_max(false), lane_max(true), done_other,
+                                   enum_small(in) ? NT_SMALL : NT));
   return GR_OK;
 }
 int launch_pack(const gr_batch *in, int which, const gr_result *out, const WS &w, cudaStream_t st) {
@@ -1362,11 +1401,9 @@ extern "C" int gr_exact_level(const gr_batch *in, int which, int k, int shard, i
   // the finish kernel leaves next_chunk at 0; several shards of one level on
   // one device (multi-shard emulation) need it reset between them
   if (nshard > 1) GR_CUDA(cudaMemsetAsync(&w.ctrl->next_chunk, 0, sizeof(u64), (cudaStream_t)s));
-  if (gr_prof_mode() == 2)
-    GR_LAUNCH("enum_kernel", (cudaStream_t)s, enum_kernel<true><<<grid, NT, ENUM_SMEM, (cudaStream_t)s>>>(p));
-  else
-    GR_LAUNCH("enum_kernel", (cudaStream_t)s, enum_kernel<false><<<grid, NT, ENUM_SMEM, (cudaStream_t)s>>>(p));
-  return GR_OK;
+  (void)grid;
+  return gr_prof_mode() == 2 ? launch_enum<true>(p, enum_small(in), (cudaStream_t)s)
+                             : launch_enum<false>(p, enum_small(in), (cudaStream_t)s);
 }
 
 extern "C" int64_t *gr_exact_level_keys(const gr_batch *in, int which, void *ws) {
@@ -1387,7 +1424,8 @@ extern "C" int gr_exact_finish(const gr_batch *in, int which, int k, gr_result *
   const int fgrid = std::max(1, std::min((in->B + FT - 1) / FT, 64));
   GR_LAUNCH("finish_kernel", (cudaStream_t)s, finish_kernel<<<fgrid, FT, 0, st>>>(in_of(in, which), out_of(out), w, which, k,
                                    (in->flags & GR_FLAG_EXHAUSTIVE) ? 1 : 0, enum_grid() * NT, lane_cands(), windows_per_lane(false) | (windows_per_lane(true) << 16),
-                                   lane_max(false), lane_max(true), nullptr));
+                                   lane_max(false), lane_max(true), nullptr,
+                                   enum_small(in) ? NT_SMALL : NT));
   if (n_active) {
     int *h = pinned_i32();
     if (!h) { gr_set_error("cudaMallocHost failed"); return GR_ECUDA; }
@@ -1484,17 +1522,18 @@ extern "C" int gr_solve_pms_mhs(const gr_batch *in, gr_result *out_pms, gr_resul
         p.shard = 0;
         p.nshard = 1;
         p.fused = 1;
-        if (gr_prof_mode() == 2)
-          GR_LAUNCH("enum_kernel", st, enum_kernel<true><<<grid, NT, ENUM_SMEM, st>>>(p));
-        else
-          GR_LAUNCH("enum_kernel", st, enum_kernel<false><<<grid, NT, ENUM_SMEM, st>>>(p));
+        (void)grid;
+        if ((rc = gr_prof_mode() == 2 ? launch_enum<true>(p, enum_small(in), st)
+                                      : launch_enum<false>(p, enum_small(in), st)))
+          return rc;
         const int P = std::max(1, std::min((in->B + FT - 1) / FT, 32));
         GR_LAUNCH("finish_kernel", st, finish_fused_kernel<<<2 * P, FT, 0, st>>>(
                                            in_of(in, 0), out_of(out_pms), w1, in_of(in, 1),
                                            out_of(out_mhs), w2, k,
                                            (in->flags & GR_FLAG_EXHAUSTIVE) ? 1 : 0, enum_grid() * NT, lane_cands(),
                                            windows_per_lane(false) | (windows_per_lane(true) << 16),
-                                           lane_max(false), lane_max(true)));
+                                           lane_max(false), lane_max(true),
+                                           enum_small(in) ? NT_SMALL : NT));
       }
       GR_CUDA(cudaMemcpyAsync(h, &w1.ctrl->n_remaining, sizeof(int), cudaMemcpyDeviceToHost, st));
       GR_CUDA(cudaStreamSynchronize(st));
