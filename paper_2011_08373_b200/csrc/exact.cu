@@ -444,7 +444,9 @@ static __device__ const HitTable g_hit = HitTable();
 // H_j(p): bit i set iff the i-th j-subset of [0, R_j) (colex order) meets p,
 // i.e. the union of HIT_j({x}) over the elements x of p
 __device__ F2 hitting(int j, u64 p) {
+  if (j == 1) return F2{p, 0ull};  // H_1(P) = P
   F2 r{0ull, 0ull};
+  p &= nbits((u64)region_of(j));   // HIT_j({x}) = 0 for x >= R_j
   for (; p; p &= p - 1) {
     const int x = __ffsll((long long)p) - 1;
     r.lo |= g_hit.lo[64 * j + x];
