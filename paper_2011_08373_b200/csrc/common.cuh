@@ -71,19 +71,19 @@ template <typename M> __device__ __forceinline__ M lowbit(M x) { return x & (~x 
 // order-preserving relabel onto a support set (pext) and back (pdep), 128-bit
 // support given as two words, result <= 64 bits.
 __device__ __forceinline__ u64 pext128(u64 x0, u64 x1, u64 s0, u64 s1) {
+  // bits of x outside the support are dropped; one step per bit of x: its
+  // position among the support bits below it
+  x0 &= s0;
+  x1 &= s1;
   u64 r = 0;
-  int j = 0;
-  while (s0) {
-    u64 l = s0 & (~s0 + 1);
-    if (x0 & l) r |= 1ull << j;
-    j++;
-    s0 ^= l;
+  for (; x0; x0 &= x0 - 1) {
+    const u64 l = x0 & (~x0 + 1);
+    r |= 1ull << __popcll(s0 & (l - 1));
   }
-  while (s1) {
-    u64 l = s1 & (~s1 + 1);
-    if (x1 & l) r |= 1ull << j;
-    j++;
-    s1 ^= l;
+  const int o = __popcll(s0);
+  for (; x1; x1 &= x1 - 1) {
+    const u64 l = x1 & (~x1 + 1);
+    r |= 1ull << (o + __popcll(s1 & (l - 1)));
   }
   return r;
 }
