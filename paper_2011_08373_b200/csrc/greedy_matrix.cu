@@ -15,6 +15,7 @@
 // completing on mbarriers; 8 consumer warps AND each segment with the
 // register-resident U tile and POPC-accumulate per-row counts in registers,
 // reducing across lanes only once per work item (64 rows x 16 tiles).
+#include <cooperative_groups.h>
 #include <cub/block/block_reduce.cuh>
 
 #include <algorithm>
@@ -467,6 +468,69 @@ __global__ void shard_mark_kernel(const u64 *R, int64_t ld, u64 *U, const GCtrl 
     U[w] &= ~Rv[w];
 }
 
+// the whole incremental greedy in one cooperative launch: per pick, every CTA
+// covers its slice of R[v] and decrements (shared histogram), a grid barrier,
+// then every CTA takes the same argmax of the counts (identical reads), a
+// second barrier before the counts change again.  CTA 0 records the pick.
+template <typename V>
+__global__ void __launch_bounds__(IT) incr_all_kernel(const u64 *R, int64_t ld, int m, u64 *U,
+                                                     u32 *counts, const int64_t *off,
+                                                     const V *var, const u32 *w, GCtrl *ctrl,
+                                                     int *picks) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ u32 hist[];
+  typedef cub::BlockReduce<Cand, IT> Red;
+  __shared__ typename Red::TempStorage tmp;
+  __shared__ int s_v;
+  if (threadIdx.x == 0) s_v = ctrl->done ? -1 : ctrl->pending;
+  __syncthreads();
+  int npk = ctrl->npicks;
+  const int64_t a = ld * blockIdx.x / gridDim.x, b = ld * (blockIdx.x + 1) / gridDim.x;
+  while (s_v >= 0) {
+    const int v = s_v;
+    for (int u = threadIdx.x; u < m; u += IT) hist[u] = 0;
+    __syncthreads();
+    const u64 *Rv = R + (size_t)v * ld;
+    for (int64_t wd = a + threadIdx.x; wd < b; wd += IT) {
+      const u64 r = Rv[wd];
+      if (!r) continue;
+      const u64 uu = U[wd];
+      u64 nw = uu & r;  // clauses newly covered by v
+      if (!nw) continue;
+      U[wd] = uu & ~r;
+      while (nw) {
+        const int64_t c = wd * 64 + (__ffsll((long long)nw) - 1);
+        nw &= nw - 1;
+        for (int64_t e = off[c]; e < off[c + 1]; e++) atomicAdd(&hist[(int)var[e]], 1u);
+      }
+    }
+    __syncthreads();
+    for (int u = threadIdx.x; u < m; u += IT)
+      if (hist[u]) atomicSub(&counts[u], hist[u]);
+    grid.sync();
+    Cand best{0u, 1u, 0x7fffffff};
+    for (int u = threadIdx.x; u < m; u += IT)
+      best = CandBetter()(Cand{__ldcg(&counts[u]), w ? w[u] : 1u, u}, best);
+    best = Red(tmp).Reduce(best, CandBetter());
+    if (threadIdx.x == 0) {
+      s_v = best.c == 0 ? -1 : best.v;
+      if (blockIdx.x == 0) {
+        if (best.c == 0) {
+          ctrl->done = 1;
+          ctrl->pending = -1;
+        } else {
+          picks[npk] = best.v;
+          ctrl->pending = best.v;
+        }
+        ctrl->npicks = best.c == 0 ? npk : npk + 1;
+      }
+    }
+    if (best.c != 0) npk++;
+    grid.sync();  // every CTA has read the counts
+  }
+}
+
 // ---- prune: bit-sliced hit counters over the picks ----------------------------
 // planes[i][w] is bit i of the per-clause hit count; add/sub ripple carries.
 __global__ void planes_build_kernel(const u64 *R, int64_t ld, const int *picks, const GCtrl *ctrl,
@@ -785,6 +849,38 @@ extern "C" int gr_mhs_greedy_matrix(const gr_bitmatrix *in, uint64_t *assign, in
       GR_LAUNCH("csr_hist_kernel", st, csr_hist_kernel<int32_t><<<std::max(hgrid, 1), 256, hs, st>>>(
                                           in->n_pos, in->pos_off, (const int32_t *)in->pos_var, in->m, counts));
     GR_LAUNCH("first_pick_kernel", st, first_pick_kernel<<<1, IT, 0, st>>>(counts, in->m, in->w, ctrl, wpicks));
+    bool coop_done = false;
+    {
+      // one cooperative launch for all picks (its grid must be co-resident)
+      static int cgrid = -1;
+      if (cgrid < 0) {
+        int per = 0, sms = 0, dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        int coop = 0;
+        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+        cudaFuncSetAttribute(incr_all_kernel<int16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(incr_all_kernel<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, incr_all_kernel<int32_t>, IT, hs);
+        cgrid = (coop && per > 0 && !getenv("GR_NO_COOP")) ? sms * std::min(per, 2) : 0;
+      }
+      if (cgrid > 0) {
+        const int64_t ldv = ld;
+        const int mv = in->m;
+        void *args[] = {(void *)&in->bits, (void *)&ldv, (void *)&mv, (void *)&U, (void *)&counts,
+                        (void *)&in->pos_off, (void *)&in->pos_var, (void *)&in->w, (void *)&ctrl,
+                        (void *)&wpicks};
+        const void *fn = in->var_bytes == 2 ? (const void *)incr_all_kernel<int16_t>
+                                            : (const void *)incr_all_kernel<int32_t>;
+        gr_prof_pre("incr_all_kernel", st);
+        cudaError_t e = cudaLaunchCooperativeKernel(fn, cgrid, IT, args, hs, st);
+        gr_prof_post("incr_all_kernel", st);
+        if (e != cudaSuccess) return gr_cuda_fail(e, "incr_all_kernel");
+        GR_CUDA(cudaMemcpyAsync(h, ctrl, sizeof(GCtrl), cudaMemcpyDeviceToHost, st));
+        GR_CUDA(cudaStreamSynchronize(st));
+        coop_done = ((GCtrl *)h)->done != 0;
+      }
+    }
     const int STEPS = 32;
     static int igrid = 0;  // CTAs of the incremental step (GR_INCR_GRID)
     if (!igrid) {
@@ -792,7 +888,7 @@ extern "C" int gr_mhs_greedy_matrix(const gr_bitmatrix *in, uint64_t *assign, in
       igrid = e ? atoi(e) : 2 * grid;  // two per SM: measured 10.8 -> 7.7 ms on C5
       if (igrid < 1 || igrid > 4 * grid) igrid = grid;
     }
-    for (int round = 0;; round++) {
+    for (int round = 0; !coop_done; round++) {
       for (int j = 0; j < STEPS; j++) {
         if (in->var_bytes == 2)
           GR_LAUNCH("incr_step_kernel", st, incr_step_kernel<int16_t><<<igrid, IT, hs, st>>>(
