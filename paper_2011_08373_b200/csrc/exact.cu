@@ -630,6 +630,10 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
   // partition the level in rank order, so the next sub-block starts where
   // this one ends: base += n.
   M U = Utop;
+  // weighted: W(U), kept up to date as the iterator adds / removes elements
+  u64 wU = 0;
+  if (MODE == 2)
+    for (M tt = U; tt; tt &= tt - 1) wU += w[ctz(tt)];
   u64 base = base_top;
   int d = 0, j = J, e = e_top, ep = e_top;
   u64 tp = 0;
@@ -652,6 +656,7 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
     ep = e;
     e = t;
     U |= (M)1 << t;
+    if (MODE == 2) wU += w[t];
     base += CS(t, j);
     d++;
     j--;
@@ -671,13 +676,12 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
     // U.  Then all C(e, j) candidates of the subtree are decided at once.
     bool dead = dead0;
     dead0 = false;
-    u64 WU = 0;  // weighted: W(U), and a bound on the whole subtree -- every x
-                 // in it weighs >= W(U) + S_j (the j smallest weights); it can
-                 // only matter below the incumbent of earlier levels (W*,
-                 // strictly, R3) and below this lane's best so far (ties lose
-                 // on rank: the walk is in rank order)
+    const u64 WU = wU;  // weighted: W(U), and a bound on the whole subtree -- every
+                        // x in it weighs >= W(U) + S_j (the j smallest weights);
+                        // it can only matter below the incumbent of earlier
+                        // levels (W*, strictly, R3) and below this lane's best
+                        // so far (ties lose on rank: the walk is in rank order)
     if (MODE == 2) {
-      for (M tt = U; tt; tt &= tt - 1) WU += w[ctz(tt)];
       if (prune && !dead) {
         const u64 lb = (u64)best >> rb;
         const u64 lim = best == GR_KEY_NONE ? wstar : (lb < wstar ? lb : wstar);
@@ -740,6 +744,7 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
       ep = e;
       e = R;
       U |= (M)1 << R;
+      if (MODE == 2) wU += w[R];
       d++;
       j--;
       R = c.reg[j];
@@ -748,6 +753,7 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
     if (d > 0 && e + 1 >= ep) {  // no next sibling here: pop until there is one
       do {
         U &= ~((M)1 << e);
+        if (MODE == 2) wU -= w[e];
         d--;
         j++;
         e = ep;
@@ -758,6 +764,7 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
     }
     if (d > 0) {  // next sibling: t -> t + 1
       U ^= (M)3 << e;
+      if (MODE == 2) wU += (u64)w[e + 1] - (u64)w[e];
       e++;
       continue;
     }
@@ -770,6 +777,10 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
     Utop = (M)(S << J);
     e_top = ctz(Utop);
     U = Utop;
+    if (MODE == 2) {
+      wU = 0;
+      for (M tt = U; tt; tt &= tt - 1) wU += w[ctz(tt)];
+    }
     e = ep = e_top;
   }
 #undef CS
