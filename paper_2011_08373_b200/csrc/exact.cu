@@ -55,7 +55,7 @@ struct Ctrl {
 };
 
 #ifndef GR_JMAX
-#define GR_JMAX 10
+#define GR_JMAX 11
 #endif
 constexpr int JMAX = GR_JMAX;  // S = the J = min(k, JMAX) lowest elements of a candidate
 constexpr int HREC = JMAX;     // per-clause record: H_1 (= P), H_2, ..., H_JMAX
@@ -413,7 +413,7 @@ __device__ __forceinline__ int f2_popc(F2 a) { return __popcll(a.lo) + __popcll(
 // R_j = the largest region with C(R_j, j) <= 128 (j = 1: every variable)
 __host__ __device__ constexpr int region_of(int j) {
   return j <= 8 ? (int)((0x0A0A0909090A1040ull >> (8 * (j - 1))) & 0xffull)  // 64 16 10 9 9 9 10 10
-                : (j == 9 ? 11 : 12);                                           // 11 12
+                : (j == 9 ? 11 : (j == 10 ? 12 : 13));                           // 11 12 13
 }
 __device__ __forceinline__ u64 nbits(u64 n) { return n >= 64 ? ~0ull : ((1ull << n) - 1ull); }
 
