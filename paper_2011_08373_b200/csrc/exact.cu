@@ -55,9 +55,10 @@ struct Ctrl {
 };
 
 #ifndef GR_JMAX
-#define GR_JMAX 11
+#define GR_JMAX 12
 #endif
 constexpr int JMAX = GR_JMAX;  // S = the J = min(k, JMAX) lowest elements of a candidate
+static_assert(JMAX >= 1 && JMAX <= 12, "the iterator's 6-bit ancestor stack holds JMAX - 2 entries");
 constexpr int HREC = JMAX;     // per-clause record: H_1 (= P), H_2, ..., H_JMAX
 constexpr int HX = 16;         // HIT_j({x}) is 0 for x >= R_j, and R_j <= 16 for j >= 2
 
@@ -413,7 +414,7 @@ __device__ __forceinline__ int f2_popc(F2 a) { return __popcll(a.lo) + __popcll(
 // R_j = the largest region with C(R_j, j) <= 128 (j = 1: every variable)
 __host__ __device__ constexpr int region_of(int j) {
   return j <= 8 ? (int)((0x0A0A0909090A1040ull >> (8 * (j - 1))) & 0xffull)  // 64 16 10 9 9 9 10 10
-                : (j == 9 ? 11 : (j == 10 ? 12 : 13));                           // 11 12 13
+                : (j == 9 ? 11 : (j == 10 ? 12 : (j == 11 ? 13 : 14)));        // 11 12 13 14
 }
 __device__ __forceinline__ u64 nbits(u64 n) { return n >= 64 ? ~0ull : ((1ull << n) - 1ull); }
 
@@ -626,7 +627,8 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
   // Iterator state: the path t_0 > t_1 > ... > t_{d-1} of part-B choices
   // below Utop; the current node is (j = J - d, U, e = t_{d-1} or e_top) with
   // region R = R_j and ep = the parent's e (t_{d-2} or e_top).  tp is a stack
-  // of the older ancestors (6 bits each, most recent lowest).  Sub-blocks
+  // of the older ancestors t_{d-3} .. t_0, e_top (6 bits each, most recent
+  // lowest; at depth d it holds d - 1 entries, so JMAX <= 12).  Sub-blocks
   // partition the level in rank order, so the next sub-block starts where
   // this one ends: base += n.
   M U = Utop;
@@ -652,7 +654,7 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
       }
     }
     const int t = s[j - 1];
-    tp = (tp << 6) | (u64)ep;
+    if (d > 0) tp = (tp << 6) | (u64)ep;
     ep = e;
     e = t;
     U |= (M)1 << t;
@@ -740,7 +742,7 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
     // ---- advance: first child t = R of this node, else the next sibling up
     // the path
     if (!dead && j >= 2 && R < e) {
-      tp = (tp << 6) | (u64)ep;
+      if (d > 0) tp = (tp << 6) | (u64)ep;
       ep = e;
       e = R;
       U |= (M)1 << R;
@@ -757,8 +759,10 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
         d--;
         j++;
         e = ep;
-        ep = (int)(tp & 63u);
-        tp >>= 6;
+        if (d > 0) {  // the stack holds the ancestors above the parent
+          ep = (int)(tp & 63u);
+          tp >>= 6;
+        }
       } while (d > 0 && e + 1 >= ep);
       R = c.reg[j];
     }
