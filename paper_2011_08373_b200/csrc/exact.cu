@@ -55,11 +55,11 @@ struct Ctrl {
 };
 
 #ifndef GR_JMAX
-#define GR_JMAX 12
+#define GR_JMAX 13
 #endif
 constexpr int JMAX = GR_JMAX;  // S = the J = min(k, JMAX) lowest elements of a candidate
-static_assert(JMAX >= 1 && JMAX <= 12, "the iterator's 6-bit ancestor stack holds JMAX - 2 entries");
-constexpr int HREC = JMAX;     // per-clause record: H_1 (= P), H_2, ..., H_JMAX
+static_assert(JMAX >= 2 && JMAX <= 14, "the iterator's ancestor stack holds J - 2 entries");
+constexpr int HREC = JMAX - 1;  // per-clause records H_2, ..., H_JMAX (H_1(P) = P itself)
 constexpr int HX = 16;         // HIT_j({x}) is 0 for x >= R_j, and R_j <= 16 for j >= 2
 
 struct Layout {
@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(PT) pack_kernel(In in, Out out, WS ws, int whi
     const int64_t dst = lo + (j < np ? 0 : npr) + d;
     ws.pk[dst] = R[j];
     if (j < np)
-      for (int jj = 1; jj <= HREC; jj++) ((F2 *)ws.hrec)[dst * HREC + jj - 1] = hitting(jj, R[j]);
+      for (int jj = 2; jj <= JMAX; jj++) ((F2 *)ws.hrec)[dst * HREC + jj - 2] = hitting(jj, R[j]);
   }
   // weights of the support variables (relabelled order) and S_k
   if (t < 64) {
@@ -414,7 +414,7 @@ __device__ __forceinline__ int f2_popc(F2 a) { return __popcll(a.lo) + __popcll(
 // R_j = the largest region with C(R_j, j) <= 128 (j = 1: every variable)
 __host__ __device__ constexpr int region_of(int j) {
   return j <= 8 ? (int)((0x0A0A0909090A1040ull >> (8 * (j - 1))) & 0xffull)  // 64 16 10 9 9 9 10 10
-                : (j == 9 ? 11 : (j == 10 ? 12 : (j == 11 ? 13 : 14)));        // 11 12 13 14
+                : (j == 9 ? 11 : (j == 10 ? 12 : (j == 11 ? 13 : (j == 12 ? 14 : (j == 13 ? 15 : 16)))));
 }
 __device__ __forceinline__ u64 nbits(u64 n) { return n >= 64 ? ~0ull : ((1ull << n) - 1ull); }
 
@@ -479,7 +479,16 @@ struct Clauses {
 template <typename M, bool COUNT>
 __device__ __forceinline__ F2 test_pos(int j, M U, F2 F, const Clauses<M> &c, Work &wk) {
   const int np = c.np;
-  const F2 *H = c.H + (j - 1);
+  if (j == 1) {  // H_1(P) = P
+    for (int q = 0; q < np; q++) {
+      const M pq = c.P[q];
+      if (!(U & pq)) F.lo &= (u64)pq;
+      if (COUNT) wk.tests += 1;
+      if (!(q & 3) && !F.lo) return F2{0ull, 0ull};
+    }
+    return F2{F.lo, 0ull};
+  }
+  const F2 *H = c.H + (j - 2);
   int q = 0;
   for (; q + 4 <= np; q += 4) {
     const M p0 = c.P[q], p1 = c.P[q + 1], p2 = c.P[q + 2], p3 = c.P[q + 3];
@@ -591,7 +600,10 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
   i64 dummy = GR_KEY_NONE;
   i64 &bm = MODE == 3 ? *best_m : dummy;
   bool wp = MODE != 3 || need_p, wm = MODE == 3 && need_m;
-  const int J = k < JMAX ? k : JMAX;
+  // the ancestor stack: 5-bit entries below 32 variables, else 6 (J <= 12)
+  constexpr int SB = sizeof(M) == 4 ? 5 : 6;
+  constexpr int JM = sizeof(M) == 4 ? JMAX : (JMAX < 12 ? JMAX : 12);
+  const int J = k < JM ? k : JM;
   const u64 *cs = c.cs;  // C(n, j), j <= JMAX
 #define CS(n, j) (cs[(n) * (JMAX + 1) + (j)])
   i64 best = GR_KEY_NONE;
@@ -654,7 +666,7 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
       }
     }
     const int t = s[j - 1];
-    if (d > 0) tp = (tp << 6) | (u64)ep;
+    if (d > 0) tp = (tp << SB) | (u64)ep;
     ep = e;
     e = t;
     U |= (M)1 << t;
@@ -742,7 +754,7 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
     // ---- advance: first child t = R of this node, else the next sibling up
     // the path
     if (!dead && j >= 2 && R < e) {
-      if (d > 0) tp = (tp << 6) | (u64)ep;
+      if (d > 0) tp = (tp << SB) | (u64)ep;
       ep = e;
       e = R;
       U |= (M)1 << R;
@@ -760,8 +772,8 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
         j++;
         e = ep;
         if (d > 0) {  // the stack holds the ancestors above the parent
-          ep = (int)(tp & 63u);
-          tp >>= 6;
+          ep = (int)(tp & ((1u << SB) - 1u));
+          tp >>= SB;
         }
       } while (d > 0 && e + 1 >= ep);
       R = c.reg[j];
@@ -834,8 +846,7 @@ constexpr int ENUM_CTAS = GR_ENUM_CTAS;  // resident enumeration CTAs per SM (re
 // walks two windows per thread.
 template <int NTK>
 __host__ __device__ constexpr int smc_of() {
-  return (int)(((227 * 1024) / (ENUM_CTAS * NT / NTK) - 1024 - 400 - TAB_SMEM) / (16 * HREC + 8)) /
-         32 * 32;
+  return (int)(((227 * 1024) / (ENUM_CTAS * NT / NTK) - 1024 - 600 - TAB_SMEM) / (16 * HREC + 8));
 }
 template <int NTK>
 __host__ __device__ constexpr size_t enum_smem_of() {
