@@ -1013,10 +1013,33 @@ __global__ void __launch_bounds__(NTK, COUNT ? 1 : ENUM_CTAS * NT / NTK) enum_ke
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ int bitlen(u64 x) { return x ? 64 - __clzll((long long)x) : 0; }
 
+// colex unrank (common.cuh's unrank_colex) against a shared-memory copy of
+// the binomial table: the finish is a latency chain (k binary searches of
+// dependent reads per witness), so each read is a shared-memory hit instead of
+// an L2 round trip
+__device__ __forceinline__ u64 unrank_colex_smem(const u64 (*tb)[65], u64 r, int k, int n) {
+  u64 x = 0;
+  int hi = n - 1;
+  for (int j = k; j >= 1; j--) {
+    int lo = j - 1, h = hi;
+    while (lo < h) {
+      const int mid = (lo + h + 1) >> 1;
+      if (tb[mid][j] <= r) lo = mid; else h = mid - 1;
+    }
+    x |= 1ull << lo;
+    r -= tb[lo][j];
+    hi = lo - 1;
+  }
+  return x;
+}
+
 // phase 1 of the finish: commit level k of every listed instance
 __device__ void finish_commit(const In &in, const Out &out, const WS &ws, int which, int k,
                               int exhaustive, int part, int nparts) {
   const int t = threadIdx.x;
+  __shared__ u64 s_binom[65][65];  // C(n, j), zero for j > n (as g_binom)
+  for (int i = t; i < 65 * 65; i += FT) (&s_binom[0][0])[i] = __ldg(&g_binom.v[0][0] + i);
+  __syncthreads();
   const bool weighted = in.w != nullptr;
   const int nact_in = k == 0 ? in.B : ws.ctrl->n_active;
   const int *cur = ws.active + (size_t)(k & 1) * in.B;  // list enumerated at level k
@@ -1025,13 +1048,13 @@ __device__ void finish_commit(const In &in, const Out &out, const WS &ws, int wh
       const int b = cur[i];
       if (ws.done[b]) continue;  // fused: listed for the other solve only
       const int me = ws.meff[b];
-      const u64 ck = binom(me, k);
+      const u64 ck = s_binom[me][k];
       const i64 key = ws.lvlkey[b];
       const u64 s0 = ws.sup[2 * b], s1 = ws.sup[2 * b + 1];
       if (!weighted) {
         if (key != GR_KEY_NONE) {
           const u64 rank = (u64)key;
-          const u64 x = unrank_colex(rank, k, me);
+          const u64 x = unrank_colex_smem(s_binom, rank, k, me);
           const u64 d = sat_add(ws.decided[b], exhaustive ? ck : rank + 1);
           ws.done[b] = 1;
           write_result(in, out, b, GR_SAT, x, s0, s1, (u64)k, d, which);
@@ -1050,7 +1073,7 @@ __device__ void finish_commit(const In &in, const Out &out, const WS &ws, int wh
           const u64 rank = (u64)key & ((rb ? (1ull << rb) : 1ull) - 1ull);
           if (Wk < ws.bestw[b]) {  // strictly smaller W replaces the incumbent (R3)
             ws.bestw[b] = Wk;
-            ws.bestx[b] = unrank_colex(rank, k, me);
+            ws.bestx[b] = unrank_colex_smem(s_binom, rank, k, me);
           }
         }
         const u64 bw = ws.bestw[b];
@@ -1078,6 +1101,8 @@ __device__ void finish_plan(const In &in, const Out &out, const WS &ws, int whic
   __shared__ u64 s_carry;
   __shared__ int s_cnt, s_wait;
   const int t = threadIdx.x;
+  if (t == 0) s_wait = 0;  // shared memory starts undefined
+  __syncthreads();
   const bool weighted = in.w != nullptr;
   const int nact_in = k == 0 ? in.B : ws.ctrl->n_active;
   int *cur = ws.active + (size_t)(k & 1) * in.B;        // list enumerated at level k
