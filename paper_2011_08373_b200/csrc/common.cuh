@@ -123,6 +123,27 @@ __device__ __forceinline__ u64 unrank_colex(u64 r, int k, int n) {
   return x;
 }
 
+// "last block" election over a global ticket (the threadFenceReduction
+// pattern): the CTA barrier orders every thread's writes before thread 0's
+// gpu-scope fence (fences are cumulative), so one thread fences instead of
+// every warp issuing a MEMBAR.SC.GPU.  The last CTA to arrive gets true
+// (after an acquire fence) and resets the ticket.
+__device__ __forceinline__ bool cta_last_arrival(unsigned *ticket, unsigned nblocks) {
+  __shared__ int s_last_arrival;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const bool last = atomicAdd(ticket, 1u) == nblocks - 1;
+    if (last) {
+      __threadfence();
+      *ticket = 0;
+    }
+    s_last_arrival = last;
+  }
+  __syncthreads();
+  return s_last_arrival != 0;
+}
+
 __device__ __forceinline__ u64 sat_add(u64 a, u64 b) { u64 c = a + b; return c < a ? ~0ull : c; }
 
 __host__ __device__ __forceinline__ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }

@@ -1037,8 +1037,11 @@ __device__ __forceinline__ u64 unrank_colex_smem(const u64 (*tb)[65], u64 r, int
 __device__ void finish_commit(const In &in, const Out &out, const WS &ws, int which, int k,
                               int exhaustive, int part, int nparts) {
   const int t = threadIdx.x;
-  __shared__ u64 s_binom[65][65];  // C(n, j), zero for j > n (as g_binom)
-  for (int i = t; i < 65 * 65; i += FT) (&s_binom[0][0])[i] = __ldg(&g_binom.v[0][0] + i);
+  __shared__ u64 s_binom[65][65];  // C(n, j), zero for j > n (as g_binom); columns j <= k only
+  for (int i = t; i < 65 * (k + 1); i += FT) {
+    const int n = i / (k + 1), j = i - n * (k + 1);
+    s_binom[n][j] = __ldg(&g_binom.v[n][j]);
+  }
   __syncthreads();
   const bool weighted = in.w != nullptr;
   const int nact_in = k == 0 ? in.B : ws.ctrl->n_active;
@@ -1222,16 +1225,7 @@ __global__ void __launch_bounds__(FT, 1) finish_kernel(In in, Out out, WS ws, in
   // the commit is per instance: every block takes a share; the last block to
   // finish it plans the next level for all
   if (k > 0) finish_commit(in, out, ws, which, k, exhaustive, blockIdx.x, gridDim.x);
-  if (gridDim.x > 1) {
-    __shared__ int s_last;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) s_last = atomicAdd(&ws.ctrl->fin_ticket, 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    if (threadIdx.x == 0) ws.ctrl->fin_ticket = 0;
-  }
+  if (gridDim.x > 1 && !cta_last_arrival(&ws.ctrl->fin_ticket, gridDim.x)) return;
   finish_plan(in, out, ws, which, k, enum_lanes, fixed_lane, windows_per_lane, lane_max, lane_max_w,
               done_other, chunk_lanes);
 }
@@ -1249,16 +1243,7 @@ __global__ void __launch_bounds__(FT, 1) finish_fused_kernel(In in1, Out out1, W
     if ((int)blockIdx.x < P) finish_commit(in1, out1, ws1, 0, k, exhaustive, blockIdx.x, P);
     else finish_commit(in2, out2, ws2, 1, k, exhaustive, blockIdx.x - P, P);
   }
-  {
-    __shared__ int s_last;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) s_last = atomicAdd(&ws1.ctrl->fin_ticket, 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    if (threadIdx.x == 0) ws1.ctrl->fin_ticket = 0;
-  }
+  if (!cta_last_arrival(&ws1.ctrl->fin_ticket, gridDim.x)) return;
   finish_plan(in2, out2, ws2, 1, k, enum_lanes, fixed_lane, windows_per_lane, lane_max, lane_max_w,
               nullptr, chunk_lanes, false);  // its list only: the PMS workspace plans the chunks
   __syncthreads();

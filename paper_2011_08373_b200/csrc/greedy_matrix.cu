@@ -389,7 +389,6 @@ __global__ void __launch_bounds__(IT) incr_step_kernel(const u64 *R, int64_t ld,
                                                       const V *var, const u32 *w, GCtrl *ctrl,
                                                       int *picks) {
   extern __shared__ u32 hist[];
-  __shared__ int s_last;
   if (*(volatile int *)&ctrl->done) return;
   const int v = ctrl->pending;
   for (int u = threadIdx.x; u < m; u += IT) hist[u] = 0;
@@ -413,17 +412,9 @@ __global__ void __launch_bounds__(IT) incr_step_kernel(const u64 *R, int64_t ld,
   for (int u = threadIdx.x; u < m; u += IT)
     if (hist[u]) atomicSub(&counts[u], hist[u]);
   if (!PICK) return;  // sharded greedy: the next pick needs the all-reduced counts
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(&ctrl->ticket, 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (s_last) {
-    __threadfence();
+  if (cta_last_arrival(&ctrl->ticket, gridDim.x)) {
     pick_argmax(counts, m, w, ctrl, picks);
-    if (threadIdx.x == 0) {
-      ctrl->ticket = 0;
-      ctrl->steps += 1;
-    }
+    if (threadIdx.x == 0) ctrl->steps += 1;
   }
 }
 
