@@ -185,6 +185,33 @@ def test_c2_full_batch():
     check_batch(sub)
 
 
+def test_c2_level_loop_accounting():
+    """The finish kernel's instance count drives the host level loop: after
+    level k it is at most B, never grows, covers every instance whose optimum
+    lies above k, and reaches 0 right after the last witness level (an
+    uninitialised counter once let the loop run empty levels)."""
+    cb = synth.c2_batch()
+    e = np.load(os.path.join(GOLDEN, "expected_c2.npz"))
+    sat = e["pms_status"] == gr.GR_SAT
+    db = gr.DeviceBatch.from_host(cb)
+    s = gr.ExactSession(db, gr.PMS)
+    n = s.prepare()
+    assert 0 <= n <= cb.B
+    k, prev = 0, n
+    while n:
+        k += 1
+        assert k <= 64
+        s.level(k)
+        n = s.finish(k)
+        assert 0 <= n <= prev
+        assert n >= int((sat & (e["pms_cost"] > k)).sum())
+        prev = n
+    assert k >= int(e["pms_cost"][sat].max())
+    got = s.out.to_host()
+    for f in ("status", "assign", "cost"):
+        assert (got[f] == e[f"pms_{f}"]).all()
+
+
 def test_c3_first_witness_exhaustive_and_shards():
     cb, H, grp = synth.c3_instance()
     e = np.load(os.path.join(GOLDEN, "expected_c3.npz"))
