@@ -39,7 +39,10 @@
 namespace {
 
 constexpr int NT = 256;          // enumeration CTA size
-constexpr int FT = 1024;         // finish CTA size
+#ifndef GR_FT
+#define GR_FT 1024
+#endif
+constexpr int FT = GR_FT;        // finish CTA size
 constexpr int PT = 128;          // pack CTA size
 constexpr int MAXC = 4096;       // max clauses per instance (exact solvers)
 
