@@ -145,7 +145,8 @@ static int validate(int m, int W, int n, const uint64_t *masks, const uint32_t *
  *              definition); reduce = 1: reading R13 -- restrict to the
  *              support of phi+ (order-preserving relabel), drop negative
  *              clauses touching non-support variables, stop at
- *              k_max = min(|support|, n_pos).
+ *              k_max = min(|support|, #clauses of phi+ not subsumed by
+ *              another, equal clauses counted once).
  * Algorithm (levelled Gosper):
  *   for k = 0, 1, ...: (weighted: stop once S_k >= W_best, S_k = sum of the
  *   k smallest weights, reading R3)
@@ -204,7 +205,19 @@ static int or_pms_from(int m, int W, int n_pos, int n_neg, const uint64_t *masks
       if (inside)
         neg[nn++] = compress(N[0], sup[0]) | (W > 1 ? compress(N[1], sup[1]) << popc64(sup[0]) : 0);
     }
-    kmax = me < n_pos ? me : n_pos;
+    /* k_max (reading R13): a minimal hitting set has at most one element per
+     * clause of phi+ that no other clause subsumes (a private clause of x
+     * can be taken inside every clause it contains, and equal clauses count
+     * once), and an optimum is a minimal hitting set (dropping a variable
+     * keeps phi- satisfied and lowers the weight) */
+    int nmin = 0;
+    for (int j = 0; j < n_pos; j++) {
+      int subsumed = 0;
+      for (int i = 0; i < n_pos && !subsumed; i++)
+        if (i != j && (pos[i] & ~pos[j]) == 0 && (pos[i] != pos[j] || i < j)) subsumed = 1;
+      nmin += !subsumed;
+    }
+    kmax = me < nmin ? me : nmin;
   } else {
     sup[0] = (m == 64) ? ~0ull : ((1ull << m) - 1);
     for (int j = 0; j < n_pos; j++) pos[j] = masks[(size_t)j * W];
@@ -309,7 +322,9 @@ int or_mhs(int m, int W, int n_pos, int n_neg, const uint64_t *masks, int reduce
  *     c[v] = |{P in U : v in P}| for every v;
  *     v* = the lowest v with c[v] = max c          (reading R11)
  *     S.append(v*); U = {P in U : v* not in P}
- *   for x in reversed(S): drop x if every P in phi+ meets S \ {x}.
+ *   for x in reversed(S) (weighted mhs: by descending weight, equal weights
+ *   in reverse pick order -- reading R12): drop x if every P in phi+ meets
+ *   S \ {x}.
  *   status = SAT_NEG_VIOLATED if some N in phi- has N subset of S, else SAT.
  * Outputs: picks[0..n_unpruned-1] = pick order (before pruning);
  *   in_S[m] = final (pruned) set as 0/1 bytes; n_final = |S| after pruning.
@@ -389,9 +404,20 @@ static int greedy_core(int m, int64_t n_pos, const int64_t *pos_off, const int32
     }
   }
   *n_unpruned = nS;
-  /* reverse-delete: x is dropped if every positive clause meets S \ {x} */
-  for (int i = nS - 1; i >= 0; i--) {
-    int x = picks[i];
+  /* reverse-delete: x is dropped if every positive clause meets S \ {x}.
+   * Order (reading R12): unit weights -- reverse pick order; weighted mhs --
+   * descending weight ("in descending-weight order"), equal
+   * weights in reverse pick order.  ord[] lists pick positions in that order
+   * (insertion sort: stable, plain). */
+  int *ord = malloc(sizeof(int) * ((size_t)nS + 1));
+  if (!ord) { free(covered); free(cnt_all); free(cnt); return OR_ENOMEM; }
+  for (int i = 0; i < nS; i++) {
+    int p = nS - 1 - i, j = i - 1; /* reverse pick order first */
+    while (w && j >= 0 && w[picks[ord[j]]] < w[picks[p]]) { ord[j + 1] = ord[j]; j--; }
+    ord[j + 1] = p;
+  }
+  for (int r = 0; r < nS; r++) {
+    int x = picks[ord[r]];
     in_S[x] = 0;
     int64_t unhit = 0;
 #pragma omp parallel for schedule(static) reduction(+ : unhit)
@@ -402,6 +428,7 @@ static int greedy_core(int m, int64_t n_pos, const int64_t *pos_off, const int32
     }
     if (unhit) in_S[x] = 1;
   }
+  free(ord);
   int nf = 0;
   for (int v = 0; v < m; v++) nf += in_S[v];
   *n_final = nf;

@@ -30,7 +30,9 @@ def masks_of(pos, neg, W=1):
 
 
 def vars_of(mask):
-    return synth.mask_to_vars([mask])
+    """joined assignment mask (any width) -> sorted 1-based b_i"""
+    mask = int(mask)
+    return [i + 1 for i in range(mask.bit_length()) if mask >> i & 1]
 
 
 # ---------------------------------------------------------------- golden pins
@@ -523,3 +525,183 @@ def check_greedy_invariants_weighted(pos, chosen):
     assert all(set(c) & S for c in pos)
     for x in S:
         assert any(set(c) & S == {x} for c in pos)
+
+
+def test_weighted_prune_order_golden():
+    """tests/golden/weighted_prune_order.txt: with weights the reverse-delete
+    runs in descending-weight order (reading R12), which here
+    keeps {b2, b3} (weight 101) where reverse pick order would keep {b1, b3}."""
+    g = load_golden("weighted_prune_order.txt")
+    m, pos, w, e = g["m"], g["pos"], g["w"], g["expect"]
+    mk = masks_of(pos, [])
+    st, a, picks = oracle.greedy(m, len(pos), mk, w=w)
+    assert [int(p) + 1 for p in picks] == [int(x) for x in e["picks"]]
+    assert synth.mask_to_vars(a) == [int(x) for x in e["greedy"]]
+    assert sum(w[v - 1] for v in synth.mask_to_vars(a)) == int(e["greedy_cost"][0])
+    assert st == STATUS[e["greedy_status"][0]]
+    # the CSR entry point agrees
+    off = np.cumsum([0] + [len(c) for c in pos]).astype(np.int64)
+    var = np.asarray([v - 1 for c in pos for v in c], np.int32)
+    g2 = oracle.greedy_csr(m, off, var, np.zeros(1, np.int64), np.zeros(0, np.int32), w=w)
+    assert [i + 1 for i in np.flatnonzero(g2.in_S)] == [int(x) for x in e["greedy"]]
+
+
+def py_weighted_prune(pos, picks, w):
+    """Reverse-delete written out over Python sets: descending weight, equal
+    weights in reverse pick order (reading R12)."""
+    order = sorted(range(len(picks)), key=lambda i: (-w[picks[i] - 1], -i))
+    S = set(picks)
+    for i in order:
+        x = picks[i]
+        if all(set(c) & (S - {x}) for c in pos):
+            S.discard(x)
+    return sorted(S)
+
+
+def test_weighted_prune_order_random():
+    rng = random.Random(4242)
+    for _ in range(200):
+        m = rng.randint(2, 10)
+        pos, neg, _ = rand_instance(rng, m, rng.randint(1, 14))
+        w = [rng.choice([1, 2, 3, 10, 100]) for _ in range(m)]
+        st, a, picks = oracle.greedy(m, len(pos), masks_of(pos, neg), w=w)
+        if st not in (SAT, NEGV):
+            continue
+        assert synth.mask_to_vars(a) == py_weighted_prune(pos, [int(p) + 1 for p in picks], w)
+
+
+# ------------------------------------------------- two-word masks (W = 2)
+# Variables above b_64 live in word 1; the oracle then relabels the support of
+# phi+ across both words (compress(word0) | compress(word1) << popc(sup0)) and
+# expands the optimum back.  These pins fix that branch by closed forms and an
+# independent Python-sets brute force over the variables that occur.
+def py_brute_support(pos, neg, w=None):
+    """min (weight, size, colex rank) over subsets of the variables that occur
+    in some clause (a variable in no clause is false in every optimum: it only
+    adds weight >= 1), clauses as Python sets, original 1-based indices."""
+    V = sorted({v for c in pos + neg for v in c})
+    best = None
+    for bits in itertools.product((0, 1), repeat=len(V)):
+        true = {V[i] for i in range(len(V)) if bits[i]}
+        if all(set(c) & true for c in pos) and all(not set(c) <= true for c in neg):
+            key = (sum((w[i - 1] if w else 1) for i in true), len(true), colex_rank(true))
+            if best is None or key < best[0]:
+                best = (key, sorted(true))
+    return best
+
+
+@pytest.mark.parametrize("sizes,start", [([2, 3, 4], 60), ([1, 5, 2, 7], 58), ([3] * 8, 50),
+                                         ([4, 4], 63), ([9, 1, 1], 100)])
+def test_w2_disjoint_clauses(sizes, start):
+    """P5 across the word boundary: MHS = PMS = the lowest variable of each
+    disjoint clause; the greedy returns the same set; decided closed form."""
+    pos, v = [], start
+    for s in sizes:
+        pos.append(list(range(v, v + s)))
+        v += s
+    m = 128
+    mk = masks_of(pos, [], W=2)
+    want = [c[0] for c in pos]
+    for r in (oracle.mhs(m, len(pos), mk, W=2), oracle.pms(m, len(pos), mk, W=2)):
+        assert r.status == SAT and vars_of(r.assign) == want and r.cost == len(pos)
+        # relabelled: support = the clauses' variables in order; x* = the first
+        # of each group; decided = sum_{k<K} C(m_eff, k) + rank + 1
+        sup = sorted(v for c in pos for v in c)
+        x = [sup.index(c[0]) + 1 for c in pos]
+        K = len(pos)
+        assert r.decided == sum(math.comb(len(sup), j) for j in range(K)) + colex_rank(x) + 1
+    st, a, _ = oracle.greedy(m, len(pos), mk, W=2)
+    assert st == SAT and synth.mask_to_vars(a) == want
+
+
+@pytest.mark.parametrize("lo,n", [(60, 8), (55, 15), (64, 5), (65, 9), (40, 30)])
+def test_w2_path(lo, n):
+    """P6 across the word boundary: a path b_lo - ... - b_{lo+n-1} has minimum
+    vertex cover floor(n/2); canonical (smallest colex rank) = odd positions for
+    odd n ({lo+1, lo+3, ...}), and for even n the colex-smallest cover."""
+    pos = [[i, i + 1] for i in range(lo, lo + n - 1)]
+    mk = masks_of(pos, [], W=2)
+    r = oracle.mhs(128, len(pos), mk, W=2)
+    assert r.cost == n // 2
+    if n % 2 == 1:
+        assert vars_of(r.assign) == list(range(lo + 1, lo + n - 1, 2))
+    if n <= 15:
+        bf = py_brute_support(pos, [])
+        assert vars_of(r.assign) == bf[1]
+
+
+def test_w2_mixed_brute_force():
+    """reduce = 1 on two-word instances with support <= 12 spread over both
+    words, unit and weighted, against the Python-sets brute force; plus the
+    MHS and its phi- flag."""
+    rng = random.Random(2022)
+    n_sat = 0
+    for trial in range(150):
+        nv = rng.randint(2, 12)
+        vars_ = sorted(rng.sample(range(1, 129), nv))
+        if not any(v > 64 for v in vars_) or not any(v <= 64 for v in vars_):
+            vars_[0], vars_[-1] = rng.randint(1, 64), rng.randint(65, 128)
+            vars_ = sorted(set(vars_))
+        pos, neg, seen = [], [], set()
+        for _ in range(rng.randint(1, 10)):
+            c = tuple(sorted(rng.sample(vars_, rng.randint(1, min(4, len(vars_))))))
+            isneg = rng.random() < 0.3
+            if (isneg, c) in seen:
+                continue
+            seen.add((isneg, c))
+            (neg if isneg else pos).append(list(c))
+        w = [rng.randint(1, 100) for _ in range(128)] if trial % 2 else None
+        mk = masks_of(pos, neg, W=2)
+        r = oracle.pms(128, len(pos), mk, w=w, reduce=1, W=2)
+        # the brute force over the occurring variables; negatives touching a
+        # variable outside phi+'s support are satisfied by keeping it false
+        bf = py_brute_support(pos, neg, w)
+        if bf is None:
+            assert r.status == UNSAT
+            continue
+        n_sat += 1
+        assert r.status == SAT and vars_of(r.assign) == bf[1] and r.cost == bf[0][0]
+        h = oracle.mhs(128, len(pos), mk, W=2)
+        bh = py_brute_support(pos, [])
+        assert vars_of(h.assign) == bh[1]
+        viol = any(set(c) <= set(bh[1]) for c in neg)
+        assert h.status == (NEGV if viol else SAT)
+    assert n_sat > 60
+
+
+def test_w2_greedy_relabel_invariance():
+    """The greedy over an instance shifted into word 1 (b_i -> b_{i+s}) picks
+    the shifted variables in the same order (ties: the shift preserves the
+    index order)."""
+    rng = random.Random(7)
+    for _ in range(60):
+        m = rng.randint(2, 12)
+        pos, neg, _ = rand_instance(rng, m, rng.randint(1, 14))
+        st, a, picks = oracle.greedy(m, len(pos), masks_of(pos, neg))
+        for s in (50, 64, 100):
+            sp = [[v + s for v in c] for c in pos]
+            sn = [[v + s for v in c] for c in neg]
+            st2, a2, p2 = oracle.greedy(128, len(pos), masks_of(sp, sn, W=2), W=2)
+            assert st2 == st and p2.tolist() == [p + s for p in picks.tolist()]
+            assert synth.mask_to_vars(a2) == [v + s for v in synth.mask_to_vars(a)]
+
+
+def test_kmax_after_subsumption_r13():
+    """Reading R13: with reduce = 1 the levels stop at k_max = min(|support|,
+    #positive clauses no other clause subsumes).  Nested clauses {b1} c {b1,b2}
+    c {b1,b2,b3} leave one minimal clause, so with not-b1 the UNSAT proof
+    enumerates levels 0 and 1 only: 1 + C(3,1) = 4 candidates (the raw clause
+    count would give 1 + 3 + 3 + 1 = 8); duplicates count once."""
+    pos, neg = [[1], [1, 2], [1, 2, 3]], [[1]]
+    r = oracle.pms(3, 3, masks_of(pos, neg), reduce=1)
+    assert r.status == UNSAT and r.decided == 1 + 3
+    assert oracle.pms(3, 3, masks_of(pos, neg), reduce=0).decided == 8
+    assert py_brute(3, pos, neg, [1] * 3) is None
+    # two disjoint minimal clauses and a superset: k_max = 2
+    pos, neg = [[1, 2], [3, 4], [1, 2, 3]], [[1], [2], [3], [4]]
+    r = oracle.pms(4, 3, masks_of(pos, neg), reduce=1)
+    assert r.status == UNSAT and r.decided == sum(math.comb(4, k) for k in range(3))
+    # a duplicated clause counts once (masks_of keeps both copies)
+    pos = [[1, 2], [1, 2]]
+    r = oracle.pms(2, 2, masks_of(pos, [[1], [2]]), reduce=1)
+    assert r.status == UNSAT and r.decided == 1 + 2
