@@ -219,27 +219,35 @@ class DeviceResult:
     def struct(self) -> GrResult:
         return GrResult(_ptr(self.assign), _ptr(self.cost), _ptr(self.status), _ptr(self.decided))
 
-    def to_host(self):
-        """-> dict of numpy arrays (assign/cost/decided as uint64)."""
-        return to_host_many([self])[0]
+    def to_host(self, stream=None):
+        """-> dict of numpy arrays (assign/cost/decided as uint64).  ``stream``:
+        the stream the result was produced on (default: the current stream of
+        its device)."""
+        return to_host_many([self], stream)[0]
 
 
-def to_host_many(results):
-    """Several DeviceResults -> dicts of numpy arrays with one synchronisation:
-    every field is copied (non-blocking) into pinned host memory on the
-    current stream, then the stream is synchronised once."""
+def to_host_many(results, stream=None):
+    """Several DeviceResults -> dicts of numpy arrays with one synchronisation
+    per device: every field is copied (non-blocking) into pinned host memory
+    on the stream that produced it -- ``stream`` if given (a torch stream, for
+    results of calls made with stream=...), else the current stream of the
+    result's device -- then each of those streams is synchronised once."""
     torch = _torch()
-    pend = []
+    pend, used = [], {}
     for r in results:
+        dev = r.status.device
+        st = stream if stream is not None else torch.cuda.current_stream(dev)
+        used[(dev, id(st))] = st
         d = {}
-        for k in ("assign", "cost", "status", "decided"):
-            t = getattr(r, k)
-            h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
-            h.copy_(t, non_blocking=True)
-            d[k] = h
+        with torch.cuda.stream(st):
+            for k in ("assign", "cost", "status", "decided"):
+                t = getattr(r, k)
+                h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+                h.copy_(t, non_blocking=True)
+                d[k] = h
         pend.append(d)
-    if results:
-        torch.cuda.current_stream(results[0].status.device).synchronize()
+    for st in used.values():
+        st.synchronize()
     out = []
     for d in pend:
         out.append({"assign": d["assign"].numpy().view(np.uint64),

@@ -44,6 +44,34 @@ void gr_prof_post(const char *name, cudaStream_t s);
 // work counters of the enumeration kernel's counting instantiation (exact.cu)
 void gr_exact_work_read(unsigned long long out[4], int reset);
 
+// ---- per-device launch settings ---------------------------------------------
+// cudaFuncSetAttribute applies per device context and occupancy depends on
+// the device: settings are computed once per device ordinal (thread-safe,
+// std::call_once) instead of once per process.
+#include <mutex>
+constexpr int GR_MAX_DEVICES = 64;
+inline int gr_device() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= GR_MAX_DEVICES) d = 0;
+  return d;
+}
+struct PerDevice {
+  std::once_flag once[GR_MAX_DEVICES];
+  int val[GR_MAX_DEVICES] = {};
+  // f() runs the first time the current device asks; its value is cached
+  template <typename F>
+  int get(F f) {
+    const int d = gr_device();
+    std::call_once(once[d], [&] { val[d] = f(); });
+    return val[d];
+  }
+};
+inline int gr_sm_count() {
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, gr_device());
+  return sms > 0 ? sms : 1;
+}
+
 // ---- binomial table C(n, k), 0 <= n, k <= 64 (C(64,32) < 2^61) ------------
 struct BinomTable {
   u64 v[65][65];

@@ -31,6 +31,7 @@
 #include <cub/block/block_scan.cuh>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <mutex>
 
@@ -54,8 +55,42 @@ struct Ctrl {
   u64 lane_cands;     // candidates per lane per chunk (L)
   unsigned fin_ticket;  // finish: blocks done committing (the last one plans)
   unsigned pad0;
-  u64 pad1[3];
+  // the level loop on the device (queue_kernel)
+  u64 q_tickets;        // tickets handed out: a CTA takes ticket e and works the task of ring entry e
+  u64 q_entries;        // ring entries allocated by enqueuers
+  long long q_budget;   // ring entries available beyond one per open instance
+  u64 q_tasks;          // task records allocated
+  int q_remaining;      // open (instance, solve) units; 0 ends the launch
+  int pad2;
+  u64 q_work;           // candidates of the published, uncommitted tasks (lane window sizing)
+  u64 pad3[5];
 };
+static_assert(sizeof(Ctrl) == 128, "Ctrl layout");
+
+// Level k of instance b of solve sv: one task record, worked by every CTA
+// whose ticket maps to one of its ring entries.
+struct Task {
+  u64 claimed;   // warp chunks handed out (atomic)
+  u64 done;      // warp chunks finished (atomic); the warp finishing the last one commits
+  u64 nchunks;   // warp chunks of the level: 32 lane windows of L candidates each
+  u64 L;         // lane window
+  int b, k, sv, pad;
+  u64 pad2[2];
+};
+static_assert(sizeof(Task) == 64, "Task layout");
+// A ring entry is one u64: generation (12 bits) | ring round of its ticket
+// (12 bits) | extra-entry flag | solve | task record index (38 bits); the
+// waiter of ticket e knows the generation and e's round, so a stale entry of
+// an earlier launch or round never matches.
+typedef u64 RingEntry;
+constexpr int QLEVELS = 66;  // task records per (instance, solve): levels 0..64 + 1
+// ring entries: a power of two above one entry per open unit of two solves
+// plus the tickets the grid can hold
+__host__ __device__ inline u64 ring_cap(int B) {
+  u64 need = 8ull * (u64)B + 16384ull, c = 65536;
+  while (c < need) c <<= 1;
+  return c;
+}
 
 #ifndef GR_JMAX
 #define GR_JMAX 13
@@ -67,7 +102,7 @@ constexpr int HX = 16;         // HIT_j({x}) is 0 for x >= R_j, and R_j <= 16 fo
 
 struct Layout {
   size_t ctrl, meff, npr, nnr, kmax, ks, done, rb, sup, decided, bestx, bestw, wtot, lvlkey, sk, wr,
-      active, chunk_base, pk, hrec, ptmp, total;
+      active, chunk_base, pk, hrec, ptmp, tasks, ring, total;
 };
 
 Layout layout_of(const gr_batch *in) {
@@ -95,6 +130,8 @@ Layout layout_of(const gr_batch *in) {
   L.ptmp = take(8 * B);
   L.pk = take(8 * (size_t)std::max<int64_t>(in->total_clauses, 1));
   L.hrec = take(16 * HREC * (size_t)std::max<int64_t>(in->total_clauses, 1));
+  L.tasks = take(sizeof(Task) * QLEVELS * B);
+  L.ring = take(sizeof(RingEntry) * ring_cap(in->B));
   L.total = o;
   return L;
 }
@@ -110,6 +147,8 @@ struct WS {
   u64 *chunk_base;
   u64 *ptmp;       // finish scratch: level size per listed position (~0: not listed)
   u64 *pk, *hrec;  // packed clause masks; [clause][HREC] two-word H_j(P) records of the positives
+  Task *tasks;     // queue_kernel: task records of this solve
+  RingEntry *ring; // queue_kernel: the ticket ring (the first solve's)
 };
 
 WS ws_of(const gr_batch *in, void *base) {
@@ -137,6 +176,8 @@ WS ws_of(const gr_batch *in, void *base) {
   w.ptmp = (u64 *)(p + L.ptmp);
   w.pk = (u64 *)(p + L.pk);
   w.hrec = (u64 *)(p + L.hrec);
+  w.tasks = (Task *)(p + L.tasks);
+  w.ring = (RingEntry *)(p + L.ring);
   return w;
 }
 
@@ -613,8 +654,8 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
   // ---- position the iterator on the sub-block that holds rank r_lo: colex
   // unrank of r_lo (element i is the largest c with C(c, i) <= the remaining
   // rank); the top k - J elements (binary search) form Utop, the J lowest go
-  // to s[] (downward scan over the shared binomial table)
-  int s[JMAX];  // the J lowest elements of x, ascending
+  // to the mask Slow (downward scan over the shared binomial table)
+  M Slow = 0;  // the J lowest elements of x (a register mask: no local-memory array)
   M Utop = 0;
   u64 rr = r_lo, base_top;
   {
@@ -633,7 +674,7 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
     for (int i = J; i >= 1; i--) {
       u64 v;
       while ((v = CS(cc, i)) > rr) cc--;
-      s[i - 1] = cc;
+      Slow |= (M)1 << cc;
       rr -= v;
       cc--;
     }
@@ -654,13 +695,16 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
   u64 base = base_top;
   int d = 0, j = J, e = e_top, ep = e_top;
   u64 tp = 0;
-  // descend: at node j, x lies in part B iff its j-th lowest element
-  // s[j-1] >= R_j; then the child is t = s[j-1].  An ancestor whose whole
-  // subtree is refuted stops the descent: the walk resumes after it (without
-  // this a window starting deep inside a refuted subtree would refute each
-  // remaining sibling on the path one by one).
+  // descend: at node j, x lies in part B iff its j-th lowest element (the
+  // highest of the j elements left in Slow) is >= R_j; then the child is
+  // t = that element.  An ancestor whose whole subtree is refuted stops the
+  // descent: the walk resumes after it (without this a window starting deep
+  // inside a refuted subtree would refute each remaining sibling on the path
+  // one by one).
   bool dead0 = false;
-  while (j >= 2 && s[j - 1] >= region_of(j)) {
+  while (j >= 2) {
+    const int t = (int)(8 * sizeof(M) - 1) - (sizeof(M) == 4 ? __clz((int)Slow) : __clzll((long long)Slow));
+    if (t < c.reg[j]) break;
     if (prune) {
       const int kind = refuted_by<M, COUNT>(j, U, e, c, wk);
       if (kind == 1 || (kind == 2 && !wm)) {
@@ -668,7 +712,7 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
         break;
       }
     }
-    const int t = s[j - 1];
+    Slow ^= (M)1 << t;
     if (d > 0) tp = (tp << SB) | (u64)ep;
     ep = e;
     e = t;
@@ -1255,6 +1299,424 @@ __global__ void __launch_bounds__(FT, 1) finish_fused_kernel(In in1, Out out1, W
 }
 
 // ---------------------------------------------------------------------------
+// queue_kernel: the whole level loop of a solve in ONE persistent launch
+// ---------------------------------------------------------------------------
+// each instance runs its own level loop on the device.  The
+// unit of work is a task = level k of instance b of solve sv (§8(a) a3); its
+// colex rank range [0, C(m_eff, k)) is cut into warp chunks of 32 lane
+// windows (a4).  Tasks are published into a ticket ring: a CTA takes the next
+// ticket (one atomic), waits until the ring entry of that ticket is written,
+// stages the task's instance (clause records, a5) and its warps pull warp
+// chunks from the task's claim counter until it is exhausted -- a warp never
+// waits for the other warps of its CTA except when the CTA changes task.  A
+// task with many chunks gets up to one ring entry per CTA so that every idle
+// CTA can join it.  The warp that finishes the last chunk of a task commits
+// the level (a6, a7: decode, weighted incumbent, S_k stop rule, k_max) and
+// either finishes the instance or publishes level k+1.  Instances progress
+// independently: no grid-wide barrier per level, no finish launch, no host
+// round trip.
+struct QParams {
+  WS ws[2];        // solve workspaces: ws[0] holds the ring and the control block
+  In in[2];
+  Out out[2];
+  int which[2];    // 0 PMS / WPMS, 1 MHS (for write_result)
+  int weighted[2]; // solve sv is weighted (MODE 2)
+  int nsolve;      // 1, or 2 independent solves sharing the launch
+  int fused;       // 1: one walk decides PMS (ws[0]) and MHS (ws[1]) of each instance (MODE 3)
+  int exhaustive, prune;
+  u64 gen;         // launch generation, 1..4095 (ring entries)
+  u64 ring_mask;   // ring entries - 1
+  int ring_log2;   // log2(ring entries)
+  int lanes;       // threads of the grid (lane window sizing)
+  int grid, nwarps;  // CTAs of the queue_kernel grid, warps per CTA (ring entries per task)
+  int wpl;         // lane windows per lane (unit | weighted << 16)
+  u64 lane_max, lane_max_w, fixed_lane;
+};
+
+__device__ __forceinline__ u64 vld(const u64 *p) { return *(const volatile u64 *)p; }
+__device__ __forceinline__ i64 vld(const i64 *p) { return *(const volatile i64 *)p; }
+__device__ __forceinline__ int vld(const int *p) { return *(const volatile int *)p; }
+
+// the ring entry a waiter of ticket e expects, minus its payload
+__device__ __forceinline__ u64 ring_stamp(const QParams &P, u64 e) {
+  return (P.gen << 52) | (((e >> P.ring_log2) & 0xfffull) << 40);
+}
+
+// Prepare level k of (b, sv) and write its task record (lane 0 of a warp, or
+// one seed thread).  work = candidates in flight including this level (lane
+// window sizing).  Returns the number of ring entries to publish (0 if the
+// instance cannot go on: its weighted key would not fit 63 bits -- status
+// GR_UNSUPPORTED, written here), the task word in *word and the first entry
+// index in *e0.
+__device__ u64 q_prepare(const QParams &P, int sv, int b, int k, u64 work, u64 *word, u64 *e0) {
+  const WS &w = P.ws[sv];
+  const int me = w.meff[b];
+  const u64 ck = binom(me, k);
+  if (P.weighted[sv]) {
+    const int rb = bitlen(ck - 1);
+    if (bitlen(vld(&w.wtot[b])) + rb > 63) {  // key (W << rb | rank) would not fit
+      w.done[b] = 1;
+      write_result(P.in[sv], P.out[sv], b, GR_UNSUPPORTED, 0, 0, 0, 0, vld(&w.decided[b]), P.which[sv]);
+      return 0;
+    }
+    w.rb[b] = rb;
+  }
+  w.lvlkey[b] = GR_KEY_NONE;
+  if (P.fused && !vld(&P.ws[1].done[b])) P.ws[1].lvlkey[b] = GR_KEY_NONE;
+  // lane window: about wpl windows per lane of the grid over all the work in
+  // flight, a power of two in [256, lane_max]
+  const bool wt = P.weighted[sv] != 0;
+  const u64 wpl = wt ? (u64)(P.wpl >> 16) : (u64)(P.wpl & 0xffff);
+  const u64 Lmax = wt ? P.lane_max_w : P.lane_max;
+  u64 L = work / ((u64)P.lanes * (wpl ? wpl : 2));
+  L = L < 256 ? 256 : (L > Lmax ? Lmax : L);
+  L = 1ull << (63 - __clzll((long long)L));
+  if (P.fixed_lane) L = P.fixed_lane;
+  const u64 nch = (ck + 32 * L - 1) / (32 * L);
+  // task records of solve sv live in its own workspace (<= 65 per instance)
+  const u64 ti = atomicAdd((unsigned long long *)&w.ctrl->q_tasks, 1ull);
+  Task *T = w.tasks + ti;
+  T->claimed = 0;
+  T->done = 0;
+  T->nchunks = nch;
+  T->L = L;
+  T->b = b;
+  T->k = k;
+  T->sv = sv;
+  // ring entries: one, plus one per further (warps per CTA) chunks up to the
+  // grid, as far as the extra-entry budget allows
+  Ctrl *c = P.ws[0].ctrl;
+  const u64 nw = (u64)P.nwarps;
+  u64 extra = (nch + nw - 1) / nw;
+  extra = (extra > (u64)P.grid ? (u64)P.grid : extra) - 1;
+  if (extra) {
+    const long long got = (long long)atomicAdd((unsigned long long *)&c->q_budget,
+                                               (unsigned long long)(-(long long)extra));
+    if (got < (long long)extra) {
+      atomicAdd((unsigned long long *)&c->q_budget, (unsigned long long)extra);
+      extra = 0;
+    }
+  }
+  *e0 = atomicAdd((unsigned long long *)&c->q_entries, extra + 1);
+  *word = ti | ((u64)sv << 38);
+  __threadfence();  // the task record before any of its entries
+  return extra + 1;
+}
+// entry i of a task: written by any thread after q_prepare's fence
+__device__ __forceinline__ void q_publish(const QParams &P, u64 word, u64 e0, u64 i) {
+  const u64 e = e0 + i;
+  *(volatile u64 *)&P.ws[0].ring[e & P.ring_mask] = ring_stamp(P, e) | (i ? (1ull << 39) : 0ull) | word;
+}
+
+// Commit level k of solve s for instance b (finish_commit for one instance).
+// Returns whether solve s still searches.  Single thread.
+__device__ bool q_commit_one(const QParams &P, int s, int b, int k) {
+  const WS &w = P.ws[s];
+  if (vld(&w.done[b])) return false;
+  const In &in = P.in[s];
+  const Out &out = P.out[s];
+  const int me = w.meff[b];
+  const u64 ck = binom(me, k);
+  const i64 key = vld(&w.lvlkey[b]);
+  const u64 s0 = w.sup[2 * b], s1 = w.sup[2 * b + 1];
+  const u64 dec = vld(&w.decided[b]);
+  if (!P.weighted[s]) {
+    if (key != GR_KEY_NONE) {
+      const u64 x = unrank_colex((u64)key, k, me);
+      const u64 d = sat_add(dec, P.exhaustive ? ck : (u64)key + 1);
+      w.done[b] = 1;
+      write_result(in, out, b, GR_SAT, x, s0, s1, (u64)k, d, P.which[s]);
+      return false;
+    }
+    w.decided[b] = sat_add(dec, ck);
+    if (k >= w.kmax[b]) {
+      w.done[b] = 1;
+      write_result(in, out, b, GR_UNSAT, 0, s0, s1, 0, sat_add(dec, ck), P.which[s]);
+      return false;
+    }
+    return true;
+  }
+  const u64 d = sat_add(dec, ck);
+  w.decided[b] = d;
+  u64 bw = vld(&w.bestw[b]);
+  if (key != GR_KEY_NONE) {
+    const int rb = w.rb[b];
+    const u64 Wk = (u64)key >> rb;
+    const u64 rank = (u64)key & ((rb ? (1ull << rb) : 1ull) - 1ull);
+    if (Wk < bw) {  // strictly smaller W replaces the incumbent (R3)
+      bw = Wk;
+      w.bestw[b] = Wk;
+      w.bestx[b] = unrank_colex(rank, k, me);
+    }
+  }
+  const bool stop = k >= w.kmax[b] || (bw != ~0ull && w.sk[(size_t)b * 65 + k + 1] >= bw);
+  if (stop) {
+    w.done[b] = 1;
+    if (bw != ~0ull) write_result(in, out, b, GR_SAT, vld(&w.bestx[b]), s0, s1, bw, d, P.which[s]);
+    else write_result(in, out, b, GR_UNSAT, 0, s0, s1, 0, d, P.which[s]);
+    return false;
+  }
+  return true;
+}
+
+// The warp that finished the last chunk of (sv, b, k), all 32 lanes: lane 0
+// commits and prepares level k+1 (or retires the instance), then the lanes
+// publish its ring entries together.
+__device__ void q_commit_warp(const QParams &P, int sv, int b, int k) {
+  const int lane = threadIdx.x & 31;
+  u64 n = 0, word = 0, e0 = 0;
+  if (lane == 0) {
+    Ctrl *c = P.ws[0].ctrl;
+    const u64 ck = binom(P.ws[sv].meff[b], k);
+    atomicAdd((unsigned long long *)&c->q_work, (unsigned long long)(-(long long)ck));
+    bool open;
+    if (P.fused) {
+      const bool o0 = q_commit_one(P, 0, b, k);
+      const bool o1 = q_commit_one(P, 1, b, k);
+      open = o0 || o1;
+    } else {
+      open = q_commit_one(P, sv, b, k);
+    }
+    if (open && k < 64) {
+      const u64 ck1 = binom(P.ws[sv].meff[b], k + 1);
+      const u64 wk = atomicAdd((unsigned long long *)&c->q_work, (unsigned long long)ck1) + ck1;
+      n = q_prepare(P, sv, b, k + 1, wk, &word, &e0);
+      if (!n) atomicAdd((unsigned long long *)&c->q_work, (unsigned long long)(-(long long)ck1));
+    }
+    if (!n) {
+      __threadfence();  // results before the count that ends the launch
+      atomicSub(&c->q_remaining, 1);
+    }
+  }
+  n = __shfl_sync(0xffffffffu, n, 0);
+  word = __shfl_sync(0xffffffffu, word, 0);
+  e0 = __shfl_sync(0xffffffffu, e0, 0);
+  for (u64 i = lane; i < n; i += 32) q_publish(P, word, e0, i);
+}
+
+// one CTA: initialise the ring budget and the work in flight, then publish
+// the first level of every open (instance, solve) and count them (the pack
+// zeroed the queue counters)
+__global__ void __launch_bounds__(1024) queue_seed_kernel(QParams P, long long budget) {
+  __shared__ unsigned long long s_work;
+  if (threadIdx.x == 0) {
+    P.ws[0].ctrl->q_budget = budget;
+    s_work = 0;
+  }
+  __syncthreads();
+  const int ns = P.fused ? 1 : P.nsolve;
+  u64 my = 0;
+  for (int sv = 0; sv < ns; sv++)
+    for (int b = threadIdx.x; b < P.in[sv].B; b += blockDim.x) {
+      const WS &w = P.ws[sv];
+      if (!w.done[b] || (P.fused && !P.ws[1].done[b])) my += binom(w.meff[b], w.ks[b]);
+    }
+  atomicAdd(&s_work, (unsigned long long)my);
+  __syncthreads();
+  const u64 work = s_work;
+  if (threadIdx.x == 0) P.ws[0].ctrl->q_work = work;
+  for (int sv = 0; sv < ns; sv++)
+    for (int b = threadIdx.x; b < P.in[sv].B; b += blockDim.x) {
+      const WS &w = P.ws[sv];
+      if (!(!w.done[b] || (P.fused && !P.ws[1].done[b]))) continue;
+      atomicAdd(&P.ws[0].ctrl->q_remaining, 1);
+      u64 word, e0;
+      const u64 n = q_prepare(P, sv, b, w.ks[b], work, &word, &e0);
+      if (!n) {
+        atomicSub(&P.ws[0].ctrl->q_remaining, 1);
+        atomicAdd((unsigned long long *)&P.ws[0].ctrl->q_work,
+                  (unsigned long long)(-(long long)binom(w.meff[b], w.ks[b])));
+      }
+      for (u64 i = 0; i < n; i++) q_publish(P, word, e0, i);
+    }
+}
+
+// KIND 0: unit-weight solves (MODE 0, or 1 when exhaustive); 1: the fused
+// PMS + MHS walk (MODE 3); 2: weighted PMS (MODE 2), possibly with an MHS
+// (MODE 0) in the same launch
+template <typename M, int KIND, bool COUNT>
+__device__ __forceinline__ i64 q_walk(const QParams &P, int sv, int need, int k, int me, u64 r_lo,
+                                      u64 cnt, const Clauses<M> &cc, const u32 *sw, int rb,
+                                      Work &wk, const u64 *skj, u64 wstar, i64 *key_m) {
+  if (KIND == 1)
+    return walk<M, 3, COUNT>(k, me, r_lo, cnt, cc, sw, rb, P.prune, wk, nullptr, ~0ull, need & 1,
+                             need >> 1, key_m, P.exhaustive);
+  if (KIND == 2 && P.weighted[sv])
+    return walk<M, 2, COUNT>(k, me, r_lo, cnt, cc, sw, rb, P.prune, wk, skj, wstar);
+  if (P.exhaustive) return walk<M, 1, COUNT>(k, me, r_lo, cnt, cc, sw, rb, P.prune, wk);
+  return walk<M, 0, COUNT>(k, me, r_lo, cnt, cc, sw, rb, P.prune, wk);
+}
+
+template <bool COUNT, int NTK, int KIND>
+__global__ void __launch_bounds__(NTK, COUNT ? 1 : ENUM_CTAS * NT / NTK) queue_kernel(QParams P) {
+  extern __shared__ u64 cls[];  // tables, then the staged clause records
+  __shared__ int s_b, s_k, s_sv, s_cur, s_exit;
+  __shared__ u64 s_ti, s_L, s_nch, s_ck;
+  __shared__ u64 s_skj[JMAX + 1], s_wstar;  // weighted: S_j and the incumbent W*
+  __shared__ u32 s_w[64];
+  const int t = threadIdx.x, lane = t & 31;
+  if (t == 0) s_cur = -1;
+  F2 *hitx = (F2 *)cls;
+  u64 *cs = cls + 2 * (JMAX + 1) * HX;
+  F2 *lowb = (F2 *)(cs + 65 * (JMAX + 1));
+  for (int q = t; q < (JMAX + 1) * HX; q += NTK)
+    hitx[q] = F2{g_hit.lo[64 * (q / HX) + q % HX], g_hit.hi[64 * (q / HX) + q % HX]};
+  for (int q = t; q < 65 * (JMAX + 1); q += NTK) cs[q] = binom(q / (JMAX + 1), q % (JMAX + 1));
+  for (int q = t; q < 129; q += NTK) lowb[q] = f2_nbits((u64)q);
+  int *reg = (int *)(lowb + 129);
+  if (t <= JMAX) reg[t] = t ? region_of(t) : 0;
+  unsigned char *nb = (unsigned char *)(reg + 16);
+  for (int q = t; q < (JMAX + 1) * 65; q += NTK) {
+    const int jj = q / 65, ee = q % 65;
+    nb[q] = jj ? (unsigned char)binom(ee < region_of(jj) ? ee : region_of(jj), jj) : 0;
+  }
+  u64 *stage = cls + TAB_SMEM / 8;
+  for (;;) {
+    // ---- thread 0: take a ticket, wait for its ring entry (or the end)
+    if (t == 0) {
+      Ctrl *ctrl = P.ws[0].ctrl;
+      const u64 e = atomicAdd((unsigned long long *)&ctrl->q_tickets, 1ull);
+      const u64 *r = P.ws[0].ring + (e & P.ring_mask);
+      const u64 want = ring_stamp(P, e);
+      int ex = 0;
+      u64 v = 0;
+      for (int spin = 0;; spin++) {
+        v = vld(r);
+        if ((v & ~((1ull << 40) - 1ull)) == want) break;
+        if (vld(&ctrl->q_remaining) == 0) { ex = 1; break; }
+        __nanosleep(spin < 16 ? 32 : 128);
+      }
+      s_exit = ex;
+      if (!ex) {
+        __threadfence();  // the task record after its entry
+        if (v >> 39 & 1ull) atomicAdd((unsigned long long *)&ctrl->q_budget, 1ull);  // an extra entry is read
+        const int tsv = (int)((v >> 38) & 1ull);
+        const u64 ti = v & ((1ull << 38) - 1ull);
+        const Task *T = P.ws[tsv].tasks + ti;
+        s_ti = ti;
+        s_sv = tsv;
+        s_b = vld(&T->b);
+        s_k = vld(&T->k);
+        s_L = vld(&T->L);
+        s_nch = vld(&T->nchunks);
+        s_ck = binom(P.ws[tsv].meff[s_b], s_k);
+      }
+    }
+    __syncthreads();
+    if (s_exit) break;
+    {
+      const int b = s_b, sv = s_sv;
+      const WS &w = P.ws[sv];
+      const int np = w.npr[b], nn = w.nnr[b];
+      const int64_t lo = P.in[sv].off[b];
+      const bool staged = np + nn <= smc_of<NTK>();
+      F2 *sH = (F2 *)stage;
+      u64 *sP = stage + (size_t)2 * HREC * np;
+      const int key_cur = sv * P.in[0].B + b;
+      if (key_cur != s_cur) {  // stage the instance's clause records
+        if (staged) {
+          for (int q = t; q < np * HREC; q += NTK) sH[q] = ((const F2 *)w.hrec)[lo * HREC + q];
+          if (w.meff[b] <= 32) {
+            u32 *c32 = (u32 *)sP;
+            for (int q = t; q < np + nn; q += NTK) c32[q] = (u32)w.pk[lo + q];
+          } else {
+            for (int q = t; q < np + nn; q += NTK) sP[q] = w.pk[lo + q];
+          }
+        }
+        if (t < 64) s_w[t] = w.wr[(size_t)b * 64 + t];
+        if (KIND == 2 && t <= JMAX) s_skj[t] = w.sk[(size_t)b * 65 + t];
+      }
+      if (KIND == 2 && t == 0) s_wstar = vld(&w.bestw[b]);  // incumbent of earlier levels
+    }
+    __syncthreads();
+    if (t == 0) s_cur = s_sv * P.in[0].B + s_b;
+    // ---- warps pull warp chunks of this task until it is exhausted
+    for (;;) {
+      const int b = s_b, sv = s_sv;
+      Task *T = P.ws[sv].tasks + s_ti;
+      const u64 nch = s_nch;
+      u64 c = 0;
+      int need = 0;  // bit 0: the chunk is needed (fused: for the PMS); bit 1: fused, for the MHS
+      if (lane == 0) {
+        c = atomicAdd((unsigned long long *)&T->claimed, 1ull);
+        if (c < nch) {
+          const u64 r0 = c * 32 * s_L;
+          if (KIND == 1) {
+            const i64 c1 = vld(&P.ws[0].lvlkey[b]), c2 = vld(&P.ws[1].lvlkey[b]);
+            const int np_ = !vld(&P.ws[0].done[b]) && !(c1 != GR_KEY_NONE && (u64)c1 < r0 && !P.exhaustive);
+            const int nm_ = !vld(&P.ws[1].done[b]) && !(c2 != GR_KEY_NONE && (u64)c2 < r0 && !P.exhaustive);
+            need = np_ | (nm_ << 1);
+          } else if (!P.weighted[sv] && !P.exhaustive) {
+            const i64 cur = vld(&P.ws[sv].lvlkey[b]);
+            need = !(cur != GR_KEY_NONE && (u64)cur < r0);  // a lower witness exists
+          } else {
+            need = 1;
+          }
+        }
+      }
+      c = __shfl_sync(0xffffffffu, c, 0);
+      if (c >= nch) break;
+      need = __shfl_sync(0xffffffffu, need, 0);
+      i64 key = GR_KEY_NONE, key_m = GR_KEY_NONE;
+      Work wk;
+      {
+        const WS &w = P.ws[sv];
+        const u64 L = s_L, ck = s_ck;
+        const int k = s_k, me = w.meff[b], np = w.npr[b], nn = w.nnr[b];
+        const u64 r_lo = c * 32 * L + (u64)lane * L;
+        if (need && r_lo < ck) {
+          const u64 cnt = (ck - r_lo) < L ? (ck - r_lo) : L;
+          const int64_t lo = P.in[sv].off[b];
+          const bool staged = np + nn <= smc_of<NTK>();
+          const int rb = KIND == 2 ? w.rb[b] : 0;
+          F2 *sH = (F2 *)stage;
+          u64 *sP = stage + (size_t)2 * HREC * np;
+          if (staged && me <= 32) {
+            Clauses<u32> cc{(const u32 *)sP, sH, hitx, lowb, reg, nb, cs, np, nn};
+            key = q_walk<u32, KIND, COUNT>(P, sv, need, k, me, r_lo, cnt, cc, s_w, rb, wk, s_skj, s_wstar, &key_m);
+          } else if (staged) {
+            Clauses<u64> cc{sP, sH, hitx, lowb, reg, nb, cs, np, nn};
+            key = q_walk<u64, KIND, COUNT>(P, sv, need, k, me, r_lo, cnt, cc, s_w, rb, wk, s_skj, s_wstar, &key_m);
+          } else {
+            Clauses<u64> cc{w.pk + lo, (const F2 *)w.hrec + lo * HREC, hitx, lowb, reg, nb, cs, np, nn};
+            key = q_walk<u64, KIND, COUNT>(P, sv, need, k, me, r_lo, cnt, cc, s_w, rb, wk, s_skj, s_wstar, &key_m);
+          }
+        }
+      }
+      if (COUNT) {
+        u64 a0 = wk.tests, a1 = wk.blocks, a2 = wk.cands;
+        for (int o = 16; o; o >>= 1) {
+          a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+          a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+          a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+        }
+        if (lane == 0) {
+          atomicAdd(&g_work[0], (unsigned long long)a0);
+          atomicAdd(&g_work[1], (unsigned long long)a1);
+          atomicAdd(&g_work[2], (unsigned long long)a2);
+          if (P.ws[s_sv].meff[s_b] > 32) atomicAdd(&g_work[3], (unsigned long long)a0);
+        }
+      }
+      key = warp_min(key);
+      if (KIND == 1) key_m = warp_min(key_m);
+      int last = 0;
+      if (lane == 0) {
+        const int b2 = s_b, sv2 = s_sv;
+        if (key != GR_KEY_NONE) atomicMin((long long *)&P.ws[sv2].lvlkey[b2], (long long)key);
+        if (KIND == 1 && key_m != GR_KEY_NONE) atomicMin((long long *)&P.ws[1].lvlkey[b2], (long long)key_m);
+        __threadfence();  // the keys before the completion count
+        Task *T2 = P.ws[sv2].tasks + s_ti;
+        last = atomicAdd((unsigned long long *)&T2->done, 1ull) == s_nch - 1;
+        if (last) __threadfence();
+      }
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (last) q_commit_warp(P, s_sv, s_b, s_k);
+    }
+    __syncthreads();  // every warp is done with this task's staging
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 int validate_batch(const gr_batch *in, int which) {
@@ -1270,26 +1732,20 @@ int validate_batch(const gr_batch *in, int which) {
   return GR_OK;
 }
 
-std::mutex g_occ_mu;
-int g_enum_grid[2] = {0, 0};
-
 template <int NTK>
 int enum_grid_of() {
-  int dev = 0, sms = 0, per = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int per = 0;
   const size_t smem = enum_smem_of<NTK>();
   cudaFuncSetAttribute(enum_kernel<false, NTK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(enum_kernel<true, NTK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, enum_kernel<false, NTK>, NTK, smem);
-  return sms * (per < 1 ? 1 : per);
+  return gr_sm_count() * (per < 1 ? 1 : per);
 }
-// grid of the NT-thread (small = false) or NT/2-thread enumeration CTA
+// grid of the NT-thread (small = false) or NT/2-thread enumeration CTA, per
+// device (the smem attribute is set on each device's first use)
+PerDevice g_enum_grid[2];
 int enum_grid(bool small = false) {
-  std::lock_guard<std::mutex> lk(g_occ_mu);
-  int &g = g_enum_grid[small ? 1 : 0];
-  if (!g) g = small ? enum_grid_of<NT_SMALL>() : enum_grid_of<NT>();
-  return g;
+  return small ? g_enum_grid[1].get(enum_grid_of<NT_SMALL>) : g_enum_grid[0].get(enum_grid_of<NT>);
 }
 // the small CTA shape when every instance's clauses fit its staging area
 bool enum_small(const gr_batch *in) {
@@ -1306,38 +1762,34 @@ int launch_enum(const EnumParams &p, bool small, cudaStream_t st) {
   return GR_OK;
 }
 
+// environment knobs, read once (thread-safe static init)
 u64 lane_cands_raw() {
-  static u64 v = 0;
-  if (!v) {
+  static const u64 v = [] {
     const char *e = getenv("GR_LANE_CANDIDATES");
-    v = e ? strtoull(e, nullptr, 10) : 0ull;  // 0: adaptive per level
-    if (v > (1ull << 20)) v = 1ull << 20;      // the walk keeps window positions in 32 bits
-    if (!e) v = ~0ull;
-  }
+    if (!e) return ~0ull;
+    u64 x = strtoull(e, nullptr, 10);       // 0: adaptive per level
+    return x > (1ull << 20) ? (1ull << 20) : x;  // the walk keeps window positions in 32 bits
+  }();
   return v;
 }
 int windows_per_lane(bool weighted) {  // adaptive lane window: windows per lane per level
-  static int v[2] = {0, 0};              // GR_WINDOWS_PER_LANE / _W override
-  const int i = weighted ? 1 : 0;
-  if (!v[i]) {
-    const char *e = getenv(weighted ? "GR_WINDOWS_PER_LANE_W" : "GR_WINDOWS_PER_LANE");
-    const int dflt = weighted ? 4 : 3;
-    v[i] = e ? atoi(e) : dflt;
-    if (v[i] < 1 || v[i] > 0xffff) v[i] = dflt;
-  }
-  return v[i];
+  auto rd = [](const char *name, int dflt) {  // GR_WINDOWS_PER_LANE / _W override
+    const char *e = getenv(name);
+    const int x = e ? atoi(e) : dflt;
+    return (x < 1 || x > 0xffff) ? dflt : x;
+  };
+  static const int v[2] = {rd("GR_WINDOWS_PER_LANE", 3), rd("GR_WINDOWS_PER_LANE_W", 4)};
+  return v[weighted ? 1 : 0];
 }
 u64 lane_max(bool weighted) {  // the adaptive lane window's upper bound
-  static u64 v[2] = {0, 0};     // GR_LANE_MAX / GR_LANE_MAX_W override
-  const int i = weighted ? 1 : 0;
-  if (!v[i]) {
-    const char *e = getenv(weighted ? "GR_LANE_MAX_W" : "GR_LANE_MAX");
-    const u64 dflt = weighted ? 65536ull : 262144ull;
-    v[i] = e ? strtoull(e, nullptr, 10) : dflt;
-    if (v[i] > (1ull << 24)) v[i] = 1ull << 24;
-    if (v[i] < 256) v[i] = dflt;
-  }
-  return v[i];
+  auto rd = [](const char *name, u64 dflt) {  // GR_LANE_MAX / GR_LANE_MAX_W override
+    const char *e = getenv(name);
+    u64 x = e ? strtoull(e, nullptr, 10) : dflt;
+    if (x > (1ull << 24)) x = 1ull << 24;
+    return x < 256 ? dflt : x;
+  };
+  static const u64 v[2] = {rd("GR_LANE_MAX", 262144ull), rd("GR_LANE_MAX_W", 65536ull)};
+  return v[weighted ? 1 : 0];
 }
 u64 lane_cands() {  // 0 = adaptive (GR_LANE_CANDIDATES overrides)
   const u64 v = lane_cands_raw();
@@ -1385,11 +1837,8 @@ int launch_pack(const gr_batch *in, int which, const gr_result *out, const WS &w
   c.lane_cands = lane_cands();
   GR_CUDA(cudaMemcpyAsync(w.ctrl, &c, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
   size_t smem = (size_t)std::max(in->max_clauses, 1) * 13 + 16;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MAXC * 13 + 16);
-    attr = true;
-  }
+  static PerDevice attr;
+  attr.get([] { return (int)cudaFuncSetAttribute(pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MAXC * 13 + 16); });
   GR_LAUNCH("pack_kernel", st, pack_kernel<<<in->B, PT, smem, st>>>(in_of(in, which), out_of(out), w, which));
   return GR_OK;
 }
@@ -1477,19 +1926,127 @@ extern "C" int gr_exact_finish(const gr_batch *in, int which, int k, gr_result *
   return GR_OK;
 }
 
+// s_other waits for the work queued on st so far (results ordered on both)
+static int stream_join(cudaStream_t st, cudaStream_t s_other) {
+  if (s_other == st) return GR_OK;
+  cudaEvent_t ev;
+  GR_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  GR_CUDA(cudaEventRecord(ev, st));
+  GR_CUDA(cudaStreamWaitEvent(s_other, ev, 0));
+  GR_CUDA(cudaEventDestroy(ev));
+  return GR_OK;
+}
+
 // levels queued per host read-back of n_active (GR_SPEC_LEVELS)
 static int spec_levels() {
-  static int v = 0;
-  if (!v) {
+  static const int v = [] {
     const char *e = getenv("GR_SPEC_LEVELS");
-    v = e ? atoi(e) : 4;
-    if (v < 1 || v > 64) v = 4;
-  }
+    const int x = e ? atoi(e) : 4;
+    return (x < 1 || x > 64) ? 4 : x;
+  }();
   return v;
 }
 
+// ---- the device level loop (queue_kernel) ------------------------------------
+namespace {
+std::atomic<unsigned long long> g_qgen{0};
+template <int NTK, int KIND>
+void queue_attr() {
+  const int smem = (int)enum_smem_of<NTK>();
+  cudaFuncSetAttribute(queue_kernel<false, NTK, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(queue_kernel<true, NTK, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+}
+template <int NTK>
+int queue_grid_of() {
+  int per = 0;
+  queue_attr<NTK, 0>();
+  queue_attr<NTK, 1>();
+  queue_attr<NTK, 2>();
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, queue_kernel<false, NTK, 0>, NTK, enum_smem_of<NTK>());
+  return gr_sm_count() * (per < 1 ? 1 : per);
+}
+PerDevice g_queue_grid[2];
+int queue_grid(bool small) {
+  return small ? g_queue_grid[1].get(queue_grid_of<NT_SMALL>) : g_queue_grid[0].get(queue_grid_of<NT>);
+}
+// GR_HOST_LOOP=1: the level-synchronous host loop (enum + finish launches per
+// level) instead of queue_kernel -- A/B timing and cross-checks only
+bool host_loop() {
+  static const bool v = getenv("GR_HOST_LOOP") != nullptr;
+  return v;
+}
+
+template <bool COUNT, int NTK, int KIND>
+int launch_queue_t(QParams &P, int B, cudaStream_t st) {
+  const int grid = queue_grid(NTK == NT_SMALL);
+  P.grid = grid;
+  P.nwarps = NTK / 32;
+  P.lanes = grid * NTK;
+  // extra ring entries beyond one per open unit and the tickets the grid holds
+  const long long budget = (long long)ring_cap(B) - (long long)(P.fused ? 1 : P.nsolve) * B -
+                           2ll * grid - 64;
+  GR_LAUNCH("queue_seed_kernel", st, queue_seed_kernel<<<1, 1024, 0, st>>>(P, budget));
+  GR_LAUNCH("queue_kernel", st, (queue_kernel<COUNT, NTK, KIND><<<grid, NTK, enum_smem_of<NTK>(), st>>>(P)));
+  return GR_OK;
+}
+
+// one launch for the level loops of one solve (nsolve = 1), of two
+// independent solves of the same batch (nsolve = 2: weighted PMS + MHS), or
+// of the fused PMS + MHS walk (fused = 1); the packs already ran on st
+int launch_queue(const gr_batch *in, int nsolve, int fused, const int which[2], gr_result *o0,
+                 gr_result *o1, const WS &w0, const WS &w1, cudaStream_t st) {
+  QParams P{};
+  P.ws[0] = w0;
+  P.ws[1] = w1;
+  P.in[0] = in_of(in, which[0]);
+  P.in[1] = in_of(in, which[1]);
+  P.out[0] = out_of(o0);
+  P.out[1] = out_of(o1 ? o1 : o0);
+  for (int q = 0; q < 2; q++) {
+    P.which[q] = which[q];
+    P.weighted[q] = (!fused && P.in[q].w != nullptr) ? 1 : 0;
+  }
+  P.nsolve = nsolve;
+  P.fused = fused;
+  P.exhaustive = (in->flags & GR_FLAG_EXHAUSTIVE) ? 1 : 0;
+  P.prune = (in->flags & GR_FLAG_NO_PRUNE) ? 0 : 1;
+  P.gen = g_qgen.fetch_add(1) % 4095ull + 1ull;  // 1..4095
+  P.ring_mask = ring_cap(in->B) - 1;
+  P.ring_log2 = 63 - __builtin_clzll(ring_cap(in->B));
+  P.wpl = windows_per_lane(false) | (windows_per_lane(true) << 16);
+  P.lane_max = lane_max(false);
+  P.lane_max_w = lane_max(true);
+  P.fixed_lane = lane_cands();
+  const bool small = enum_small(in);
+  const int kind = fused ? 1 : ((P.weighted[0] || P.weighted[1]) ? 2 : 0);
+#define GR_QLAUNCH(COUNT, NTK)                                              \
+  return kind == 0 ? launch_queue_t<COUNT, NTK, 0>(P, in->B, st)            \
+         : kind == 1 ? launch_queue_t<COUNT, NTK, 1>(P, in->B, st)          \
+                     : launch_queue_t<COUNT, NTK, 2>(P, in->B, st)
+  if (gr_prof_mode() == 2) {
+    if (small) GR_QLAUNCH(true, NT_SMALL);
+    GR_QLAUNCH(true, NT);
+  }
+  if (small) GR_QLAUNCH(false, NT_SMALL);
+  GR_QLAUNCH(false, NT);
+#undef GR_QLAUNCH
+}
+}  // namespace
+
 static int solve_exact(const gr_batch *in, gr_result *out, void *ws, size_t ws_bytes, gr_stream_t s,
                        int which) {
+  if (!host_loop()) {
+    int rc = validate_batch(in, which);
+    if (rc) return rc;
+    if (!out || !out->assign || !out->cost || !out->status) { gr_set_error("null result pointer"); return GR_EINVAL; }
+    Layout L = layout_of(in);
+    if (!ws || ws_bytes < L.total) { gr_set_error("workspace too small"); return GR_EWORKSPACE; }
+    WS w = ws_of(in, ws);
+    cudaStream_t st = (cudaStream_t)s;
+    if ((rc = launch_pack(in, which, out, w, st))) return rc;
+    const int wh[2] = {which, which};
+    return launch_queue(in, 1, 0, wh, out, nullptr, w, w, st);
+  }
   int32_t n = 0;  // level 0 is handled by the pack; instances active for level 1
   int rc = gr_exact_prepare(in, which, out, ws, ws_bytes, s, &n);
   if (rc) return rc;
@@ -1538,6 +2095,13 @@ extern "C" int gr_solve_pms_mhs(const gr_batch *in, gr_result *out_pms, gr_resul
     if (!out_pms || !out_mhs) { gr_set_error("null result"); return GR_EINVAL; }
     cudaStream_t st = (cudaStream_t)s_pms;
     WS w1 = ws_of(in, ws1), w2 = ws_of(in, ws2);
+    if (!host_loop()) {  // both packs, then one device level loop for the fused walk
+      if ((rc = launch_pack(in, 1, out_mhs, w2, st))) return rc;
+      if ((rc = launch_pack(in, 0, out_pms, w1, st))) return rc;
+      const int wh[2] = {0, 1};
+      if ((rc = launch_queue(in, 1, 1, wh, out_pms, out_mhs, w1, w2, st))) return rc;
+      return stream_join(st, (cudaStream_t)s_mhs);
+    }
     if ((rc = launch_pack(in, 1, out_mhs, w2, st))) return rc;
     if ((rc = launch_finish(in, 1, out_mhs, w2, 0, st, nullptr))) return rc;
     if ((rc = launch_pack(in, 0, out_pms, w1, st))) return rc;
@@ -1588,6 +2152,16 @@ extern "C" int gr_solve_pms_mhs(const gr_batch *in, gr_result *out_pms, gr_resul
       GR_CUDA(cudaEventDestroy(ev));
     }
     return GR_OK;
+  }
+  if (!host_loop()) {  // weighted PMS + MHS (or start levels): one launch serves both solves
+    if (!out_pms || !out_mhs) { gr_set_error("null result"); return GR_EINVAL; }
+    cudaStream_t st = (cudaStream_t)s_pms;
+    WS w1 = ws_of(in, ws1), w2 = ws_of(in, ws2);
+    if ((rc = launch_pack(in, 0, out_pms, w1, st))) return rc;
+    if ((rc = launch_pack(in, 1, out_mhs, w2, st))) return rc;
+    const int wh[2] = {0, 1};
+    if ((rc = launch_queue(in, 2, 0, wh, out_pms, out_mhs, w1, w2, st))) return rc;
+    return stream_join(st, (cudaStream_t)s_mhs);
   }
   int32_t n1 = 0, n2 = 0;
   rc = gr_exact_prepare(in, 0, out_pms, ws1, half, s_pms, nullptr);

@@ -690,20 +690,20 @@ __global__ void __launch_bounds__(PK_T) pack_vm_tiled_kernel(int m, int64_t n, c
   if (bad && flags) atomicOr(bad, flags);
 }
 
-std::mutex g_mu;
-int g_count_grid = 0;
+// the count pass grid (one persistent CTA per SM); sets the kernels' dynamic
+// shared memory limits on first use of each device
+PerDevice g_count_grid;
 int count_grid() {
-  std::lock_guard<std::mutex> lk(g_mu);
-  if (g_count_grid) return g_count_grid;
-  int dev = 0, sms = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaFuncSetAttribute(count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)COUNT_SMEM_V2);
-  for (auto f : {(const void *)incr_step_kernel<int16_t>, (const void *)incr_step_kernel<int32_t>,
-                 (const void *)csr_hist_kernel<int16_t>, (const void *)csr_hist_kernel<int32_t>})
-    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  g_count_grid = sms;
-  return g_count_grid;
+  return g_count_grid.get([] {
+    cudaFuncSetAttribute(count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)COUNT_SMEM_V2);
+    for (auto f : {(const void *)incr_step_kernel<int16_t>, (const void *)incr_step_kernel<int32_t>,
+                   (const void *)csr_hist_kernel<int16_t>, (const void *)csr_hist_kernel<int32_t>,
+                   (const void *)incr_all_kernel<int16_t>, (const void *)incr_all_kernel<int32_t>})
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    for (auto f : {(const void *)pack_vm_tiled_kernel<int16_t>, (const void *)pack_vm_tiled_kernel<int32_t>})
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PK_SMEM);
+    return gr_sm_count();
+  });
 }
 
 int validate_matrix(const gr_bitmatrix *in) {
@@ -748,13 +748,7 @@ extern "C" int gr_pack_varmajor(int32_t m, int64_t n, const int64_t *off, const 
   if (n == 0) return GR_OK;
   cudaStream_t st = (cudaStream_t)s;
   if (ld % PK_W == 0) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(pack_vm_tiled_kernel<int16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PK_SMEM);
-      cudaFuncSetAttribute(pack_vm_tiled_kernel<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PK_SMEM);
-      attr = true;
-    }
-    const int grid = 148;
+    const int grid = count_grid();  // one CTA per SM (also sets the smem attribute)
     if (var_bytes == 2)
       GR_LAUNCH("pack_vm_tiled_kernel", st, pack_vm_tiled_kernel<int16_t><<<grid, PK_T, PK_SMEM, st>>>(m, n, off, (const int16_t *)var, bits, ld, d_bad));
     else
@@ -802,6 +796,22 @@ extern "C" int gr_greedy_count_shard(const gr_bitmatrix *shard, const uint64_t *
   return GR_OK;
 }
 
+// prune order of the picks (positions into picks[0..np)): reverse pick
+// order; with weights descending weight, equal weights in reverse pick order
+// (reading R12)
+static int removal_order(const gr_bitmatrix *in, const std::vector<int> &hpicks, int np, cudaStream_t st,
+                  std::vector<int> &ord) {
+  ord.resize(np);
+  for (int i = 0; i < np; i++) ord[i] = np - 1 - i;
+  if (!in->w || np < 2) return GR_OK;
+  std::vector<uint32_t> hw(in->m);
+  GR_CUDA(cudaMemcpyAsync(hw.data(), in->w, sizeof(uint32_t) * in->m, cudaMemcpyDeviceToHost, st));
+  GR_CUDA(cudaStreamSynchronize(st));
+  std::stable_sort(ord.begin(), ord.end(),
+                   [&](int a, int b) { return hw[hpicks[a]] > hw[hpicks[b]]; });
+  return GR_OK;
+}
+
 extern "C" int gr_mhs_greedy_matrix(const gr_bitmatrix *in, uint64_t *assign, int32_t *status,
                                     int32_t *picks, int32_t *n_picks, void *ws, size_t ws_bytes,
                                     gr_stream_t s) {
@@ -842,43 +852,43 @@ extern "C" int gr_mhs_greedy_matrix(const gr_bitmatrix *in, uint64_t *assign, in
     GR_LAUNCH("first_pick_kernel", st, first_pick_kernel<<<1, IT, 0, st>>>(counts, in->m, in->w, ctrl, wpicks));
     bool coop_done = false;
     {
-      // one cooperative launch for all picks (its grid must be co-resident)
-      static int cgrid = -1;
-      if (cgrid < 0) {
-        int per = 0, sms = 0, dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        int coop = 0;
-        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
-        cudaFuncSetAttribute(incr_all_kernel<int16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(incr_all_kernel<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, incr_all_kernel<int32_t>, IT, hs);
-        cgrid = (coop && per > 0 && !getenv("GR_NO_COOP")) ? sms * std::min(per, 2) : 0;
-      }
+      // one cooperative launch for all picks: its grid must be co-resident, so
+      // it is sized per call from the occupancy at this call's shared memory
+      // (hs = 4 m bytes) on this device -- 0 falls back to per-pick launches
+      count_grid();  // sets the dynamic shared memory limits on this device
+      int per = 0, coop = 0;
+      cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, gr_device());
+      const void *fn = in->var_bytes == 2 ? (const void *)incr_all_kernel<int16_t>
+                                          : (const void *)incr_all_kernel<int32_t>;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, IT, hs) != cudaSuccess) per = 0;
+      static const bool no_coop = getenv("GR_NO_COOP") != nullptr;
+      const int cgrid = (coop && per > 0 && !no_coop) ? gr_sm_count() * std::min(per, 2) : 0;
       if (cgrid > 0) {
         const int64_t ldv = ld;
         const int mv = in->m;
         void *args[] = {(void *)&in->bits, (void *)&ldv, (void *)&mv, (void *)&U, (void *)&counts,
                         (void *)&in->pos_off, (void *)&in->pos_var, (void *)&in->w, (void *)&ctrl,
                         (void *)&wpicks};
-        const void *fn = in->var_bytes == 2 ? (const void *)incr_all_kernel<int16_t>
-                                            : (const void *)incr_all_kernel<int32_t>;
         gr_prof_pre("incr_all_kernel", st);
         cudaError_t e = cudaLaunchCooperativeKernel(fn, cgrid, IT, args, hs, st);
         gr_prof_post("incr_all_kernel", st);
-        if (e != cudaSuccess) return gr_cuda_fail(e, "incr_all_kernel");
-        GR_CUDA(cudaMemcpyAsync(h, ctrl, sizeof(GCtrl), cudaMemcpyDeviceToHost, st));
-        GR_CUDA(cudaStreamSynchronize(st));
-        coop_done = ((GCtrl *)h)->done != 0;
+        if (e == cudaErrorCooperativeLaunchTooLarge) {
+          cudaGetLastError();  // not co-resident after all: per-pick launches below
+        } else {
+          if (e != cudaSuccess) return gr_cuda_fail(e, "incr_all_kernel");
+          GR_CUDA(cudaMemcpyAsync(h, ctrl, sizeof(GCtrl), cudaMemcpyDeviceToHost, st));
+          GR_CUDA(cudaStreamSynchronize(st));
+          coop_done = ((GCtrl *)h)->done != 0;
+        }
       }
     }
     const int STEPS = 32;
-    static int igrid = 0;  // CTAs of the incremental step (GR_INCR_GRID)
-    if (!igrid) {
+    static const int igrid_env = [] {  // CTAs of the incremental step (GR_INCR_GRID)
       const char *e = getenv("GR_INCR_GRID");
-      igrid = e ? atoi(e) : 2 * grid;  // two per SM: measured 10.8 -> 7.7 ms on C5
-      if (igrid < 1 || igrid > 4 * grid) igrid = grid;
-    }
+      return e ? atoi(e) : 0;
+    }();
+    int igrid = igrid_env ? igrid_env : 2 * grid;  // two per SM: measured 10.8 -> 7.7 ms on C5
+    if (igrid < 1 || igrid > 4 * grid) igrid = grid;
     for (int round = 0; !coop_done; round++) {
       for (int j = 0; j < STEPS; j++) {
         if (in->var_bytes == 2)
@@ -932,10 +942,14 @@ extern "C" int gr_mhs_greedy_matrix(const gr_bitmatrix *in, uint64_t *assign, in
     GR_CUDA(cudaStreamSynchronize(st));
   }
   // a pick that is the sole hitter of some clause stays so (counts only
-  // decrease); the others are re-checked in reverse pick order
+  // decrease); the others are re-checked in removal order (R12): reverse pick
+  // order, with weights descending weight and equal weights in reverse pick
+  // order
   std::vector<int> removed(np + 1, 0);
+  std::vector<int> ord;
+  if ((rc = removal_order(in, hpicks, np, st, ord))) return rc;
   int *hf = pinned_ctrl() + 8;
-  for (int j = np - 1; j >= 0; j--) {
+  for (int j : ord) {
     if (hflags[j]) continue;
     GR_CUDA(cudaMemsetAsync(flags + j, 0, sizeof(int), st));
     GR_LAUNCH("private_kernel", (cudaStream_t)s, private_kernel<<<148 * 4, 256, 0, st>>>(in->bits, ld, wpicks, ctrl, one, flags, j));

@@ -3,7 +3,7 @@
 //
 //   U = phi+; repeat { c[v] = |{P in U : v in P}|; v* = lowest argmax (R11);
 //   S += v*; U -= {P : v* in P} } until U is empty; reverse-delete in reverse
-//   pick order (R12); status SAT_NEG_VIOLATED if some N in phi- is a subset
+//   pick order (R12; weighted mhs: descending weight); status SAT_NEG_VIOLATED if some N in phi- is a subset
 //   of S.
 //
 // Lane v (and v+32, v+64, v+96) owns the counter of variable v; the uncovered
@@ -25,7 +25,7 @@ __global__ void __launch_bounds__(32) greedy_small_kernel(gr_batch in, gr_result
   const int b = blockIdx.x, lane = threadIdx.x;
   u64 *C = sg;
   u32 *U = (u32 *)(sg + 2 * (size_t)in.max_clauses);
-  __shared__ int s_picks[128];
+  __shared__ int s_picks[128], s_order[128];
   const int64_t lo = in.off[b], n64 = in.off[b + 1] - lo;
   const int m = in.m[b], np = in.n_pos[b], W = in.W;
   const bool wgt = (in.flags & GR_FLAG_WEIGHTED_GREEDY) && in.w;
@@ -130,9 +130,25 @@ __global__ void __launch_bounds__(32) greedy_small_kernel(gr_batch in, gr_result
         }
         __syncwarp();
       }
-      // reverse-delete: drop x if every positive clause meets S \ {x}
-      for (int i = npk - 1; i >= 0; i--) {
-        const int x = s_picks[i];
+      // reverse-delete: drop x if every positive clause meets S \ {x}.
+      // Order (R12): reverse pick order; weighted mhs: descending weight,
+      // equal weights in reverse pick order -- position of
+      // pick i = #{j : w_j > w_i or (w_j == w_i and j > i)}
+      if (wgt) {
+        __syncwarp();
+        for (int i = lane; i < npk; i += 32) {
+          const u32 wi = wb[s_picks[i]];
+          int r = 0;
+          for (int j = 0; j < npk; j++) {
+            const u32 wj = wb[s_picks[j]];
+            r += wj > wi || (wj == wi && j > i);
+          }
+          s_order[r] = s_picks[i];
+        }
+        __syncwarp();
+      }
+      for (int q = 0; q < npk; q++) {
+        const int x = wgt ? s_order[q] : s_picks[npk - 1 - q];
         const u64 T0 = x < 64 ? (S0 & ~(1ull << x)) : S0;
         const u64 T1 = x >= 64 ? (S1 & ~(1ull << (x - 64))) : S1;
         int ok = 1;
@@ -172,12 +188,11 @@ extern "C" int gr_mhs_greedy(const gr_batch *in, gr_result *out, void *ws, size_
   if (in->max_clauses < 0) { gr_set_error("max_clauses < 0"); return GR_EINVAL; }
   if (in->max_clauses > MAXC) { gr_set_error("max_clauses > 4096 for gr_mhs_greedy"); return GR_ETOOBIG; }
   const size_t smem = (size_t)in->max_clauses * 16 + ((size_t)in->max_clauses + 31) / 32 * 4 + 16;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(greedy_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         MAXC * 16 + MAXC / 32 * 4 + 16);
-    attr = true;
-  }
+  static PerDevice attr;
+  attr.get([] {
+    return (int)cudaFuncSetAttribute(greedy_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     MAXC * 16 + MAXC / 32 * 4 + 16);
+  });
   GR_LAUNCH("greedy_small_kernel", (cudaStream_t)s, greedy_small_kernel<<<in->B, 32, smem, (cudaStream_t)s>>>(*in, *out));
   return GR_OK;
 }

@@ -84,8 +84,19 @@ def solve_exact_sharded(db, which: int, rank: int, world: int, group=None, out=N
 
 
 # ---- column-sharded greedy (C5) ------------------------------------------------
+def removal_order(picks: Sequence[int], w=None) -> List[int]:
+    """Positions 0..n-1 of the picks in reverse-delete order (reading R12):
+    reverse pick order; with weights (weighted mhs) descending weight, equal
+    weights in reverse pick order."""
+    order = list(range(len(picks) - 1, -1, -1))
+    if w is not None:
+        order.sort(key=lambda j: -int(w[int(picks[j])]))  # stable: ties stay reverse-pick
+    return order
+
+
 def run_greedy_sharded(shard, allreduce_sum: Callable[[object], None],
-                       allreduce_max: Callable[[object], None], steps_per_check: int = 32):
+                       allreduce_max: Callable[[object], None], steps_per_check: int = 32,
+                       w=None):
     """Greedy mhs over phi+ split by clause columns across ranks (SURVEY.md
     §8(e) C5).  ``shard`` offers the gr_greedy_shard_* protocol (a
     GreedyShard on the GPU): ``counts`` (int32 tensor [m]), begin(), step(),
@@ -93,7 +104,9 @@ def run_greedy_sharded(shard, allreduce_sum: Callable[[object], None],
     finalize(removed, assign, status).  The exchanges are one all-reduce (SUM)
     of the m counts per pick and, in the prune, one all-reduce (MAX) of the
     private flags plus one single-flag all-reduce per re-checked pick.
-    Returns (assign, status, picks, n_picks), identical on every rank."""
+    ``w``: host weights [m] of the weighted mhs (they set the prune order),
+    or None.  Returns (assign, status, picks, n_picks), identical on every
+    rank."""
     import torch
 
     counts = shard.counts
@@ -118,7 +131,7 @@ def run_greedy_sharded(shard, allreduce_sum: Callable[[object], None],
     allreduce_max(flags)
     keep = flags[:n].cpu().tolist()
     removed = torch.zeros(m, dtype=torch.int32, device=dev)
-    for j in range(n - 1, -1, -1):  # the others in reverse pick order
+    for j in removal_order(picks[:n].cpu().tolist(), w):  # the others, in removal order
         if keep[j]:
             continue
         fj = flags[j:j + 1]
@@ -157,9 +170,11 @@ def greedy_matrix_sharded(bm_shard, rank: int, world: int, group=None, stream=No
     from . import _native as N
 
     sh = N.GreedyShard(bm_shard, stream=stream)
+    w = None if bm_shard.w is None else bm_shard.w.cpu().numpy().view(np.uint32)
     if world > 1:
-        return run_greedy_sharded(sh, nccl_allreduce("sum", group), nccl_allreduce("max", group))
-    return run_greedy_sharded(sh, lambda t: None, lambda t: None)
+        return run_greedy_sharded(sh, nccl_allreduce("sum", group), nccl_allreduce("max", group),
+                                  w=w)
+    return run_greedy_sharded(sh, lambda t: None, lambda t: None, w=w)
 
 
 # ---- batch sharding with result collection (C2 / C4) -------------------------------

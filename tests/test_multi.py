@@ -12,6 +12,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_2011_08373_b200.multigpu import run_levels_sharded, shard_instances, estimate_costs
+from gr_testutil import load_golden
 
 NONE = 2**63 - 1
 
@@ -132,8 +133,9 @@ class FakeGreedyShard:
     """CPU stand-in of one rank's gr_greedy_shard_* calls: this rank's clauses
     (lists of variable ids) and the replicated negatives."""
 
-    def __init__(self, m, clauses, neg):
+    def __init__(self, m, clauses, neg, w=None):
         self.m, self.cl, self.neg = m, [set(c) for c in clauses], [set(c) for c in neg]
+        self.w = w
         self.counts = torch.zeros(m, dtype=torch.int32)
 
     def _local_counts(self):
@@ -155,7 +157,13 @@ class FakeGreedyShard:
             if g.max() == 0:
                 self.done = True
             else:
-                v = int(np.argmax(g))  # first maximum = lowest index on ties
+                if self.w is None:
+                    v = int(np.argmax(g))  # first maximum = lowest index on ties
+                else:  # ratio rule (R20): max g/w, cross-multiplied, lowest index on ties
+                    v = 0
+                    for u in range(1, self.m):
+                        if int(g[u]) * self.w[v] > int(g[v]) * self.w[u]:
+                            v = u
                 self.picks.append(v)
                 for i, cl in enumerate(self.cl):
                     if v in cl:
@@ -201,37 +209,50 @@ def greedy_instance(seed):
     return m, cl, neg
 
 
+def weighted_golden_instance():
+    """tests/golden/weighted_prune_order.txt as 0-based clause lists + weights"""
+    g = load_golden("weighted_prune_order.txt")
+    return g["m"], [[v - 1 for v in c] for c in g["pos"]], [], g["w"]
+
+
 def _greedy_worker(rank, world, port, seed, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2011_08373_b200.multigpu import column_range, run_greedy_sharded
 
-    m, cl, neg = greedy_instance(seed)
+    if seed == "weighted":
+        m, cl, neg, w = weighted_golden_instance()
+    else:
+        (m, cl, neg), w = greedy_instance(seed), None
     c0, c1 = column_range(len(cl), rank, world)
-    sh = FakeGreedyShard(m, cl[c0:c1], neg)
+    sh = FakeGreedyShard(m, cl[c0:c1], neg, w)
 
     def red(op):
         return lambda t: dist.all_reduce(t, op=op)
 
     assign, status, picks, n = run_greedy_sharded(sh, red(dist.ReduceOp.SUM), red(dist.ReduceOp.MAX),
-                                                  steps_per_check=4)
+                                                  steps_per_check=4, w=w)
     q.put((rank, assign.tolist(), int(status[0]), picks[:n].tolist()))
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("seed", [0, 1])
+@pytest.mark.parametrize("seed", [0, 1, "weighted"])
 def test_greedy_column_sharding_gloo_world2(seed):
     """The sharded protocol over two gloo ranks gives the textbook greedy of
     the whole phi+ (the oracle): same pick order, same pruned set, same phi-
-    verdict."""
+    verdict.  "weighted": the ratio greedy on the golden prune-order instance
+    (descending-weight reverse-delete, reading R12)."""
     import oracle
 
-    m, cl, neg = greedy_instance(seed)
+    if seed == "weighted":
+        m, cl, neg, w = weighted_golden_instance()
+    else:
+        (m, cl, neg), w = greedy_instance(seed), None
     off = np.cumsum([0] + [len(c) for c in cl]).astype(np.int64)
     var = np.concatenate([np.array(c, np.int32) for c in cl])
     noff = np.cumsum([0] + [len(c) for c in neg]).astype(np.int64)
-    nvar = np.concatenate([np.array(c, np.int32) for c in neg])
-    ref = oracle.greedy_csr(m, off, var, noff, nvar)
+    nvar = np.concatenate([np.array(c, np.int32) for c in neg]) if neg else np.zeros(0, np.int32)
+    ref = oracle.greedy_csr(m, off, var, noff, nvar, w=w)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = free_port()
