@@ -306,8 +306,11 @@ typedef struct {
   char name[48];
   int64_t launches;
   double ms;          /* summed event-timed duration of the launches */
-  uint64_t work[4];   /* enum_kernel in mode 2: [0] clause tests, [1] candidate blocks
-                         (prefixes), [2] candidates decided, [3] tests on 64-bit lanes */
+  uint64_t work[8];   /* enum_kernel / queue_kernel in mode 2 (the roofline's units,
+                         DESIGN.md §5): [0] positive clause tests, [1] negative clause
+                         tests, [2] clauses read by subtree-refutation scans, [3] sub-blocks
+                         tested, [4] candidates in tested sub-blocks, [5] lane windows
+                         positioned, [6] tests + scans on 64-bit masks, [7] 0 */
 } gr_kernel_stat;
 int gr_profile(int mode);
 int gr_profile_read(gr_kernel_stat *out, int max_stats);

@@ -53,7 +53,7 @@ class GrResult(C.Structure):
 
 class GrKernelStat(C.Structure):
     _fields_ = [("name", C.c_char * 48), ("launches", C.c_int64), ("ms", C.c_double),
-                ("work", C.c_uint64 * 4)]
+                ("work", C.c_uint64 * 8)]
 
 
 class GrBitmatrix(C.Structure):

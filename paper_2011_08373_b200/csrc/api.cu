@@ -108,7 +108,7 @@ extern "C" int gr_profile(int mode) {
   std::lock_guard<std::mutex> lk(g_pmu);
   drain_locked();
   g_acc.clear();
-  unsigned long long w[4];
+  unsigned long long w[8];
   gr_exact_work_read(w, 1);
   g_mode.store(mode);
   return GR_OK;
@@ -117,7 +117,7 @@ extern "C" int gr_profile(int mode) {
 extern "C" int gr_profile_read(gr_kernel_stat *out, int max_stats) {
   std::lock_guard<std::mutex> lk(g_pmu);
   drain_locked();
-  unsigned long long w[4] = {0, 0, 0, 0};
+  unsigned long long w[8] = {};
   gr_exact_work_read(w, 0);
   int n = 0;
   for (auto &kv : g_acc) {
@@ -127,12 +127,8 @@ extern "C" int gr_profile_read(gr_kernel_stat *out, int max_stats) {
     strncpy(st.name, kv.first.c_str(), sizeof(st.name) - 1);
     st.launches = kv.second.launches;
     st.ms = kv.second.ms;
-    if (kv.first == "enum_kernel") {
-      st.work[0] = w[0];
-      st.work[1] = w[1];
-      st.work[2] = w[2];
-      st.work[3] = w[3];
-    }
+    if (kv.first == "enum_kernel" || kv.first == "queue_kernel")
+      for (int i = 0; i < 8; i++) st.work[i] = w[i];
   }
   return n;
 }

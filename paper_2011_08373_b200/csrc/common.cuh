@@ -42,7 +42,7 @@ void gr_prof_post(const char *name, cudaStream_t s);
     if (_e != cudaSuccess) return gr_cuda_fail(_e, name);          \
   } while (0)
 // work counters of the enumeration kernel's counting instantiation (exact.cu)
-void gr_exact_work_read(unsigned long long out[4], int reset);
+void gr_exact_work_read(unsigned long long out[8], int reset);
 
 // ---- per-device launch settings ---------------------------------------------
 // cudaFuncSetAttribute applies per device context and occupancy depends on

@@ -500,11 +500,15 @@ __device__ F2 hitting(int j, u64 p) {
   return r;
 }
 
-// Work counters of the counting instantiation (COUNT = true): clause tests,
-// sub-blocks tested, candidates in the tested sub-blocks.
+// Work counters of the counting instantiation (COUNT = true), the units of
+// the exact solvers' roofline: positive / negative clause
+// tests of a sub-block, clauses read by the subtree-refutation scans,
+// sub-blocks tested, candidates in them, lane windows positioned (colex
+// unrank).
 struct Work {
-  u64 tests = 0, blocks = 0, cands = 0;
+  u64 pos = 0, neg = 0, scan = 0, blocks = 0, cands = 0, windows = 0;
 };
+enum { W_POS, W_NEG, W_SCAN, W_BLOCKS, W_CANDS, W_WINDOWS, W_WIDE, W_N = 8 };
 
 template <typename M>
 struct Clauses {
@@ -527,7 +531,7 @@ __device__ __forceinline__ F2 test_pos(int j, M U, F2 F, const Clauses<M> &c, Wo
     for (int q = 0; q < np; q++) {
       const M pq = c.P[q];
       if (!(U & pq)) F.lo &= (u64)pq;
-      if (COUNT) wk.tests += 1;
+      if (COUNT) wk.pos += 1;
       if (!(q & 3) && !F.lo) return F2{0ull, 0ull};
     }
     return F2{F.lo, 0ull};
@@ -542,12 +546,12 @@ __device__ __forceinline__ F2 test_pos(int j, M U, F2 F, const Clauses<M> &c, Wo
     if (!(U & p1)) F = f2_and(F, h1);
     if (!(U & p2)) F = f2_and(F, h2);
     if (!(U & p3)) F = f2_and(F, h3);
-    if (COUNT) wk.tests += 4;
+    if (COUNT) wk.pos += 4;
     if (!f2_any(F)) return F;
   }
   for (; q < np; q++) {
     if (!(U & c.P[q])) F = f2_and(F, H[HREC * q]);
-    if (COUNT) wk.tests += 1;
+    if (COUNT) wk.pos += 1;
   }
   return F;
 }
@@ -559,7 +563,7 @@ __device__ __forceinline__ F2 test_neg(int j, M U, int e, F2 F, const Clauses<M>
   const F2 *hx = c.hitx + HX * j;
   for (int t = 0; t < c.nn; t++) {
     M rest = c.P[np + t] & ~U;
-    if (COUNT) wk.tests += 1;
+    if (COUNT) wk.neg += 1;
     if ((rest & ~lowm) || popc(rest) > j) continue;  // some variable of N stays false
     F2 kill{~0ull, ~0ull};
     if (j == 1) {  // HIT_1({x}) = bit x
@@ -624,10 +628,11 @@ __device__ __forceinline__ int refuted_by(int j, M U, int e, const Clauses<M> &c
     }
   }
   int kind = dead ? 1 : 0;
+  int q = 0;
   if (!dead)
-    for (int q = 0; q < c.nn; q++)
+    for (; q < c.nn; q++)
       if (!(c.P[c.np + q] & ~U)) { kind = 2; break; }
-  if (COUNT) wk.tests += (u64)r;
+  if (COUNT) wk.scan += (u64)r + (u64)q;
   return kind;
 }
 template <typename M, bool COUNT>
@@ -651,6 +656,7 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
   const u64 *cs = c.cs;  // C(n, j), j <= JMAX
 #define CS(n, j) (cs[(n) * (JMAX + 1) + (j)])
   i64 best = GR_KEY_NONE;
+  if (COUNT) wk.windows++;
   // ---- position the iterator on the sub-block that holds rank r_lo: colex
   // unrank of r_lo (element i is the largest c with C(c, i) <= the remaining
   // rank); the top k - J elements (binary search) form Utop, the J lowest go
@@ -858,6 +864,18 @@ __device__ __forceinline__ i64 warp_min(i64 v) {
   return v;
 }
 
+__device__ unsigned long long g_work[W_N];  // counting instantiation totals (Work units)
+// counting instantiation: add a lane's work to the totals (wide: 64-bit masks)
+__device__ __forceinline__ void work_add(const Work &wk, bool wide) {
+  atomicAdd(&g_work[W_POS], (unsigned long long)wk.pos);
+  atomicAdd(&g_work[W_NEG], (unsigned long long)wk.neg);
+  atomicAdd(&g_work[W_SCAN], (unsigned long long)wk.scan);
+  atomicAdd(&g_work[W_BLOCKS], (unsigned long long)wk.blocks);
+  atomicAdd(&g_work[W_CANDS], (unsigned long long)wk.cands);
+  atomicAdd(&g_work[W_WINDOWS], (unsigned long long)wk.windows);
+  if (wide) atomicAdd(&g_work[W_WIDE], (unsigned long long)(wk.pos + wk.neg + wk.scan));
+}
+
 struct EnumParams {
   WS ws;
   const int64_t *off;
@@ -876,7 +894,6 @@ __device__ i64 run_lane(const EnumParams &p, u64 r_lo, u64 cnt, int me, const Cl
   return walk<M, 0, COUNT>(p.k, me, r_lo, cnt, c, w, rb, p.prune, wk);
 }
 
-__device__ unsigned long long g_work[4];  // counting instantiation totals
 
 constexpr size_t TAB_SMEM =
     (JMAX + 1) * HX * 16 + 65 * (JMAX + 1) * 8 + 129 * 16 + 64 +
@@ -1030,12 +1047,7 @@ __global__ void __launch_bounds__(NTK, COUNT ? 1 : ENUM_CTAS * NT / NTK) enum_ke
     key = key1 < key ? key1 : key;
     key_m = key_m1 < key_m ? key_m1 : key_m;
     }
-    if (COUNT) {
-      atomicAdd(&g_work[0], (unsigned long long)wk.tests);
-      atomicAdd(&g_work[1], (unsigned long long)wk.blocks);
-      atomicAdd(&g_work[2], (unsigned long long)wk.cands);
-      if (!narrow) atomicAdd(&g_work[3], (unsigned long long)wk.tests);
-    }
+    if (COUNT) work_add(wk, !narrow);
     key = warp_min(key);
     if (p.fused) key_m = warp_min(key_m);
     if ((t & 31) == 0) {
@@ -1683,20 +1695,7 @@ __global__ void __launch_bounds__(NTK, COUNT ? 1 : ENUM_CTAS * NT / NTK) queue_k
           }
         }
       }
-      if (COUNT) {
-        u64 a0 = wk.tests, a1 = wk.blocks, a2 = wk.cands;
-        for (int o = 16; o; o >>= 1) {
-          a0 += __shfl_xor_sync(0xffffffffu, a0, o);
-          a1 += __shfl_xor_sync(0xffffffffu, a1, o);
-          a2 += __shfl_xor_sync(0xffffffffu, a2, o);
-        }
-        if (lane == 0) {
-          atomicAdd(&g_work[0], (unsigned long long)a0);
-          atomicAdd(&g_work[1], (unsigned long long)a1);
-          atomicAdd(&g_work[2], (unsigned long long)a2);
-          if (P.ws[s_sv].meff[s_b] > 32) atomicAdd(&g_work[3], (unsigned long long)a0);
-        }
-      }
+      if (COUNT) work_add(wk, P.ws[s_sv].meff[s_b] > 32);
       key = warp_min(key);
       if (KIND == 1) key_m = warp_min(key_m);
       int last = 0;
@@ -1800,14 +1799,14 @@ u64 lane_cands() {  // 0 = adaptive (GR_LANE_CANDIDATES overrides)
 
 extern "C" size_t gr_workspace_bytes_exact(const gr_batch *in) { return layout_of(in).total; }
 
-void gr_exact_work_read(unsigned long long out[4], int reset) {
+void gr_exact_work_read(unsigned long long out[8], int reset) {
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) { for (int i = 0; i < 4; i++) out[i] = 0; return; }
+  if (cudaGetDevice(&dev) != cudaSuccess) { for (int i = 0; i < W_N; i++) out[i] = 0; return; }
   cudaDeviceSynchronize();
-  if (cudaMemcpyFromSymbol(out, g_work, sizeof(unsigned long long) * 4) != cudaSuccess)
-    for (int i = 0; i < 4; i++) out[i] = 0;
+  if (cudaMemcpyFromSymbol(out, g_work, sizeof(unsigned long long) * W_N) != cudaSuccess)
+    for (int i = 0; i < W_N; i++) out[i] = 0;
   if (reset) {
-    unsigned long long z[4] = {0, 0, 0, 0};
+    unsigned long long z[W_N] = {};
     cudaMemcpyToSymbol(g_work, z, sizeof(z));
   }
 }
