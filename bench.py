@@ -1,22 +1,30 @@
 #!/usr/bin/env python
 """bench.py -- the Solve step of GPURepair (arXiv 2011.08373) on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c1|c3|c4|c5]
-                    [--impl ours|reference] [--no-cpu-baseline]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config all|c1|c2|c3|c4|c5]
+                    [--impl ours|reference] [--no-cpu-baseline] [--no-e2e]
 
 A *step* is one pass of the whole hot path over
 one batch of synthetic input: device clause packing, exact PMS (a), exact MHS
-(b) and greedy mhs (c) of every instance.  The default workload is
+(b) and greedy mhs (c) of every instance.  The headline workload is
 BASELINE.json configs[1] ("c2": 748 suite-shaped instances, m <= 32, <= 64
-clauses), the configuration the metric is quoted on.  Under torchrun every
-rank solves its own seeded 748-instance batch (weak scaling, no data-path
-collective; "c3" instead splits each level's colex rank range across the
-ranks with an NCCL all-reduce MIN per level -- strong scaling).
+clauses), the configuration the metric is quoted on (DESIGN.md §5 says why
+C2 and not the larger C4).  With the default ``--config all`` the same JSON
+line also carries one sub-record per other config (``configs``: C1, C3, C4,
+C5), each with its own timing, clocks, e2e, roofline and cpu_baseline.
 
-The timed region is device-resident inputs -> device results, CUDA events on
-the launching stream, L2 flushed (256 MiB write) between steps, barrier +
-synchronize on both sides, max over ranks.  `e2e` repeats the step through the
-public API from pinned host buffers with the H2D / D2H copies inside.
+Timed region: device-resident inputs -> device results, CUDA events on the
+launching stream, L2 flushed (256 MiB write) between steps, barrier +
+synchronize on both sides, max over ranks.  `e2e` repeats the step through
+the public API from pinned host buffers with the H2D / D2H copies inside.
+
+Multi-GPU (torchrun, one rank per GPU): C2/C4 -- every rank solves its own
+seeded batch (independent problems: no data-path collective, weak scaling);
+at N > 1 a `strong` sub-record also splits ONE batch by cost over the ranks
+with one NCCL all-gather of the results.  C3 -- each level's colex rank range
+split over the ranks, one NCCL all-reduce MIN per level (strong scaling, on
+the exhaustive no-refutation workload).  C5 -- clause columns split, one
+all-reduce SUM of the counts per pick (strong).  C1 -- replicas.
 
 value = candidate assignments decided per second over all ranks (exact PMS +
 MHS; DESIGN.md §5 defines the count); instances_per_s alongside.
@@ -38,11 +46,27 @@ sys.path.insert(0, ROOT)
 
 METRIC = "candidate assignments checked/sec and instances solved/sec at 1/2/4/8 B200"
 L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
-INT_LANES_PER_SM_CLK = 128  # INT32 issue: 4 SMSPs x 32 lanes x 1 warp-instruction/clk
-# SURVEY.md §8(d) per-unit figure: a candidate-at-a-time enumerator spends one
-# clause test (W + 1 ops) plus an amortised successor (~4 ops) per candidate.
-OPS_PER_CANDIDATE = {32: 6, 64: 7}   # m_eff <= 32 (one 32-bit word) / <= 64
-TEST_OPS = {32: 3, 64: 4}   # SASS per clause test: LOP3.P (U & P) + 2 predicated LOP3 (F &= H)
+
+# ---- the exact solvers' roofline ----------------------------
+# bound "alu": INT32 ALU-pipe lane-ops.  Peak = the LOP3/IADD3 micro-benchmark
+# (scripts/int_peak.cu) measured on a B200 of this pool: 64 lanes/clk/SM
+# (profiles/r02_int_peak.json); B300_MICROARCH.md "IADD3/LOP3 ... on alu-pipe,
+# rt_SMSP = 2" gives the same 16 lanes/clk per SMSP.
+INT_PEAK_FILE = os.path.join(ROOT, "profiles", "r02_int_peak.json")
+ALU_LANES_PER_CLK_SM = 64
+# Algorithmic INT ALU ops per unit of work the queue kernel performs (units
+# counted by the kernel's counting instantiation, gr_profile(2)); the minimum
+# ALU instructions of each step as written (DESIGN.md §5 derives each):
+#   positive clause test  U & P == 0 ? (1) ; F &= H_j(P) on two words (2)
+#   negative clause test  rest = N & ~U (1) ; rest outside the region ? (1) ;
+#                         |rest| <= j ? (POPC + compare: 2)
+#   refutation-scan clause  P & U (1), P & [0,e) (1), & used (1), used |= (1)
+#   sub-block             window masks (3), base/pos advance (2), iterator
+#                         step (sibling / child / pop: 3), witness ctz (1)
+#   lane window           colex unrank: one compare + decrement per scanned
+#                         row of the binomial table (about m_eff rows)
+OPS_U32 = {"pos": 3, "neg": 4, "scan": 4, "blocks": 9, "windows": 64}
+WIDE_EXTRA = 1  # one more op per clause test / scan clause on 64-bit masks
 
 
 def parse():
@@ -50,7 +74,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--config", default="all", choices=["all", "c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -69,34 +93,28 @@ def peaks():
     return p
 
 
-def ncu_evidence(kernel: str):
-    """Selected counters of the committed ncu --set full capture (profiles/)."""
-    path = os.path.join(ROOT, "profiles", "r01_ncu_selected_metrics.json")
+def int_peak(sms: int):
+    """INT32 ALU lane-ops/s: the committed micro-benchmark measurement
+    (LOP3.LUT, 1184 CTAs x 256 threads x 8 chains), else 64 lanes/clk/SM x
+    148 x the max SM clock."""
+    if os.path.exists(INT_PEAK_FILE):
+        with open(INT_PEAK_FILE) as f:
+            d = json.load(f)
+        return (float(d["lop3"]["lane_ops_per_s"]),
+                f"measured: scripts/int_peak.cu LOP3 on a B200 ({d['lop3']['lane_ops_per_clk_per_sm']} "
+                f"lanes/clk/SM at {d['lop3']['sm_mhz_in_kernel']} MHz; {os.path.relpath(INT_PEAK_FILE, ROOT)})")
+    pk = peaks()
+    return (sms * ALU_LANES_PER_CLK_SM * pk["sm_max_mhz"] * 1e6,
+            f"{sms} SMs x {ALU_LANES_PER_CLK_SM} lanes/clk x {pk['sm_max_mhz']:.0f} MHz")
+
+
+def ncu_summary(name: str):
+    """Selected counters of a committed ncu --set full capture (profiles/)."""
+    path = os.path.join(ROOT, "profiles", "r02_ncu_summary.json")
     if not os.path.exists(path):
         return None
     with open(path) as f:
-        d = json.load(f).get(kernel)
-    if not d:
-        return None
-    m = d[0]
-    pick = {"alu_pipe_pct": "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
-            "issue_active_pct": "smsp__issue_active.avg.pct_of_peak_sustained_active",
-            "active_lanes_per_warp_inst": "smsp__thread_inst_executed_per_inst_executed.ratio",
-            "dram_pct": "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"}
-    out = {k: float(m[v][0]) for k, v in pick.items() if v in m}
-    out["source"] = "profiles/r01_ncu_selected_metrics.json"
-    return out
-
-
-def traffic_of(kernel: str):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the
-    committed ncu --set full capture (profiles/traffic.json), else None."""
-    path = os.path.join(ROOT, "profiles", "traffic.json")
-    if not os.path.exists(path):
-        return None
-    with open(path) as f:
-        d = json.load(f)
-    return d.get(kernel)
+        return json.load(f).get(name)
 
 
 # ---------------------------------------------------------------- clocks
@@ -126,6 +144,7 @@ class ClockSampler:
 
     def _handle(self):
         import pynvml as nv
+        import torch
 
         nv.nvmlInit()
         try:
@@ -228,20 +247,25 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- workloads
+DESC = {
+    "c1": "C1: the paper's worked example (PAPER.md:26) in m=8, instances A+B; PMS + MHS + greedy",
+    "c2": "C2: 748 suite-shaped instances, m<=32, <=64 clauses (PAPER.md:194, 593-602); PMS + MHS + greedy",
+    "c3": "C3: one instance m=48, 200 mixed clauses, k*=16; PMS + MHS, levels 0..16 exhaustive",
+    "c4": "C4: 10000 WPMS instances, m=40, w~U{50..100}, planted SAT; WPMS + MHS + greedy",
+}
+
+
 def make_workload(cfg: str, rank: int):
     from paper_2011_08373_b200 import synth
 
     if cfg == "c1":
-        return synth.c1_instances(), "C1: the paper's example (PAPER.md:26) in m=8, instances A+B"
+        return synth.c1_instances()
     if cfg == "c2":
-        return (synth.c2_batch(seed=synth.seed_for(2, rank)),
-                "C2: 748 suite-shaped instances, m<=32, <=64 clauses (PAPER.md:194, 593-602)")
+        return synth.c2_batch(seed=synth.seed_for(2, rank))
     if cfg == "c3":
-        cb, _, _ = synth.c3_instance()
-        return cb, "C3: one instance m=48, 200 clauses, k*=16, levels 0..16 exhaustive"
+        return synth.c3_instance()[0]
     if cfg == "c4":
-        return (synth.c4_batch(seed=synth.seed_for(4, rank)),
-                "C4: 10000 WPMS instances, m=40, w~U{50..100}, planted SAT")
+        return synth.c4_batch(seed=synth.seed_for(4, rank))
     raise ValueError(cfg)
 
 
@@ -272,126 +296,192 @@ def device_batch(h, cb, dev, flags):
                           wstride=int(cb.w.shape[1]) if cb.w is not None else 0, flags=flags)
 
 
-def main():
-    a = parse()
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if a.impl == "reference":
-        return run_reference(a, rank, world)
+class Ctx:
+    """rank / world / device / collectives of this process"""
+
+    def __init__(self, rank, world, local, dev):
+        self.rank, self.world, self.local, self.dev = rank, world, local, dev
+
+    def max_(self, vals):
+        """elementwise max over ranks (device time: max over ranks)"""
+        import torch
+
+        t = torch.tensor(vals, dtype=torch.float64, device=self.dev)
+        if self.world > 1:
+            import torch.distributed as dist
+
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.tolist()
+
+    def sum_(self, vals):
+        import torch
+
+        t = torch.tensor(vals, dtype=torch.float64, device=self.dev)
+        if self.world > 1:
+            import torch.distributed as dist
+
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return t.tolist()
+
+    def barrier(self):
+        if self.world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+
+
+def time_steps(step, steps, ctx, flush, clocks=True):
+    """K timed steps (CUDA events on the current stream, L2 flushed between
+    steps, synchronised, barrier before); returns (total ms, clocks)."""
     import torch
-    import torch.distributed as dist
+
+    stream = torch.cuda.current_stream()
+    torch.cuda.synchronize()
+    ctx.barrier()
+    total = 0.0
+    with ClockSampler(ctx.local) as clk:
+        clk.start()
+        for _ in range(steps):
+            flush.fill_(1)  # L2 flush between timed iterations (untimed)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step()
+            e1.record(stream)
+            e1.synchronize()
+            total += e0.elapsed_time(e1)
+        clk.stop()
+    torch.cuda.synchronize()
+    return total, (clk.summary() if clocks else None)
+
+
+def exact_roofline(cb, step, flush, step_ms, sms):
+    """The dominant kernel (queue_kernel, the device level loop) of one
+    untimed step: its event-timed duration (gr_profile(1)) and its work units
+    (gr_profile(2), the counting instantiation) -> algorithmic INT ALU ops
+    per second against the measured INT32 ALU peak."""
+    import paper_2011_08373_b200 as gr
+    import torch
+
+    flush.fill_(1)
+    torch.cuda.synchronize()
+    prof = gr.profiler(1).start()
+    step()
+    kern = prof.stop()
+    wprof = gr.profiler(2).start()
+    step()
+    wk = wprof.stop()
+    torch.cuda.synchronize()
+    q = kern.get("queue_kernel")
+    w = wk.get("queue_kernel", {}).get("work")
+    if not q or not w:
+        return None, kern
+    units = dict(zip(["pos", "neg", "scan", "blocks", "cands", "windows", "wide", "_"], w))
+    ops = sum(OPS_U32[k] * units[k] for k in OPS_U32) + WIDE_EXTRA * units["wide"]
+    sec = q["ms"] / 1e3
+    peak, src = int_peak(sms)
+    ach = ops / sec
+    roof = {"bound": "alu", "achieved": ach / 1e12, "peak": peak / 1e12, "unit": "Tops/s",
+            "frac": ach / peak, "traffic": None, "kernel": "queue_kernel",
+            "per_launch": {"launches": q["launches"], "ms": q["ms"] / q["launches"],
+                           "alu_ops": ops / q["launches"],
+                           "units": {k: v / q["launches"] for k, v in units.items() if k != "_"}},
+            "per_unit": ("INT ALU ops: positive clause test 3, negative 4, refutation-scan clause "
+                         "4 (+1 on 64-bit masks), sub-block 9, lane window 64 (DESIGN.md §5)"),
+            "peak_source": src,
+            "share_of_step": q["ms"] / step_ms if step_ms else None,
+            "timing": "one untimed step, CUDA events around the launch (gr_profile(1))",
+            "traffic_note": "on-chip work: clause records in shared memory, ~0 HBM bytes"}
+    hw = ncu_summary("queue_kernel_c2")
+    if hw:
+        roof["ncu"] = hw
+    return roof, kern
+
+
+def kernels_of(k):
+    return {n: {"launches": v["launches"], "ms_per_step": v["ms"]} for n, v in k.items()}
+
+
+def run_exact(a, cfg, ctx, flush, sub=False):
+    """C1-C4: pack + PMS + MHS (one launch for both) + greedy of the batch."""
+    import torch
 
     import paper_2011_08373_b200 as gr
     from paper_2011_08373_b200 import multigpu
 
-    # functional check of the multi-rank code on one GPU (never a measurement):
-    # GR_BENCH_ONE_GPU=1 puts every rank on cuda:0 with the gloo backend --
-    # the ranks' kernels never wait on each other, only host collectives do
-    one_gpu = os.environ.get("GR_BENCH_ONE_GPU") == "1"
-    if one_gpu:
-        local = 0
-    torch.cuda.set_device(local)
-    if world > 1:
-        if one_gpu:
-            dist.init_process_group("gloo")
-        else:
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
-    if a.config == "c5":
-        return run_c5(a, rank, world, local, dev)
-    cb, desc = make_workload(a.config, rank)
-    flags = gr.GR_FLAG_EXHAUSTIVE if a.config == "c3" else 0
+    rank, world, dev = ctx.rank, ctx.world, ctx.dev
+    sharded = cfg == "c3" and world > 1
+    cb = make_workload(cfg, rank)
+    flags = gr.GR_FLAG_EXHAUSTIVE if cfg == "c3" else 0
     hb = host_tensors(cb, pinned=True)
     db = device_batch(hb, cb, dev, flags)
     torch.cuda.synchronize()
     outs = [gr.DeviceResult.empty(cb.B, cb.W, dev) for _ in range(3)]
-    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
-    stream = torch.cuda.current_stream()
-    sharded = a.config == "c3" and world > 1
 
-    def step(dbx, o):
-        if sharded:  # rank-range sharding of each level, NCCL all-reduce MIN per level
-            multigpu.solve_exact_sharded(dbx, gr.PMS, rank, world, out=o[0])
-            multigpu.solve_exact_sharded(dbx, gr.MHS, rank, world, out=o[1])
-        else:  # PMS and MHS level loops interleaved on two streams
-            gr.solve_pms_mhs(dbx, o[0], o[1])
+    def step_local(dbx, o):
+        gr.solve_pms_mhs(dbx, o[0], o[1])
         gr.mhs_greedy(dbx, o[2])
 
+    def step_sharded(dbx, o):  # C3 at N > 1: level rank ranges over the ranks, NCCL MIN per level
+        multigpu.solve_pair_sharded(dbx, rank, world, out_pms=o[0], out_mhs=o[1])
+        gr.mhs_greedy(dbx, o[2])
+
+    step = step_sharded if sharded else step_local
+    steps = a.steps
     for _ in range(a.warmup):
         step(db, outs)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    # ---------------- timed region (device-resident inputs) ----------------
-    # (no per-launch events in here: the kernel breakdown comes from one
-    # extra, untimed step below)
     l0 = gr.launch_count()
-    total_ms = 0.0
-    with ClockSampler(local) as clk:
-        clk.start()
-        for _ in range(a.steps):
-            flush.fill_(1)  # L2 flush between timed iterations (untimed)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            step(db, outs)
-            e1.record(stream)
-            e1.synchronize()
-            total_ms += e0.elapsed_time(e1)
-        clk.stop()
+    total_ms, clocks = time_steps(lambda: step(db, outs), steps, ctx, flush)
     launches = gr.launch_count() - l0
-    torch.cuda.synchronize()
-    # per-kernel breakdown of one step, untimed, under gr_profile(1)
-    flush.fill_(1)
-    prof = gr.profiler(1).start()
-    step(db, outs)
-    kern = prof.stop()
-    torch.cuda.synchronize()
-    res = [o.to_host() for o in outs]
+    res = gr.to_host_many(outs)
     cands = float(res[0]["decided"].astype(np.float64).sum() + res[1]["decided"].astype(np.float64).sum())
-    if sharded:
-        cands_rank = cands / world  # every rank holds the full result
-    else:
-        cands_rank = cands
-    # ---------------- roofline pass (untimed): the solves serialised so launch
-    # durations are not shared between streams, then the counting instantiation
-    def serial_step(dbx, o):
-        if sharded:
-            step(dbx, o)
-        else:
-            gr.solve_pms(dbx, o[0])
-            gr.mhs_exact(dbx, o[1])
-            gr.mhs_greedy(dbx, o[2])
-
-    flush.fill_(1)
-    rprof = gr.profiler(1).start()
-    serial_step(db, outs)
-    kern_serial = rprof.stop()
-    wprof = gr.profiler(2).start()
-    serial_step(db, outs)
-    wk = wprof.stop()
-    # ---------------- the same step without subtree refutation (untimed for
-    # the headline): every sub-block decided by its own clause tests
-    nop_ms = None
+    cands_rank = cands / world if sharded else cands
+    inst_rank = cb.B / world if sharded else cb.B
+    tmax = ctx.max_([total_ms])[0]
+    cands_all, inst_all = ctx.sum_([cands_rank, inst_rank])
+    sec = tmax / 1e3
+    rec = {"workload": DESC[cfg], "value": cands_all * steps / sec, "unit": "candidates/s",
+           "ms_per_step": tmax / steps, "steps": steps, "warmup": a.warmup,
+           "instances_per_s": inst_all * steps / sec, "candidates_per_step": cands_all,
+           "instances_per_step": inst_all,
+           "scaling": "strong" if sharded else "weak",
+           "parallelism": (f"level rank ranges x{world} (NCCL allreduce MIN per level)" if sharded
+                           else (f"one seeded batch per rank x{world}" if world > 1 else "single GPU")),
+           "gpu_launches": launches, "clocks": clocks,
+           "status_counts": {str(int(k)): int(v) for k, v in
+                             zip(*np.unique(res[0]["status"], return_counts=True))}}
+    # ---- roofline of the dominant kernel + per-kernel breakdown (untimed)
     if not sharded:
+        roof, kern = exact_roofline(cb, lambda: step(db, outs), flush, tmax / steps,
+                                    torch.cuda.get_device_properties(dev).multi_processor_count)
+        rec["roofline"] = roof
+        rec["kernels"] = kernels_of(kern)
+        rec["kernels_note"] = "one extra untimed step with CUDA events around every launch"
+    # ---- C3: the deterministic no-refutation workload for scaling
+    if cfg == "c3":
         dbn = device_batch(hb, cb, dev, flags | gr.GR_FLAG_NO_PRUNE)
-        step(dbn, outs)
-        torch.cuda.synchronize()
-        nop_ms = 0.0
-        for _ in range(a.steps):
-            flush.fill_(1)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            step(dbn, outs)
-            e1.record(stream)
-            e1.synchronize()
-            nop_ms += e0.elapsed_time(e1)
+        nsteps = 3
+        stepn = (lambda: step(dbn, outs))
+        stepn()
+        ms_n, clk_n = time_steps(stepn, nsteps, ctx, flush)
+        ms_n = ctx.max_([ms_n])[0]
+        rn = gr.to_host_many(outs[:2])
+        cn = float(rn[0]["decided"].astype(np.float64).sum() + rn[1]["decided"].astype(np.float64).sum())
+        rec["exhaustive_no_refutation"] = {
+            "ms_per_step": ms_n / nsteps, "steps": nsteps, "value": cn * nsteps / (ms_n / 1e3),
+            "unit": "candidates/s", "clocks": clk_n,
+            "note": ("the scaling workload (SURVEY §8(d) C3): levels 0..16 decided sub-block by "
+                     "sub-block (GR_FLAG_NO_PRUNE, deterministic work), same results; the headline "
+                     "C3 figure above is the pruned walk (latency)")}
         del dbn
-    # ---------------- e2e through the public API from pinned host buffers --
-    e2e_ms, h2d, d2h = None, 0, 0
+    # ---- C2 / C4 at N > 1: one batch split over the ranks (strong scaling)
+    if cfg in ("c2", "c4") and world > 1:
+        rec["strong"] = strong_batch(a, cfg, ctx, flush)
+    # ---- e2e through the public API from pinned host buffers
     if not a.no_e2e:
         h2d = sum(int(v.numel() * v.element_size()) for v in hb.values())
-        for s in range(a.warmup + a.steps):
+        e2e_ms, host = 0.0, None
+        stream = torch.cuda.current_stream()
+        for s in range(a.warmup + steps):
             flush.fill_(1)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
@@ -401,106 +491,61 @@ def main():
             e1.record(stream)
             e1.synchronize()
             if s >= a.warmup:
-                e2e_ms = (e2e_ms or 0.0) + e0.elapsed_time(e1)
+                e2e_ms += e0.elapsed_time(e1)
         d2h = sum(int(x.nbytes) for r in host for x in r.values())
-    # ---------------- reduce over ranks ---------------------------------------
-    t = torch.tensor([total_ms, cands_rank, float(cb.B if not sharded else cb.B / world),
-                      e2e_ms or 0.0], dtype=torch.float64, device=dev)
-    if world > 1:
-        tmax, tsum = t.clone(), t.clone()
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-        dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
-        total_ms, cands_all, inst_all, e2e_ms = float(tmax[0]), float(tsum[1]), float(tsum[2]), float(tmax[3])
-    else:
-        cands_all, inst_all = cands_rank, float(cb.B)
-    sec = total_ms / 1e3
-    value = cands_all * a.steps / sec
-    # ---------------- roofline of the dominant kernel (enum_kernel) ---------
-    pk = peaks()
-    ek = kern_serial.get("enum_kernel", {"launches": 0, "ms": 0.0})
-    ew = wk.get("enum_kernel", {"launches": 0, "work": [0, 0, 0, 0]})
-    tests, blocks, wcands, tests64 = ew["work"]
-    wide = int((cb.m > 32).sum()) > cb.B // 2
-    roof = None
-    if ek["launches"] and ew["launches"]:
-        per_launch_s = ek["ms"] / ek["launches"] / 1e3
-        # units: candidates decided per launch (the metric's unit), averaged
-        # over the serialised pass's enum_kernel launches
-        cands_launch = cands_rank / ek["launches"]
-        opc = OPS_PER_CANDIDATE[64 if wide else 32]
-        achieved = cands_launch * opc / per_launch_s / 1e12
-        peak_tops = 148 * INT_LANES_PER_SM_CLK * pk["sm_max_mhz"] * 1e6 / 1e12
-        test_ops = TEST_OPS[32] * (tests - tests64) + TEST_OPS[64] * tests64
-        roof = {"bound": "alu", "achieved": achieved, "peak": peak_tops, "unit": "Tops/s",
-                "frac": achieved / peak_tops, "traffic": traffic_of("enum_kernel"),
-                "kernel": "enum_kernel",
-                "per_unit": f"{opc} INT ops per candidate decided (SURVEY.md §8(d): 1 clause test "
-                            f"+ amortised successor of a candidate-at-a-time enumerator)",
-                "frac_note": ("> 1 is expected: the kernel decides up to 128 candidates per clause "
-                              "test (bit-parallel sub-blocks) and refutes whole subtrees with one "
-                              "clause; the hardware view is ncu's ALU-pipe / issue utilisation "
-                              "(below) and clause_test_frac"),
-                "per_launch": {"candidates": cands_launch, "ms": per_launch_s * 1e3,
-                               "clause_tests": tests / ew["launches"],
-                               "candidates_in_tested_blocks": wcands / ew["launches"],
-                               "candidate_blocks": blocks / ew["launches"]},
-                "peak_source": f"INT32 issue: 148 SMs x {INT_LANES_PER_SM_CLK} lanes/clk x "
-                               f"{pk['sm_max_mhz']:.0f} MHz ({pk['source']})",
-                "clause_test_frac": test_ops / ew["launches"] / per_launch_s / 1e12 / peak_tops,
-                "ncu": ncu_evidence("enum_kernel"),
-                "launch_timing": "untimed serialised pass (PMS and MHS solved one after the other)",
-                "share_of_step": (kern.get("enum_kernel", {"ms": 0.0})["ms"] / (total_ms / a.steps)
-                                  if total_ms else None),
-                "share_note": "enum_kernel event time of one extra untimed step / timed step time"}
-    line = {
-        "metric": METRIC, "value": value, "unit": "candidates/s", "n_gpus": world,
-        "steps": a.steps, "warmup": a.warmup, "ms_per_step": total_ms / a.steps,
-        "higher_is_better": True, "scaling": "strong" if sharded else "weak",
-        "vs_baseline": None, "dtype": "u64",
-        "data": "synthetic (seeded, SURVEY.md §8(d) recipe; DESIGN.md §6)",
-        "config": {"workload": desc, "instances_per_gpu": cb.B,
-                   "l2": "flushed between timed steps (256 MiB write)",
-                   "parallelism": (f"level rank-range sharded x{world} (NCCL allreduce MIN per level)"
-                                   if sharded else (f"batch x{world} (one seeded batch per rank)"
-                                                    if world > 1 else "single GPU"))},
-        "instances_per_s": inst_all * a.steps / sec,
-        "candidates_per_step": cands_all,
-        "e2e": ({"value": cands_all * a.steps / (e2e_ms / 1e3), "unit": "candidates/s",
-                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                 "ms_per_step": e2e_ms / a.steps} if e2e_ms else None),
-        "gpu_launches": launches,
-        "roofline": roof,
-        "without_subtree_refutation": ({"ms_per_step": nop_ms / a.steps,
-                                        "value": cands_all * a.steps / (nop_ms / 1e3),
-                                        "unit": "candidates/s",
-                                        "note": "GR_FLAG_NO_PRUNE: every sub-block decided by its "
-                                                "own clause tests; same results"}
-                                       if nop_ms else None),
-        "clocks": clk.summary(),
-        "status_counts": {str(int(k)): int(v) for k, v in zip(*np.unique(res[0]["status"], return_counts=True))},
-        "kernels": {k: {"launches": v["launches"], "ms_per_step": v["ms"]} for k, v in kern.items()},
-        "kernels_note": "one extra untimed step with CUDA events around every launch",
-    }
+        e2e_ms = ctx.max_([e2e_ms])[0]
+        rec["e2e"] = {"value": cands_all * steps / (e2e_ms / 1e3), "unit": "candidates/s",
+                      "instances_per_s": inst_all * steps / (e2e_ms / 1e3),
+                      "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                      "ms_per_step": e2e_ms / steps}
+    # ---- the oracle on the host, and the GPU on the same sample
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(a.config, cb)
-    if rank == 0:
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+        rec["cpu_baseline"] = cpu_baseline(cfg, cb, ctx, flush)
+    return rec
 
 
-# ---------------------------------------------------------------- C5
-def run_c5(a, rank, world, local, dev):
+def strong_batch(a, cfg, ctx, flush):
+    """One shared batch dealt over the ranks by measured per-instance work
+    (multigpu.shard_instances on the decided counts of a first solve), each
+    rank solving its slice, one NCCL all-gather of the results -- the whole
+    job's wall time on the device, max over ranks."""
     import torch
 
     import paper_2011_08373_b200 as gr
-    from paper_2011_08373_b200 import synth
-
     from paper_2011_08373_b200 import multigpu
 
-    # N > 1: one C5 phi+ split by clause columns across the ranks (SURVEY.md
-    # §8(e) C5): each rank packs and streams its own column range, one NCCL
-    # all-reduce (SUM) of the 4096 counts per pick -- strong scaling
+    cb = make_workload(cfg, 0)
+    costs = multigpu.measured_costs(cb, ctx.dev)
+    parts = multigpu.shard_instances(costs, ctx.world)
+    mine = cb.subset(parts[ctx.rank]) if parts[ctx.rank] else None
+    db = gr.DeviceBatch.from_host(mine, device=ctx.dev) if mine is not None else None
+    outs = [gr.DeviceResult.empty(mine.B, mine.W, ctx.dev) for _ in range(3)] if mine else None
+    gather = multigpu.nccl_allgather(device=ctx.dev)
+
+    def step():
+        return multigpu.solve_batch_sharded_device(cb, parts, ctx.rank, db, outs, gather)
+
+    for _ in range(max(1, a.warmup)):
+        got = step()
+    ms, _ = time_steps(step, a.steps, ctx, flush, clocks=False)
+    ms = ctx.max_([ms])[0]
+    cands = float(got["decided_pms"].astype(np.float64).sum() + got["decided_mhs"].astype(np.float64).sum())
+    return {"ms_per_step": ms / a.steps, "value": cands * a.steps / (ms / 1e3), "unit": "candidates/s",
+            "instances_per_s": cb.B * a.steps / (ms / 1e3), "scaling": "strong",
+            "parallelism": f"one batch dealt by measured cost over {ctx.world} ranks + NCCL all_gather"}
+
+
+# ---------------------------------------------------------------- C5
+C5_SAMPLE_N = 1 << 21
+
+
+def run_c5(a, ctx, flush):
+    import torch
+
+    import paper_2011_08373_b200 as gr
+    from paper_2011_08373_b200 import multigpu, synth
+
+    rank, world, dev = ctx.rank, ctx.world, ctx.dev
     sharded = world > 1
     csr, H = synth.c5_clauses(seed=synth.seed_for(5, 0 if sharded else rank))
     po, pv = csr.pos_off, csr.pos_var
@@ -523,16 +568,20 @@ def run_c5(a, rank, world, local, dev):
                                check=False, keep_csr=keep_csr)
         return bm, solve(bm)
 
-    def timed(keep_csr, steps):
-        for _ in range(max(1, min(a.warmup, 2))):
+    steps = max(1, min(a.steps, 5))  # a recounting step streams ~257 x 8.6 GB
+    warm = max(1, min(a.warmup, 2))
+
+    def timed(keep_csr, nsteps):
+        for _ in range(warm):
             bm, r = step(keep_csr)
             del bm
         torch.cuda.synchronize()
+        ctx.barrier()
         l0 = gr.launch_count()
         ms = 0.0
-        with ClockSampler(local) as clk:
+        with ClockSampler(ctx.local) as clk:
             clk.start()
-            for _ in range(steps):
+            for _ in range(nsteps):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
                 bm, r = step(keep_csr)
@@ -543,8 +592,7 @@ def run_c5(a, rank, world, local, dev):
                 del bm
             clk.stop()
         launches = gr.launch_count() - l0
-        # per-kernel breakdown of one step, untimed, under gr_profile(1)
-        prof = gr.profiler(1).start()
+        prof = gr.profiler(1).start()  # per-kernel breakdown of one step, untimed
         bm, r1 = step(keep_csr)
         del bm
         kern = prof.stop()
@@ -552,35 +600,50 @@ def run_c5(a, rank, world, local, dev):
 
     # primary: the north-star design -- recounting passes streaming the 8 GiB
     # bit matrix (count_kernel, HBM roofline); then the f3 incremental greedy
-    total_ms, r, ld, kern, launches, clocks = timed(False, a.steps)
-    inc_ms, r2, _, kern2, _, _ = timed(True, a.steps)
-    if world > 1:  # device time, max over ranks
-        import torch.distributed as dist
-
-        t = torch.tensor([total_ms, inc_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms, inc_ms = t.tolist()
+    total_ms, r, ld, kern, launches, clocks = timed(False, steps)
+    inc_ms, r2, _, kern2, _, clocks2 = timed(True, a.steps)
+    total_ms, inc_ms = ctx.max_([total_ms, inc_ms])
     same = (r2.picks.cpu() == r.picks.cpu()).all().item() and r2.n_picks == r.n_picks
     pk = peaks()
     ck = kern["count_kernel"]
     bytes_per_launch = csr.m * ld * 8 + 3 * ld * 8  # R + U_in + U_out + R[v*] row (mark)
-    # passes that did work: n_picks + 1 per solve (up to 7 more are queued
-    # no-ops after `done`; their few microseconds stay in the total)
-    eff = r.n_picks + 1  # of the one profiled step
+    eff = r.n_picks + 1  # passes that did work in the profiled step
     ach = bytes_per_launch / (ck["ms"] / eff / 1e3) / 1e9
     a_ = r.assign.cpu().numpy().view(np.uint64)
     size = int(sum(bin(int(x)).count("1") for x in a_))
-    # whole-job clauses per step: the one split phi+ (sharded) or one per rank
-    n = csr.n_pos if sharded else csr.n_pos * world
-    # e2e through the public API: pinned host CSR -> device, pack + greedy,
-    # result (assignment, picks, status) -> host, every step
-    e2e = None
-    if not a.no_e2e:
+    n = csr.n_pos if sharded else csr.n_pos * world  # whole-job clauses per step
+    rec = {"workload": ("C5: greedy mhs, m=4096, n=2^24 positive clauses (8 GiB bit matrix); "
+                        "step = device pack + greedy + prune + phi- check"),
+           "value": n * steps / (total_ms / 1e3), "unit": "clauses/s (greedy)",
+           "ms_per_step": total_ms / steps, "steps": steps, "warmup": warm,
+           "scaling": "strong" if sharded else "weak",
+           "parallelism": (f"clause columns x{world} (NCCL allreduce SUM of the counts per pick)"
+                           if sharded else "single GPU"),
+           "l2": "inputs (8 GiB) larger than L2",
+           "greedy": {"picks": r.n_picks, "size": size, "status": int(r.status.item()), "planted": 256,
+                      "passes": ck["launches"]},
+           "f3_incremental": {"ms_per_step": inc_ms / a.steps, "steps": a.steps,
+                              "value": n * a.steps / (inc_ms / 1e3), "unit": "clauses/s (greedy)",
+                              "speedup": (total_ms / steps) / (inc_ms / a.steps),
+                              "identical_picks": bool(same), "clocks": clocks2,
+                              "kernels": kernels_of(kern2)},
+           "gpu_launches": launches, "clocks": clocks,
+           "roofline": {"bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                        "frac": ach / pk["hbm_gbs"], "traffic": None, "kernel": "count_kernel",
+                        "share_of_step": ck["ms"] / (total_ms / steps),
+                        "per_launch": {"bytes": bytes_per_launch, "ms": ck["ms"] / eff},
+                        "peak_source": pk["source"] + " (copy, read+write)"},
+           "kernels": kernels_of(kern)}
+    hw = ncu_summary("count_kernel_c5")
+    if hw:
+        rec["roofline"]["ncu"] = hw
+        rec["roofline"]["traffic"] = hw.get("dram_bytes_per_launch")
+    if not a.no_e2e:  # pinned host CSR -> device, pack + greedy, result -> host, every step
         hp = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory()
               for k, v in (("po", po), ("pv", pv), ("no", csr.neg_off), ("nv", csr.neg_var))}
         h2d = sum(int(t.numel() * t.element_size()) for t in hp.values())
-        ems, d2h = 0.0, 0
-        for s_ in range(max(1, min(a.warmup, 2)) + a.steps):
+        ems, host = 0.0, None
+        for s_ in range(warm + steps):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             dd = {k: v.to(dev, non_blocking=True) for k, v in hp.items()}
@@ -589,52 +652,15 @@ def run_c5(a, rank, world, local, dev):
             e1.record(stream)
             e1.synchronize()
             del bm, dd
-            if s_ >= max(1, min(a.warmup, 2)):
+            if s_ >= warm:
                 ems += e0.elapsed_time(e1)
         d2h = sum(int(x.numel() * x.element_size()) for x in host)
-        if world > 1:
-            import torch.distributed as dist
-
-            t = torch.tensor([ems], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t.item())
-        e2e = {"value": n * a.steps / (ems / 1e3), "unit": "clauses/s (greedy)",
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ems / a.steps}
-    cpu = None
-    if rank == 0 and not a.no_cpu_baseline:
-        cpu = cpu_baseline_c5(rank)
-    line = {
-        "metric": METRIC, "value": n * a.steps / (total_ms / 1e3), "unit": "clauses/s (greedy)",
-        "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": total_ms / a.steps,
-        "higher_is_better": True, "scaling": "strong" if sharded else "weak", "vs_baseline": None,
-        "dtype": "u64",
-        "data": "synthetic", "config": {"workload": "C5: greedy mhs, m=4096, n=2^24 positive clauses (8 GiB bit matrix); step = device pack + greedy + prune",
-                                        "l2": "inputs (8 GiB) larger than L2",
-                                        "parallelism": (f"clause columns sharded x{world} (NCCL allreduce SUM of the counts per pick)"
-                                                        if sharded else "single GPU")},
-        "greedy": {"picks": r.n_picks, "size": size, "status": int(r.status.item()), "planted": 256,
-                   "passes": ck["launches"]},
-        "f3_incremental": {"ms_per_step": inc_ms / a.steps, "speedup": total_ms / inc_ms,
-                           "identical_picks": bool(same),
-                           "kernels": {k: {"launches": v["launches"], "ms_per_step": v["ms"]}
-                                       for k, v in kern2.items()}},
-        "gpu_launches": launches,
-        "roofline": {"bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                     "frac": ach / pk["hbm_gbs"], "traffic": traffic_of("count_kernel_c5"),
-                     "traffic_source": "profiles/traffic.json (ncu --set full, scripts/prof_c5.py --full)",
-                     "kernel": "count_kernel", "share_of_step": ck["ms"] / (total_ms / a.steps),
-                     "per_launch": {"bytes": bytes_per_launch, "ms": ck["ms"] / eff},
-                     "ncu": ncu_evidence("count_kernel")},
-        "clocks": clocks,
-        "e2e": e2e,
-        "cpu_baseline": cpu,
-        "kernels": {k: {"launches": v["launches"], "ms_per_step": v["ms"]} for k, v in kern.items()},
-    }
-    if rank == 0:
-        print(json.dumps(line), flush=True)
-
-
-C5_SAMPLE_N = 1 << 21
+        ems = ctx.max_([ems])[0]
+        rec["e2e"] = {"value": n * steps / (ems / 1e3), "unit": "clauses/s (greedy)",
+                      "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ems / steps}
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        rec["cpu_baseline"] = cpu_baseline_c5(ctx, flush)
+    return rec
 
 
 def c5_oracle_once(csr):
@@ -645,22 +671,35 @@ def c5_oracle_once(csr):
     return time.perf_counter() - t0, g
 
 
-def cpu_baseline_c5(rank):
+def cpu_baseline_c5(ctx, flush):
     """The oracle's textbook greedy (recount per pick) on a C5-recipe instance
-    with 1/8 of the clauses, repeated for >= 10 s."""
+    with 1/8 of the clauses, repeated for >= 10 s; the GPU (recounting path,
+    same pack + greedy) timed on the same instance."""
     import oracle
+    import paper_2011_08373_b200 as gr
     from paper_2011_08373_b200 import synth
 
-    csr, _ = synth.c5_clauses(seed=synth.seed_for(5, rank), n=C5_SAMPLE_N)
+    csr, _ = synth.c5_clauses(seed=synth.seed_for(5, 0), n=C5_SAMPLE_N)
     sec, reps = 0.0, 0
     while sec < 10.0 and reps < 20:
         dt, _ = c5_oracle_once(csr)
         sec += dt
         reps += 1
+
+    def gstep():
+        bm = gr.pack_bitmatrix(csr.m, csr.pos_off, csr.pos_var, csr.neg_off, csr.neg_var,
+                               device=ctx.dev, check=False, keep_csr=False)
+        gr.mhs_greedy_matrix(bm)
+
+    gstep()
+    gms, _ = time_steps(gstep, 3, ctx, flush, clocks=False)
     return {"value": C5_SAMPLE_N * reps / sec, "unit": "clauses/s (greedy)",
             "cores": oracle.num_threads(), "kind": "oracle",
             "sample": f"{reps} greedy solve(s) of a C5-recipe instance with n = 2^21 clauses "
-                      f"(1/8 of C5), m = 4096", "seconds": sec}
+                      f"(1/8 of C5), m = 4096", "seconds": sec,
+            "same_set_gpu": {"value": C5_SAMPLE_N * 3 / (gms / 1e3), "unit": "clauses/s (greedy)",
+                             "ms_per_step": gms / 3,
+                             "note": "the GPU step (host CSR already on the device) on that same instance"}}
 
 
 # ---------------------------------------------------------------- CPU oracle legs
@@ -693,44 +732,127 @@ def oracle_sample(cfg, cb):
         return cb.subset(idx), f"{len(idx)} of {cb.B} C2 instances (those with m <= 26), PMS+MHS+greedy"
     if cfg == "c4":
         idx = list(range(48))
-        return cb.subset(idx), f"first 48 of {cb.B} C4 instances, WPMS"
-    return cb, "whole workload"
+        return cb.subset(idx), f"first 48 of {cb.B} C4 instances, WPMS+MHS+greedy"
+    return cb, "whole workload, PMS+MHS+greedy"
 
 
-def run_oracle_once(cfg, sub):
+def run_oracle_once(sub):
     import oracle
 
     t0 = time.perf_counter()
     p = oracle.batch("pms", sub)
-    cands = float(p.decided.astype(np.float64).sum())
-    if cfg != "c4":
-        h = oracle.batch("mhs", sub)
-        oracle.batch("greedy", sub)
-        cands += float(h.decided.astype(np.float64).sum())
+    h = oracle.batch("mhs", sub)
+    oracle.batch("greedy", sub)
+    cands = float(p.decided.astype(np.float64).sum() + h.decided.astype(np.float64).sum())
     return time.perf_counter() - t0, cands
 
 
-def cpu_baseline(cfg, cb):
+def cpu_baseline(cfg, cb, ctx, flush):
+    """The oracle as it stands on this host's cores, on a bounded sample of
+    the workload; and the GPU step timed on that same sample (like-for-like
+    instances/s and candidates/s: the decided counts are the same by parity)."""
     import oracle
+    import paper_2011_08373_b200 as gr
 
     sub, desc = oracle_sample(cfg, cb)
     sec, cands, reps = 0.0, 0.0, 0
-    while sec < 10.0 and reps < 50:
-        dt, c = run_oracle_once(cfg, sub)
+    while sec < 10.0 and reps < 50 and (cfg != "c1" or reps < 100000):
+        dt, c = run_oracle_once(sub)
         sec += dt
         cands += c
         reps += 1
-    return {"value": cands / sec, "unit": "candidates/s", "cores": oracle.num_threads(),
-            "kind": "oracle", "sample": f"{reps} pass(es) over {desc}", "seconds": sec}
+        if cfg == "c1" and sec >= 2.0:
+            break
+    flags = gr.GR_FLAG_EXHAUSTIVE if cfg == "c3" else 0
+    flags = 0 if cfg == "c3" else flags  # the oracle sample runs first-witness
+    db = gr.DeviceBatch.from_host(sub, device=ctx.dev, flags=flags)
+    outs = [gr.DeviceResult.empty(sub.B, sub.W, ctx.dev) for _ in range(3)]
+
+    def gstep():
+        gr.solve_pms_mhs(db, outs[0], outs[1])
+        gr.mhs_greedy(db, outs[2])
+
+    gstep()
+    gms, _ = time_steps(gstep, 5, ctx, flush, clocks=False)
+    g = gr.to_host_many(outs[:2])
+    gc = float(g[0]["decided"].astype(np.float64).sum() + g[1]["decided"].astype(np.float64).sum())
+    ov, oi = cands / sec, sub.B * reps / sec
+    gv, gi = gc * 5 / (gms / 1e3), sub.B * 5 / (gms / 1e3)
+    return {"value": ov, "unit": "candidates/s", "cores": oracle.num_threads(), "kind": "oracle",
+            "instances_per_s": oi, "sample": f"{reps} pass(es) over {desc}", "seconds": sec,
+            "same_set_gpu": {"value": gv, "unit": "candidates/s", "instances_per_s": gi,
+                             "ms_per_step": gms / 5, "ratio_instances_per_s": gi / oi,
+                             "note": "the GPU step on the oracle's sample (same instances, same "
+                                     "decided counts by parity)"}}
+
+
+# ---------------------------------------------------------------- main
+def main():
+    a = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        return run_reference(a, rank, world)
+    import torch
+    import torch.distributed as dist
+
+    import paper_2011_08373_b200 as gr  # noqa: F401  (fails loudly without the CUDA library)
+
+    # functional check of the multi-rank code on one GPU (never a measurement):
+    # GR_BENCH_ONE_GPU=1 puts every rank on cuda:0 with the gloo backend --
+    # the ranks' kernels never wait on each other, only host collectives do
+    one_gpu = os.environ.get("GR_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
+    torch.cuda.set_device(local)
+    if world > 1:
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    ctx = Ctx(rank, world, local, dev)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    head_cfg = "c2" if a.config == "all" else a.config
+    head = run_c5(a, ctx, flush) if head_cfg == "c5" else run_exact(a, head_cfg, ctx, flush)
+    line = {
+        "metric": METRIC, "value": head["value"], "unit": head["unit"], "n_gpus": world,
+        "steps": head["steps"], "warmup": head["warmup"], "ms_per_step": head["ms_per_step"],
+        "higher_is_better": True, "scaling": head["scaling"], "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic (seeded, SURVEY.md §8(d) recipe; DESIGN.md §6)",
+        "config": {"workload": head["workload"],
+                   "l2": head.get("l2", "flushed between timed steps (256 MiB write)"),
+                   "parallelism": head["parallelism"]},
+    }
+    for k, v in head.items():
+        if k not in ("workload", "value", "unit", "steps", "warmup", "ms_per_step", "scaling",
+                     "parallelism", "l2"):
+            line[k] = v
+    if a.config == "all":
+        subs = {}
+        for cfg in ("c1", "c3", "c4", "c5"):
+            try:
+                subs[cfg] = run_c5(a, ctx, flush) if cfg == "c5" else run_exact(a, cfg, ctx, flush, sub=True)
+            except Exception as e:  # a failing sub-config must not hide the headline
+                subs[cfg] = {"error": f"{type(e).__name__}: {e}"}
+            torch.cuda.empty_cache()
+        line["configs"] = subs
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def run_reference(a, rank, world):
-    """--impl reference: the CPU oracle (this tier's reference) on the host."""
+    """--impl reference: the CPU oracle (this tier's reference) on the host,
+    on the headline config (C2; --config c1..c5 for the others)."""
     if rank != 0:
         return
     import oracle
 
-    if a.config == "c5":
+    cfg = "c2" if a.config == "all" else a.config
+    if cfg == "c5":
         from paper_2011_08373_b200 import synth
 
         csr, _ = synth.c5_clauses(seed=synth.seed_for(5, 0), n=C5_SAMPLE_N)
@@ -753,12 +875,11 @@ def run_reference(a, rank, world):
                     "d2h_bytes_per_step": 0},
         }), flush=True)
         return
-    cfg = a.config if a.config in ("c1", "c2", "c3", "c4") else "c2"
-    cb, desc = make_workload(cfg, 0)
+    cb = make_workload(cfg, 0)
     sub, sdesc = oracle_sample(cfg, cb)
     ts, cands = [], 0.0
     for s in range(a.warmup + a.steps):
-        dt, c = run_oracle_once(cfg, sub)
+        dt, c = run_oracle_once(sub)
         if s >= a.warmup:
             ts.append(dt)
             cands += c
@@ -768,7 +889,8 @@ def run_reference(a, rank, world):
         "impl": "reference", "metric": METRIC, "value": v, "unit": "candidates/s", "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * sec / a.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
-        "data": "synthetic", "config": {"workload": desc},
+        "data": "synthetic", "config": {"workload": DESC[cfg]},
+        "instances_per_s": sub.B * a.steps / sec,
         "cpu_baseline": {"value": v, "unit": "candidates/s", "cores": oracle.num_threads(),
                          "kind": "oracle", "sample": sdesc},
         "e2e": {"value": v, "unit": "candidates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

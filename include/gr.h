@@ -197,6 +197,23 @@ int64_t *gr_exact_level_keys(const gr_batch *in, int which, void *ws);
 int gr_exact_finish(const gr_batch *in, int which, int k, gr_result *out, void *ws,
                     size_t ws_bytes, gr_stream_t s, int32_t *n_active);
 
+/* ---- fused PMS + MHS, step-wise (rank-range sharding of the fused walk) --
+ * The pair session: gr_solve_pms_mhs's fused walk (unit weights, no k_start)
+ * with the level loop owned by the caller, exactly like the gr_exact_*
+ * session above -- ws holds two halves of gr_workspace_bytes(in, 0) (the PMS
+ * state, then the MHS state).  Per level every rank calls
+ * gr_pair_level(in, k, r, G, ...), all-reduces (MIN, int64) BOTH key arrays
+ * (gr_pair_level_keys(in, ws, 0) -- PMS -- and (.., 1) -- MHS), then
+ * gr_pair_finish.  Results equal gr_solve_pms / gr_mhs_exact.  Errors:
+ * GR_EINVAL also for weights or k_start (the fused walk is cardinality-only). */
+int gr_pair_prepare(const gr_batch *in, gr_result *out_pms, gr_result *out_mhs, void *ws,
+                    size_t ws_bytes, gr_stream_t s, int32_t *n_active);
+int gr_pair_level(const gr_batch *in, int k, int shard, int nshard, void *ws, size_t ws_bytes,
+                  gr_stream_t s);
+int64_t *gr_pair_level_keys(const gr_batch *in, void *ws, int which);
+int gr_pair_finish(const gr_batch *in, int k, gr_result *out_pms, gr_result *out_mhs, void *ws,
+                   size_t ws_bytes, gr_stream_t s, int32_t *n_active);
+
 /* ---- greedy at scale: one phi+ as a variable-major bit matrix ----------- */
 typedef struct {
   int32_t m;              /* host: number of variables (rows), >= 1 */

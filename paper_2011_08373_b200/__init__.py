@@ -4,7 +4,8 @@ Public API (thin marshalling over libgrsolve.so, include/gr.h):
     DeviceBatch, DeviceResult           device-resident clause batches / results
     solve_pms, mhs_exact, mhs_greedy    the three solvers
     solve                               the composite Solve with the MaxSAT fallback
-    ExactSession                        prepare / level / finish for sharded runs
+    ExactSession, PairSession           prepare / level / finish for sharded runs (PairSession:
+                                        the fused PMS + MHS walk)
     pack_bitmatrix, mhs_greedy_matrix   greedy at scale over a bit matrix
     greedy_count_shard                  shard hook for the multi-GPU greedy
 Seeded synthetic workloads: paper_2011_08373_b200.synth.
@@ -15,4 +16,5 @@ from ._native import (  # noqa: F401
     bitmatrix_ld, greedy_count_shard, lib, mhs_exact, mhs_greedy, mhs_greedy_matrix,
     pack_bitmatrix, solve_pms, version, launch_count, profiler, Profiler, solve,
     GR_STRATEGY_MHS, GR_STRATEGY_MAXSAT, solve_pms_mhs, GreedyShard, to_host_many, GreedyMatrixResult,
+    PairSession,
 )

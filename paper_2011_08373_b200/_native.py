@@ -32,7 +32,8 @@ EXPORTED = [
     "gr_profile", "gr_profile_read", "gr_launch_count", "gr_solve", "gr_solve_pms_mhs",
     "gr_greedy_shard_workspace_bytes", "gr_greedy_shard_begin", "gr_greedy_shard_step",
     "gr_greedy_shard_state", "gr_greedy_shard_private", "gr_greedy_shard_remove",
-    "gr_greedy_shard_finalize",
+    "gr_greedy_shard_finalize", "gr_pair_prepare", "gr_pair_level", "gr_pair_level_keys",
+    "gr_pair_finish",
 ]
 GR_STRATEGY_MHS, GR_STRATEGY_MAXSAT = 0, 1
 
@@ -111,6 +112,13 @@ def lib():
         L.gr_greedy_shard_finalize.argtypes = [vp, vp, vp, vp, vp, sz, vp]
         for f in (L.gr_greedy_shard_begin, L.gr_greedy_shard_step, L.gr_greedy_shard_state,
                   L.gr_greedy_shard_private, L.gr_greedy_shard_remove, L.gr_greedy_shard_finalize):
+            f.restype = C.c_int
+        L.gr_pair_prepare.argtypes = [vp, vp, vp, vp, sz, vp, vp]
+        L.gr_pair_level.argtypes = [vp, C.c_int, C.c_int, C.c_int, vp, sz, vp]
+        L.gr_pair_level_keys.argtypes = [vp, vp, C.c_int]
+        L.gr_pair_level_keys.restype = vp
+        L.gr_pair_finish.argtypes = [vp, C.c_int, vp, vp, vp, sz, vp, vp]
+        for f in (L.gr_pair_prepare, L.gr_pair_level, L.gr_pair_finish):
             f.restype = C.c_int
         L.gr_last_error.restype = C.c_char_p
         L.gr_version.restype = C.c_char_p
@@ -405,6 +413,57 @@ class ExactSession:
 
 
 # ---- greedy at scale ---------------------------------------------------------
+class PairSession:
+    """Step-wise fused PMS + MHS (gr_pair_prepare / level / finish) for the
+    rank-range-sharded driver: same protocol as ExactSession, but level_keys()
+    returns both key arrays (PMS, MHS) to all-reduce."""
+
+    def __init__(self, db: DeviceBatch, out_pms: Optional[DeviceResult] = None,
+                 out_mhs: Optional[DeviceResult] = None, stream=None):
+        self.L = lib()
+        self.db = db
+        self.b = db.struct(False)
+        nbytes = self.L.gr_workspace_bytes(C.byref(self.b), PMS)
+        if nbytes == 0:
+            raise GrError("gr_workspace_bytes rejected the batch")
+        half = (nbytes + 255) // 256 * 256
+        self.ws = workspace(2 * half, db.m.device, tag="pair_session")
+        dev = db.m.device
+        self.out_pms = out_pms if out_pms is not None else DeviceResult.empty(db.B, db.W, dev)
+        self.out_mhs = out_mhs if out_mhs is not None else DeviceResult.empty(db.B, db.W, dev)
+        self.r1, self.r2 = self.out_pms.struct(), self.out_mhs.struct()
+        self.stream = stream
+
+    def prepare(self) -> int:
+        n = C.c_int32(0)
+        _check(self.L.gr_pair_prepare(C.byref(self.b), C.byref(self.r1), C.byref(self.r2),
+                                      _ptr(self.ws), self.ws.numel(), _stream(self.stream),
+                                      C.byref(n)), "gr_pair_prepare")
+        return int(n.value)
+
+    def level(self, k: int, shard: int = 0, nshard: int = 1):
+        _check(self.L.gr_pair_level(C.byref(self.b), k, shard, nshard, _ptr(self.ws),
+                                    self.ws.numel(), _stream(self.stream)), "gr_pair_level")
+
+    def level_keys(self):
+        """(PMS keys, MHS keys): torch int64 views [B] of the workspace."""
+        torch = _torch()
+        base = _ptr(self.ws)
+        out = []
+        for which in (0, 1):
+            p = self.L.gr_pair_level_keys(C.byref(self.b), _ptr(self.ws), which)
+            off = p - base
+            out.append(self.ws[off: off + 8 * self.db.B].view(torch.int64))
+        return tuple(out)
+
+    def finish(self, k: int) -> int:
+        n = C.c_int32(0)
+        _check(self.L.gr_pair_finish(C.byref(self.b), k, C.byref(self.r1), C.byref(self.r2),
+                                     _ptr(self.ws), self.ws.numel(), _stream(self.stream),
+                                     C.byref(n)), "gr_pair_finish")
+        return int(n.value)
+
+
 def bitmatrix_ld(n_pos: int) -> int:
     return int(lib().gr_bitmatrix_ld(n_pos))
 

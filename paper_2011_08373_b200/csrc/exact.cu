@@ -677,9 +677,21 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
       cc = lo - 1;
     }
     base_top = r_lo - rr;  // rank of (Utop, the J lowest elements of [0, min Utop))
+    // element i = the largest c <= cc with C(c, i) <= rr; the rows are
+    // scanned downward four at a time (four independent shared-memory loads
+    // per step instead of a chain of dependent ones); C(i-1, i) = 0 ends the
+    // scan at row i-1 at the latest, so clamping rows at 0 is harmless
     for (int i = J; i >= 1; i--) {
       u64 v;
-      while ((v = CS(cc, i)) > rr) cc--;
+      for (;;) {
+        const u64 v0 = CS(cc, i), v1 = CS(max(cc - 1, 0), i), v2 = CS(max(cc - 2, 0), i),
+                  v3 = CS(max(cc - 3, 0), i);
+        if (v0 <= rr) { v = v0; break; }
+        if (v1 <= rr) { v = v1; cc -= 1; break; }
+        if (v2 <= rr) { v = v2; cc -= 2; break; }
+        if (v3 <= rr) { v = v3; cc -= 3; break; }
+        cc -= 4;
+      }
       Slow |= (M)1 << cc;
       rr -= v;
       cc--;
@@ -689,8 +701,11 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
   // Iterator state: the path t_0 > t_1 > ... > t_{d-1} of part-B choices
   // below Utop; the current node is (j = J - d, U, e = t_{d-1} or e_top) with
   // region R = R_j and ep = the parent's e (t_{d-2} or e_top).  tp is a stack
-  // of the older ancestors t_{d-3} .. t_0, e_top (6 bits each, most recent
-  // lowest; at depth d it holds d - 1 entries, so JMAX <= 12).  Sub-blocks
+  // of the older ancestors t_{d-3} .. t_0, e_top (SB bits each, most recent
+  // lowest; at depth d it holds d - 1 entries).  An entry stores e - 1: every
+  // stored e is >= 1 and e_top can be m_eff = 32, which does not fit 5 bits
+  // (a round-1 build stored e itself and read e_top = 32 back as 0, cutting
+  // depth-1 siblings off in long windows at m_eff = 32).  Sub-blocks
   // partition the level in rank order, so the next sub-block starts where
   // this one ends: base += n.
   M U = Utop;
@@ -719,7 +734,7 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
       }
     }
     Slow ^= (M)1 << t;
-    if (d > 0) tp = (tp << SB) | (u64)ep;
+    if (d > 0) tp = (tp << SB) | (u64)(ep - 1);
     ep = e;
     e = t;
     U |= (M)1 << t;
@@ -743,6 +758,13 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
     // U.  Then all C(e, j) candidates of the subtree are decided at once.
     bool dead = dead0;
     dead0 = false;
+#ifdef GR_DIRECT_WU
+    if (MODE == 2) {
+      u64 wd = 0;
+      for (M tt = U; tt; tt &= tt - 1) wd += w[ctz(tt)];
+      wU = wd;
+    }
+#endif
     const u64 WU = wU;  // weighted: W(U), and a bound on the whole subtree -- every
                         // x in it weighs >= W(U) + S_j (the j smallest weights);
                         // it can only matter below the incumbent of earlier
@@ -807,7 +829,7 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
     // ---- advance: first child t = R of this node, else the next sibling up
     // the path
     if (!dead && j >= 2 && R < e) {
-      if (d > 0) tp = (tp << SB) | (u64)ep;
+      if (d > 0) tp = (tp << SB) | (u64)(ep - 1);
       ep = e;
       e = R;
       U |= (M)1 << R;
@@ -825,7 +847,7 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
         j++;
         e = ep;
         if (d > 0) {  // the stack holds the ancestors above the parent
-          ep = (int)(tp & ((1u << SB) - 1u));
+          ep = (int)(tp & ((1u << SB) - 1u)) + 1;
           tp >>= SB;
         }
       } while (d > 0 && e + 1 >= ep);
@@ -1342,9 +1364,21 @@ struct QParams {
   int lanes;       // threads of the grid (lane window sizing)
   int grid, nwarps;  // CTAs of the queue_kernel grid, warps per CTA (ring entries per task)
   int wpl;         // lane windows per lane (unit | weighted << 16)
-  u64 lane_max, lane_max_w, fixed_lane;
+  u64 lane_max, lane_max_w, fixed_lane, lane_min;
 };
 
+// gpu-scope acquire load / acq_rel add (PTX memory model): the completion
+// count and the ring entries order what they publish without a full fence
+__device__ __forceinline__ u64 ld_acquire(const u64 *p) {
+  u64 v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ u64 atom_add_acq_rel(u64 *p, u64 v) {
+  u64 old;
+  asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+  return old;
+}
 __device__ __forceinline__ u64 vld(const u64 *p) { return *(const volatile u64 *)p; }
 __device__ __forceinline__ i64 vld(const i64 *p) { return *(const volatile i64 *)p; }
 __device__ __forceinline__ int vld(const int *p) { return *(const volatile int *)p; }
@@ -1381,7 +1415,7 @@ __device__ u64 q_prepare(const QParams &P, int sv, int b, int k, u64 work, u64 *
   const u64 wpl = wt ? (u64)(P.wpl >> 16) : (u64)(P.wpl & 0xffff);
   const u64 Lmax = wt ? P.lane_max_w : P.lane_max;
   u64 L = work / ((u64)P.lanes * (wpl ? wpl : 2));
-  L = L < 256 ? 256 : (L > Lmax ? Lmax : L);
+  L = L < P.lane_min ? P.lane_min : (L > Lmax ? Lmax : L);
   L = 1ull << (63 - __clzll((long long)L));
   if (P.fixed_lane) L = P.fixed_lane;
   const u64 nch = (ck + 32 * L - 1) / (32 * L);
@@ -1479,8 +1513,9 @@ __device__ void q_commit_warp(const QParams &P, int sv, int b, int k) {
   u64 n = 0, word = 0, e0 = 0;
   if (lane == 0) {
     Ctrl *c = P.ws[0].ctrl;
+    u64 *qw = &P.ws[sv].ctrl->q_work;  // work in flight of this solve
     const u64 ck = binom(P.ws[sv].meff[b], k);
-    atomicAdd((unsigned long long *)&c->q_work, (unsigned long long)(-(long long)ck));
+    atomicAdd((unsigned long long *)qw, (unsigned long long)(-(long long)ck));
     bool open;
     if (P.fused) {
       const bool o0 = q_commit_one(P, 0, b, k);
@@ -1491,9 +1526,9 @@ __device__ void q_commit_warp(const QParams &P, int sv, int b, int k) {
     }
     if (open && k < 64) {
       const u64 ck1 = binom(P.ws[sv].meff[b], k + 1);
-      const u64 wk = atomicAdd((unsigned long long *)&c->q_work, (unsigned long long)ck1) + ck1;
+      const u64 wk = atomicAdd((unsigned long long *)qw, (unsigned long long)ck1) + ck1;
       n = q_prepare(P, sv, b, k + 1, wk, &word, &e0);
-      if (!n) atomicAdd((unsigned long long *)&c->q_work, (unsigned long long)(-(long long)ck1));
+      if (!n) atomicAdd((unsigned long long *)qw, (unsigned long long)(-(long long)ck1));
     }
     if (!n) {
       __threadfence();  // results before the count that ends the launch
@@ -1510,33 +1545,30 @@ __device__ void q_commit_warp(const QParams &P, int sv, int b, int k) {
 // the first level of every open (instance, solve) and count them (the pack
 // zeroed the queue counters)
 __global__ void __launch_bounds__(1024) queue_seed_kernel(QParams P, long long budget) {
-  __shared__ unsigned long long s_work;
-  if (threadIdx.x == 0) {
-    P.ws[0].ctrl->q_budget = budget;
-    s_work = 0;
-  }
+  __shared__ unsigned long long s_work[2];
+  if (threadIdx.x < 2) s_work[threadIdx.x] = 0;
+  if (threadIdx.x == 0) P.ws[0].ctrl->q_budget = budget;
   __syncthreads();
   const int ns = P.fused ? 1 : P.nsolve;
-  u64 my = 0;
-  for (int sv = 0; sv < ns; sv++)
-    for (int b = threadIdx.x; b < P.in[sv].B; b += blockDim.x) {
-      const WS &w = P.ws[sv];
-      if (!w.done[b] || (P.fused && !P.ws[1].done[b])) my += binom(w.meff[b], w.ks[b]);
-    }
-  atomicAdd(&s_work, (unsigned long long)my);
+  auto open = [&](int sv, int b) { return !P.ws[sv].done[b] || (P.fused && !P.ws[1].done[b]); };
+  for (int sv = 0; sv < ns; sv++) {  // the work in flight of each solve: its first levels
+    u64 my = 0;
+    for (int b = threadIdx.x; b < P.in[sv].B; b += blockDim.x)
+      if (open(sv, b)) my += binom(P.ws[sv].meff[b], P.ws[sv].ks[b]);
+    atomicAdd(&s_work[sv], (unsigned long long)my);
+  }
   __syncthreads();
-  const u64 work = s_work;
-  if (threadIdx.x == 0) P.ws[0].ctrl->q_work = work;
+  if (threadIdx.x < ns) P.ws[threadIdx.x].ctrl->q_work = s_work[threadIdx.x];
   for (int sv = 0; sv < ns; sv++)
     for (int b = threadIdx.x; b < P.in[sv].B; b += blockDim.x) {
       const WS &w = P.ws[sv];
-      if (!(!w.done[b] || (P.fused && !P.ws[1].done[b]))) continue;
+      if (!open(sv, b)) continue;
       atomicAdd(&P.ws[0].ctrl->q_remaining, 1);
       u64 word, e0;
-      const u64 n = q_prepare(P, sv, b, w.ks[b], work, &word, &e0);
+      const u64 n = q_prepare(P, sv, b, w.ks[b], s_work[sv], &word, &e0);
       if (!n) {
         atomicSub(&P.ws[0].ctrl->q_remaining, 1);
-        atomicAdd((unsigned long long *)&P.ws[0].ctrl->q_work,
+        atomicAdd((unsigned long long *)&w.ctrl->q_work,
                   (unsigned long long)(-(long long)binom(w.meff[b], w.ks[b])));
       }
       for (u64 i = 0; i < n; i++) q_publish(P, word, e0, i);
@@ -1593,14 +1625,13 @@ __global__ void __launch_bounds__(NTK, COUNT ? 1 : ENUM_CTAS * NT / NTK) queue_k
       int ex = 0;
       u64 v = 0;
       for (int spin = 0;; spin++) {
-        v = vld(r);
+        v = ld_acquire(r);  // the task record is read after its entry
         if ((v & ~((1ull << 40) - 1ull)) == want) break;
         if (vld(&ctrl->q_remaining) == 0) { ex = 1; break; }
         __nanosleep(spin < 16 ? 32 : 128);
       }
       s_exit = ex;
       if (!ex) {
-        __threadfence();  // the task record after its entry
         if (v >> 39 & 1ull) atomicAdd((unsigned long long *)&ctrl->q_budget, 1ull);  // an extra entry is read
         const int tsv = (int)((v >> 38) & 1ull);
         const u64 ti = v & ((1ull << 38) - 1ull);
@@ -1642,29 +1673,32 @@ __global__ void __launch_bounds__(NTK, COUNT ? 1 : ENUM_CTAS * NT / NTK) queue_k
     }
     __syncthreads();
     if (t == 0) s_cur = s_sv * P.in[0].B + s_b;
-    // ---- warps pull warp chunks of this task until it is exhausted
+    // ---- warps pull warp chunks of this task until it is exhausted.  Lane 0
+    // claims one chunk ahead, so the atomic's latency overlaps the walk (not
+    // for the weighted walk: the claimed index held across it would spill).
+    constexpr bool AHEAD = KIND != 2;
+    u64 cn = 0;
+    if (AHEAD && lane == 0) cn = atomicAdd((unsigned long long *)&P.ws[s_sv].tasks[s_ti].claimed, 1ull);
     for (;;) {
       const int b = s_b, sv = s_sv;
-      Task *T = P.ws[sv].tasks + s_ti;
       const u64 nch = s_nch;
-      u64 c = 0;
+      u64 c = AHEAD ? cn : 0ull;
+      if (!AHEAD && lane == 0) c = atomicAdd((unsigned long long *)&P.ws[sv].tasks[s_ti].claimed, 1ull);
       int need = 0;  // bit 0: the chunk is needed (fused: for the PMS); bit 1: fused, for the MHS
-      if (lane == 0) {
-        c = atomicAdd((unsigned long long *)&T->claimed, 1ull);
-        if (c < nch) {
-          const u64 r0 = c * 32 * s_L;
-          if (KIND == 1) {
-            const i64 c1 = vld(&P.ws[0].lvlkey[b]), c2 = vld(&P.ws[1].lvlkey[b]);
-            const int np_ = !vld(&P.ws[0].done[b]) && !(c1 != GR_KEY_NONE && (u64)c1 < r0 && !P.exhaustive);
-            const int nm_ = !vld(&P.ws[1].done[b]) && !(c2 != GR_KEY_NONE && (u64)c2 < r0 && !P.exhaustive);
-            need = np_ | (nm_ << 1);
-          } else if (!P.weighted[sv] && !P.exhaustive) {
-            const i64 cur = vld(&P.ws[sv].lvlkey[b]);
-            need = !(cur != GR_KEY_NONE && (u64)cur < r0);  // a lower witness exists
-          } else {
-            need = 1;
-          }
+      if (lane == 0 && c < nch) {
+        const u64 r0 = c * 32 * s_L;
+        if (KIND == 1) {
+          const i64 c1 = vld(&P.ws[0].lvlkey[b]), c2 = vld(&P.ws[1].lvlkey[b]);
+          const int np_ = !vld(&P.ws[0].done[b]) && !(c1 != GR_KEY_NONE && (u64)c1 < r0 && !P.exhaustive);
+          const int nm_ = !vld(&P.ws[1].done[b]) && !(c2 != GR_KEY_NONE && (u64)c2 < r0 && !P.exhaustive);
+          need = np_ | (nm_ << 1);
+        } else if (!P.weighted[sv] && !P.exhaustive) {
+          const i64 cur = vld(&P.ws[sv].lvlkey[b]);
+          need = !(cur != GR_KEY_NONE && (u64)cur < r0);  // a lower witness exists
+        } else {
+          need = 1;
         }
+        if (AHEAD) cn = atomicAdd((unsigned long long *)&P.ws[sv].tasks[s_ti].claimed, 1ull);
       }
       c = __shfl_sync(0xffffffffu, c, 0);
       if (c >= nch) break;
@@ -1703,10 +1737,9 @@ __global__ void __launch_bounds__(NTK, COUNT ? 1 : ENUM_CTAS * NT / NTK) queue_k
         const int b2 = s_b, sv2 = s_sv;
         if (key != GR_KEY_NONE) atomicMin((long long *)&P.ws[sv2].lvlkey[b2], (long long)key);
         if (KIND == 1 && key_m != GR_KEY_NONE) atomicMin((long long *)&P.ws[1].lvlkey[b2], (long long)key_m);
-        __threadfence();  // the keys before the completion count
-        Task *T2 = P.ws[sv2].tasks + s_ti;
-        last = atomicAdd((unsigned long long *)&T2->done, 1ull) == s_nch - 1;
-        if (last) __threadfence();
+        // release: the keys before the completion count; acquire: the last
+        // arriver sees every chunk's keys
+        last = atom_add_acq_rel(&P.ws[sv2].tasks[s_ti].done, 1ull) == s_nch - 1;
       }
       last = __shfl_sync(0xffffffffu, last, 0);
       if (last) q_commit_warp(P, s_sv, s_b, s_k);
@@ -1789,6 +1822,25 @@ u64 lane_max(bool weighted) {  // the adaptive lane window's upper bound
   };
   static const u64 v[2] = {rd("GR_LANE_MAX", 262144ull), rd("GR_LANE_MAX_W", 65536ull)};
   return v[weighted ? 1 : 0];
+}
+// the device level loop's lane window knobs: GR_QWPL /
+// GR_QWPL_W (windows per lane over the work in flight), GR_QLANE_MIN,
+// GR_QLANE_MAX / GR_QLANE_MAX_W -- powers of two
+u64 env_u64(const char *name, u64 dflt, u64 lo, u64 hi) {
+  const char *e = getenv(name);
+  const u64 x = e ? strtoull(e, nullptr, 10) : dflt;
+  return (x < lo || x > hi) ? dflt : x;
+}
+struct QKnobs {
+  int wpl, wpl_w;
+  u64 lmin, lmax, lmax_w;
+};
+const QKnobs &qknobs() {
+  static const QKnobs k = {(int)env_u64("GR_QWPL", 1, 1, 0xffff), (int)env_u64("GR_QWPL_W", 1, 1, 0xffff),
+                           env_u64("GR_QLANE_MIN", 2048, 1, 1ull << 20),
+                           env_u64("GR_QLANE_MAX", 1ull << 20, 256, 1ull << 24),
+                           env_u64("GR_QLANE_MAX_W", 1ull << 16, 256, 1ull << 24)};
+  return k;
 }
 u64 lane_cands() {  // 0 = adaptive (GR_LANE_CANDIDATES overrides)
   const u64 v = lane_cands_raw();
@@ -2012,10 +2064,12 @@ int launch_queue(const gr_batch *in, int nsolve, int fused, const int which[2], 
   P.gen = g_qgen.fetch_add(1) % 4095ull + 1ull;  // 1..4095
   P.ring_mask = ring_cap(in->B) - 1;
   P.ring_log2 = 63 - __builtin_clzll(ring_cap(in->B));
-  P.wpl = windows_per_lane(false) | (windows_per_lane(true) << 16);
-  P.lane_max = lane_max(false);
-  P.lane_max_w = lane_max(true);
+  const QKnobs &kn = qknobs();
+  P.wpl = kn.wpl | (kn.wpl_w << 16);
+  P.lane_max = kn.lmax;
+  P.lane_max_w = kn.lmax_w;
   P.fixed_lane = lane_cands();
+  P.lane_min = kn.lmin;
   const bool small = enum_small(in);
   const int kind = fused ? 1 : ((P.weighted[0] || P.weighted[1]) ? 2 : 0);
 #define GR_QLAUNCH(COUNT, NTK)                                              \
@@ -2078,6 +2132,95 @@ extern "C" int gr_solve_pms(const gr_batch *in, gr_result *out, void *ws, size_t
   return solve_exact(in, out, ws, ws_bytes, s, 0);
 }
 
+// ---- fused PMS + MHS step-wise: the pair session (rank-range sharding) ------
+// The fused walk (MODE 3) with the level loop owned by the caller, as the
+// gr_exact_prepare / level / finish session: ws = two halves of
+// gr_workspace_bytes (PMS, then MHS); unit weights only.
+static int pair_ws(const gr_batch *in, void *ws, size_t ws_bytes, WS &w1, WS &w2) {
+  int rc = validate_batch(in, 0);
+  if (rc) return rc;
+  if (in->w || in->k_start) { gr_set_error("the fused pair session needs unit weights and no k_start"); return GR_EINVAL; }
+  const size_t half = align256(layout_of(in).total);
+  if (!ws || ws_bytes < 2 * half) { gr_set_error("workspace too small (2 x gr_workspace_bytes)"); return GR_EWORKSPACE; }
+  w1 = ws_of(in, ws);
+  w2 = ws_of(in, (char *)ws + half);
+  return GR_OK;
+}
+
+extern "C" int gr_pair_prepare(const gr_batch *in, gr_result *out_pms, gr_result *out_mhs, void *ws,
+                               size_t ws_bytes, gr_stream_t s, int32_t *n_active) {
+  WS w1, w2;
+  int rc = pair_ws(in, ws, ws_bytes, w1, w2);
+  if (rc) return rc;
+  if (!out_pms || !out_mhs || !out_pms->assign || !out_mhs->assign) { gr_set_error("null result"); return GR_EINVAL; }
+  cudaStream_t st = (cudaStream_t)s;
+  if ((rc = launch_pack(in, 1, out_mhs, w2, st))) return rc;
+  if ((rc = launch_finish(in, 1, out_mhs, w2, 0, st, nullptr))) return rc;
+  if ((rc = launch_pack(in, 0, out_pms, w1, st))) return rc;
+  if ((rc = launch_finish(in, 0, out_pms, w1, 0, st, w2.done))) return rc;
+  if (n_active) {
+    int *h = pinned_i32();
+    if (!h) { gr_set_error("cudaMallocHost failed"); return GR_ECUDA; }
+    GR_CUDA(cudaMemcpyAsync(h, &w1.ctrl->n_remaining, sizeof(int), cudaMemcpyDeviceToHost, st));
+    GR_CUDA(cudaStreamSynchronize(st));
+    *n_active = *h;
+  }
+  return GR_OK;
+}
+
+extern "C" int gr_pair_level(const gr_batch *in, int k, int shard, int nshard, void *ws,
+                             size_t ws_bytes, gr_stream_t s) {
+  WS w1, w2;
+  int rc = pair_ws(in, ws, ws_bytes, w1, w2);
+  if (rc) return rc;
+  if (k < 1 || k > 64 || nshard < 1 || shard < 0 || shard >= nshard) { gr_set_error("bad level/shard"); return GR_EINVAL; }
+  cudaStream_t st = (cudaStream_t)s;
+  EnumParams p;
+  p.ws = w1;
+  p.ws.active = w1.active + (size_t)(k & 1) * in->B;
+  p.ws2 = w2;
+  p.off = in->off;
+  p.k = k;
+  p.weighted = 0;
+  p.exhaustive = (in->flags & GR_FLAG_EXHAUSTIVE) ? 1 : 0;
+  p.prune = (in->flags & GR_FLAG_NO_PRUNE) ? 0 : 1;
+  p.shard = shard;
+  p.nshard = nshard;
+  p.fused = 1;
+  if (nshard > 1) GR_CUDA(cudaMemsetAsync(&w1.ctrl->next_chunk, 0, sizeof(u64), st));
+  return gr_prof_mode() == 2 ? launch_enum<true>(p, enum_small(in), st) : launch_enum<false>(p, enum_small(in), st);
+}
+
+extern "C" int64_t *gr_pair_level_keys(const gr_batch *in, void *ws, int which) {
+  if (!in || !ws || (which != 0 && which != 1)) return nullptr;
+  const size_t half = align256(layout_of(in).total);
+  return (int64_t *)ws_of(in, (char *)ws + (which ? half : 0)).lvlkey;
+}
+
+extern "C" int gr_pair_finish(const gr_batch *in, int k, gr_result *out_pms, gr_result *out_mhs,
+                              void *ws, size_t ws_bytes, gr_stream_t s, int32_t *n_active) {
+  WS w1, w2;
+  int rc = pair_ws(in, ws, ws_bytes, w1, w2);
+  if (rc) return rc;
+  if (k < 1 || k > 64) { gr_set_error("bad level"); return GR_EINVAL; }
+  if (!out_pms || !out_mhs) { gr_set_error("null result"); return GR_EINVAL; }
+  cudaStream_t st = (cudaStream_t)s;
+  const int P = std::max(1, std::min((in->B + FT - 1) / FT, 32));
+  GR_LAUNCH("finish_kernel", st, finish_fused_kernel<<<2 * P, FT, 0, st>>>(
+                                     in_of(in, 0), out_of(out_pms), w1, in_of(in, 1), out_of(out_mhs), w2, k,
+                                     (in->flags & GR_FLAG_EXHAUSTIVE) ? 1 : 0, enum_grid() * NT, lane_cands(),
+                                     windows_per_lane(false) | (windows_per_lane(true) << 16),
+                                     lane_max(false), lane_max(true), enum_small(in) ? NT_SMALL : NT));
+  if (n_active) {
+    int *h = pinned_i32();
+    if (!h) { gr_set_error("cudaMallocHost failed"); return GR_ECUDA; }
+    GR_CUDA(cudaMemcpyAsync(h, &w1.ctrl->n_remaining, sizeof(int), cudaMemcpyDeviceToHost, st));
+    GR_CUDA(cudaStreamSynchronize(st));
+    *n_active = *h;
+  }
+  return GR_OK;
+}
+
 // PMS and MHS of one batch: unit weights -> one fused walk (MODE 3) on s_pms;
 // otherwise their level loops interleaved on two streams (the small levels
 // and level tails of one overlap the other's work).
@@ -2101,56 +2244,19 @@ extern "C" int gr_solve_pms_mhs(const gr_batch *in, gr_result *out_pms, gr_resul
       if ((rc = launch_queue(in, 1, 1, wh, out_pms, out_mhs, w1, w2, st))) return rc;
       return stream_join(st, (cudaStream_t)s_mhs);
     }
-    if ((rc = launch_pack(in, 1, out_mhs, w2, st))) return rc;
-    if ((rc = launch_finish(in, 1, out_mhs, w2, 0, st, nullptr))) return rc;
-    if ((rc = launch_pack(in, 0, out_pms, w1, st))) return rc;
-    if ((rc = launch_finish(in, 0, out_pms, w1, 0, st, w2.done))) return rc;
-    int *h = pinned_i32();
-    if (!h) { gr_set_error("cudaMallocHost failed"); return GR_ECUDA; }
-    GR_CUDA(cudaMemcpyAsync(h, &w1.ctrl->n_remaining, sizeof(int), cudaMemcpyDeviceToHost, st));
-    GR_CUDA(cudaStreamSynchronize(st));
-    int n = h[0];
-    const int grid = enum_grid();
+    // the level-synchronous host loop over the pair session (A/B, GR_HOST_LOOP)
+    int32_t n = 0;
+    if ((rc = gr_pair_prepare(in, out_pms, out_mhs, ws, ws_bytes, s_pms, &n))) return rc;
     const int SPEC = spec_levels();
     for (int k = 1; n > 0 && k <= 64;) {
       for (int i = 0; i < SPEC && k <= 64; i++, k++) {
-        EnumParams p;
-        p.ws = w1;
-        p.ws.active = w1.active + (size_t)(k & 1) * in->B;
-        p.ws2 = w2;
-        p.off = in->off;
-        p.k = k;
-        p.weighted = 0;
-        p.exhaustive = (in->flags & GR_FLAG_EXHAUSTIVE) ? 1 : 0;
-        p.prune = (in->flags & GR_FLAG_NO_PRUNE) ? 0 : 1;
-        p.shard = 0;
-        p.nshard = 1;
-        p.fused = 1;
-        (void)grid;
-        if ((rc = gr_prof_mode() == 2 ? launch_enum<true>(p, enum_small(in), st)
-                                      : launch_enum<false>(p, enum_small(in), st)))
+        if ((rc = gr_pair_level(in, k, 0, 1, ws, ws_bytes, s_pms))) return rc;
+        const bool last = i == SPEC - 1 || k == 64;
+        if ((rc = gr_pair_finish(in, k, out_pms, out_mhs, ws, ws_bytes, s_pms, last ? &n : nullptr)))
           return rc;
-        const int P = std::max(1, std::min((in->B + FT - 1) / FT, 32));
-        GR_LAUNCH("finish_kernel", st, finish_fused_kernel<<<2 * P, FT, 0, st>>>(
-                                           in_of(in, 0), out_of(out_pms), w1, in_of(in, 1),
-                                           out_of(out_mhs), w2, k,
-                                           (in->flags & GR_FLAG_EXHAUSTIVE) ? 1 : 0, enum_grid() * NT, lane_cands(),
-                                           windows_per_lane(false) | (windows_per_lane(true) << 16),
-                                           lane_max(false), lane_max(true),
-                                           enum_small(in) ? NT_SMALL : NT));
       }
-      GR_CUDA(cudaMemcpyAsync(h, &w1.ctrl->n_remaining, sizeof(int), cudaMemcpyDeviceToHost, st));
-      GR_CUDA(cudaStreamSynchronize(st));
-      n = h[0];
     }
-    if (s_mhs != s_pms) {  // the MHS results are ordered on s_mhs too
-      cudaEvent_t ev;
-      GR_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-      GR_CUDA(cudaEventRecord(ev, st));
-      GR_CUDA(cudaStreamWaitEvent((cudaStream_t)s_mhs, ev, 0));
-      GR_CUDA(cudaEventDestroy(ev));
-    }
-    return GR_OK;
+    return stream_join(st, (cudaStream_t)s_mhs);
   }
   if (!host_loop()) {  // weighted PMS + MHS (or start levels): one launch serves both solves
     if (!out_pms || !out_mhs) { gr_set_error("null result"); return GR_EINVAL; }

@@ -58,7 +58,9 @@ def run_levels_sharded(session, rank: int, world: int,
     while n > 0:
         k += 1
         session.level(k, rank, world)
-        allreduce_min(session.level_keys())
+        keys = session.level_keys()
+        for t in (keys if isinstance(keys, tuple) else (keys,)):  # PairSession: PMS and MHS keys
+            allreduce_min(t)
         n = session.finish(k)
     return k
 
@@ -81,6 +83,19 @@ def solve_exact_sharded(db, which: int, rank: int, world: int, group=None, out=N
     levels = run_levels_sharded(s, rank, world,
                                 nccl_allreduce_min(group) if world > 1 else (lambda t: None))
     return s.out, levels
+
+
+def solve_pair_sharded(db, rank: int, world: int, group=None, out_pms=None, out_mhs=None):
+    """PMS and MHS of a unit-weight batch decided by ONE fused walk whose
+    level rank ranges are split across the ranks of ``group`` (gr_pair_*):
+    per level one NCCL all-reduce (MIN) of each key array.  Every rank returns
+    the same (out_pms, out_mhs, levels)."""
+    from . import _native as N
+
+    s = N.PairSession(db, out_pms=out_pms, out_mhs=out_mhs)
+    levels = run_levels_sharded(s, rank, world,
+                                nccl_allreduce_min(group) if world > 1 else (lambda t: None))
+    return s.out_pms, s.out_mhs, levels
 
 
 # ---- column-sharded greedy (C5) ------------------------------------------------
@@ -214,6 +229,60 @@ def solve_batch_sharded(cb, rank: int, world: int, solve_fn: Callable, allgather
         out["cost"][idx] = g[:, 2].view(np.uint64)
         out["decided"][idx] = g[:, 3].view(np.uint64)
         out["assign"][idx] = g[:, 4:].view(np.uint64)
+    return out
+
+
+def measured_costs(cb, device="cuda") -> np.ndarray:
+    """Per-instance cost for the batch split, measured: the candidates each
+    instance's exact PMS + MHS decides (gr_result.decided of one solve on
+    this rank's GPU; the level loop's work grows with it), plus a constant
+    per instance for its pack and level commits."""
+    from . import _native as N
+
+    db = N.DeviceBatch.from_host(cb, device=device)
+    p, h = N.solve_pms_mhs(db)
+    r = N.to_host_many([p, h])
+    return r[0]["decided"].astype(np.float64) + r[1]["decided"].astype(np.float64) + 1e4
+
+
+def solve_batch_sharded_device(cb, parts, rank: int, db, outs, allgather):
+    """One rank's share of a batch split over the ranks (``parts`` from
+    shard_instances): PMS + MHS (one launch) and greedy of the rank's
+    sub-batch ``db`` into ``outs`` on its GPU, then one all-gather of
+    (index, PMS status/cost/decided/assign, MHS decided) rows -- on the
+    device, NCCL -- so every rank holds the whole batch's results in input
+    order (host arrays)."""
+    import torch
+
+    from . import _native as N
+
+    mine = parts[rank]
+    W = cb.W
+    width = 5 + W
+    maxn = max(max(len(p) for p in parts), 1)
+    dev = outs[0].status.device if outs else torch.device("cuda")
+    rows = torch.full((maxn, width), -1, dtype=torch.int64, device=dev)
+    if mine:
+        N.solve_pms_mhs(db, outs[0], outs[1])
+        N.mhs_greedy(db, outs[2])
+        n = len(mine)
+        rows[:n, 0] = torch.tensor(mine, dtype=torch.int64, device=dev)
+        rows[:n, 1] = outs[0].status.to(torch.int64)
+        rows[:n, 2] = outs[0].cost
+        rows[:n, 3] = outs[0].decided
+        rows[:n, 4] = outs[1].decided
+        rows[:n, 5:] = outs[0].assign
+    got = torch.cat(allgather(rows)).cpu().numpy()
+    got = got[got[:, 0] >= 0]
+    idx = got[:, 0]
+    out = {"status": np.zeros(cb.B, np.int32), "cost": np.zeros(cb.B, np.uint64),
+           "decided_pms": np.zeros(cb.B, np.uint64), "decided_mhs": np.zeros(cb.B, np.uint64),
+           "assign": np.zeros((cb.B, W), np.uint64)}
+    out["status"][idx] = got[:, 1].astype(np.int32)
+    out["cost"][idx] = got[:, 2].view(np.uint64)
+    out["decided_pms"][idx] = got[:, 3].view(np.uint64)
+    out["decided_mhs"][idx] = got[:, 4].view(np.uint64)
+    out["assign"][idx] = got[:, 5:].view(np.uint64)
     return out
 
 

@@ -115,6 +115,101 @@ def test_level_sharding_gloo_world2(seed):
     assert [a + b for a, b in zip(got[0][3], got[1][3])] == ref.enumerated
 
 
+class FakePairSession:
+    """Stand-in of the fused pair session (gr_pair_*): one level loop decides
+    two solves per instance -- PMS (feasible ranks feas) and MHS (feasible
+    ranks feas_m, a superset: the MHS ignores phi-) -- an instance stays
+    listed while either searches, and level_keys() returns both key arrays."""
+
+    def __init__(self, inst, chunk=3):
+        self.inst, self.chunk = inst, chunk
+        self.B = len(inst)
+        self.keys = (torch.full((self.B,), NONE, dtype=torch.int64),
+                     torch.full((self.B,), NONE, dtype=torch.int64))
+        self.open = [[True] * self.B, [True] * self.B]
+        self.result = [[None] * self.B, [None] * self.B]
+        self.active = list(range(self.B))
+
+    def prepare(self):
+        return len(self.active)
+
+    def level(self, k, shard, nshard):
+        for b in self.active:
+            size = self.inst[b]["size"][k]
+            nch = (size + self.chunk - 1) // self.chunk
+            for s, key in enumerate(("feas", "feas_m")):
+                if not self.open[s][b]:
+                    continue
+                feas = self.inst[b][key].get(k, [])
+                for c in range(shard, nch, nshard):
+                    lo, hi = c * self.chunk, min((c + 1) * self.chunk, size)
+                    hit = [r for r in feas if lo <= r < hi]
+                    if hit:
+                        self.keys[s][b] = min(int(self.keys[s][b]), hit[0])
+
+    def level_keys(self):
+        return self.keys
+
+    def finish(self, k):
+        nxt = []
+        for b in self.active:
+            for s in (0, 1):
+                if not self.open[s][b]:
+                    continue
+                if int(self.keys[s][b]) != NONE:
+                    self.result[s][b], self.open[s][b] = (k, int(self.keys[s][b])), False
+                elif k >= self.inst[b]["kmax"]:
+                    self.result[s][b], self.open[s][b] = ("UNSAT",), False
+            if self.open[0][b] or self.open[1][b]:
+                nxt.append(b)
+        self.active = nxt
+        for t in self.keys:
+            t.fill_(NONE)
+        return len(nxt)
+
+
+def make_pair_instances(seed):
+    rng = np.random.default_rng(seed)
+    out = make_instances(seed)
+    for x in out:
+        fm = {}
+        for k, size in x["size"].items():
+            if rng.random() < 0.4 or k in x["feas"]:
+                extra = rng.choice(size, size=min(2, size), replace=False).tolist()
+                fm[k] = sorted(set(extra) | set(x["feas"].get(k, [])))
+        x["feas_m"] = fm
+    return out
+
+
+def _pair_worker(rank, world, port, seed, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    s = FakePairSession(make_pair_instances(seed))
+    levels = run_levels_sharded(s, rank, world, lambda t: dist.all_reduce(t, op=dist.ReduceOp.MIN))
+    q.put((rank, levels, s.result))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("seed", [3, 4])
+def test_pair_level_sharding_gloo_world2(seed):
+    """The fused pair session through the sharded driver (both key arrays
+    all-reduced per level) at world 2 = world 1, for both solves."""
+    ref = FakePairSession(make_pair_instances(seed))
+    ref_levels = run_levels_sharded(ref, 0, 1, lambda t: None)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_pair_worker, args=(r, 2, port, seed, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, levels, result in got:
+        assert levels == ref_levels and result == ref.result
+
+
 def test_shard_instances_balanced_and_complete():
     rng = np.random.default_rng(0)
     m = rng.integers(0, 33, size=748)

@@ -875,3 +875,74 @@ print("ok")
         res[mode] = np.load(path)
     for k in res["queue"].files:
         assert np.array_equal(res["queue"][k], res["host"][k]), k
+
+
+@pytest.mark.parametrize("case", ["c2", "c3", "c3x"])
+def test_pair_session_shard_emulation(case):
+    """The fused PMS + MHS pair session (gr_pair_*) with every level's rank
+    range split into G = 3 shards run one after the other on this GPU (host
+    MIN of both key arrays, as the NCCL all-reduce does) equals
+    gr_solve_pms_mhs: statuses, assignments, costs, decided counts."""
+    if case == "c2":
+        cb, flags = synth.c2_batch(), 0
+    else:
+        cb, flags = synth.c3_instance()[0], (gr.GR_FLAG_EXHAUSTIVE if case == "c3x" else 0)
+    db = gr.DeviceBatch.from_host(cb, weighted=False, flags=flags)
+    p, h = gr.solve_pms_mhs(db)
+    ref = gr.to_host_many([p, h])
+    s = gr.PairSession(db)
+    n, k = s.prepare(), 0
+    while n:
+        k += 1
+        got = [[], []]
+        for shard in range(3):
+            kp, km = s.level_keys()
+            saved = (kp.clone(), km.clone())
+            s.level(k, shard, 3)
+            for i, t in enumerate(s.level_keys()):
+                got[i].append(t.clone())
+                t.copy_(saved[i])
+        for i, t in enumerate(s.level_keys()):
+            t.copy_(torch.stack(got[i]).min(0).values)
+        n = s.finish(k)
+    out = gr.to_host_many([s.out_pms, s.out_mhs])
+    for i in (0, 1):
+        for f in ("status", "assign", "cost", "decided"):
+            assert np.array_equal(out[i][f], ref[i][f]), (case, i, f)
+
+
+def test_long_windows_at_32_support_variables():
+    """Regression (round 2): with m_eff = 32 exactly the iterator's 5-bit
+    ancestor stack could not hold e_top = 32; a long lane window that popped
+    back to depth 1 lost the rest of the level.  Instances with exactly 32
+    support variables, unit and weighted, under long fixed lane windows
+    (2^11 .. 2^20 candidates), against the oracle -- including C4 instance
+    2649 where the optimum was missed."""
+    code = """
+import random, numpy as np, oracle, paper_2011_08373_b200 as gr
+from paper_2011_08373_b200 import synth
+rng = random.Random(32)
+insts, ws = [], []
+for _ in range(60):
+    m = rng.randint(32, 40)
+    sup = sorted(rng.sample(range(1, m + 1), 32))
+    pos = {tuple(sorted(rng.sample(sup, rng.randint(2, 5)))) for _ in range(rng.randint(6, 12))}
+    pos |= {tuple(sup[i:i + 3]) for i in range(0, 30, 10)}
+    neg = {tuple(sorted(rng.sample(sup, rng.randint(1, 3)))) for _ in range(rng.randint(0, 6))}
+    insts.append((m, [list(c) for c in pos], [list(c) for c in neg]))
+    ws.append([rng.randint(50, 100) for _ in range(40)])
+c4 = synth.c4_batch().subset([2649])
+for cb in (synth.batch_from_lists(insts, weights=ws, W=1), c4):
+    for weighted in (True, False):
+        db = gr.DeviceBatch.from_host(cb, weighted=weighted)
+        p, h = gr.solve_pms_mhs(db)
+        a, b = gr.to_host_many([p, h])
+        op = oracle.batch("pms", cb, weighted=weighted)
+        oh = oracle.batch("mhs", cb)
+        for g, o in ((a, op), (b, oh)):
+            assert (g["status"] == o.status).all() and (g["assign"] == o.assign).all()
+            assert (g["cost"] == o.cost).all()
+print("ok")
+"""
+    for L in ("2048", "65536", "1048576"):
+        assert "ok" in _subprocess_solve({"GR_LANE_CANDIDATES": L}, code)
