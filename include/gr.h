@@ -167,7 +167,15 @@ int gr_mhs_greedy(const gr_batch *in, gr_result *out, void *ws, size_t ws_bytes,
  * fell_back (device [B] int32, may be NULL): 1 where the fallback ran.
  * decided is 0 for instances answered by the greedy.  Workspace:
  * gr_workspace_bytes(in, 0). */
-enum { GR_STRATEGY_MHS = 0, GR_STRATEGY_MAXSAT = 1 };
+/* strategy GR_STRATEGY_MHS_FINAL: the mhs strategy's final query -- "a single
+ *   query to a MaxSAT solver is needed to ensure that the number of b_i's
+ *   being set to true is the minimum": the greedy mhs answer is
+ *   computed, then every instance gets the (weighted) partial-MaxSAT optimum
+ *   (= gr_solve_pms, decided counts included); fell_back[b] = 1 where that
+ *   query changed the answer (the greedy set broke phi-, or the optimum is
+ *   cheaper than the greedy set), 0 where the greedy answer was already
+ *   minimum. */
+enum { GR_STRATEGY_MHS = 0, GR_STRATEGY_MAXSAT = 1, GR_STRATEGY_MHS_FINAL = 2 };
 int gr_solve(const gr_batch *in, int strategy, gr_result *out, int32_t *fell_back, void *ws,
              size_t ws_bytes, gr_stream_t s);
 
@@ -266,6 +274,37 @@ int gr_mhs_greedy_matrix(const gr_bitmatrix *in, uint64_t *assign, int32_t *stat
  * number of clauses c of this shard with U[c] = 1 and v in c. */
 int gr_greedy_count_shard(const gr_bitmatrix *shard, const uint64_t *d_U, uint32_t *d_counts,
                           gr_stream_t s);
+
+/* ---- greedy at scale from clause lists alone --------
+ * The same greedy as gr_mhs_greedy_matrix (identical picks, pruned set and
+ * phi- verdict) for one phi+ given only as clause -> variable lists, without
+ * the variable-major bit matrix: the variable -> clause lists are built on
+ * the device by a counting sort (~4 bytes per literal of workspace), every
+ * pick walks its own list, covers the clauses still uncovered and decrements
+ * the counts of their variables (exact counts, so the textbook argmax), all
+ * picks in one cooperative launch; the reverse-delete keeps exact hit counts
+ * per clause.  Ids outside [0, m): status GR_BADINPUT; an empty positive
+ * clause: GR_UNSAT (R6).  Errors: GR_ETOOBIG for m > 51200 (shared-memory
+ * histograms) or nnz / n_pos >= 2^32. */
+typedef struct {
+  int32_t m;              /* host: number of variables, >= 1 */
+  int64_t n_pos;          /* host: number of positive clauses */
+  int64_t nnz;            /* host: pos_off[n_pos], the number of literals */
+  const int64_t *pos_off; /* [n_pos+1] device */
+  const void *pos_var;    /* [nnz] device int16 / int32 variable ids (0-based); a clause
+                             must not list a variable twice */
+  int32_t var_bytes;      /* 2 or 4 */
+  int32_t n_neg;          /* host: number of negative clauses */
+  const uint64_t *neg;    /* [n_neg][ceil(m/64)] device masks (gr_pack_clausemajor), or NULL */
+  const uint32_t *w;      /* [m] weights >= 1 or NULL (the weighted mhs, R20) */
+} gr_clauselists;
+size_t gr_greedy_lists_workspace_bytes(const gr_clauselists *in);
+/* assign [ceil(m/64)] words and status (device); picks (device [m] or NULL):
+ * pick order before pruning, padded with -1; n_picks (host, may be NULL).
+ * Synchronises s. */
+int gr_mhs_greedy_lists(const gr_clauselists *in, uint64_t *assign, int32_t *status,
+                        int32_t *picks, int32_t *n_picks, void *ws, size_t ws_bytes,
+                        gr_stream_t s);
 
 /* ---- column-sharded greedy (PAPER.md:24 greedy mhs) ---
  * Each rank owns a contiguous range of phi+'s clause columns as its own

@@ -7,6 +7,7 @@ Public API (thin marshalling over libgrsolve.so, include/gr.h):
     ExactSession, PairSession           prepare / level / finish for sharded runs (PairSession:
                                         the fused PMS + MHS walk)
     pack_bitmatrix, mhs_greedy_matrix   greedy at scale over a bit matrix
+    mhs_greedy_lists                    the same greedy from clause lists alone (no bit matrix)
     greedy_count_shard                  shard hook for the multi-GPU greedy
 Seeded synthetic workloads: paper_2011_08373_b200.synth.
 """
@@ -15,6 +16,6 @@ from ._native import (  # noqa: F401
     PMS, GREEDY, DeviceBatch, DeviceBitMatrix, DeviceResult, ExactSession, GrError,
     bitmatrix_ld, greedy_count_shard, lib, mhs_exact, mhs_greedy, mhs_greedy_matrix,
     pack_bitmatrix, solve_pms, version, launch_count, profiler, Profiler, solve,
-    GR_STRATEGY_MHS, GR_STRATEGY_MAXSAT, solve_pms_mhs, GreedyShard, to_host_many, GreedyMatrixResult,
-    PairSession,
+    GR_STRATEGY_MHS, GR_STRATEGY_MAXSAT, GR_STRATEGY_MHS_FINAL, solve_pms_mhs, GreedyShard, to_host_many, GreedyMatrixResult,
+    PairSession, mhs_greedy_lists,
 )

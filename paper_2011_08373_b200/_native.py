@@ -33,9 +33,9 @@ EXPORTED = [
     "gr_greedy_shard_workspace_bytes", "gr_greedy_shard_begin", "gr_greedy_shard_step",
     "gr_greedy_shard_state", "gr_greedy_shard_private", "gr_greedy_shard_remove",
     "gr_greedy_shard_finalize", "gr_pair_prepare", "gr_pair_level", "gr_pair_level_keys",
-    "gr_pair_finish",
+    "gr_pair_finish", "gr_greedy_lists_workspace_bytes", "gr_mhs_greedy_lists",
 ]
-GR_STRATEGY_MHS, GR_STRATEGY_MAXSAT = 0, 1
+GR_STRATEGY_MHS, GR_STRATEGY_MAXSAT, GR_STRATEGY_MHS_FINAL = 0, 1, 2
 
 
 class GrBatch(C.Structure):
@@ -113,13 +113,19 @@ def lib():
         for f in (L.gr_greedy_shard_begin, L.gr_greedy_shard_step, L.gr_greedy_shard_state,
                   L.gr_greedy_shard_private, L.gr_greedy_shard_remove, L.gr_greedy_shard_finalize):
             f.restype = C.c_int
-        L.gr_pair_prepare.argtypes = [vp, vp, vp, vp, sz, vp, vp]
-        L.gr_pair_level.argtypes = [vp, C.c_int, C.c_int, C.c_int, vp, sz, vp]
-        L.gr_pair_level_keys.argtypes = [vp, vp, C.c_int]
-        L.gr_pair_level_keys.restype = vp
-        L.gr_pair_finish.argtypes = [vp, C.c_int, vp, vp, vp, sz, vp, vp]
-        for f in (L.gr_pair_prepare, L.gr_pair_level, L.gr_pair_finish):
-            f.restype = C.c_int
+        if hasattr(L, "gr_pair_prepare"):
+            L.gr_pair_prepare.argtypes = [vp, vp, vp, vp, sz, vp, vp]
+            L.gr_pair_level.argtypes = [vp, C.c_int, C.c_int, C.c_int, vp, sz, vp]
+            L.gr_pair_level_keys.argtypes = [vp, vp, C.c_int]
+            L.gr_pair_level_keys.restype = vp
+            L.gr_pair_finish.argtypes = [vp, C.c_int, vp, vp, vp, sz, vp, vp]
+            for f in (L.gr_pair_prepare, L.gr_pair_level, L.gr_pair_finish):
+                f.restype = C.c_int
+        if hasattr(L, "gr_mhs_greedy_lists"):  # (older A/B builds via GRSOLVE_LIB lack it)
+            L.gr_greedy_lists_workspace_bytes.argtypes = [vp]
+            L.gr_greedy_lists_workspace_bytes.restype = sz
+            L.gr_mhs_greedy_lists.argtypes = [vp, vp, vp, vp, vp, vp, sz, vp]
+            L.gr_mhs_greedy_lists.restype = C.c_int
         L.gr_last_error.restype = C.c_char_p
         L.gr_version.restype = C.c_char_p
         for f in (L.gr_exact_prepare, L.gr_exact_level, L.gr_exact_finish, L.gr_pack_varmajor,
@@ -551,6 +557,52 @@ def mhs_greedy_matrix(bm: DeviceBitMatrix, stream=None) -> GreedyMatrixResult:
     n = C.c_int32(0)
     _check(L.gr_mhs_greedy_matrix(C.byref(s), _ptr(assign), _ptr(status), _ptr(picks), C.byref(n),
                                   _ptr(ws), ws.numel(), _stream(stream)), "gr_mhs_greedy_matrix")
+    return GreedyMatrixResult(assign, status, picks, int(n.value))
+
+
+class GrClauseLists(C.Structure):
+    _fields_ = [("m", C.c_int32), ("n_pos", C.c_int64), ("nnz", C.c_int64),
+                ("pos_off", C.c_void_p), ("pos_var", C.c_void_p), ("var_bytes", C.c_int32),
+                ("n_neg", C.c_int32), ("neg", C.c_void_p), ("w", C.c_void_p)]
+
+
+def mhs_greedy_lists(m, pos_off, pos_var, neg_off, neg_var, w=None, device="cuda", stream=None,
+                     nnz=None) -> GreedyMatrixResult:
+    """(c) at scale from clause lists alone (gr_mhs_greedy_lists, f3): phi-
+    packed to clause-major masks on the device (gr_pack_clausemajor), then the
+    greedy over the variable -> clause lists built on the device.  CSR arrays
+    may be host (numpy) or device (torch); ``nnz`` = pos_off[-1] (read from
+    the host array when not given); w: device int32 view of uint32 [m]."""
+    torch = _torch()
+    L = lib()
+
+    def dev(a):
+        if isinstance(a, np.ndarray):
+            return torch.from_numpy(np.ascontiguousarray(a)).to(device)
+        return a.to(device)
+
+    if nnz is None:
+        nnz = int(pos_off[-1])
+    po, pv, no, nv = dev(pos_off), dev(pos_var), dev(neg_off), dev(neg_var)
+    n_pos, n_neg = int(po.numel() - 1), int(no.numel() - 1)
+    mw = (m + 63) // 64
+    neg = torch.zeros((max(n_neg, 1), mw), dtype=torch.int64, device=device)
+    st = _stream(stream)
+    if n_neg:
+        _check(L.gr_pack_clausemajor(m, n_neg, _ptr(no), _ptr(nv), nv.element_size(), _ptr(neg),
+                                     None, st), "gr_pack_clausemajor")
+    s = GrClauseLists(m, n_pos, int(nnz), _ptr(po), _ptr(pv), pv.element_size(), n_neg,
+                      _ptr(neg) if n_neg else None, _ptr(w))
+    nbytes = L.gr_greedy_lists_workspace_bytes(C.byref(s))
+    if nbytes == 0:
+        raise GrError("gr_greedy_lists_workspace_bytes rejected the lists: " + lib().gr_last_error().decode())
+    ws = workspace(nbytes, po.device, tag="greedy_lists")
+    assign = torch.zeros(mw, dtype=torch.int64, device=po.device)
+    status = torch.zeros(1, dtype=torch.int32, device=po.device)
+    picks = torch.full((m,), -1, dtype=torch.int32, device=po.device)
+    n = C.c_int32(0)
+    _check(L.gr_mhs_greedy_lists(C.byref(s), _ptr(assign), _ptr(status), _ptr(picks), C.byref(n),
+                                 _ptr(ws), ws.numel(), st), "gr_mhs_greedy_lists")
     return GreedyMatrixResult(assign, status, picks, int(n.value))
 
 

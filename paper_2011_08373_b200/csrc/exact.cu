@@ -68,22 +68,31 @@ struct Ctrl {
 static_assert(sizeof(Ctrl) == 128, "Ctrl layout");
 
 // Level k of instance b of solve sv: one task record, worked by every CTA
-// whose ticket maps to one of its ring entries.
+// whose ticket maps to one of its ring entries.  A task may be
+// speculative: level k+1 published while level k still runs; it commits only
+// after level k confirmed it, and is cancelled if level k ends the instance.
+constexpr unsigned SUCC_CLOSED = 0xffffffffu;
 struct Task {
   u64 claimed;   // warp chunks handed out (atomic)
-  u64 done;      // warp chunks finished (atomic); the warp finishing the last one commits
+  u64 pending;   // warp chunks not finished, + 1 while unconfirmed; the decrement to 0 commits
   u64 nchunks;   // warp chunks of the level: 32 lane windows of L candidates each
   u64 L;         // lane window
-  int b, k, sv, pad;
-  u64 pad2[2];
+  i64 key[2];    // the level's minimum keys (fused: PMS, MHS)
+  int b, k;
+  unsigned succ;  // 0: no successor yet; SUCC_CLOSED: none may attach; else successor index + 1
+  unsigned char sv, rb, depth, cancelled;  // solve; weighted key shift; speculation depth
+                                           // (0 = confirmed); cancelled speculation
+  u64 t_make, t_exhaust, t_commit, t_unused;  // globaltimer (ns): the level timeline
+                                              // (scripts/queue_stats.py)
+  u64 pad[4];
 };
-static_assert(sizeof(Task) == 64, "Task layout");
+static_assert(sizeof(Task) == 128, "Task layout");
 // A ring entry is one u64: generation (12 bits) | ring round of its ticket
 // (12 bits) | extra-entry flag | solve | task record index (38 bits); the
 // waiter of ticket e knows the generation and e's round, so a stale entry of
 // an earlier launch or round never matches.
 typedef u64 RingEntry;
-constexpr int QLEVELS = 66;  // task records per (instance, solve): levels 0..64 + 1
+constexpr int QLEVELS = 132;  // task records per (instance, solve): two per level (speculation)
 // ring entries: a power of two above one entry per open unit of two solves
 // plus the tickets the grid can hold
 __host__ __device__ inline u64 ring_cap(int B) {
@@ -102,7 +111,7 @@ constexpr int HX = 16;         // HIT_j({x}) is 0 for x >= R_j, and R_j <= 16 fo
 
 struct Layout {
   size_t ctrl, meff, npr, nnr, kmax, ks, done, rb, sup, decided, bestx, bestw, wtot, lvlkey, sk, wr,
-      active, chunk_base, pk, hrec, ptmp, tasks, ring, total;
+      active, chunk_base, pk, hrec, ptmp, tasks, ring, gcost, total;
 };
 
 Layout layout_of(const gr_batch *in) {
@@ -132,6 +141,7 @@ Layout layout_of(const gr_batch *in) {
   L.hrec = take(16 * HREC * (size_t)std::max<int64_t>(in->total_clauses, 1));
   L.tasks = take(sizeof(Task) * QLEVELS * B);
   L.ring = take(sizeof(RingEntry) * ring_cap(in->B));
+  L.gcost = take(8 * B);  // gr_solve(GR_STRATEGY_MHS_FINAL): the greedy answers' costs
   L.total = o;
   return L;
 }
@@ -443,6 +453,7 @@ __global__ void __launch_bounds__(PT) pack_kernel(In in, Out out, WS ws, int whi
 // same clause-test code in lock step.  An inner node's whole subtree is
 // first checked for a refutation by one clause scan (refuted_by).
 
+
 __device__ __forceinline__ F2 f2_and(F2 a, F2 b) { return F2{a.lo & b.lo, a.hi & b.hi}; }
 __device__ __forceinline__ F2 f2_andnot(F2 a, F2 b) { return F2{a.lo & ~b.lo, a.hi & ~b.hi}; }
 __device__ __forceinline__ bool f2_any(F2 a) { return (a.lo | a.hi) != 0; }
@@ -510,15 +521,21 @@ struct Work {
 };
 enum { W_POS, W_NEG, W_SCAN, W_BLOCKS, W_CANDS, W_WINDOWS, W_WIDE, W_N = 8 };
 
+extern __shared__ u64 g_dsmem[];  // dynamic shared memory of the enumeration kernels
+__device__ __forceinline__ const F2 *tab_hitx() { return (const F2 *)g_dsmem; }
+__device__ __forceinline__ const u64 *tab_cs() { return g_dsmem + 2 * (JMAX + 1) * HX; }
+__device__ __forceinline__ const F2 *tab_lowb() { return (const F2 *)(tab_cs() + 65 * (JMAX + 1)); }
+__device__ __forceinline__ const int *tab_reg() { return (const int *)(tab_lowb() + 129); }
+__device__ __forceinline__ const unsigned char *tab_nb() { return (const unsigned char *)(tab_reg() + 16); }
+
 template <typename M>
 struct Clauses {
   const M *P;       // [np + nn] positives then negatives (uniform reads)
   const F2 *H;      // [np][HREC] H_j(P) at H[q * HREC + j - 1]
-  const F2 *hitx;   // [JMAX + 1][HX] HIT_j({x}) for j >= 2 (0 when x >= R_j), shared memory
-  const F2 *lowb;   // [129] the n lowest bits, shared memory
-  const int *reg;   // [JMAX + 1] R_j, shared memory
-  const unsigned char *nb;  // [JMAX + 1][65] C(min(e, R_j), j), the sub-block sizes
-  const u64 *cs;    // [65][JMAX + 1] C(n, j) for j <= JMAX, shared memory
+  // the tables at the start of dynamic shared memory (tab_*: fixed offsets
+  // from one symbol, so the walk holds no pointer registers for them):
+  //   HIT_j({x}) [JMAX + 1][HX], C(n, j) [65][JMAX + 1] for j <= JMAX, the n
+  //   lowest bits [129], R_j [JMAX + 1], sub-block sizes C(min(e, R_j), j)
   int np, nn;
 };
 
@@ -560,7 +577,7 @@ template <typename M, bool COUNT>
 __device__ __forceinline__ F2 test_neg(int j, M U, int e, F2 F, const Clauses<M> &c, Work &wk) {
   const int np = c.np;
   const M lowm = (M)nbits((u64)e);
-  const F2 *hx = c.hitx + HX * j;
+  const F2 *hx = tab_hitx() + HX * j;
   for (int t = 0; t < c.nn; t++) {
     M rest = c.P[np + t] & ~U;
     if (COUNT) wk.neg += 1;
@@ -653,7 +670,7 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
   constexpr int SB = sizeof(M) == 4 ? 5 : 6;
   constexpr int JM = sizeof(M) == 4 ? JMAX : (JMAX < 12 ? JMAX : 12);
   const int J = k < JM ? k : JM;
-  const u64 *cs = c.cs;  // C(n, j), j <= JMAX
+  const u64 *cs = tab_cs();  // C(n, j), j <= JMAX
 #define CS(n, j) (cs[(n) * (JMAX + 1) + (j)])
   i64 best = GR_KEY_NONE;
   if (COUNT) wk.windows++;
@@ -725,7 +742,7 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
   bool dead0 = false;
   while (j >= 2) {
     const int t = (int)(8 * sizeof(M) - 1) - (sizeof(M) == 4 ? __clz((int)Slow) : __clzll((long long)Slow));
-    if (t < c.reg[j]) break;
+    if (t < tab_reg()[j]) break;
     if (prune) {
       const int kind = refuted_by<M, COUNT>(j, U, e, c, wk);
       if (kind == 1 || (kind == 2 && !wm)) {
@@ -743,14 +760,14 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
     d++;
     j--;
   }
-  int R = c.reg[j];
+  int R = tab_reg()[j];
   // positions relative to r_lo fit 32 bits (windows hold <= 2^14 candidates)
   int pos = (int)((i64)base - (i64)r_lo);
   const int cnt32 = (int)cnt;
   // ---- iterate over sub-blocks in rank order
   for (;;) {
     if (pos >= cnt32) return best;
-    const int n = c.nb[j * 65 + e];  // C(min(e, R_j), j)
+    const int n = tab_nb()[j * 65 + e];  // C(min(e, R_j), j)
     // An inner node (one with children) first asks whether its whole subtree
     // -- every x = U | S, S a j-subset of [0, e) -- is infeasible: a positive
     // clause missing U and [0, e), more than j pairwise disjoint positive
@@ -782,9 +799,9 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
       dead = kind == 1 || (kind == 2 && !wm);  // the MHS ignores phi-
     }
     if (!dead && n && pos + n > 0) {
-      F2 F = c.lowb[n];
-      if (pos < 0) F = f2_andnot(F, c.lowb[-pos]);
-      if (cnt32 - pos < n) F = f2_and(F, c.lowb[cnt32 - pos]);
+      F2 F = tab_lowb()[n];
+      if (pos < 0) F = f2_andnot(F, tab_lowb()[-pos]);
+      if (cnt32 - pos < n) F = f2_and(F, tab_lowb()[cnt32 - pos]);
       if (COUNT) { wk.blocks++; wk.cands += (u64)f2_popc(F); }
       const int ea = e < R ? e : R;
       if (MODE == 3) {
@@ -836,7 +853,7 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
       if (MODE == 2) wU += w[R];
       d++;
       j--;
-      R = c.reg[j];
+      R = tab_reg()[j];
       continue;
     }
     if (d > 0 && e + 1 >= ep) {  // no next sibling here: pop until there is one
@@ -851,7 +868,7 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
           tp >>= SB;
         }
       } while (d > 0 && e + 1 >= ep);
-      R = c.reg[j];
+      R = tab_reg()[j];
     }
     if (d > 0) {  // next sibling: t -> t + 1
       U ^= (M)3 << e;
@@ -1043,26 +1060,26 @@ __global__ void __launch_bounds__(NTK, COUNT ? 1 : ENUM_CTAS * NT / NTK) enum_ke
       if (p.fused) {
         const int nq = s_needp, nm = s_needm;
         if (narrow) {
-          Clauses<u32> c{(const u32 *)sP, sH, hitx, lowb, reg, nb, cs, np, nn};
+          Clauses<u32> c{(const u32 *)sP, sH, np, nn};
           key1 = walk<u32, 3, COUNT>(p.k, me, r_lo, cnt, c, s_w, rb, p.prune, wk, nullptr, ~0ull,
                                     nq, nm, &key_m1, p.exhaustive);
         } else if (staged) {
-          Clauses<u64> c{sP, sH, hitx, lowb, reg, nb, cs, np, nn};
+          Clauses<u64> c{sP, sH, np, nn};
           key1 = walk<u64, 3, COUNT>(p.k, me, r_lo, cnt, c, s_w, rb, p.prune, wk, nullptr, ~0ull,
                                     nq, nm, &key_m1, p.exhaustive);
         } else {
-          Clauses<u64> c{p.ws.pk + lo, (const F2 *)p.ws.hrec + lo * HREC, hitx, lowb, reg, nb, cs, np, nn};
+          Clauses<u64> c{p.ws.pk + lo, (const F2 *)p.ws.hrec + lo * HREC, np, nn};
           key1 = walk<u64, 3, COUNT>(p.k, me, r_lo, cnt, c, s_w, rb, p.prune, wk, nullptr, ~0ull,
                                     nq, nm, &key_m1, p.exhaustive);
         }
       } else if (narrow) {
-        Clauses<u32> c{(const u32 *)sP, sH, hitx, lowb, reg, nb, cs, np, nn};
+        Clauses<u32> c{(const u32 *)sP, sH, np, nn};
         key1 = run_lane<u32, COUNT>(p, r_lo, cnt, me, c, s_w, rb, wk, s_skj, s_wstar);
       } else if (staged) {
-        Clauses<u64> c{sP, sH, hitx, lowb, reg, nb, cs, np, nn};
+        Clauses<u64> c{sP, sH, np, nn};
         key1 = run_lane<u64, COUNT>(p, r_lo, cnt, me, c, s_w, rb, wk, s_skj, s_wstar);
       } else {
-        Clauses<u64> c{p.ws.pk + lo, (const F2 *)p.ws.hrec + lo * HREC, hitx, lowb, reg, nb, cs, np, nn};
+        Clauses<u64> c{p.ws.pk + lo, (const F2 *)p.ws.hrec + lo * HREC, np, nn};
         key1 = run_lane<u64, COUNT>(p, r_lo, cnt, me, c, s_w, rb, wk, s_skj, s_wstar);
       }
     }
@@ -1358,6 +1375,8 @@ struct QParams {
   int nsolve;      // 1, or 2 independent solves sharing the launch
   int fused;       // 1: one walk decides PMS (ws[0]) and MHS (ws[1]) of each instance (MODE 3)
   int exhaustive, prune;
+  int spec;        // levels a speculative chain may run ahead of the last committed one
+  u64 spec_max;    // largest level (candidates) published speculatively
   u64 gen;         // launch generation, 1..4095 (ring entries)
   u64 ring_mask;   // ring entries - 1
   int ring_log2;   // log2(ring entries)
@@ -1379,38 +1398,39 @@ __device__ __forceinline__ u64 atom_add_acq_rel(u64 *p, u64 v) {
   asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
   return old;
 }
+__device__ __forceinline__ u64 gtime() {
+  u64 t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ u64 vld(const u64 *p) { return *(const volatile u64 *)p; }
 __device__ __forceinline__ i64 vld(const i64 *p) { return *(const volatile i64 *)p; }
 __device__ __forceinline__ int vld(const int *p) { return *(const volatile int *)p; }
+__device__ __forceinline__ unsigned vldu(const unsigned *p) { return *(const volatile unsigned *)p; }
+__device__ __forceinline__ void work_sub(u64 *qw, u64 v) {
+  atomicAdd((unsigned long long *)qw, (unsigned long long)(-(long long)v));
+}
 
 // the ring entry a waiter of ticket e expects, minus its payload
 __device__ __forceinline__ u64 ring_stamp(const QParams &P, u64 e) {
   return (P.gen << 52) | (((e >> P.ring_log2) & 0xfffull) << 40);
 }
 
-// Prepare level k of (b, sv) and write its task record (lane 0 of a warp, or
-// one seed thread).  work = candidates in flight including this level (lane
-// window sizing).  Returns the number of ring entries to publish (0 if the
-// instance cannot go on: its weighted key would not fit 63 bits -- status
-// GR_UNSUPPORTED, written here), the task word in *word and the first entry
-// index in *e0.
-__device__ u64 q_prepare(const QParams &P, int sv, int b, int k, u64 work, u64 *word, u64 *e0) {
+// Fill the task record of level k of (b, sv) -- not published.  work =
+// candidates in flight including this level (lane window sizing); depth > 0:
+// an unconfirmed speculation.  false: the weighted key (W << rb | rank) of
+// this level would not fit 63 bits (the caller reports GR_UNSUPPORTED).
+__device__ bool q_make(const QParams &P, int sv, int b, int k, u64 work, int depth, u64 *ti_out) {
   const WS &w = P.ws[sv];
   const int me = w.meff[b];
   const u64 ck = binom(me, k);
+  int rb = 0;
   if (P.weighted[sv]) {
-    const int rb = bitlen(ck - 1);
-    if (bitlen(vld(&w.wtot[b])) + rb > 63) {  // key (W << rb | rank) would not fit
-      w.done[b] = 1;
-      write_result(P.in[sv], P.out[sv], b, GR_UNSUPPORTED, 0, 0, 0, 0, vld(&w.decided[b]), P.which[sv]);
-      return 0;
-    }
-    w.rb[b] = rb;
+    rb = bitlen(ck - 1);
+    if (bitlen(vld(&w.wtot[b])) + rb > 63) return false;
   }
-  w.lvlkey[b] = GR_KEY_NONE;
-  if (P.fused && !vld(&P.ws[1].done[b])) P.ws[1].lvlkey[b] = GR_KEY_NONE;
   // lane window: about wpl windows per lane of the grid over all the work in
-  // flight, a power of two in [256, lane_max]
+  // flight, a power of two in [lane_min, lane_max]
   const bool wt = P.weighted[sv] != 0;
   const u64 wpl = wt ? (u64)(P.wpl >> 16) : (u64)(P.wpl & 0xffff);
   const u64 Lmax = wt ? P.lane_max_w : P.lane_max;
@@ -1419,18 +1439,32 @@ __device__ u64 q_prepare(const QParams &P, int sv, int b, int k, u64 work, u64 *
   L = 1ull << (63 - __clzll((long long)L));
   if (P.fixed_lane) L = P.fixed_lane;
   const u64 nch = (ck + 32 * L - 1) / (32 * L);
-  // task records of solve sv live in its own workspace (<= 65 per instance)
+  // task records of solve sv live in its own workspace (<= 2 per level)
   const u64 ti = atomicAdd((unsigned long long *)&w.ctrl->q_tasks, 1ull);
   Task *T = w.tasks + ti;
   T->claimed = 0;
-  T->done = 0;
+  T->pending = nch + (depth ? 1 : 0);
   T->nchunks = nch;
   T->L = L;
+  T->key[0] = GR_KEY_NONE;
+  T->key[1] = GR_KEY_NONE;
   T->b = b;
   T->k = k;
-  T->sv = sv;
-  // ring entries: one, plus one per further (warps per CTA) chunks up to the
-  // grid, as far as the extra-entry budget allows
+  T->succ = 0;
+  T->sv = (unsigned char)sv;
+  T->rb = (unsigned char)rb;
+  T->depth = (unsigned char)depth;
+  T->cancelled = 0;
+  T->t_make = gtime();
+  T->t_exhaust = T->t_commit = T->t_unused = 0;
+  *ti_out = ti;
+  return true;
+}
+
+// Ring entries of a task with nch warp chunks (single thread): one, plus one
+// per further (warps per CTA) chunks up to the grid, as far as the
+// extra-entry budget allows.  Returns the count; *e0 = the first entry.
+__device__ u64 q_entries(const QParams &P, u64 nch, u64 *e0) {
   Ctrl *c = P.ws[0].ctrl;
   const u64 nw = (u64)P.nwarps;
   u64 extra = (nch + nw - 1) / nw;
@@ -1444,26 +1478,24 @@ __device__ u64 q_prepare(const QParams &P, int sv, int b, int k, u64 work, u64 *
     }
   }
   *e0 = atomicAdd((unsigned long long *)&c->q_entries, extra + 1);
-  *word = ti | ((u64)sv << 38);
-  __threadfence();  // the task record before any of its entries
   return extra + 1;
 }
-// entry i of a task: written by any thread after q_prepare's fence
+// entry i of a task: written by any thread after the task record's fence
 __device__ __forceinline__ void q_publish(const QParams &P, u64 word, u64 e0, u64 i) {
   const u64 e = e0 + i;
   *(volatile u64 *)&P.ws[0].ring[e & P.ring_mask] = ring_stamp(P, e) | (i ? (1ull << 39) : 0ull) | word;
 }
 
-// Commit level k of solve s for instance b (finish_commit for one instance).
-// Returns whether solve s still searches.  Single thread.
-__device__ bool q_commit_one(const QParams &P, int s, int b, int k) {
+// Commit level k of solve s for instance b with the level's key (decode,
+// weighted incumbent, S_k stop rule, k_max).  Returns whether solve s still
+// searches.  Single thread.
+__device__ bool q_commit_one(const QParams &P, int s, int b, int k, i64 key, int rb) {
   const WS &w = P.ws[s];
   if (vld(&w.done[b])) return false;
   const In &in = P.in[s];
   const Out &out = P.out[s];
   const int me = w.meff[b];
   const u64 ck = binom(me, k);
-  const i64 key = vld(&w.lvlkey[b]);
   const u64 s0 = w.sup[2 * b], s1 = w.sup[2 * b + 1];
   const u64 dec = vld(&w.decided[b]);
   if (!P.weighted[s]) {
@@ -1486,7 +1518,6 @@ __device__ bool q_commit_one(const QParams &P, int s, int b, int k) {
   w.decided[b] = d;
   u64 bw = vld(&w.bestw[b]);
   if (key != GR_KEY_NONE) {
-    const int rb = w.rb[b];
     const u64 Wk = (u64)key >> rb;
     const u64 rank = (u64)key & ((rb ? (1ull << rb) : 1ull) - 1ull);
     if (Wk < bw) {  // strictly smaller W replaces the incumbent (R3)
@@ -1505,40 +1536,75 @@ __device__ bool q_commit_one(const QParams &P, int s, int b, int k) {
   return true;
 }
 
-// The warp that finished the last chunk of (sv, b, k), all 32 lanes: lane 0
-// commits and prepares level k+1 (or retires the instance), then the lanes
-// publish its ring entries together.
-__device__ void q_commit_warp(const QParams &P, int sv, int b, int k) {
-  const int lane = threadIdx.x & 31;
-  u64 n = 0, word = 0, e0 = 0;
-  if (lane == 0) {
-    Ctrl *c = P.ws[0].ctrl;
-    u64 *qw = &P.ws[sv].ctrl->q_work;  // work in flight of this solve
-    const u64 ck = binom(P.ws[sv].meff[b], k);
-    atomicAdd((unsigned long long *)qw, (unsigned long long)(-(long long)ck));
+// the instance cannot go on to the next level: its weighted key would not fit
+__device__ void q_unsupported(const QParams &P, int sv, int b) {
+  const WS &w = P.ws[sv];
+  w.done[b] = 1;
+  write_result(P.in[sv], P.out[sv], b, GR_UNSUPPORTED, 0, 0, 0, 0, vld(&w.decided[b]), P.which[sv]);
+}
+
+// cancel a speculative chain (its levels are not needed: the instance ended)
+__device__ void q_cancel(const QParams &P, int sv, Task *S) {
+  for (;;) {
+    *(volatile unsigned char *)&S->cancelled = 1;
+    work_sub(&P.ws[sv].ctrl->q_work, binom(P.ws[sv].meff[S->b], S->k));
+    const unsigned s2 = atomicCAS(&S->succ, 0u, SUCC_CLOSED);
+    if (s2 == 0u || s2 == SUCC_CLOSED) return;
+    S = P.ws[sv].tasks + (s2 - 1);
+  }
+}
+
+// All chunks of task ti are done (and it is confirmed): commit it; then either
+// confirm its speculative successor (and commit that one too if its chunks
+// are done as well), publish level k+1, or retire the instance.  Lane 0 of
+// the committing warp.  Returns the ring entries the warp must publish
+// (*word, *e0) -- 0 if none.
+__device__ u64 q_commit_chain(const QParams &P, int sv, u64 ti, u64 *word, u64 *e0) {
+  Ctrl *c = P.ws[0].ctrl;
+  u64 *qw = &P.ws[sv].ctrl->q_work;
+  for (;;) {
+    Task *T = P.ws[sv].tasks + ti;
+    const int b = T->b, k = T->k;
+    const int me = P.ws[sv].meff[b];
+    T->t_commit = gtime();
+    work_sub(qw, binom(me, k));
     bool open;
     if (P.fused) {
-      const bool o0 = q_commit_one(P, 0, b, k);
-      const bool o1 = q_commit_one(P, 1, b, k);
+      const bool o0 = q_commit_one(P, 0, b, k, vld(&T->key[0]), 0);
+      const bool o1 = q_commit_one(P, 1, b, k, vld(&T->key[1]), 0);
       open = o0 || o1;
     } else {
-      open = q_commit_one(P, sv, b, k);
+      open = q_commit_one(P, sv, b, k, vld(&T->key[0]), T->rb);
     }
-    if (open && k < 64) {
-      const u64 ck1 = binom(P.ws[sv].meff[b], k + 1);
-      const u64 wk = atomicAdd((unsigned long long *)qw, (unsigned long long)ck1) + ck1;
-      n = q_prepare(P, sv, b, k + 1, wk, &word, &e0);
-      if (!n) atomicAdd((unsigned long long *)qw, (unsigned long long)(-(long long)ck1));
-    }
-    if (!n) {
+    const unsigned s = atomicCAS(&T->succ, 0u, SUCC_CLOSED);
+    if (s == 0u) {  // no speculative successor: publish level k+1, or retire
+      if (open && k < 64) {
+        const u64 ck1 = binom(me, k + 1);
+        const u64 wk = atomicAdd((unsigned long long *)qw, (unsigned long long)ck1) + ck1;
+        u64 ti2;
+        if (q_make(P, sv, b, k + 1, wk, 0, &ti2)) {
+          __threadfence();  // the task record before its entries
+          *word = ti2 | ((u64)sv << 38);
+          return q_entries(P, P.ws[sv].tasks[ti2].nchunks, e0);
+        }
+        work_sub(qw, ck1);
+        q_unsupported(P, sv, b);
+      }
       __threadfence();  // results before the count that ends the launch
       atomicSub(&c->q_remaining, 1);
+      return 0;
     }
+    Task *S = P.ws[sv].tasks + (s - 1);
+    if (!open) {  // the instance ended: its speculative levels are not needed
+      q_cancel(P, sv, S);
+      __threadfence();
+      atomicSub(&c->q_remaining, 1);
+      return 0;
+    }
+    *(volatile unsigned char *)&S->depth = 0;  // confirmed
+    if (atom_add_acq_rel(&S->pending, ~0ull) != 1ull) return 0;  // its last chunk will commit it
+    ti = s - 1;  // every chunk of the successor is done already: commit it here
   }
-  n = __shfl_sync(0xffffffffu, n, 0);
-  word = __shfl_sync(0xffffffffu, word, 0);
-  e0 = __shfl_sync(0xffffffffu, e0, 0);
-  for (u64 i = lane; i < n; i += 32) q_publish(P, word, e0, i);
 }
 
 // one CTA: initialise the ring budget and the work in flight, then publish
@@ -1563,15 +1629,16 @@ __global__ void __launch_bounds__(1024) queue_seed_kernel(QParams P, long long b
     for (int b = threadIdx.x; b < P.in[sv].B; b += blockDim.x) {
       const WS &w = P.ws[sv];
       if (!open(sv, b)) continue;
-      atomicAdd(&P.ws[0].ctrl->q_remaining, 1);
-      u64 word, e0;
-      const u64 n = q_prepare(P, sv, b, w.ks[b], s_work[sv], &word, &e0);
-      if (!n) {
-        atomicSub(&P.ws[0].ctrl->q_remaining, 1);
-        atomicAdd((unsigned long long *)&w.ctrl->q_work,
-                  (unsigned long long)(-(long long)binom(w.meff[b], w.ks[b])));
+      u64 ti, e0;
+      if (!q_make(P, sv, b, w.ks[b], s_work[sv], 0, &ti)) {
+        work_sub(&w.ctrl->q_work, binom(w.meff[b], w.ks[b]));
+        q_unsupported(P, sv, b);
+        continue;
       }
-      for (u64 i = 0; i < n; i++) q_publish(P, word, e0, i);
+      atomicAdd(&P.ws[0].ctrl->q_remaining, 1);
+      __threadfence();
+      const u64 n = q_entries(P, w.tasks[ti].nchunks, &e0);
+      for (u64 i = 0; i < n; i++) q_publish(P, ti | ((u64)sv << 38), e0, i);
     }
 }
 
@@ -1584,7 +1651,7 @@ __device__ __forceinline__ i64 q_walk(const QParams &P, int sv, int need, int k,
                                       Work &wk, const u64 *skj, u64 wstar, i64 *key_m) {
   if (KIND == 1)
     return walk<M, 3, COUNT>(k, me, r_lo, cnt, cc, sw, rb, P.prune, wk, nullptr, ~0ull, need & 1,
-                             need >> 1, key_m, P.exhaustive);
+                                   need >> 1, key_m, P.exhaustive);
   if (KIND == 2 && P.weighted[sv])
     return walk<M, 2, COUNT>(k, me, r_lo, cnt, cc, sw, rb, P.prune, wk, skj, wstar);
   if (P.exhaustive) return walk<M, 1, COUNT>(k, me, r_lo, cnt, cc, sw, rb, P.prune, wk);
@@ -1592,9 +1659,9 @@ __device__ __forceinline__ i64 q_walk(const QParams &P, int sv, int need, int k,
 }
 
 template <bool COUNT, int NTK, int KIND>
-__global__ void __launch_bounds__(NTK, COUNT ? 1 : ENUM_CTAS * NT / NTK) queue_kernel(QParams P) {
+__global__ void __launch_bounds__(NTK, COUNT ? 1 : ENUM_CTAS * NT / NTK) queue_kernel(const __grid_constant__ QParams P) {
   extern __shared__ u64 cls[];  // tables, then the staged clause records
-  __shared__ int s_b, s_k, s_sv, s_cur, s_exit;
+  __shared__ int s_b, s_k, s_sv, s_cur, s_exit, s_rb;
   __shared__ u64 s_ti, s_L, s_nch, s_ck;
   __shared__ u64 s_skj[JMAX + 1], s_wstar;  // weighted: S_j and the incumbent W*
   __shared__ u32 s_w[64];
@@ -1638,10 +1705,11 @@ __global__ void __launch_bounds__(NTK, COUNT ? 1 : ENUM_CTAS * NT / NTK) queue_k
         const Task *T = P.ws[tsv].tasks + ti;
         s_ti = ti;
         s_sv = tsv;
-        s_b = vld(&T->b);
-        s_k = vld(&T->k);
-        s_L = vld(&T->L);
-        s_nch = vld(&T->nchunks);
+        s_b = T->b;
+        s_k = T->k;
+        s_L = T->L;
+        s_nch = T->nchunks;
+        s_rb = T->rb;
         s_ck = binom(P.ws[tsv].meff[s_b], s_k);
       }
     }
@@ -1669,13 +1737,18 @@ __global__ void __launch_bounds__(NTK, COUNT ? 1 : ENUM_CTAS * NT / NTK) queue_k
         if (t < 64) s_w[t] = w.wr[(size_t)b * 64 + t];
         if (KIND == 2 && t <= JMAX) s_skj[t] = w.sk[(size_t)b * 65 + t];
       }
-      if (KIND == 2 && t == 0) s_wstar = vld(&w.bestw[b]);  // incumbent of earlier levels
+      // incumbent of earlier levels (a speculative level may see an older,
+      // larger one: it only prunes less)
+      if (KIND == 2 && t == 0) s_wstar = vld(&w.bestw[b]);
     }
     __syncthreads();
     if (t == 0) s_cur = s_sv * P.in[0].B + s_b;
     // ---- warps pull warp chunks of this task until it is exhausted.  Lane 0
     // claims one chunk ahead, so the atomic's latency overlaps the walk (not
     // for the weighted walk: the claimed index held across it would spill).
+    // The warp whose claim is the first one past the end may publish the next
+    // level speculatively, so that idle CTAs work on it while this level's
+    // last chunks finish.
     constexpr bool AHEAD = KIND != 2;
     u64 cn = 0;
     if (AHEAD && lane == 0) cn = atomicAdd((unsigned long long *)&P.ws[s_sv].tasks[s_ti].claimed, 1ull);
@@ -1686,22 +1759,64 @@ __global__ void __launch_bounds__(NTK, COUNT ? 1 : ENUM_CTAS * NT / NTK) queue_k
       if (!AHEAD && lane == 0) c = atomicAdd((unsigned long long *)&P.ws[sv].tasks[s_ti].claimed, 1ull);
       int need = 0;  // bit 0: the chunk is needed (fused: for the PMS); bit 1: fused, for the MHS
       if (lane == 0 && c < nch) {
+        const Task *T = P.ws[sv].tasks + s_ti;
         const u64 r0 = c * 32 * s_L;
-        if (KIND == 1) {
-          const i64 c1 = vld(&P.ws[0].lvlkey[b]), c2 = vld(&P.ws[1].lvlkey[b]);
+        if (*(const volatile unsigned char *)&T->cancelled) {
+          c = nch + 1;  // cancelled speculation: stop claiming
+        } else if (KIND == 1) {
+          const i64 c1 = vld(&T->key[0]), c2 = vld(&T->key[1]);
           const int np_ = !vld(&P.ws[0].done[b]) && !(c1 != GR_KEY_NONE && (u64)c1 < r0 && !P.exhaustive);
           const int nm_ = !vld(&P.ws[1].done[b]) && !(c2 != GR_KEY_NONE && (u64)c2 < r0 && !P.exhaustive);
           need = np_ | (nm_ << 1);
         } else if (!P.weighted[sv] && !P.exhaustive) {
-          const i64 cur = vld(&P.ws[sv].lvlkey[b]);
+          const i64 cur = vld(&T->key[0]);
           need = !(cur != GR_KEY_NONE && (u64)cur < r0);  // a lower witness exists
         } else {
           need = 1;
         }
-        if (AHEAD) cn = atomicAdd((unsigned long long *)&P.ws[sv].tasks[s_ti].claimed, 1ull);
+        if (AHEAD && c < nch) cn = atomicAdd((unsigned long long *)&P.ws[sv].tasks[s_ti].claimed, 1ull);
       }
       c = __shfl_sync(0xffffffffu, c, 0);
-      if (c >= nch) break;
+      if (c >= nch) {
+        if (c == nch && lane == 0) P.ws[sv].tasks[s_ti].t_exhaust = gtime();
+        if (c == nch && P.spec) {  // the first claim past the end: maybe publish level k+1 now
+          u64 n = 0, word = 0, e0 = 0;
+          if (lane == 0) {
+            Task *T = P.ws[sv].tasks + s_ti;
+            const WS &w = P.ws[sv];
+            const int k = s_k;
+            // only when CTAs are idle (they hold tickets no entry was published
+            // for yet): a speculative level never displaces queued work
+            const Ctrl *qc = P.ws[0].ctrl;
+            const u64 ck1 = binom(w.meff[b], k + 1);
+            // ... and only for a level small enough that its chunks in flight
+            // cost little if it turns out not to be needed (GR_QSPEC_MAX)
+            // (not for weighted levels: the S_k stop rule ends them often)
+            if (T->depth < P.spec && !P.weighted[sv] && !*(const volatile unsigned char *)&T->cancelled && k < w.kmax[b] &&
+                ck1 <= P.spec_max && vldu(&T->succ) == 0u && vld(&qc->q_tickets) > vld(&qc->q_entries)) {
+              u64 *qw = &w.ctrl->q_work;
+              const u64 wk = atomicAdd((unsigned long long *)qw, (unsigned long long)ck1) + ck1;
+              u64 ti2;
+              bool ok = q_make(P, sv, b, k + 1, wk, T->depth + 1, &ti2);
+              if (ok) {
+                __threadfence();  // the record before it is linked and published
+                ok = atomicCAS(&T->succ, 0u, (unsigned)(ti2 + 1)) == 0u;
+              }
+              if (ok) {
+                word = ti2 | ((u64)sv << 38);
+                n = q_entries(P, w.tasks[ti2].nchunks, &e0);
+              } else {
+                work_sub(qw, ck1);  // level k committed meanwhile (or no room): not needed
+              }
+            }
+          }
+          n = __shfl_sync(0xffffffffu, n, 0);
+          word = __shfl_sync(0xffffffffu, word, 0);
+          e0 = __shfl_sync(0xffffffffu, e0, 0);
+          for (u64 i = lane; i < n; i += 32) q_publish(P, word, e0, i);
+        }
+        break;
+      }
       need = __shfl_sync(0xffffffffu, need, 0);
       i64 key = GR_KEY_NONE, key_m = GR_KEY_NONE;
       Work wk;
@@ -1714,17 +1829,17 @@ __global__ void __launch_bounds__(NTK, COUNT ? 1 : ENUM_CTAS * NT / NTK) queue_k
           const u64 cnt = (ck - r_lo) < L ? (ck - r_lo) : L;
           const int64_t lo = P.in[sv].off[b];
           const bool staged = np + nn <= smc_of<NTK>();
-          const int rb = KIND == 2 ? w.rb[b] : 0;
+          const int rb = KIND == 2 ? s_rb : 0;
           F2 *sH = (F2 *)stage;
           u64 *sP = stage + (size_t)2 * HREC * np;
           if (staged && me <= 32) {
-            Clauses<u32> cc{(const u32 *)sP, sH, hitx, lowb, reg, nb, cs, np, nn};
+            Clauses<u32> cc{(const u32 *)sP, sH, np, nn};
             key = q_walk<u32, KIND, COUNT>(P, sv, need, k, me, r_lo, cnt, cc, s_w, rb, wk, s_skj, s_wstar, &key_m);
           } else if (staged) {
-            Clauses<u64> cc{sP, sH, hitx, lowb, reg, nb, cs, np, nn};
+            Clauses<u64> cc{sP, sH, np, nn};
             key = q_walk<u64, KIND, COUNT>(P, sv, need, k, me, r_lo, cnt, cc, s_w, rb, wk, s_skj, s_wstar, &key_m);
           } else {
-            Clauses<u64> cc{w.pk + lo, (const F2 *)w.hrec + lo * HREC, hitx, lowb, reg, nb, cs, np, nn};
+            Clauses<u64> cc{w.pk + lo, (const F2 *)w.hrec + lo * HREC, np, nn};
             key = q_walk<u64, KIND, COUNT>(P, sv, need, k, me, r_lo, cnt, cc, s_w, rb, wk, s_skj, s_wstar, &key_m);
           }
         }
@@ -1732,17 +1847,21 @@ __global__ void __launch_bounds__(NTK, COUNT ? 1 : ENUM_CTAS * NT / NTK) queue_k
       if (COUNT) work_add(wk, P.ws[s_sv].meff[s_b] > 32);
       key = warp_min(key);
       if (KIND == 1) key_m = warp_min(key_m);
-      int last = 0;
+      u64 n = 0, word = 0, e0 = 0;
       if (lane == 0) {
-        const int b2 = s_b, sv2 = s_sv;
-        if (key != GR_KEY_NONE) atomicMin((long long *)&P.ws[sv2].lvlkey[b2], (long long)key);
-        if (KIND == 1 && key_m != GR_KEY_NONE) atomicMin((long long *)&P.ws[1].lvlkey[b2], (long long)key_m);
+        Task *T = P.ws[s_sv].tasks + s_ti;
+        if (key != GR_KEY_NONE) atomicMin((long long *)&T->key[0], (long long)key);
+        if (KIND == 1 && key_m != GR_KEY_NONE) atomicMin((long long *)&T->key[1], (long long)key_m);
         // release: the keys before the completion count; acquire: the last
         // arriver sees every chunk's keys
-        last = atom_add_acq_rel(&P.ws[sv2].tasks[s_ti].done, 1ull) == s_nch - 1;
+        if (atom_add_acq_rel(&T->pending, ~0ull) == 1ull) n = q_commit_chain(P, s_sv, s_ti, &word, &e0);
       }
-      last = __shfl_sync(0xffffffffu, last, 0);
-      if (last) q_commit_warp(P, s_sv, s_b, s_k);
+      n = __shfl_sync(0xffffffffu, n, 0);
+      if (n) {  // publish the next level's ring entries together
+        word = __shfl_sync(0xffffffffu, word, 0);
+        e0 = __shfl_sync(0xffffffffu, e0, 0);
+        for (u64 i = lane; i < n; i += 32) q_publish(P, word, e0, i);
+      }
     }
     __syncthreads();  // every warp is done with this task's staging
   }
@@ -1850,6 +1969,16 @@ u64 lane_cands() {  // 0 = adaptive (GR_LANE_CANDIDATES overrides)
 }  // namespace
 
 extern "C" size_t gr_workspace_bytes_exact(const gr_batch *in) { return layout_of(in).total; }
+
+// diagnostics (scripts/queue_stats.py): byte offset of the task records in a
+// workspace of gr_workspace_bytes(in, 0)
+extern "C" size_t gr_debug_tasks_offset(const gr_batch *in) { return layout_of(in).tasks; }
+
+// per-instance u64 scratch of the exact workspace that no solve touches
+// (gr_solve keeps the greedy costs there across the final MaxSAT query)
+uint64_t *gr_exact_scratch(const gr_batch *in, void *ws) {
+  return (uint64_t *)((char *)ws + layout_of(in).gcost);
+}
 
 void gr_exact_work_read(unsigned long long out[8], int reset) {
   int dev = 0;
@@ -2061,6 +2190,8 @@ int launch_queue(const gr_batch *in, int nsolve, int fused, const int which[2], 
   P.fused = fused;
   P.exhaustive = (in->flags & GR_FLAG_EXHAUSTIVE) ? 1 : 0;
   P.prune = (in->flags & GR_FLAG_NO_PRUNE) ? 0 : 1;
+  P.spec = (int)env_u64("GR_QSPEC", 2, 0, 16);  // speculative levels ahead (0: off)
+  P.spec_max = env_u64("GR_QSPEC_MAX", 1ull << 32, 0, ~0ull);
   P.gen = g_qgen.fetch_add(1) % 4095ull + 1ull;  // 1..4095
   P.ring_mask = ring_cap(in->B) - 1;
   P.ring_log2 = 63 - __builtin_clzll(ring_cap(in->B));

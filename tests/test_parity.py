@@ -869,12 +869,18 @@ np.savez(%r, **out)
 print("ok")
 """
     res = {}
-    for mode, env in (("queue", {}), ("host", {"GR_HOST_LOOP": "1"})):
+    # speculation 4 levels deep on every level size, no speculation, small windows
+    modes = (("queue", {}), ("host", {"GR_HOST_LOOP": "1"}),
+             ("queue_spec4", {"GR_QSPEC": "4", "GR_QSPEC_MAX": "18446744073709551615"}),
+             ("queue_nospec", {"GR_QSPEC": "0"}),
+             ("queue_small", {"GR_QLANE_MIN": "256", "GR_QLANE_MAX": "4096"}))
+    for mode, env in modes:
         path = str(tmp_path / f"{mode}.npz")
         assert "ok" in _subprocess_solve(env, code % path)
         res[mode] = np.load(path)
-    for k in res["queue"].files:
-        assert np.array_equal(res["queue"][k], res["host"][k]), k
+    for mode, _ in modes[1:]:
+        for k in res["queue"].files:
+            assert np.array_equal(res["queue"][k], res[mode][k]), (mode, k)
 
 
 @pytest.mark.parametrize("case", ["c2", "c3", "c3x"])
@@ -946,3 +952,125 @@ print("ok")
 """
     for L in ("2048", "65536", "1048576"):
         assert "ok" in _subprocess_solve({"GR_LANE_CANDIDATES": L}, code)
+
+
+@pytest.mark.parametrize("weighted", [False, True])
+def test_final_maxsat_query(weighted):
+    """GR_STRATEGY_MHS_FINAL, the mhs strategy's final 'single query to a
+    MaxSAT solver ... to ensure that the number of b_i's being set to true is
+    the minimum': every instance gets the oracle's (weighted)
+    PMS optimum; fell_back flags exactly the instances whose greedy answer
+    broke phi- or was not minimum."""
+    cb = rand_batch(600 + weighted, 300, 14, 16, weighted=weighted)
+    db = gr.DeviceBatch.from_host(cb)
+    fb = torch.zeros(cb.B, dtype=torch.int32, device="cuda")
+    r = gr.solve(db, gr.GR_STRATEGY_MHS_FINAL, fell_back=fb).to_host()
+    p = oracle.batch("pms", cb)
+    g = oracle.batch("greedy", cb)
+    keep = p.status != -1
+    for f, o in (("status", p.status), ("assign", p.assign), ("cost", p.cost)):
+        assert (r[f][keep] == o[keep]).all(), f
+    want = np.zeros(cb.B, np.int32)
+    for b in range(cb.B):
+        if g.status[b] != 0:
+            want[b] = 1
+            continue
+        chosen = [v - 1 for v in synth.mask_to_vars(g.assign[b])]  # 0-based
+        gcost = sum(int(cb.w[b, v]) for v in chosen) if weighted else len(chosen)
+        want[b] = int(p.status[b] == 0 and int(p.cost[b]) < gcost)
+    got = fb.cpu().numpy()
+    assert (got[keep] == want[keep]).all()
+    assert want.sum() > 0 and (want == 0).sum() > 0
+
+
+def test_weighted_key_overflow_unsupported():
+    """A weighted key (W << rb | rank) that would not fit 63 bits gives
+    GR_UNSUPPORTED for that instance, on the device level loop
+    and on the host loop; the other instances of the batch are unaffected.
+    Ten disjoint 4-variable clauses put the optimum at level 10 of m = 40;
+    with weights near 2^31 the level-9 key needs bitlen(40 * 2^31) +
+    bitlen(C(40, 9) - 1) = 37 + 28 > 63 bits."""
+    pos = [list(range(4 * i + 1, 4 * i + 5)) for i in range(10)]
+    insts = [(40, pos, []), (40, [[1, 2], [3, 4]], [[1]])]
+    ws = [[(1 << 31) + i for i in range(40)], [(1 << 31) + i for i in range(40)]]
+    cb = synth.batch_from_lists(insts, weights=ws, W=1)
+    code = """
+import numpy as np, oracle, paper_2011_08373_b200 as gr
+from paper_2011_08373_b200 import synth
+pos = [list(range(4 * i + 1, 4 * i + 5)) for i in range(10)]
+insts = [(40, pos, []), (40, [[1, 2], [3, 4]], [[1]])]
+ws = [[(1 << 31) + i for i in range(40)], [(1 << 31) + i for i in range(40)]]
+cb = synth.batch_from_lists(insts, weights=ws, W=1)
+r = gr.solve_pms(gr.DeviceBatch.from_host(cb)).to_host()
+o = oracle.batch("pms", cb)
+assert r["status"][0] == gr.GR_UNSUPPORTED, r["status"]
+assert r["status"][1] == o.status[1] == 0 and (r["assign"][1] == o.assign[1]).all() and r["cost"][1] == o.cost[1]
+print("ok")
+"""
+    for env in ({}, {"GR_HOST_LOOP": "1"}):
+        assert "ok" in _subprocess_solve(env, code)
+
+
+# ------------------------------------------------------------------ greedy from lists (f3)
+def check_lists(m, pos, neg, w=None):
+    po, pv = csr_from_lists(pos)
+    no, nv = csr_from_lists(neg)
+    o = oracle.greedy_csr(m, po, pv, no, nv, w=w)
+    wt = None if w is None else torch.from_numpy(np.asarray(w, np.uint32).view(np.int32)).cuda()
+    r = gr.mhs_greedy_lists(m, po, pv.astype(np.int32), no, nv.astype(np.int32), w=wt)
+    torch.cuda.synchronize()
+    assert r.n_picks == len(o.picks)
+    assert r.picks.cpu().numpy()[: r.n_picks].tolist() == o.picks.tolist()
+    a = r.assign.cpu().numpy().view(np.uint64)
+    got = [i for i in range(m) if (int(a[i // 64]) >> (i % 64)) & 1]
+    assert got == np.nonzero(o.in_S)[0].tolist()
+    assert int(r.status.item()) == o.status
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_greedy_lists_random(seed):
+    """gr_mhs_greedy_lists (no bit matrix: device-built variable -> clause
+    lists) = the oracle's textbook greedy: picks, pruned set, phi- status."""
+    rng = random.Random(900 + seed)
+    m = [7, 64, 300, 5000][seed]
+    n = [1, 5000, 40000, 20000][seed]
+    pos = [sorted(rng.sample(range(m), rng.randint(1, min(m, 6)))) for _ in range(n)]
+    neg = [sorted(rng.sample(range(m), min(m, 2))) for _ in range(5)]
+    check_lists(m, pos, neg)
+
+
+def test_greedy_lists_weighted_and_golden():
+    """The weighted mhs (R20) from lists, and the prune-order golden
+    instance (descending weight, R12)."""
+    rng = random.Random(19)
+    m, n = 300, 20000
+    pos = [sorted(rng.sample(range(m), rng.randint(1, 6))) for _ in range(n)]
+    neg = [sorted(rng.sample(range(m), 2)) for _ in range(5)]
+    check_lists(m, pos, neg, w=[rng.randint(1, 40) for _ in range(m)])
+    g = load_golden("weighted_prune_order.txt")
+    check_lists(g["m"], [[v - 1 for v in c] for c in g["pos"]], [], w=g["w"])
+
+
+def test_greedy_lists_bad_and_empty():
+    po, pv = csr_from_lists([[0, 1], [5]])
+    r = gr.mhs_greedy_lists(4, po, pv, np.zeros(1, np.int64), np.zeros(0, np.int32))
+    assert int(r.status.item()) == gr.GR_BADINPUT
+    po, pv = csr_from_lists([[0, 1], []])
+    r = gr.mhs_greedy_lists(4, po, pv, np.zeros(1, np.int64), np.zeros(0, np.int32))
+    assert int(r.status.item()) == gr.GR_UNSAT
+
+
+def test_c5_full_greedy_lists_vs_oracle():
+    """The full C5 (2^24 clauses) through the list greedy, against the
+    oracle's stored result."""
+    e = np.load(os.path.join(GOLDEN, "expected_c5.npz"))
+    csr, digest = c5_full()
+    assert str(e["digest"]) == digest
+    r = gr.mhs_greedy_lists(csr.m, csr.pos_off, csr.pos_var, csr.neg_off, csr.neg_var)
+    torch.cuda.synchronize()
+    assert r.n_picks == e["picks"].size
+    assert np.array_equal(r.picks.cpu().numpy()[: r.n_picks], e["picks"])
+    a = r.assign.cpu().numpy().view(np.uint64)
+    got = np.array([i for i in range(csr.m) if (int(a[i // 64]) >> (i % 64)) & 1], np.int32)
+    assert np.array_equal(got, e["in_S"])
+    assert int(r.status.item()) == int(e["status"])
