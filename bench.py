@@ -354,7 +354,7 @@ def time_steps(step, steps, ctx, flush, clocks=True):
     return total, (clk.summary() if clocks else None)
 
 
-def exact_roofline(cb, step, flush, step_ms, sms):
+def exact_roofline(cb, step, flush, step_ms, sms, cfg="c2"):
     """The dominant kernel (queue_kernel, the device level loop) of one
     untimed step: its event-timed duration (gr_profile(1)) and its work units
     (gr_profile(2), the counting instantiation) -> algorithmic INT ALU ops
@@ -391,9 +391,13 @@ def exact_roofline(cb, step, flush, step_ms, sms):
             "share_of_step": q["ms"] / step_ms if step_ms else None,
             "timing": "one untimed step, CUDA events around the launch (gr_profile(1))",
             "traffic_note": "on-chip work: clause records in shared memory, ~0 HBM bytes"}
-    hw = ncu_summary("queue_kernel_c2")
+    hw = ncu_summary(f"queue_kernel_{cfg}")
     if hw:
         roof["ncu"] = hw
+        roof["traffic"] = hw.get("dram_bytes_per_launch")
+        roof["ncu_note"] = ("ncu --set full of this config's queue_kernel launch (scripts/prof_c2.py "
+                            f"{cfg}; profiles/r02_ncu_summary.json): the hardware view -- issue slots, "
+                            "pipes, stall cycles per issue (barrier = CTAs idle waiting for work)")
     return roof, kern
 
 
@@ -452,7 +456,7 @@ def run_exact(a, cfg, ctx, flush, sub=False):
     # ---- roofline of the dominant kernel + per-kernel breakdown (untimed)
     if not sharded:
         roof, kern = exact_roofline(cb, lambda: step(db, outs), flush, tmax / steps,
-                                    torch.cuda.get_device_properties(dev).multi_processor_count)
+                                    torch.cuda.get_device_properties(dev).multi_processor_count, cfg)
         rec["roofline"] = roof
         rec["kernels"] = kernels_of(kern)
         rec["kernels_note"] = "one extra untimed step with CUDA events around every launch"

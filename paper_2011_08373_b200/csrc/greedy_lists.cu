@@ -27,6 +27,7 @@
 #include <cub/block/block_scan.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -34,7 +35,7 @@
 namespace {
 
 constexpr int LT = 512;     // CTA size of the list kernels
-constexpr int LCTA = 512;   // histogram rows reserved in the workspace (>= the grid used)
+constexpr int LCTA = 1184;  // histogram rows reserved in the workspace (>= the grid used)
 constexpr int ST = 1024;    // CTA size of the scan
 
 struct LCtrl {
@@ -291,7 +292,13 @@ int run_lists(const gr_clauselists *in, const LLayout &L, char *base, uint64_t *
   const V *var = (const V *)in->pos_var;
   const size_t hs = 4 * (size_t)m;
   const int sms = gr_sm_count();
-  const int G = std::min(LCTA, 2 * sms);
+  // counting-sort CTAs (GR_LSORT_PER_SM per SM; latency-bound: more in flight)
+  static const int sort_per = [] {
+    const char *e = getenv("GR_LSORT_PER_SM");
+    const int x = e ? atoi(e) : 4;
+    return (x < 1 || x > 8) ? 4 : x;
+  }();
+  const int G = std::min(LCTA, sort_per * sms);
   lattr();
   GR_CUDA(cudaMemsetAsync(ctrl, 0, sizeof(LCtrl), st));
   GR_CUDA(cudaMemsetAsync(cov, 0, std::max<size_t>((size_t)n, 1), st));
@@ -312,7 +319,12 @@ int run_lists(const gr_clauselists *in, const LLayout &L, char *base, uint64_t *
     gr_set_error("the list greedy does not fit an SM");
     return GR_ETOOBIG;
   }
-  const int cgrid = sms * std::min(per, 2);
+  static const int greedy_per = [] {  // CTAs per SM of the pick loop (GR_LGREEDY_PER_SM)
+    const char *e = getenv("GR_LGREEDY_PER_SM");
+    const int x = e ? atoi(e) : 1;
+    return (x < 1 || x > 4) ? 1 : x;
+  }();
+  const int cgrid = sms * std::min(per, greedy_per);
   {
     const int64_t *po = in->pos_off;
     const u32 *wv = in->w;

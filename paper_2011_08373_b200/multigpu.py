@@ -287,11 +287,16 @@ def solve_batch_sharded_device(cb, parts, rank: int, db, outs, allgather):
 
 
 def nccl_allgather(group=None, device=None):
+    """all_gather over the group: on the device with NCCL (gloo, e.g. the
+    one-GPU functional check, gathers host copies)."""
     import torch
     import torch.distributed as dist
 
     def f(t):
-        t = t.to(device) if device is not None else t
+        if dist.get_backend(group) == "gloo":
+            t = t.cpu()
+        elif device is not None:
+            t = t.to(device)
         outs = [torch.empty_like(t) for _ in range(dist.get_world_size(group))]
         dist.all_gather(outs, t, group=group)
         return outs

@@ -56,6 +56,9 @@ def summary(rep):
                 scale = 1.0
             if k == "gpu__time_duration.sum" and u.get(k) == "ms":
                 scale = 1e3
+            if k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
+                         "KB": 1e3, "MB": 1e6, "GB": 1e9}.get(u.get(k), 1.0)
             if k == "sm__cycles_elapsed.avg.per_second":
                 scale = {"Ghz": 1e3, "GHz": 1e3, "Mhz": 1.0, "MHz": 1.0}.get(u.get(k), 1e-6)
             out[name] = v * scale
