@@ -31,6 +31,7 @@
 #include <cub/block/block_scan.cuh>
 
 #include <algorithm>
+#include <cstddef>
 #include <atomic>
 #include <cstdlib>
 #include <mutex>
@@ -252,13 +253,34 @@ __device__ F2 hitting(int j, u64 p);
 // ---------------------------------------------------------------------------
 // pack: one CTA per instance
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(PT) pack_kernel(In in, Out out, WS ws, int which) {
+// one pack launch packs one batch for up to two solves (the PMS and the MHS
+// workspaces of gr_solve_pms_mhs): CTA i < in0.B packs instance i for
+// (in0, ws0), CTA in0.B + i for (in1, ws1); the first CTA of each solve also
+// resets its control block (lane_cands = the fixed window, 0 = adaptive)
+struct PackArgs {
+  In in[2];
+  Out out[2];
+  WS ws[2];
+  int which[2];
+  u64 lane_cands;
+};
+__device__ void pack_body(const In &in, const Out &out, const WS &ws, int which, int b);
+__global__ void __launch_bounds__(PT) pack_kernel(const __grid_constant__ PackArgs A) {
+  const int s = (int)blockIdx.x >= A.in[0].B ? 1 : 0;
+  const int b = (int)blockIdx.x - (s ? A.in[0].B : 0);
+  if (b == 0 && threadIdx.x < sizeof(Ctrl) / 8) {
+    u64 *c = (u64 *)A.ws[s].ctrl;
+    c[threadIdx.x] = threadIdx.x == offsetof(Ctrl, lane_cands) / 8 ? A.lane_cands : 0ull;
+  }
+  pack_body(A.in[s], A.out[s], A.ws[s], A.which[s], b);
+}
+__device__ void pack_body(const In &in, const Out &out, const WS &ws, int which, int b) {
   extern __shared__ u64 sm[];  // [max_clauses] masks, [max_clauses] int info, [max_clauses] u8 keep
   __shared__ int s_bad, s_unsat, s_negempty, s_npr, s_nnr;
   __shared__ unsigned long long s_sup0, s_sup1;
   __shared__ u32 s_w[64];
   __shared__ u64 s_ws[64];
-  const int b = blockIdx.x, t = threadIdx.x;
+  const int t = threadIdx.x;
   if (in.sel && in.sel[b] != in.sel_val) {  // not selected: leave its results alone
     if (t == 0) ws.done[b] = 1;
     return;
@@ -1636,7 +1658,8 @@ __global__ void __launch_bounds__(1024) queue_seed_kernel(QParams P, long long b
         continue;
       }
       atomicAdd(&P.ws[0].ctrl->q_remaining, 1);
-      __threadfence();
+      // (no fence: queue_kernel starts after this launch completes, which
+      // orders every record before every entry)
       const u64 n = q_entries(P, w.tasks[ti].nchunks, &e0);
       for (u64 i = 0; i < n; i++) q_publish(P, ti | ((u64)sv << 38), e0, i);
     }
@@ -2012,14 +2035,25 @@ int launch_finish(const gr_batch *in, int which, const gr_result *out, const WS 
                                    enum_small(in) ? NT_SMALL : NT));
   return GR_OK;
 }
-int launch_pack(const gr_batch *in, int which, const gr_result *out, const WS &w, cudaStream_t st) {
-  Ctrl c{};
-  c.lane_cands = lane_cands();
-  GR_CUDA(cudaMemcpyAsync(w.ctrl, &c, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
+// pack the batch for one solve, or for two (which1 >= 0: the second solve's
+// result and workspace) in the same launch
+int launch_pack(const gr_batch *in, int which, const gr_result *out, const WS &w, cudaStream_t st,
+                int which1 = -1, const gr_result *out1 = nullptr, const WS *w1 = nullptr) {
+  PackArgs A{};
+  A.in[0] = in_of(in, which);
+  A.out[0] = out_of(out);
+  A.ws[0] = w;
+  A.which[0] = which;
+  const int two = which1 >= 0 ? 1 : 0;
+  A.in[1] = two ? in_of(in, which1) : A.in[0];
+  A.out[1] = two ? out_of(out1) : A.out[0];
+  A.ws[1] = two ? *w1 : w;
+  A.which[1] = two ? which1 : which;
+  A.lane_cands = lane_cands();
   size_t smem = (size_t)std::max(in->max_clauses, 1) * 13 + 16;
   static PerDevice attr;
   attr.get([] { return (int)cudaFuncSetAttribute(pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MAXC * 13 + 16); });
-  GR_LAUNCH("pack_kernel", st, pack_kernel<<<in->B, PT, smem, st>>>(in_of(in, which), out_of(out), w, which));
+  GR_LAUNCH("pack_kernel", st, pack_kernel<<<in->B * (1 + two), PT, smem, st>>>(A));
   return GR_OK;
 }
 }  // namespace
@@ -2368,9 +2402,8 @@ extern "C" int gr_solve_pms_mhs(const gr_batch *in, gr_result *out_pms, gr_resul
     if (!out_pms || !out_mhs) { gr_set_error("null result"); return GR_EINVAL; }
     cudaStream_t st = (cudaStream_t)s_pms;
     WS w1 = ws_of(in, ws1), w2 = ws_of(in, ws2);
-    if (!host_loop()) {  // both packs, then one device level loop for the fused walk
-      if ((rc = launch_pack(in, 1, out_mhs, w2, st))) return rc;
-      if ((rc = launch_pack(in, 0, out_pms, w1, st))) return rc;
+    if (!host_loop()) {  // both packs in one launch, then one device level loop for the fused walk
+      if ((rc = launch_pack(in, 0, out_pms, w1, st, 1, out_mhs, &w2))) return rc;
       const int wh[2] = {0, 1};
       if ((rc = launch_queue(in, 1, 1, wh, out_pms, out_mhs, w1, w2, st))) return rc;
       return stream_join(st, (cudaStream_t)s_mhs);
@@ -2393,8 +2426,7 @@ extern "C" int gr_solve_pms_mhs(const gr_batch *in, gr_result *out_pms, gr_resul
     if (!out_pms || !out_mhs) { gr_set_error("null result"); return GR_EINVAL; }
     cudaStream_t st = (cudaStream_t)s_pms;
     WS w1 = ws_of(in, ws1), w2 = ws_of(in, ws2);
-    if ((rc = launch_pack(in, 0, out_pms, w1, st))) return rc;
-    if ((rc = launch_pack(in, 1, out_mhs, w2, st))) return rc;
+    if ((rc = launch_pack(in, 0, out_pms, w1, st, 1, out_mhs, &w2))) return rc;
     const int wh[2] = {0, 1};
     if ((rc = launch_queue(in, 2, 0, wh, out_pms, out_mhs, w1, w2, st))) return rc;
     return stream_join(st, (cudaStream_t)s_mhs);

@@ -295,8 +295,8 @@ int run_lists(const gr_clauselists *in, const LLayout &L, char *base, uint64_t *
   // counting-sort CTAs (GR_LSORT_PER_SM per SM; latency-bound: more in flight)
   static const int sort_per = [] {
     const char *e = getenv("GR_LSORT_PER_SM");
-    const int x = e ? atoi(e) : 4;
-    return (x < 1 || x > 8) ? 4 : x;
+    const int x = e ? atoi(e) : 2;
+    return (x < 1 || x > 8) ? 2 : x;
   }();
   const int G = std::min(LCTA, sort_per * sms);
   lattr();
@@ -321,8 +321,8 @@ int run_lists(const gr_clauselists *in, const LLayout &L, char *base, uint64_t *
   }
   static const int greedy_per = [] {  // CTAs per SM of the pick loop (GR_LGREEDY_PER_SM)
     const char *e = getenv("GR_LGREEDY_PER_SM");
-    const int x = e ? atoi(e) : 1;
-    return (x < 1 || x > 4) ? 1 : x;
+    const int x = e ? atoi(e) : 2;
+    return (x < 1 || x > 4) ? 2 : x;
   }();
   const int cgrid = sms * std::min(per, greedy_per);
   {

@@ -43,8 +43,12 @@ ctl = ws[0:128].cpu().numpy().view(np.uint64)
 cnt, nchild = int(ctl[8]), int(ctl[11])
 r = ws[toff: toff + 128 * cnt].cpu().numpy().view(np.uint64).reshape(-1, 16)
 print(f"  root tasks {cnt}, child tasks (donated remainders) {nchild}")
-if cnt > 40:  # batches: the 25 largest levels only
-    r = r[np.argsort(-r[:, 2].astype(np.int64))[:25]]
+if cnt > 40:  # batches: the level chain of the instance that commits last (the critical path)
+    bcol = (r[:, 6] & np.uint64(0xffffffff)).astype(np.int64)
+    last = int(bcol[np.argmax(r[:, 10].astype(np.int64))])
+    print(f"  critical instance b={last} (m={int(cb.m[last])}, clauses={int(cb.off[last + 1] - cb.off[last])})")
+    r = r[bcol == last]
+    r = r[np.argsort(r[:, 8].astype(np.int64))]
 t0 = int(r[:, 8].min())
 for row in r:
     k = int(row[6] >> np.uint64(32))
