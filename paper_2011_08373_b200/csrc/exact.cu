@@ -1405,7 +1405,8 @@ struct QParams {
   int lanes;       // threads of the grid (lane window sizing)
   int grid, nwarps;  // CTAs of the queue_kernel grid, warps per CTA (ring entries per task)
   int wpl;         // lane windows per lane (unit | weighted << 16)
-  u64 lane_max, lane_max_w, fixed_lane, lane_min;
+  u64 lane_max, lane_max_w, fixed_lane, lane_min;  // lane_min: unit | weighted << 32
+  int local_max;   // a next level of at most this many chunks stays with the committing CTA
 };
 
 // gpu-scope acquire load / acq_rel add (PTX memory model): the completion
@@ -1456,8 +1457,9 @@ __device__ bool q_make(const QParams &P, int sv, int b, int k, u64 work, int dep
   const bool wt = P.weighted[sv] != 0;
   const u64 wpl = wt ? (u64)(P.wpl >> 16) : (u64)(P.wpl & 0xffff);
   const u64 Lmax = wt ? P.lane_max_w : P.lane_max;
+  const u64 Lmin = wt ? P.lane_min >> 32 : P.lane_min & 0xffffffffull;
   u64 L = work / ((u64)P.lanes * (wpl ? wpl : 2));
-  L = L < P.lane_min ? P.lane_min : (L > Lmax ? Lmax : L);
+  L = L < Lmin ? Lmin : (L > Lmax ? Lmax : L);
   L = 1ull << (63 - __clzll((long long)L));
   if (P.fixed_lane) L = P.fixed_lane;
   const u64 nch = (ck + 32 * L - 1) / (32 * L);
@@ -1581,7 +1583,10 @@ __device__ void q_cancel(const QParams &P, int sv, Task *S) {
 // are done as well), publish level k+1, or retire the instance.  Lane 0 of
 // the committing warp.  Returns the ring entries the warp must publish
 // (*word, *e0) -- 0 if none.
-__device__ u64 q_commit_chain(const QParams &P, int sv, u64 ti, u64 *word, u64 *e0) {
+// local_max > 0: a next level of at most local_max chunks is not published
+// but returned in *local (task index + 1) for the committing CTA to walk.
+__device__ u64 q_commit_chain(const QParams &P, int sv, u64 ti, u64 *word, u64 *e0, u64 local_max = 0,
+                              u64 *local = nullptr) {
   Ctrl *c = P.ws[0].ctrl;
   u64 *qw = &P.ws[sv].ctrl->q_work;
   for (;;) {
@@ -1607,6 +1612,10 @@ __device__ u64 q_commit_chain(const QParams &P, int sv, u64 ti, u64 *word, u64 *
         if (q_make(P, sv, b, k + 1, wk, 0, &ti2)) {
           __threadfence();  // the task record before its entries
           *word = ti2 | ((u64)sv << 38);
+          if (local && P.ws[sv].tasks[ti2].nchunks <= local_max) {
+            *local = ti2 + 1;
+            return 0;
+          }
           return q_entries(P, P.ws[sv].tasks[ti2].nchunks, e0);
         }
         work_sub(qw, ck1);
@@ -1686,10 +1695,11 @@ __global__ void __launch_bounds__(NTK, COUNT ? 1 : ENUM_CTAS * NT / NTK) queue_k
   extern __shared__ u64 cls[];  // tables, then the staged clause records
   __shared__ int s_b, s_k, s_sv, s_cur, s_exit, s_rb;
   __shared__ u64 s_ti, s_L, s_nch, s_ck;
+  __shared__ u64 s_next;  // a next level this CTA committed and keeps (ti + 1 | sv << 40), 0: none
   __shared__ u64 s_skj[JMAX + 1], s_wstar;  // weighted: S_j and the incumbent W*
   __shared__ u32 s_w[64];
   const int t = threadIdx.x, lane = t & 31;
-  if (t == 0) s_cur = -1;
+  if (t == 0) s_cur = -1, s_next = 0;
   F2 *hitx = (F2 *)cls;
   u64 *cs = cls + 2 * (JMAX + 1) * HX;
   F2 *lowb = (F2 *)(cs + 65 * (JMAX + 1));
@@ -1706,23 +1716,29 @@ __global__ void __launch_bounds__(NTK, COUNT ? 1 : ENUM_CTAS * NT / NTK) queue_k
   }
   u64 *stage = cls + TAB_SMEM / 8;
   for (;;) {
-    // ---- thread 0: take a ticket, wait for its ring entry (or the end)
+    // ---- thread 0: the small next level this CTA committed, else take a
+    // ticket and wait for its ring entry (or the end)
     if (t == 0) {
       Ctrl *ctrl = P.ws[0].ctrl;
-      const u64 e = atomicAdd((unsigned long long *)&ctrl->q_tickets, 1ull);
-      const u64 *r = P.ws[0].ring + (e & P.ring_mask);
-      const u64 want = ring_stamp(P, e);
       int ex = 0;
       u64 v = 0;
-      for (int spin = 0;; spin++) {
-        v = ld_acquire(r);  // the task record is read after its entry
-        if ((v & ~((1ull << 40) - 1ull)) == want) break;
-        if (vld(&ctrl->q_remaining) == 0) { ex = 1; break; }
-        __nanosleep(spin < 16 ? 32 : 128);
+      if (s_next) {
+        v = ((s_next >> 40) << 38) | ((s_next & ((1ull << 40) - 1ull)) - 1ull);
+        s_next = 0;
+      } else {
+        const u64 e = atomicAdd((unsigned long long *)&ctrl->q_tickets, 1ull);
+        const u64 *r = P.ws[0].ring + (e & P.ring_mask);
+        const u64 want = ring_stamp(P, e);
+        for (int spin = 0;; spin++) {
+          v = ld_acquire(r);  // the task record is read after its entry
+          if ((v & ~((1ull << 40) - 1ull)) == want) break;
+          if (vld(&ctrl->q_remaining) == 0) { ex = 1; break; }
+          __nanosleep(spin < 16 ? 32 : 128);
+        }
+        if (!ex && (v >> 39 & 1ull)) atomicAdd((unsigned long long *)&ctrl->q_budget, 1ull);  // an extra entry is read
       }
       s_exit = ex;
       if (!ex) {
-        if (v >> 39 & 1ull) atomicAdd((unsigned long long *)&ctrl->q_budget, 1ull);  // an extra entry is read
         const int tsv = (int)((v >> 38) & 1ull);
         const u64 ti = v & ((1ull << 38) - 1ull);
         const Task *T = P.ws[tsv].tasks + ti;
@@ -1877,7 +1893,13 @@ __global__ void __launch_bounds__(NTK, COUNT ? 1 : ENUM_CTAS * NT / NTK) queue_k
         if (KIND == 1 && key_m != GR_KEY_NONE) atomicMin((long long *)&T->key[1], (long long)key_m);
         // release: the keys before the completion count; acquire: the last
         // arriver sees every chunk's keys
-        if (atom_add_acq_rel(&T->pending, ~0ull) == 1ull) n = q_commit_chain(P, s_sv, s_ti, &word, &e0);
+        if (atom_add_acq_rel(&T->pending, ~0ull) == 1ull) {
+          // a small next level stays with this CTA: no ring entry, its
+          // instance is staged already
+          u64 loc = 0;
+          n = q_commit_chain(P, s_sv, s_ti, &word, &e0, (u64)P.local_max, &loc);
+          if (loc) s_next = loc | ((u64)s_sv << 40);
+        }
       }
       n = __shfl_sync(0xffffffffu, n, 0);
       if (n) {  // publish the next level's ring entries together
@@ -1975,13 +1997,14 @@ u64 env_u64(const char *name, u64 dflt, u64 lo, u64 hi) {
 }
 struct QKnobs {
   int wpl, wpl_w;
-  u64 lmin, lmax, lmax_w;
+  u64 lmin, lmax, lmax_w, lmin_w;
 };
 const QKnobs &qknobs() {
   static const QKnobs k = {(int)env_u64("GR_QWPL", 1, 1, 0xffff), (int)env_u64("GR_QWPL_W", 1, 1, 0xffff),
-                           env_u64("GR_QLANE_MIN", 2048, 1, 1ull << 20),
+                           env_u64("GR_QLANE_MIN", 4096, 1, 1ull << 20),
                            env_u64("GR_QLANE_MAX", 1ull << 20, 256, 1ull << 24),
-                           env_u64("GR_QLANE_MAX_W", 1ull << 16, 256, 1ull << 24)};
+                           env_u64("GR_QLANE_MAX_W", 1ull << 16, 256, 1ull << 24),
+                           env_u64("GR_QLANE_MIN_W", 2048, 1, 1ull << 20)};
   return k;
 }
 u64 lane_cands() {  // 0 = adaptive (GR_LANE_CANDIDATES overrides)
@@ -2195,6 +2218,7 @@ int launch_queue_t(QParams &P, int B, cudaStream_t st) {
   const int grid = queue_grid(NTK == NT_SMALL);
   P.grid = grid;
   P.nwarps = NTK / 32;
+  if (P.local_max > P.nwarps) P.local_max = P.nwarps;
   P.lanes = grid * NTK;
   // extra ring entries beyond one per open unit and the tickets the grid holds
   const long long budget = (long long)ring_cap(B) - (long long)(P.fused ? 1 : P.nsolve) * B -
@@ -2234,7 +2258,9 @@ int launch_queue(const gr_batch *in, int nsolve, int fused, const int which[2], 
   P.lane_max = kn.lmax;
   P.lane_max_w = kn.lmax_w;
   P.fixed_lane = lane_cands();
-  P.lane_min = kn.lmin;
+  P.lane_min = kn.lmin | (kn.lmin_w << 32);
+  static const int ql = (int)env_u64("GR_QLOCAL", 1, 0, 1ull << 30);  // (capped at the warps per CTA)
+  P.local_max = ql;
   const bool small = enum_small(in);
   const int kind = fused ? 1 : ((P.weighted[0] || P.weighted[1]) ? 2 : 0);
 #define GR_QLAUNCH(COUNT, NTK)                                              \
