@@ -292,7 +292,9 @@ typedef struct {
   int64_t nnz;            /* host: pos_off[n_pos], the number of literals */
   const int64_t *pos_off; /* [n_pos+1] device */
   const void *pos_var;    /* [nnz] device int16 / int32 variable ids (0-based); a clause
-                             must not list a variable twice */
+                             must not list a variable twice.  16-byte aligned (read in
+                             16-byte groups, up to the next 16-byte boundary past nnz;
+                             GR_EINVAL otherwise) */
   int32_t var_bytes;      /* 2 or 4 */
   int32_t n_neg;          /* host: number of negative clauses */
   const uint64_t *neg;    /* [n_neg][ceil(m/64)] device masks (gr_pack_clausemajor), or NULL */

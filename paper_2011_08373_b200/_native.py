@@ -584,6 +584,8 @@ def mhs_greedy_lists(m, pos_off, pos_var, neg_off, neg_var, w=None, device="cuda
     if nnz is None:
         nnz = int(pos_off[-1])
     po, pv, no, nv = dev(pos_off), dev(pos_var), dev(neg_off), dev(neg_var)
+    if pv.data_ptr() % 16:  # the C-ABI reads pos_var in aligned 16-byte groups
+        pv = pv.clone()
     n_pos, n_neg = int(po.numel() - 1), int(no.numel() - 1)
     mw = (m + 63) // 64
     neg = torch.zeros((max(n_neg, 1), mw), dtype=torch.int64, device=device)

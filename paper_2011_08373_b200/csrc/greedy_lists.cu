@@ -131,25 +131,63 @@ __global__ void __launch_bounds__(ST) lscan_kernel(const u32 *tot, int m, u32 *v
   if (threadIdx.x == 0) voff[m] = all;
 }
 
-// scatter the clause ids into the variable lists: vcl[voff[v] + ...] = c
+// scatter the clause ids into the variable lists: vcl[voff[v] + ...] = c.
+// The CTA walks its clause range in tiles of LTC clauses: the tile's offsets
+// and a literal -> clause map go to shared memory, then the literals are read
+// coalesced and independent of each other (a thread per clause would chain
+// the offset and literal loads of each clause: latency-bound).  A tile with
+// more than `cap` literals falls back to a thread per clause.
+constexpr int LTC = 1024;
 template <typename V>
-__global__ void __launch_bounds__(LT) lscatter_kernel(int64_t n, const int64_t *off, const V *var, int m,
-                                                     const u32 *hist, const u32 *voff, u32 *vcl) {
-  extern __shared__ u32 cur[];  // the next free slot of each variable's segment of this CTA
+__global__ void __launch_bounds__(LT) lscatter_kernel(int64_t n, const int64_t *__restrict__ off,
+                                                     const V *__restrict__ var, int m,
+                                                     const u32 *__restrict__ hist, const u32 *__restrict__ voff,
+                                                     u32 *__restrict__ vcl, int cap) {
+  extern __shared__ u32 cur[];  // [m] the next free slot of each variable's segment of this CTA
+  u32 *s_off = cur + m;         // [LTC + 1] the tile's clause offsets, relative to its first literal
+  unsigned short *s_cid = (unsigned short *)(s_off + LTC + 2);  // [cap] literal -> clause of the tile
   for (int v = threadIdx.x; v < m; v += LT) cur[v] = voff[v] + hist[(size_t)blockIdx.x * m + v];
-  __syncthreads();
   const int64_t j0 = n * blockIdx.x / gridDim.x, j1 = n * (blockIdx.x + 1) / gridDim.x;
-  for (int64_t j = j0 + threadIdx.x; j < j1; j += LT)
-    for (int64_t e = off[j]; e < off[j + 1]; e++) {
-      const int v = (int)var[e];
-      if (v >= 0 && v < m) vcl[atomicAdd(&cur[v], 1u)] = (u32)j;
+  for (int64_t jt = j0; jt < j1; jt += LTC) {
+    const int jn = (int)min((int64_t)LTC, j1 - jt);
+    const int64_t e0 = off[jt];
+    __syncthreads();  // (the previous tile's map is consumed)
+    for (int q = threadIdx.x; q <= jn; q += LT) s_off[q] = (u32)(off[jt + q] - e0);
+    __syncthreads();
+    const u32 E = s_off[jn];
+    if (E > (u32)cap) {  // long clauses: a thread per clause
+      for (int q = threadIdx.x; q < jn; q += LT)
+        for (u32 k = s_off[q]; k < s_off[q + 1]; k++) {
+          const int v = (int)var[e0 + k];
+          if (v >= 0 && v < m) vcl[atomicAdd(&cur[v], 1u)] = (u32)(jt + q);
+        }
+      continue;
     }
+    for (int q = threadIdx.x; q < jn; q += LT)
+      for (u32 k = s_off[q]; k < s_off[q + 1]; k++) s_cid[k] = (unsigned short)q;
+    __syncthreads();
+    // 16-byte loads of the tile's literals (aligned groups of PV ids): enough
+    // bytes in flight per SM to stream var at HBM rate
+    constexpr int PV = 16 / (int)sizeof(V);
+    const int64_t g0 = e0 / PV, g1 = (e0 + (int64_t)E + PV - 1) / PV;
+    for (int64_t g = g0 + threadIdx.x; g < g1; g += LT) {
+      const uint4 pk = __ldg((const uint4 *)var + g);
+      const V *lit = (const V *)&pk;
+#pragma unroll
+      for (int i = 0; i < PV; i++) {
+        const int64_t k = g * PV + i - e0;
+        if (k < 0 || k >= (int64_t)E) continue;
+        const int v = (int)lit[i];
+        if (v >= 0 && v < m) vcl[atomicAdd(&cur[v], 1u)] = (u32)(jt + s_cid[k]);
+      }
+    }
+  }
 }
 
 // ---- all picks in one cooperative launch ---------------------------------------
 template <typename V>
-__global__ void __launch_bounds__(LT) lgreedy_kernel(int m, const int64_t *off, const V *var,
-                                                    const u32 *voff, const u32 *vcl,
+__global__ void __launch_bounds__(LT) lgreedy_kernel(int m, const int64_t *__restrict__ off, const V *__restrict__ var,
+                                                    const u32 *__restrict__ voff, const u32 *__restrict__ vcl,
                                                     unsigned char *cov, u32 *counts, const u32 *w,
                                                     LCtrl *ctrl, int *picks) {
   namespace cg = cooperative_groups;
@@ -186,10 +224,14 @@ __global__ void __launch_bounds__(LT) lgreedy_kernel(int m, const int64_t *off, 
     const u32 s1 = a + (u32)((u64)len * (blockIdx.x + 1) / gridDim.x);
     for (u32 i = s0 + threadIdx.x; i < s1; i += LT) {
       const u32 c = vcl[i];
-      if (__ldcg(&cov[c])) continue;  // L2: other SMs covered it at earlier picks; each clause
-                                     // appears once in a list, so no race within a pick
+      // the flag and the clause's bounds are loaded together (one round trip)
+      const unsigned char done = __ldcg(&cov[c]);  // L2: other SMs covered it at earlier picks; each
+                                                  // clause appears once in a list: no race within a pick
+      const int64_t ea = off[c], eb = off[c + 1];
+      if (done) continue;
       cov[c] = 1;
-      for (int64_t e = off[c]; e < off[c + 1]; e++) atomicAdd(&hist[(int)var[e]], 1u);
+#pragma unroll 4
+      for (int64_t e = ea; e < eb; e++) atomicAdd(&hist[(int)var[e]], 1u);
     }
     __syncthreads();
     for (int u = threadIdx.x; u < m; u += LT)
@@ -256,6 +298,7 @@ int validate_lists(const gr_clauselists *in) {
     gr_set_error("bad clause lists");
     return GR_EINVAL;
   }
+  if ((uintptr_t)in->pos_var % 16 != 0) { gr_set_error("pos_var not 16-byte aligned"); return GR_EINVAL; }
   if (in->nnz >= (1ll << 32) || in->n_pos >= (1ll << 32)) { gr_set_error("nnz or n_pos >= 2^32"); return GR_ETOOBIG; }
   if ((size_t)in->m * 4 > 200 * 1024) { gr_set_error("m > 51200 (shared histograms)"); return GR_ETOOBIG; }
   return GR_OK;
@@ -267,7 +310,7 @@ int lattr() {
     for (auto f : {(const void *)lhist_kernel<int16_t>, (const void *)lhist_kernel<int32_t>,
                    (const void *)lscatter_kernel<int16_t>, (const void *)lscatter_kernel<int32_t>,
                    (const void *)lgreedy_kernel<int16_t>, (const void *)lgreedy_kernel<int32_t>})
-      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024);
     return 1;
   });
 }
@@ -295,8 +338,8 @@ int run_lists(const gr_clauselists *in, const LLayout &L, char *base, uint64_t *
   // counting-sort CTAs (GR_LSORT_PER_SM per SM; latency-bound: more in flight)
   static const int sort_per = [] {
     const char *e = getenv("GR_LSORT_PER_SM");
-    const int x = e ? atoi(e) : 2;
-    return (x < 1 || x > 8) ? 2 : x;
+    const int x = e ? atoi(e) : 1;
+    return (x < 1 || x > 8) ? 1 : x;
   }();
   const int G = std::min(LCTA, sort_per * sms);
   lattr();
@@ -307,7 +350,11 @@ int run_lists(const gr_clauselists *in, const LLayout &L, char *base, uint64_t *
     GR_LAUNCH("lhist_kernel", st, lhist_kernel<V><<<G, LT, hs, st>>>(n, in->pos_off, var, m, hist, ctrl));
     GR_LAUNCH("lsum_kernel", st, lsum_kernel<<<(m + 255) / 256, 256, 0, st>>>(hist, G, m, tot, counts));
     GR_LAUNCH("lscan_kernel", st, lscan_kernel<<<1, ST, 0, st>>>(tot, m, voff));
-    GR_LAUNCH("lscatter_kernel", st, lscatter_kernel<V><<<G, LT, hs, st>>>(n, in->pos_off, var, m, hist, voff, vcl));
+    // shared memory of the scatter: the cursors, the tile offsets, the literal map
+    const size_t base_s = hs + 4 * (LTC + 2);
+    const int cap = (int)std::max<int64_t>(0, std::min<int64_t>(16384, ((int64_t)220 * 1024 - (int64_t)base_s) / 2));
+    GR_LAUNCH("lscatter_kernel", st,
+              lscatter_kernel<V><<<G, LT, base_s + 2 * (size_t)cap, st>>>(n, in->pos_off, var, m, hist, voff, vcl, cap));
   } else {
     GR_CUDA(cudaMemsetAsync(counts, 0, hs, st));
     GR_CUDA(cudaMemsetAsync(voff, 0, 4 * ((size_t)m + 1), st));
