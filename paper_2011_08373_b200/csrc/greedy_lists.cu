@@ -19,7 +19,9 @@
 //
 // -- the same counts and the same argmax as the textbook recount greedy, so
 // the same picks (tested against the oracle on the full C5).  All picks run in
-// one cooperative launch (two grid barriers per pick).  The prune (reverse-
+// one cooperative launch with one grid barrier per pick: the counts of pick p
+// are formed on the fly as the counts of pick p-1 minus that pick's
+// decrements (two count buffers, three decrement buffers, see lgreedy_kernel).  The prune (reverse-
 // delete, reading R12) keeps exact per-clause hit counts over the picks'
 // lists; the phi- check runs on the negative clause masks.
 #include <cooperative_groups.h>
@@ -58,7 +60,7 @@ LLayout llayout(const gr_clauselists *in) {
   L.tot = take(4 * m);
   L.vcl = take(4 * (size_t)std::max<int64_t>(in->nnz, 1));
   L.cov = take(std::max<size_t>(n, 1));
-  L.counts = take(4 * m);
+  L.counts = take(4 * m * 5);  // counts of two picks (ping-pong), decrements of three
   L.picks = take(4 * (m + 1));
   L.hits = take(4 * std::max<size_t>(n, 1));
   L.flags = take(4 * (m + 1));
@@ -196,12 +198,29 @@ __global__ void __launch_bounds__(LT) lgreedy_kernel(int m, const int64_t *__res
   typedef cub::BlockReduce<Cand, LT> Red;
   __shared__ typename Red::TempStorage tmp;
   __shared__ int s_v;
+  // counts: C[2][m] then D[3][m].  The counts of pick p are
+  //   c_p(u) = C[(p-1) & 1][u] - D[(p-1) % 3][u]
+  // (C[1] = the initial counts, D = 0 before pick 0); during pick p each CTA
+  // stores its slice of c_p into C[p & 1] and zeroes its slice of D[(p+1) % 3],
+  // and the cover of pick p adds its decrements into D[p % 3].  Every buffer a
+  // pick writes was last read before the previous pick's grid barrier, and is
+  // next read after this pick's: one barrier per pick.
+  u32 *C = counts, *D = counts + 2 * (size_t)m;
+  const int u0 = (int)((int64_t)m * blockIdx.x / gridDim.x), u1 = (int)((int64_t)m * (blockIdx.x + 1) / gridDim.x);
   int npk = 0;
   for (;;) {
+    const int p = npk;
+    const u32 *Cp = C + (size_t)((p + 1) & 1) * m, *Dp = D + (size_t)((p + 2) % 3) * m;
     // every CTA takes the same argmax of the same counts
     Cand best{0u, 1u, 0x7fffffff};
-    for (int u = threadIdx.x; u < m; u += LT)
-      best = CandBetter()(Cand{__ldcg(&counts[u]), w ? w[u] : 1u, u}, best);
+    for (int u = threadIdx.x; u < m; u += LT) {
+      const u32 c = __ldcg(&Cp[u]) - __ldcg(&Dp[u]);
+      best = CandBetter()(Cand{c, w ? w[u] : 1u, u}, best);
+    }
+    for (int u = u0 + threadIdx.x; u < u1; u += LT) {
+      C[(size_t)(p & 1) * m + u] = __ldcg(&Cp[u]) - __ldcg(&Dp[u]);
+      D[(size_t)((p + 1) % 3) * m + u] = 0u;
+    }
     best = Red(tmp).Reduce(best, CandBetter());
     if (threadIdx.x == 0) {
       s_v = best.c == 0 ? -1 : best.v;
@@ -214,8 +233,7 @@ __global__ void __launch_bounds__(LT) lgreedy_kernel(int m, const int64_t *__res
     for (int u = threadIdx.x; u < m; u += LT) hist[u] = 0;
     __syncthreads();
     const int v = s_v;
-    grid.sync();  // every CTA has read the counts
-    if (v < 0) return;
+    if (v < 0) return;  // (every CTA saw the same counts)
     npk++;
     // cover the clauses of v's list (a slice per CTA) and count the decrements
     const u32 a = voff[v], b = voff[v + 1];
@@ -234,8 +252,9 @@ __global__ void __launch_bounds__(LT) lgreedy_kernel(int m, const int64_t *__res
       for (int64_t e = ea; e < eb; e++) atomicAdd(&hist[(int)var[e]], 1u);
     }
     __syncthreads();
+    u32 *Dq = D + (size_t)(p % 3) * m;
     for (int u = threadIdx.x; u < m; u += LT)
-      if (hist[u]) atomicSub(&counts[u], hist[u]);
+      if (hist[u]) atomicAdd(&Dq[u], hist[u]);
     grid.sync();
   }
 }
@@ -348,7 +367,8 @@ int run_lists(const gr_clauselists *in, const LLayout &L, char *base, uint64_t *
   GR_CUDA(cudaMemsetAsync(picks, 0xff, 4 * ((size_t)m + 1), st));
   if (n > 0) {
     GR_LAUNCH("lhist_kernel", st, lhist_kernel<V><<<G, LT, hs, st>>>(n, in->pos_off, var, m, hist, ctrl));
-    GR_LAUNCH("lsum_kernel", st, lsum_kernel<<<(m + 255) / 256, 256, 0, st>>>(hist, G, m, tot, counts));
+    GR_CUDA(cudaMemsetAsync(counts + 2 * (size_t)m, 0, 3 * hs, st));  // D = 0
+    GR_LAUNCH("lsum_kernel", st, lsum_kernel<<<(m + 255) / 256, 256, 0, st>>>(hist, G, m, tot, counts + m));
     GR_LAUNCH("lscan_kernel", st, lscan_kernel<<<1, ST, 0, st>>>(tot, m, voff));
     // shared memory of the scatter: the cursors, the tile offsets, the literal map
     const size_t base_s = hs + 4 * (LTC + 2);
@@ -356,7 +376,7 @@ int run_lists(const gr_clauselists *in, const LLayout &L, char *base, uint64_t *
     GR_LAUNCH("lscatter_kernel", st,
               lscatter_kernel<V><<<G, LT, base_s + 2 * (size_t)cap, st>>>(n, in->pos_off, var, m, hist, voff, vcl, cap));
   } else {
-    GR_CUDA(cudaMemsetAsync(counts, 0, hs, st));
+    GR_CUDA(cudaMemsetAsync(counts, 0, 5 * hs, st));
     GR_CUDA(cudaMemsetAsync(voff, 0, 4 * ((size_t)m + 1), st));
   }
   // the picks: one cooperative launch, its grid co-resident (sized per call)
