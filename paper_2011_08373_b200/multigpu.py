@@ -193,23 +193,32 @@ def greedy_matrix_sharded(bm_shard, rank: int, world: int, group=None, stream=No
 
 
 # ---- batch sharding with result collection (C2 / C4) -------------------------------
-def solve_batch_sharded(cb, rank: int, world: int, solve_fn: Callable, allgather: Callable):
-    """Solve a host ClauseBatch split across ranks: instances are dealt by
-    estimated cost (``shard_instances``), each rank solves its slice with
-    ``solve_fn(sub_batch) -> dict`` (status int32 [n], assign uint64 [n, W],
-    cost uint64 [n], decided uint64 [n]; e.g. a gr.solve_pms on this rank's
-    GPU), and one all-gather of (index, status, cost, decided, assign) rows
-    gives every rank the whole batch's results in input order.  The gather is
-    result collection after the solve, not part of the data path.
-    ``allgather(t) -> list of tensors`` (one per rank, same shape as t)."""
+def split_heavy(costs: Sequence[float], world: int, factor: float = 1.0):
+    """§8(e) heavy-instance rule: an instance whose cost alone exceeds
+    ``factor`` x the fair share (total / world) cannot be balanced by dealing
+    whole instances; it is split by level rank ranges over all ranks instead.
+    Returns (heavy, light) index lists (ascending)."""
+    c = np.asarray(costs, np.float64)
+    if world <= 1 or c.size == 0:
+        return [], list(range(c.size))
+    fair = c.sum() / world
+    heavy = [int(b) for b in np.nonzero(c > factor * fair)[0]]
+    hs = set(heavy)
+    return heavy, [b for b in range(c.size) if b not in hs]
+
+
+def _gather_rows(cb, parts, rank: int, solve_fn: Callable, allgather: Callable):
+    """Each rank solves its slice ``parts[rank]`` with solve_fn(sub_batch) ->
+    dict (status, assign, cost, decided); one all-gather of (index, status,
+    cost, decided, assign) rows gives every rank the results in input order
+    (entries of instances in no part stay 0)."""
     import torch
 
-    parts = shard_instances(estimate_costs(cb.m, cb.n_pos), world)
     mine = parts[rank]
     W = cb.W
     width = 4 + W
-    maxn = max(len(p) for p in parts)
-    rows = torch.full((max(maxn, 1), width), -1, dtype=torch.int64)
+    maxn = max(max(len(p) for p in parts), 1)
+    rows = torch.full((maxn, width), -1, dtype=torch.int64)
     if mine:
         r = solve_fn(cb.subset(mine))
         n = len(mine)
@@ -230,6 +239,41 @@ def solve_batch_sharded(cb, rank: int, world: int, solve_fn: Callable, allgather
         out["decided"][idx] = g[:, 3].view(np.uint64)
         out["assign"][idx] = g[:, 4:].view(np.uint64)
     return out
+
+
+def solve_batch_split_heavy(cb, rank: int, world: int, costs: Sequence[float], solve_fn: Callable,
+                            solve_heavy_fn: Callable, allgather: Callable, factor: float = 1.0):
+    """Batch split with the heavy-instance rule (``split_heavy``): the light
+    instances are dealt whole by cost and gathered as in solve_batch_sharded;
+    the heavy ones are solved by all ranks together with
+    ``solve_heavy_fn(sub_batch) -> dict`` -- a level loop whose rank ranges
+    are split over the ranks (solve_exact_sharded / solve_pair_sharded on the
+    GPU), which returns the same result on every rank.  Returns (results in
+    input order, heavy indices)."""
+    heavy, light = split_heavy(costs, world, factor)
+    lc = np.asarray(costs, np.float64)[light] if light else np.zeros(0)
+    parts = [[light[i] for i in p] for p in shard_instances(lc, world)] if light else [[] for _ in range(world)]
+    out = _gather_rows(cb, parts, rank, solve_fn, allgather)
+    if heavy:
+        r = solve_heavy_fn(cb.subset(heavy))
+        out["status"][heavy] = np.asarray(r["status"], np.int32)
+        out["cost"][heavy] = np.asarray(r["cost"], np.uint64)
+        out["decided"][heavy] = np.asarray(r["decided"], np.uint64)
+        out["assign"][heavy] = np.asarray(r["assign"], np.uint64).reshape(len(heavy), cb.W)
+    return out, heavy
+
+
+def solve_batch_sharded(cb, rank: int, world: int, solve_fn: Callable, allgather: Callable):
+    """Solve a host ClauseBatch split across ranks: instances are dealt by
+    estimated cost (``shard_instances``), each rank solves its slice with
+    ``solve_fn(sub_batch) -> dict`` (status int32 [n], assign uint64 [n, W],
+    cost uint64 [n], decided uint64 [n]; e.g. a gr.solve_pms on this rank's
+    GPU), and one all-gather of (index, status, cost, decided, assign) rows
+    gives every rank the whole batch's results in input order.  The gather is
+    result collection after the solve, not part of the data path.
+    ``allgather(t) -> list of tensors`` (one per rank, same shape as t)."""
+    parts = shard_instances(estimate_costs(cb.m, cb.n_pos), world)
+    return _gather_rows(cb, parts, rank, solve_fn, allgather)
 
 
 def measured_costs(cb, device="cuda") -> np.ndarray:

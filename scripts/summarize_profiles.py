@@ -1,13 +1,18 @@
-"""Turn a gpurun_out/prof/ evidence run (scripts/box_profiles.sh) into the
+"""Turn an evidence run of scripts/box_evidence.sh (gpurun_out/<R>/) into the
 committed summaries under profiles/ (dev aid).
 
-  profiles/<R>_bench_<cfg>.json         bench lines
-  profiles/<R>_launches_c2_summary.csv  per-kernel totals of the ncu launch list
-  profiles/<R>_ncu_enum_details.txt     ncu --page details of the enum capture
-  profiles/<R>_ncu_selected_metrics.json  (enum_kernel entry replaced)
-  profiles/traffic.json                 (enum_kernel entry replaced)
+  profiles/<R>_bench.json, <R>_bench_reference.json   the bench lines
+  profiles/<R>_gpu_tests_tail.txt                     tail of pytest -m gpu
+  profiles/<R>_launches_c2_summary.csv                per-kernel totals of the ncu launch list
+  profiles/<R>_ncu_<name>_details.txt                 ncu --page details of each capture
+  profiles/<R>_ncu_<name>_lines.txt                   per-source-line stall summary (scripts/ncu_lines.py)
+  profiles/<R>_ncu_summary.json                       selected counters (scripts/ncu_summary.py)
+  profiles/<R>_onegpu_n2/                             bench.py N = 2 on one GPU (functional)
+
+    python scripts/summarize_profiles.py r02
 """
 import csv
+import io
 import json
 import os
 import shutil
@@ -15,21 +20,40 @@ import subprocess
 import sys
 from collections import OrderedDict
 
-R = sys.argv[1] if len(sys.argv) > 1 else "r01"
-SRC = os.path.join("gpurun_out", "prof")
-DST = "profiles"
-NCU = "/usr/local/cuda/bin/ncu"
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import ncu_lines  # noqa: E402
+import ncu_summary  # noqa: E402
 
-for cfg in ("c2", "c3", "c4", "c5", "reference", "reference_c5"):
-    p = os.path.join(SRC, f"{R}_bench_{cfg}.json")
+R = sys.argv[1] if len(sys.argv) > 1 else "r02"
+SRC = os.path.join("gpurun_out", R)
+DST = "profiles"
+NCU = ncu_summary.NCU
+
+
+def last_json_line(p):
+    for line in reversed(open(p).read().strip().splitlines()):
+        line = line.strip()
+        if line.startswith("{"):
+            json.loads(line)
+            return line
+    raise ValueError(f"no JSON line in {p}")
+
+
+for name in ("bench", "bench_reference"):
+    p = os.path.join(SRC, f"{name}.json")
     if os.path.exists(p) and os.path.getsize(p) > 0:
-        line = open(p).read().strip().splitlines()[-1]
-        json.loads(line)
-        with open(os.path.join(DST, f"{R}_bench_{cfg}.json"), "w") as f:
-            f.write(line + "\n")
+        with open(os.path.join(DST, f"{R}_{name}.json"), "w") as f:
+            f.write(last_json_line(p) + "\n")
+        print("bench line", name)
+
+p = os.path.join(SRC, "tests.log")
+if os.path.exists(p):
+    tail = open(p).read().strip().splitlines()[-6:]
+    with open(os.path.join(DST, f"{R}_gpu_tests_tail.txt"), "w") as f:
+        f.write("# python -m pytest tests -m gpu -q  (one B200)\n" + "\n".join(tail) + "\n")
 
 # launch list -> per-kernel summary
-p = os.path.join(SRC, f"{R}_launches_c2.csv")
+p = os.path.join(SRC, "launches_c2.csv")
 if os.path.exists(p):
     rows = [r for r in csv.reader(open(p)) if len(r) > 10]
     h = rows[0]
@@ -45,56 +69,57 @@ if os.path.exists(p):
         a[1] += v
     tot = sum(a[1] for a in agg.values())
     with open(os.path.join(DST, f"{R}_launches_c2_summary.csv"), "w") as f:
-        f.write("# ncu launch list of `python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e` (C2)\n")
+        f.write("# ncu launch list of `python bench.py --config c2 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e`\n")
         f.write("# ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised): compare SHARES\n")
-        f.write("# enum_kernel<1> is the untimed work-counting instantiation bench.py runs after the timed region\n")
+        f.write("# queue_kernel<1,...> launches are the untimed work-counting instantiation bench.py runs after the timed region\n")
         f.write("kernel,launches,total_us,share\n")
         for k, (n, us) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
             f.write(f"{k},{n},{us:.1f},{us / tot:.4f}\n")
+    print("launch list", len(rows) - 1, "launches")
 
-# full capture of enum_kernel
-rep = os.path.join(SRC, f"{R}_enum_c2.ncu-rep")
-if os.path.exists(rep):
-    det = subprocess.run([NCU, "-i", rep, "--page", "details", "--csv"], capture_output=True,
-                         text=True).stdout
-    out = []
-    for r in csv.reader(det.splitlines()):
-        if len(r) >= 15 and r[0] != "ID":
-            out.append(f"{r[0]} | {r[-5]} | {r[-4]} | {r[-2]} {r[-3]}".rstrip())
-    with open(os.path.join(DST, f"{R}_ncu_enum_details.txt"), "w") as f:
-        f.write("# ncu --set full --clock-control none -k regex:enum_kernel --launch-skip 15 -c 1 "
-                "python scripts/prof_c2.py  (C2 PMS solve, level k = 16)\n")
-        f.write("\n".join(out) + "\n")
-    raw = list(csv.reader(subprocess.run([NCU, "-i", rep, "--page", "raw", "--csv"],
-                                         capture_output=True, text=True).stdout.splitlines()))
-    h, u, v = raw[0], raw[1], raw[2]
-    want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
-            "sm__throughput.avg.pct_of_peak_sustained_elapsed",
-            "smsp__issue_active.avg.pct_of_peak_sustained_active",
-            "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
-            "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
-            "smsp__thread_inst_executed_per_inst_executed.ratio", "smsp__inst_executed.sum",
-            "launch__registers_per_thread", "launch__occupancy_limit_shared_mem",
-            "launch__occupancy_limit_registers", "sm__warps_active.avg.pct_of_peak_sustained_active",
-            "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
-            "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
-            "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio",
-            "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio",
-            "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio",
-            "sm__cycles_elapsed.avg.per_second", "launch__grid_size"]
-    m = {w: [v[h.index(w)], u[h.index(w)]] for w in want if w in h}
-    sel_p = os.path.join(DST, f"{R}_ncu_selected_metrics.json")
-    sel = json.load(open(sel_p)) if os.path.exists(sel_p) else {}
-    sel["enum_kernel"] = [m]
-    sel["_enum_kernel_source"] = ("ncu --set full --clock-control none, scripts/prof_c2.py "
-                                  "(C2 PMS solve), enum_kernel launch 16 (level k = 16)")
-    json.dump(sel, open(sel_p, "w"), indent=1)
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    traffic = sum(float(m[k][0]) * scale.get(m[k][1], 1) for k in
-                  ("dram__bytes_read.sum", "dram__bytes_write.sum") if k in m)
-    tp = os.path.join(DST, "traffic.json")
-    t = json.load(open(tp)) if os.path.exists(tp) else {}
-    t["enum_kernel"] = int(traffic)
-    json.dump(t, open(tp, "w"), indent=1)
-    print("enum_kernel traffic", traffic, "bytes")
+CAPTURES = {  # capture file -> (summary key, what)
+    "q_c2": ("queue_kernel_c2", "queue_kernel, C2 fused PMS + MHS walk (scripts/prof_c2.py c2)"),
+    "q_c3": ("queue_kernel_c3", "queue_kernel, C3 fused exhaustive walk (scripts/prof_c2.py c3)"),
+    "q_c4": ("queue_kernel_c4", "queue_kernel, C4 WPMS + MHS (scripts/prof_c2.py c4)"),
+    "count_c5": ("count_kernel_c5", "count_kernel, C5 recount pass on the 8 GiB matrix (scripts/prof_c5.py --full)"),
+    "lscatter_c5": ("lscatter_kernel_c5", "lscatter_kernel, C5 list build (scripts/time_lists.py)"),
+    "lgreedy_c5": ("lgreedy_kernel_c5", "lgreedy_kernel, C5 pick loop (scripts/time_lists.py)"),
+}
+sp = os.path.join(DST, f"{R}_ncu_summary.json")
+summ = json.load(open(sp)) if os.path.exists(sp) else {}
+for cap, (key, what) in CAPTURES.items():
+    rep = os.path.join(SRC, f"{cap}.ncu-rep")
+    if not os.path.exists(rep):
+        continue
+    det = subprocess.run([NCU, "-i", rep, "--page", "details"], capture_output=True, text=True).stdout
+    with open(os.path.join(DST, f"{R}_ncu_{cap}_details.txt"), "w") as f:
+        f.write(f"# ncu --set full --import-source on --clock-control none: {what}\n")
+        f.write(det)
+    src = subprocess.run([NCU, "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+                         capture_output=True, text=True).stdout
+    tmp = os.path.join(SRC, f"{cap}_source.csv")
+    open(tmp, "w").write(src)
+    buf = io.StringIO()
+    old = sys.stdout
+    sys.stdout = buf
+    try:
+        ncu_lines.main(tmp, 40)
+    finally:
+        sys.stdout = old
+    with open(os.path.join(DST, f"{R}_ncu_{cap}_lines.txt"), "w") as f:
+        f.write(f"# per source line: % of warp-stall samples, % of instructions, top stalls -- {what}\n")
+        f.write(buf.getvalue())
+    s = ncu_summary.summary(rep)
+    s["what"] = what
+    summ[key] = s
+    print("capture", cap, "->", key, round(s.get("duration_us", 0), 1), "us")
+json.dump(summ, open(sp, "w"), indent=1)
+
+src_dir = os.path.join(SRC, "onegpu")
+if os.path.isdir(src_dir):
+    dst_dir = os.path.join(DST, f"{R}_onegpu_n2")
+    os.makedirs(dst_dir, exist_ok=True)
+    for fn in os.listdir(src_dir):
+        shutil.copy(os.path.join(src_dir, fn), os.path.join(dst_dir, fn))
+    print("onegpu", sorted(os.listdir(dst_dir)))
 print("done")

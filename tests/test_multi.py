@@ -415,3 +415,142 @@ def test_batch_sharding_allgather_gloo_world2():
         assert np.array_equal(np.asarray(out["assign"], np.uint64).reshape(-1),
                               np.asarray(ref.assign, np.uint64).reshape(-1))
         assert out["decided"] == np.asarray(ref.decided, np.uint64).tolist()
+
+
+# ---- batch split with the heavy-instance rule (§8(e)) --------------------------
+class CpuPmsSession:
+    """Unit-weight PMS of a small batch by brute force, level by level: the
+    colex ranks of level k are cut into chunks of `chunk` ranks and chunk c
+    goes to shard c mod G (gr_exact_level's protocol); level_keys() holds
+    each instance's lowest feasible rank seen (NONE if none).  Stand-in for
+    the GPU session on CPU (small m only)."""
+
+    def __init__(self, cb, chunk=5):
+        import itertools
+
+        self.it = itertools
+        self.inst = [cb.instance(b) for b in range(cb.B)]
+        self.B, self.chunk = cb.B, chunk
+        self.keys = torch.full((self.B,), NONE, dtype=torch.int64)
+        self.res = {"status": np.zeros(self.B, np.int32), "cost": np.zeros(self.B, np.uint64),
+                    "decided": np.zeros(self.B, np.uint64), "assign": np.zeros((self.B, 1), np.uint64)}
+        self.subs = {}
+
+    def _level(self, b, k):
+        if (b, k) not in self.subs:
+            m = self.inst[b][0]
+            self.subs[(b, k)] = sorted(self.it.combinations(range(m), k), key=lambda s: tuple(reversed(s)))
+        return self.subs[(b, k)]
+
+    def _feasible(self, b, x):
+        m, npos, mk, _ = self.inst[b]
+        mk = [int(v) for v in mk[:, 0]]
+        return all(mk[j] & x for j in range(npos)) and not any((mk[j] & ~x) == 0 for j in range(npos, len(mk)))
+
+    def prepare(self):
+        self.active = []
+        for b in range(self.B):
+            if self._feasible(b, 0):
+                self.res["status"][b] = 0  # level 0: the empty set (no positive clause)
+            else:
+                self.active.append(b)
+        return len(self.active)
+
+    def level(self, k, shard, nshard):
+        for b in self.active:
+            subs = self._level(b, k)
+            nch = (len(subs) + self.chunk - 1) // self.chunk
+            for c in range(shard, nch, nshard):
+                for r in range(c * self.chunk, min((c + 1) * self.chunk, len(subs))):
+                    if self._feasible(b, sum(1 << i for i in subs[r])):
+                        self.keys[b] = min(int(self.keys[b]), r)
+                        break
+
+    def level_keys(self):
+        return self.keys
+
+    def finish(self, k):
+        nxt = []
+        for b in self.active:
+            key = int(self.keys[b])
+            if key != NONE:
+                self.res["cost"][b] = k
+                self.res["assign"][b, 0] = sum(1 << i for i in self._level(b, k)[key])
+            elif k >= self.inst[b][0]:
+                self.res["status"][b] = 1  # UNSAT
+            else:
+                nxt.append(b)
+        self.active = nxt
+        self.keys.fill_(NONE)
+        return len(nxt)
+
+
+def _heavy_batch():
+    from paper_2011_08373_b200 import synth
+
+    cb = synth.c2_batch()
+    cb = cb.subset([b for b in range(cb.B) if cb.m[b] <= 11][:40])
+    costs = np.ones(cb.B)
+    costs[3] = 100.0  # heavier than the fair share of two ranks
+    return cb, costs
+
+
+def _heavy_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    from paper_2011_08373_b200.multigpu import solve_batch_split_heavy
+
+    cb, costs = _heavy_batch()
+
+    def solve(sub):  # CPU stand-in for this rank's GPU solve of its whole instances
+        r = oracle.batch("pms", sub)
+        return {"status": r.status, "assign": r.assign, "cost": r.cost, "decided": r.decided}
+
+    def solve_heavy(sub):  # the heavy instances: level rank ranges over both ranks
+        s = CpuPmsSession(sub)
+        run_levels_sharded(s, rank, world, lambda t: dist.all_reduce(t, op=dist.ReduceOp.MIN))
+        return s.res
+
+    def allgather(t):
+        outs = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(outs, t)
+        return outs
+
+    out, heavy = solve_batch_split_heavy(cb, rank, world, costs, solve, solve_heavy, allgather)
+    q.put((rank, heavy, {k: v.tolist() for k, v in out.items()}))
+    dist.destroy_process_group()
+
+
+def test_split_heavy_rule():
+    from paper_2011_08373_b200.multigpu import split_heavy
+
+    assert split_heavy([1, 1, 10, 1], 2) == ([2], [0, 1, 3])
+    assert split_heavy([1, 1, 1, 1], 2) == ([], [0, 1, 2, 3])
+    assert split_heavy([5], 1) == ([], [0])
+
+
+def test_batch_split_heavy_gloo_world2():
+    """Light instances dealt whole + one all-gather, the heavy ones split by
+    level rank ranges over both ranks (all-reduce MIN per level): the
+    single-rank oracle's status, cost and assignment on every rank."""
+    import oracle
+
+    cb, _ = _heavy_batch()
+    ref = oracle.batch("pms", cb)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_heavy_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=180) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, heavy, out in got:
+        assert heavy == [3]
+        assert out["status"] == ref.status.tolist()
+        assert out["cost"] == np.asarray(ref.cost, np.uint64).tolist()
+        assert np.array_equal(np.asarray(out["assign"], np.uint64).reshape(-1),
+                              np.asarray(ref.assign, np.uint64).reshape(-1))
