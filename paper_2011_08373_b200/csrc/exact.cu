@@ -1443,7 +1443,8 @@ __device__ __forceinline__ u64 ring_stamp(const QParams &P, u64 e) {
 // candidates in flight including this level (lane window sizing); depth > 0:
 // an unconfirmed speculation.  false: the weighted key (W << rb | rank) of
 // this level would not fit 63 bits (the caller reports GR_UNSUPPORTED).
-__device__ bool q_make(const QParams &P, int sv, int b, int k, u64 work, int depth, u64 *ti_out) {
+__device__ bool q_make(const QParams &P, int sv, int b, int k, u64 work, int depth, u64 *ti_out,
+                       u64 ti_pre = ~0ull) {
   const WS &w = P.ws[sv];
   const int me = w.meff[b];
   const u64 ck = binom(me, k);
@@ -1464,7 +1465,8 @@ __device__ bool q_make(const QParams &P, int sv, int b, int k, u64 work, int dep
   if (P.fixed_lane) L = P.fixed_lane;
   const u64 nch = (ck + 32 * L - 1) / (32 * L);
   // task records of solve sv live in its own workspace (<= 2 per level)
-  const u64 ti = atomicAdd((unsigned long long *)&w.ctrl->q_tasks, 1ull);
+  // (ti_pre: an index the caller took for a whole warp with one atomic)
+  const u64 ti = ti_pre != ~0ull ? ti_pre : atomicAdd((unsigned long long *)&w.ctrl->q_tasks, 1ull);
   Task *T = w.tasks + ti;
   T->claimed = 0;
   T->pending = nch + (depth ? 1 : 0);
@@ -1483,6 +1485,13 @@ __device__ bool q_make(const QParams &P, int sv, int b, int k, u64 work, int dep
   T->t_exhaust = T->t_commit = T->t_unused = 0;
   *ti_out = ti;
   return true;
+}
+
+// level k of (b, sv) can be a task: its weighted key fits 63 bits (q_make)
+__device__ __forceinline__ bool q_fits(const QParams &P, int sv, int b, int k) {
+  if (!P.weighted[sv]) return true;
+  const WS &w = P.ws[sv];
+  return bitlen(vld(&w.wtot[b])) + bitlen(binom(w.meff[b], k) - 1) <= 63;
 }
 
 // Ring entries of a task with nch warp chunks (single thread): one, plus one
@@ -1638,40 +1647,97 @@ __device__ u64 q_commit_chain(const QParams &P, int sv, u64 ti, u64 *word, u64 *
   }
 }
 
-// one CTA: initialise the ring budget and the work in flight, then publish
-// the first level of every open (instance, solve) and count them (the pack
-// zeroed the queue counters)
-__global__ void __launch_bounds__(1024) queue_seed_kernel(QParams P, long long budget) {
+// The seed, in two launches over all instances (warp-aggregated atomics: a
+// single CTA doing one atomic per instance took 0.3 ms at C4's 2 x 10 000):
+// queue_work_kernel sums the work in flight of each solve (its open
+// instances' first levels) and sets the ring budget; queue_seed_kernel
+// makes and publishes the first level of every open (instance, solve) and
+// counts them (the pack zeroed the queue counters).
+__device__ __forceinline__ bool q_open(const QParams &P, int sv, int b) {
+  return !P.ws[sv].done[b] || (P.fused && !P.ws[1].done[b]);
+}
+__global__ void __launch_bounds__(256) queue_work_kernel(QParams P, long long budget) {
   __shared__ unsigned long long s_work[2];
   if (threadIdx.x < 2) s_work[threadIdx.x] = 0;
-  if (threadIdx.x == 0) P.ws[0].ctrl->q_budget = budget;
+  if (blockIdx.x == 0 && threadIdx.x == 0) P.ws[0].ctrl->q_budget = budget;
   __syncthreads();
   const int ns = P.fused ? 1 : P.nsolve;
-  auto open = [&](int sv, int b) { return !P.ws[sv].done[b] || (P.fused && !P.ws[1].done[b]); };
-  for (int sv = 0; sv < ns; sv++) {  // the work in flight of each solve: its first levels
+  const int B = P.in[0].B;
+  for (int sv = 0; sv < ns; sv++) {
     u64 my = 0;
-    for (int b = threadIdx.x; b < P.in[sv].B; b += blockDim.x)
-      if (open(sv, b)) my += binom(P.ws[sv].meff[b], P.ws[sv].ks[b]);
-    atomicAdd(&s_work[sv], (unsigned long long)my);
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < B; b += gridDim.x * blockDim.x)
+      if (q_open(P, sv, b)) my += binom(P.ws[sv].meff[b], P.ws[sv].ks[b]);
+    for (int o = 16; o; o >>= 1) my += __shfl_xor_sync(0xffffffffu, my, o);
+    if ((threadIdx.x & 31) == 0 && my) atomicAdd(&s_work[sv], (unsigned long long)my);
   }
   __syncthreads();
-  if (threadIdx.x < ns) P.ws[threadIdx.x].ctrl->q_work = s_work[threadIdx.x];
-  for (int sv = 0; sv < ns; sv++)
-    for (int b = threadIdx.x; b < P.in[sv].B; b += blockDim.x) {
-      const WS &w = P.ws[sv];
-      if (!open(sv, b)) continue;
-      u64 ti, e0;
-      if (!q_make(P, sv, b, w.ks[b], s_work[sv], 0, &ti)) {
+  if (threadIdx.x < ns && s_work[threadIdx.x])
+    atomicAdd((unsigned long long *)&P.ws[threadIdx.x].ctrl->q_work, s_work[threadIdx.x]);
+}
+__global__ void __launch_bounds__(256) queue_seed_kernel(QParams P) {
+  const int ns = P.fused ? 1 : P.nsolve;
+  const int B = P.in[0].B;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  Ctrl *c0 = P.ws[0].ctrl;
+  for (int sv = 0; sv < ns; sv++) {
+    const WS &w = P.ws[sv];
+    const u64 work = vld(&w.ctrl->q_work);
+    for (int b0 = blockIdx.x * blockDim.x; b0 < B; b0 += gridDim.x * blockDim.x) {  // warp-uniform
+      const int b = b0 + (int)threadIdx.x;
+      const bool open = b < B && q_open(P, sv, b);
+      const bool fits = open && q_fits(P, sv, b, w.ks[b]);
+      if (open && !fits) {
         work_sub(&w.ctrl->q_work, binom(w.meff[b], w.ks[b]));
         q_unsupported(P, sv, b);
-        continue;
       }
-      atomicAdd(&P.ws[0].ctrl->q_remaining, 1);
+      // task indices and the count of open units: one atomic each per warp
+      const unsigned bal = __ballot_sync(0xffffffffu, fits);
+      if (!bal) continue;
+      u64 base = 0;
+      if (lane == 0) {
+        base = atomicAdd((unsigned long long *)&w.ctrl->q_tasks, (unsigned long long)__popc(bal));
+        atomicAdd(&c0->q_remaining, __popc(bal));
+      }
+      base = __shfl_sync(0xffffffffu, base, 0);
+      const u64 ti = base + (u64)__popc(bal & lt);
+      u64 extra = 0;
+      if (fits) {
+        u64 t2;
+        q_make(P, sv, b, w.ks[b], work, 0, &t2, ti);
+        const u64 nw = (u64)P.nwarps, nch = w.tasks[ti].nchunks;
+        extra = (nch + nw - 1) / nw;
+        extra = (extra > (u64)P.grid ? (u64)P.grid : extra) - 1;
+      }
+      // extra entries from the budget (all of the warp's or none) and the
+      // warp's entries: one atomic each
+      u64 tx = extra;
+      for (int o = 16; o; o >>= 1) tx += __shfl_xor_sync(0xffffffffu, tx, o);
+      int ok = 1;
+      if (lane == 0 && tx) {
+        const long long got = (long long)atomicAdd((unsigned long long *)&c0->q_budget,
+                                                   (unsigned long long)(-(long long)tx));
+        if (got < (long long)tx) {
+          atomicAdd((unsigned long long *)&c0->q_budget, (unsigned long long)tx);
+          ok = 0;
+        }
+      }
+      ok = __shfl_sync(0xffffffffu, ok, 0);
+      const u64 n = fits ? 1 + (ok ? extra : 0) : 0;
+      u64 incl = n;
+      for (int o = 1; o < 32; o <<= 1) {
+        const u64 y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const u64 tot = __shfl_sync(0xffffffffu, incl, 31);
+      u64 eb = 0;
+      if (lane == 0) eb = atomicAdd((unsigned long long *)&c0->q_entries, (unsigned long long)tot);
+      eb = __shfl_sync(0xffffffffu, eb, 0);
       // (no fence: queue_kernel starts after this launch completes, which
       // orders every record before every entry)
-      const u64 n = q_entries(P, w.tasks[ti].nchunks, &e0);
-      for (u64 i = 0; i < n; i++) q_publish(P, ti | ((u64)sv << 38), e0, i);
+      for (u64 i = 0; i < n; i++) q_publish(P, ti | ((u64)sv << 38), eb + incl - n, i);
     }
+  }
 }
 
 // KIND 0: unit-weight solves (MODE 0, or 1 when exhaustive); 1: the fused
@@ -2223,7 +2289,9 @@ int launch_queue_t(QParams &P, int B, cudaStream_t st) {
   // extra ring entries beyond one per open unit and the tickets the grid holds
   const long long budget = (long long)ring_cap(B) - (long long)(P.fused ? 1 : P.nsolve) * B -
                            2ll * grid - 64;
-  GR_LAUNCH("queue_seed_kernel", st, queue_seed_kernel<<<1, 1024, 0, st>>>(P, budget));
+  const int sg = std::max(1, std::min((B + 255) / 256, 4 * gr_sm_count()));
+  GR_LAUNCH("queue_work_kernel", st, queue_work_kernel<<<sg, 256, 0, st>>>(P, budget));
+  GR_LAUNCH("queue_seed_kernel", st, queue_seed_kernel<<<sg, 256, 0, st>>>(P));
   GR_LAUNCH("queue_kernel", st, (queue_kernel<COUNT, NTK, KIND><<<grid, NTK, enum_smem_of<NTK>(), st>>>(P)));
   return GR_OK;
 }
