@@ -1407,6 +1407,7 @@ struct QParams {
   int wpl;         // lane windows per lane (unit | weighted << 16)
   u64 lane_max, lane_max_w, fixed_lane, lane_min;  // lane_min: unit | weighted << 32
   int local_max;   // a next level of at most this many chunks stays with the committing CTA
+  u64 lane_split;  // smallest lane window a small level is split to (a chunk per warp)
 };
 
 // gpu-scope acquire load / acq_rel add (PTX memory model): the completion
@@ -1462,6 +1463,9 @@ __device__ bool q_make(const QParams &P, int sv, int b, int k, u64 work, int dep
   u64 L = work / ((u64)P.lanes * (wpl ? wpl : 2));
   L = L < Lmin ? Lmin : (L > Lmax ? Lmax : L);
   L = 1ull << (63 - __clzll((long long)L));
+  // a small level still gets a chunk per warp of a CTA (down to P.lane_split
+  // candidates per window): its CTA's warps share it instead of waiting
+  while (L > P.lane_split && (ck + 32 * L - 1) / (32 * L) < (u64)P.nwarps) L >>= 1;
   if (P.fixed_lane) L = P.fixed_lane;
   const u64 nch = (ck + 32 * L - 1) / (32 * L);
   // task records of solve sv live in its own workspace (<= 2 per level)
@@ -2329,6 +2333,8 @@ int launch_queue(const gr_batch *in, int nsolve, int fused, const int which[2], 
   P.lane_min = kn.lmin | (kn.lmin_w << 32);
   static const int ql = (int)env_u64("GR_QLOCAL", 1, 0, 1ull << 30);  // (capped at the warps per CTA)
   P.local_max = ql;
+  static const u64 qs = env_u64("GR_QLANE_SPLIT", 1ull << 62, 1, 1ull << 62);  // default: off
+  P.lane_split = qs;
   const bool small = enum_small(in);
   const int kind = fused ? 1 : ((P.weighted[0] || P.weighted[1]) ? 2 : 0);
 #define GR_QLAUNCH(COUNT, NTK)                                              \
