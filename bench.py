@@ -421,9 +421,8 @@ def run_exact(a, cfg, ctx, flush, sub=False):
     torch.cuda.synchronize()
     outs = [gr.DeviceResult.empty(cb.B, cb.W, dev) for _ in range(3)]
 
-    def step_local(dbx, o):
-        gr.solve_pms_mhs(dbx, o[0], o[1])
-        gr.mhs_greedy(dbx, o[2])
+    def step_local(dbx, o):  # PMS + MHS (one launch) and the greedy beside it on a side stream
+        gr.solve_step(dbx, o[0], o[1], o[2])
 
     def step_sharded(dbx, o):  # C3 at N > 1: level rank ranges over the ranks, NCCL MIN per level
         multigpu.solve_pair_sharded(dbx, rank, world, out_pms=o[0], out_mhs=o[1])
@@ -782,8 +781,7 @@ def cpu_baseline(cfg, cb, ctx, flush):
     outs = [gr.DeviceResult.empty(sub.B, sub.W, ctx.dev) for _ in range(3)]
 
     def gstep():
-        gr.solve_pms_mhs(db, outs[0], outs[1])
-        gr.mhs_greedy(db, outs[2])
+        gr.solve_step(db, outs[0], outs[1], outs[2])
 
     gstep()
     gms, _ = time_steps(gstep, 5, ctx, flush, clocks=False)

@@ -355,6 +355,30 @@ def mhs_greedy(db: DeviceBatch, out: Optional[DeviceResult] = None, stream=None)
     return out
 
 
+_greedy_streams = {}
+
+
+def solve_step(db: DeviceBatch, out_pms: Optional[DeviceResult] = None,
+               out_mhs: Optional[DeviceResult] = None, out_greedy: Optional[DeviceResult] = None,
+               stream=None):
+    """One Solve step of a batch: exact PMS + MHS (gr_solve_pms_mhs) and the
+    greedy mhs (gr_mhs_greedy).  The two are independent, so the greedy is
+    launched first on a side stream of the device: its CTAs run beside the
+    pack and the start of the exact solve's persistent grid instead of after
+    it.  ``stream`` (default: the current stream) waits for both."""
+    torch = _torch()
+    dev = db.m.device
+    s1 = stream if stream is not None else torch.cuda.current_stream(dev)
+    g = _greedy_streams.get(str(dev))
+    if g is None:
+        g = _greedy_streams[str(dev)] = torch.cuda.Stream(device=dev)
+    g.wait_stream(s1)  # inputs produced on s1
+    out_greedy = mhs_greedy(db, out_greedy, stream=g)
+    out_pms, out_mhs = solve_pms_mhs(db, out_pms, out_mhs, stream=s1)
+    s1.wait_stream(g)
+    return out_pms, out_mhs, out_greedy
+
+
 def solve(db: DeviceBatch, strategy: int = GR_STRATEGY_MHS, out: Optional[DeviceResult] = None,
           fell_back=None, stream=None) -> DeviceResult:
     """The composite Solve (gr_solve): mhs strategy with MaxSAT fallback, or MaxSAT."""

@@ -55,5 +55,21 @@ for cfg in which:
     h = gr.to_host_many(outs[:2])
     d = float(h[0]["decided"].astype(np.float64).sum() + h[1]["decided"].astype(np.float64).sum())
     gm, _ = timed(lambda: gr.mhs_greedy(db, outs[2]))
+    side = torch.cuda.Stream()
+
+    def both_serial():
+        gr.solve_pms_mhs(db, outs[0], outs[1])
+        gr.mhs_greedy(db, outs[2])
+
+    def both_overlap():  # the greedy on a side stream, launched first
+        cur = torch.cuda.current_stream()
+        side.wait_stream(cur)
+        gr.mhs_greedy(db, outs[2], stream=side)
+        gr.solve_pms_mhs(db, outs[0], outs[1])
+        cur.wait_stream(side)
+
+    sm, _ = timed(both_serial)
+    om, _ = timed(both_overlap)
     print(f"{cfg}: pms+mhs median {med:.3f} ms (min {mn:.3f})  greedy {gm:.3f} ms  "
-          f"decided {d:.4e}  sat {int((h[0]['status'] == 0).sum())}/{cb.B}", flush=True)
+          f"decided {d:.4e}  sat {int((h[0]['status'] == 0).sum())}/{cb.B}  "
+          f"step serial {sm:.3f} overlapped {om:.3f} ms", flush=True)

@@ -1074,3 +1074,20 @@ def test_c5_full_greedy_lists_vs_oracle():
     got = np.array([i for i in range(csr.m) if (int(a[i // 64]) >> (i % 64)) & 1], np.int32)
     assert np.array_equal(got, e["in_S"])
     assert int(r.status.item()) == int(e["status"])
+
+
+@pytest.mark.gpu
+def test_solve_step_side_stream_matches_serial():
+    """gr.solve_step (greedy on a side stream beside the PMS + MHS launch)
+    gives the serial calls' results, on C2 (the bench's step)."""
+    cb = synth.c2_batch()
+    db = gr.DeviceBatch.from_host(cb)
+    p, h = gr.solve_pms_mhs(db)
+    g = gr.mhs_greedy(db)
+    ref = gr.to_host_many([p, h, g])
+    for _ in range(3):
+        outs = gr.solve_step(db)
+        got = gr.to_host_many(list(outs))
+        for a, b in zip(got, ref):
+            for k in ("status", "cost", "assign", "decided"):
+                assert np.array_equal(a[k], b[k]), k
