@@ -1051,6 +1051,28 @@ def test_greedy_lists_weighted_and_golden():
     check_lists(g["m"], [[v - 1 for v in c] for c in g["pos"]], [], w=g["w"])
 
 
+def test_greedy_lists_long_clauses_int16_unaligned():
+    """Tiles whose literals exceed the scatter's shared literal map (clauses of
+    20-60 variables: the thread-per-clause fallback), and int16 ids handed
+    over as a slice that is not 16-byte aligned (the binding copies it)."""
+    rng = random.Random(77)
+    m, n = 3000, 3000
+    pos = [sorted(rng.sample(range(m), rng.randint(20, 60))) for _ in range(n)]
+    neg = [sorted(rng.sample(range(m), 2)) for _ in range(4)]
+    check_lists(m, pos, neg)
+    po, pv = csr_from_lists(pos)
+    no, nv = csr_from_lists(neg)
+    o = oracle.greedy_csr(m, po, pv, no, nv)
+    buf = torch.zeros(pv.size + 1, dtype=torch.int16, device="cuda")
+    buf[1:] = torch.from_numpy(pv.astype(np.int16)).cuda()
+    pv16 = buf[1:]  # data_ptr % 16 == 2
+    assert pv16.data_ptr() % 16 != 0
+    r = gr.mhs_greedy_lists(m, po, pv16, no, nv.astype(np.int16))
+    torch.cuda.synchronize()
+    assert r.picks.cpu().numpy()[: r.n_picks].tolist() == o.picks.tolist()
+    assert int(r.status.item()) == o.status
+
+
 def test_greedy_lists_bad_and_empty():
     po, pv = csr_from_lists([[0, 1], [5]])
     r = gr.mhs_greedy_lists(4, po, pv, np.zeros(1, np.int64), np.zeros(0, np.int32))
