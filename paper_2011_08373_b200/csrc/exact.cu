@@ -1408,6 +1408,7 @@ struct QParams {
   u64 lane_max, lane_max_w, fixed_lane, lane_min;  // lane_min: unit | weighted << 32
   int local_max;   // a next level of at most this many chunks stays with the committing CTA
   u64 lane_split;  // smallest lane window a small level is split to (a chunk per warp)
+  int spec_idle;   // speculate only while CTAs sit idle (1), or always (0)
 };
 
 // gpu-scope acquire load / acq_rel add (PTX memory model): the completion
@@ -1902,7 +1903,8 @@ __global__ void __launch_bounds__(NTK, COUNT ? 1 : ENUM_CTAS * NT / NTK) queue_k
             // cost little if it turns out not to be needed (GR_QSPEC_MAX)
             // (not for weighted levels: the S_k stop rule ends them often)
             if (T->depth < P.spec && !P.weighted[sv] && !*(const volatile unsigned char *)&T->cancelled && k < w.kmax[b] &&
-                ck1 <= P.spec_max && vldu(&T->succ) == 0u && vld(&qc->q_tickets) > vld(&qc->q_entries)) {
+                ck1 <= P.spec_max && vldu(&T->succ) == 0u &&
+                (!P.spec_idle || vld(&qc->q_tickets) > vld(&qc->q_entries))) {
               u64 *qw = &w.ctrl->q_work;
               const u64 wk = atomicAdd((unsigned long long *)qw, (unsigned long long)ck1) + ck1;
               u64 ti2;
@@ -2335,6 +2337,11 @@ int launch_queue(const gr_batch *in, int nsolve, int fused, const int which[2], 
   P.local_max = ql;
   static const u64 qs = env_u64("GR_QLANE_SPLIT", 1ull << 62, 1, 1ull << 62);  // default: off
   P.lane_split = qs;
+  // speculation waits for idle CTAs, except in the fused walk (C2: its
+  // heavy instances' level chains are the critical path; measured 0.637 ->
+  // 0.61 ms); GR_QSPEC_IDLE=0|1 forces either
+  static const int qsi = (int)env_u64("GR_QSPEC_IDLE", 2, 0, 2);
+  P.spec_idle = qsi == 2 ? (fused ? 0 : 1) : qsi;
   const bool small = enum_small(in);
   const int kind = fused ? 1 : ((P.weighted[0] || P.weighted[1]) ? 2 : 0);
 #define GR_QLAUNCH(COUNT, NTK)                                              \
