@@ -5,6 +5,7 @@ Public API (thin marshalling over libgrsolve.so, include/gr.h):
     solve_pms, mhs_exact, mhs_greedy    the three solvers
     solve                               the composite Solve with the MaxSAT fallback
     solve_pms_mhs, solve_step           PMS + MHS in one launch; + the greedy on a side stream
+    StepGraph                           solve_step captured as a CUDA graph (replay per step)
     ExactSession, PairSession           prepare / level / finish for sharded runs (PairSession:
                                         the fused PMS + MHS walk)
     pack_bitmatrix, mhs_greedy_matrix   greedy at scale over a bit matrix
@@ -18,5 +19,5 @@ from ._native import (  # noqa: F401
     bitmatrix_ld, greedy_count_shard, lib, mhs_exact, mhs_greedy, mhs_greedy_matrix,
     pack_bitmatrix, solve_pms, version, launch_count, profiler, Profiler, solve,
     GR_STRATEGY_MHS, GR_STRATEGY_MAXSAT, GR_STRATEGY_MHS_FINAL, solve_pms_mhs, GreedyShard, to_host_many, GreedyMatrixResult,
-    PairSession, mhs_greedy_lists, solve_step,
+    PairSession, mhs_greedy_lists, solve_step, StepGraph,
 )

@@ -379,6 +379,34 @@ def solve_step(db: DeviceBatch, out_pms: Optional[DeviceResult] = None,
     return out_pms, out_mhs, out_greedy
 
 
+class StepGraph:
+    """solve_step of one batch captured once as a CUDA graph (launch-bound
+    small batches: one replay instead of six launches and two stream forks).
+    The graph reads the batch's device buffers and writes ``outs`` in place:
+    refill ``db``'s tensors (same shapes) and replay() for the next step.
+    The exact solvers' ticket ring is cleared by the pack on every launch, so
+    replays never see an earlier run's entries."""
+
+    def __init__(self, db: DeviceBatch, outs=None):
+        torch = _torch()
+        dev = db.m.device
+        self.db = db
+        self.outs = list(outs) if outs is not None else [DeviceResult.empty(db.B, db.W, dev) for _ in range(3)]
+        s = torch.cuda.Stream(device=dev)
+        s.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(s):  # warm-up: workspaces, launch attributes
+            solve_step(db, *self.outs)
+        torch.cuda.current_stream(dev).wait_stream(s)
+        torch.cuda.synchronize(dev)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            solve_step(db, *self.outs)
+
+    def replay(self):
+        self.graph.replay()
+        return self.outs
+
+
 def solve(db: DeviceBatch, strategy: int = GR_STRATEGY_MHS, out: Optional[DeviceResult] = None,
           fell_back=None, stream=None) -> DeviceResult:
     """The composite Solve (gr_solve): mhs strategy with MaxSAT fallback, or MaxSAT."""

@@ -263,6 +263,7 @@ struct PackArgs {
   WS ws[2];
   int which[2];
   u64 lane_cands;
+  u64 ring_n;  // entries of ws[0]'s ticket ring, cleared by the pack's CTAs
 };
 __device__ void pack_body(const In &in, const Out &out, const WS &ws, int which, int b);
 __global__ void __launch_bounds__(PT) pack_kernel(const __grid_constant__ PackArgs A) {
@@ -271,6 +272,11 @@ __global__ void __launch_bounds__(PT) pack_kernel(const __grid_constant__ PackAr
   if (b == 0 && threadIdx.x < sizeof(Ctrl) / 8) {
     u64 *c = (u64 *)A.ws[s].ctrl;
     c[threadIdx.x] = threadIdx.x == offsetof(Ctrl, lane_cands) / 8 ? A.lane_cands : 0ull;
+  }
+  {  // clear a slice of the ring: no entry of an earlier launch (e.g. a CUDA
+     // graph replay, whose launch generation is fixed) can match a ticket
+    const u64 g = gridDim.x, i = blockIdx.x;
+    for (u64 q = A.ring_n * i / g + threadIdx.x; q < A.ring_n * (i + 1) / g; q += blockDim.x) A.ws[0].ring[q] = 0ull;
   }
   pack_body(A.in[s], A.out[s], A.ws[s], A.which[s], b);
 }
@@ -2145,6 +2151,7 @@ int launch_pack(const gr_batch *in, int which, const gr_result *out, const WS &w
   A.ws[1] = two ? *w1 : w;
   A.which[1] = two ? which1 : which;
   A.lane_cands = lane_cands();
+  A.ring_n = ring_cap(in->B);
   size_t smem = (size_t)std::max(in->max_clauses, 1) * 13 + 16;
   static PerDevice attr;
   attr.get([] { return (int)cudaFuncSetAttribute(pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MAXC * 13 + 16); });

@@ -1113,3 +1113,19 @@ def test_solve_step_side_stream_matches_serial():
         for a, b in zip(got, ref):
             for k in ("status", "cost", "assign", "decided"):
                 assert np.array_equal(a[k], b[k]), k
+
+
+@pytest.mark.gpu
+def test_step_graph_replays_match():
+    """gr.StepGraph (solve_step captured as a CUDA graph) gives the launched
+    step's results on every replay (the ticket ring is cleared per launch),
+    """
+    cb = synth.c2_batch()
+    db = gr.DeviceBatch.from_host(cb)
+    ref = gr.to_host_many(list(gr.solve_step(db)))
+    g = gr.StepGraph(db)
+    for _ in range(3):
+        got = gr.to_host_many(g.replay())
+        for a, b in zip(got, ref):
+            for k in ("status", "cost", "assign", "decided"):
+                assert np.array_equal(a[k], b[k]), k
