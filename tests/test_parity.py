@@ -1118,8 +1118,7 @@ def test_solve_step_side_stream_matches_serial():
 @pytest.mark.gpu
 def test_step_graph_replays_match():
     """gr.StepGraph (solve_step captured as a CUDA graph) gives the launched
-    step's results on every replay (the ticket ring is cleared per launch),
-    """
+    step's results on every replay (the ticket ring is cleared per launch)."""
     cb = synth.c2_batch()
     db = gr.DeviceBatch.from_host(cb)
     ref = gr.to_host_many(list(gr.solve_step(db)))
