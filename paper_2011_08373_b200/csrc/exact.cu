@@ -685,10 +685,15 @@ __device__ __forceinline__ bool refuted(int j, M U, int e, const Clauses<M> &c, 
   return refuted_by<M, COUNT>(j, U, e, c, wk) != 0;
 }
 
-template <typename M, int MODE, bool COUNT>
+// TIMED: stop at a sub-block boundary once clock() passes `deadline` (after
+// some progress); *stop = the window position reached (cnt when finished or
+// when nothing more is needed), for the warp to hand the rest to idle lanes
+template <typename M, int MODE, bool COUNT, bool TIMED = false>
 __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const u32 *w, int rb,
                     int prune, Work &wk, const u64 *skj = nullptr, u64 wstar = ~0ull,
-                    int need_p = 1, int need_m = 0, i64 *best_m = nullptr, bool exh = false) {
+                    int need_p = 1, int need_m = 0, i64 *best_m = nullptr, bool exh = false,
+                    unsigned deadline = 0, int *stop = nullptr) {
+  if (TIMED) *stop = (int)cnt;
   // MODE 3 (PMS and MHS of one instance in one walk): the first witness of
   // phi (returned) and of phi+ alone (*best_m), each only while needed
   i64 dummy = GR_KEY_NONE;
@@ -795,6 +800,10 @@ __device__ i64 walk(int k, int me, u64 r_lo, u64 cnt, const Clauses<M> &c, const
   // ---- iterate over sub-blocks in rank order
   for (;;) {
     if (pos >= cnt32) return best;
+    if (TIMED && pos > 0 && (int)(clock() - deadline) > 0) {
+      *stop = pos;
+      return best;
+    }
     const int n = tab_nb()[j * 65 + e];  // C(min(e, R_j), j)
     // An inner node (one with children) first asks whether its whole subtree
     // -- every x = U | S, S a j-subset of [0, e) -- is infeasible: a positive
@@ -1415,6 +1424,8 @@ struct QParams {
   int local_max;   // a next level of at most this many chunks stays with the committing CTA
   u64 lane_split;  // smallest lane window a small level is split to (a chunk per warp)
   int spec_idle;   // speculate only while CTAs sit idle (1), or always (0)
+  unsigned slice;  // fused walk: clock cycles per time slice (0: untimed windows)
+  int split_min;   // smallest share of a window handed to an idle lane
 };
 
 // gpu-scope acquire load / acq_rel add (PTX memory model): the completion
@@ -1754,13 +1765,15 @@ __global__ void __launch_bounds__(256) queue_seed_kernel(QParams P) {
 // KIND 0: unit-weight solves (MODE 0, or 1 when exhaustive); 1: the fused
 // PMS + MHS walk (MODE 3); 2: weighted PMS (MODE 2), possibly with an MHS
 // (MODE 0) in the same launch
-template <typename M, int KIND, bool COUNT>
+template <typename M, int KIND, bool COUNT, bool TIMED = false>
 __device__ __forceinline__ i64 q_walk(const QParams &P, int sv, int need, int k, int me, u64 r_lo,
                                       u64 cnt, const Clauses<M> &cc, const u32 *sw, int rb,
-                                      Work &wk, const u64 *skj, u64 wstar, i64 *key_m) {
+                                      Work &wk, const u64 *skj, u64 wstar, i64 *key_m,
+                                      unsigned deadline = 0, int *stop = nullptr) {
   if (KIND == 1)
-    return walk<M, 3, COUNT>(k, me, r_lo, cnt, cc, sw, rb, P.prune, wk, nullptr, ~0ull, need & 1,
-                                   need >> 1, key_m, P.exhaustive);
+    return walk<M, 3, COUNT, TIMED>(k, me, r_lo, cnt, cc, sw, rb, P.prune, wk, nullptr, ~0ull, need & 1,
+                                    need >> 1, key_m, P.exhaustive, deadline, stop);
+  if (TIMED) *stop = (int)cnt;
   if (KIND == 2 && P.weighted[sv])
     return walk<M, 2, COUNT>(k, me, r_lo, cnt, cc, sw, rb, P.prune, wk, skj, wstar);
   if (P.exhaustive) return walk<M, 1, COUNT>(k, me, r_lo, cnt, cc, sw, rb, P.prune, wk);
@@ -1942,13 +1955,52 @@ __global__ void __launch_bounds__(NTK, COUNT ? 1 : ENUM_CTAS * NT / NTK) queue_k
         const u64 L = s_L, ck = s_ck;
         const int k = s_k, me = w.meff[b], np = w.npr[b], nn = w.nnr[b];
         const u64 r_lo = c * 32 * L + (u64)lane * L;
-        if (need && r_lo < ck) {
+        const bool staged = np + nn <= smc_of<NTK>();
+        F2 *sH = (F2 *)stage;
+        u64 *sP = stage + (size_t)2 * HREC * np;
+        if (KIND == 1 && P.slice && staged && me <= 32) {  // (warp-uniform)
+          // the fused walk in time slices: a lane whose window outlasts a
+          // slice hands the rest out to the warp's idle lanes (every lane
+          // takes part, with or without a window of its own)
+          Clauses<u32> cc{(const u32 *)sP, sH, np, nn};
+          u64 my_lo = r_lo, my_cnt = (need && r_lo < ck) ? ((ck - r_lo) < L ? (ck - r_lo) : L) : 0ull;
+          for (;;) {
+            if (my_cnt) {
+              int stop = 0;
+              i64 km = GR_KEY_NONE;
+              const i64 kp = q_walk<u32, KIND, COUNT, true>(P, sv, need, k, me, my_lo, my_cnt, cc, s_w, 0, wk,
+                                                            s_skj, s_wstar, &km, (unsigned)clock() + P.slice, &stop);
+              key = kp < key ? kp : key;
+              key_m = km < key_m ? km : key_m;
+              my_lo += (u64)stop;
+              my_cnt -= (u64)stop;
+            }
+            const unsigned busy = __ballot_sync(0xffffffffu, my_cnt != 0);
+            if (!busy) break;
+            if (busy == 0xffffffffu) continue;
+            u64 v = my_cnt;  // the busy lane with the most left gives it out
+            int src = lane;
+            for (int o = 16; o; o >>= 1) {
+              const u64 v2 = __shfl_xor_sync(0xffffffffu, v, o);
+              const int s2 = __shfl_xor_sync(0xffffffffu, src, o);
+              if (v2 > v || (v2 == v && s2 < src)) { v = v2; src = s2; }
+            }
+            const u64 dlo = __shfl_sync(0xffffffffu, my_lo, src);
+            const int nidle = 32 - __popc(busy);
+            if (v < (u64)P.split_min * (u64)(nidle + 1)) continue;
+            const u64 part = v / (u64)(nidle + 1);
+            if (lane == src) {
+              my_cnt = part;
+            } else if (!((busy >> lane) & 1u)) {
+              const int ir = __popc(~busy & ((1u << lane) - 1u));
+              my_lo = dlo + (u64)(ir + 1) * part;
+              my_cnt = ir + 1 == nidle ? v - (u64)nidle * part : part;
+            }
+          }
+        } else if (need && r_lo < ck) {
           const u64 cnt = (ck - r_lo) < L ? (ck - r_lo) : L;
           const int64_t lo = P.in[sv].off[b];
-          const bool staged = np + nn <= smc_of<NTK>();
           const int rb = KIND == 2 ? s_rb : 0;
-          F2 *sH = (F2 *)stage;
-          u64 *sP = stage + (size_t)2 * HREC * np;
           if (staged && me <= 32) {
             Clauses<u32> cc{(const u32 *)sP, sH, np, nn};
             key = q_walk<u32, KIND, COUNT>(P, sv, need, k, me, r_lo, cnt, cc, s_w, rb, wk, s_skj, s_wstar, &key_m);
@@ -2349,6 +2401,13 @@ int launch_queue(const gr_batch *in, int nsolve, int fused, const int which[2], 
   // 0.61 ms); GR_QSPEC_IDLE=0|1 forces either
   static const int qsi = (int)env_u64("GR_QSPEC_IDLE", 2, 0, 2);
   P.spec_idle = qsi == 2 ? (fused ? 0 : 1) : qsi;
+  // fused walk time slice: 10^5 clocks (~51 us); the heavy windows of C2's
+  // critical instance are then shared by their warps' idle lanes
+  // (C2 0.61 -> 0.575 ms; 0: untimed)
+  static const unsigned qsl = (unsigned)env_u64("GR_QSLICE", 100000, 0, 1u << 30);
+  static const int qsm = (int)env_u64("GR_QSPLIT_MIN", 256, 1, 1u << 30);
+  P.slice = qsl;
+  P.split_min = qsm;
   const bool small = enum_small(in);
   const int kind = fused ? 1 : ((P.weighted[0] || P.weighted[1]) ? 2 : 0);
 #define GR_QLAUNCH(COUNT, NTK)                                              \
