@@ -1780,6 +1780,51 @@ __device__ __forceinline__ i64 q_walk(const QParams &P, int sv, int need, int k,
   return walk<M, 0, COUNT>(k, me, r_lo, cnt, cc, sw, rb, P.prune, wk);
 }
 
+// The fused walk of one warp chunk in time slices: a lane walks its window
+// for at most P.slice clocks at a time; then the warp ballots and the lane
+// with the most range left hands equal shares of it to the lanes that are
+// done (every lane takes part, with or without a window of its own).
+template <typename M, int KIND, bool COUNT>
+__device__ __forceinline__ void q_sliced(const QParams &P, int sv, int need, int k, int me, u64 r_lo, u64 ck,
+                                         u64 L, const Clauses<M> &cc, const u32 *sw, Work &wk,
+                                         const u64 *skj, u64 wstar, i64 &key, i64 &key_m) {
+  const int lane = threadIdx.x & 31;
+  u64 my_lo = r_lo, my_cnt = (need && r_lo < ck) ? ((ck - r_lo) < L ? (ck - r_lo) : L) : 0ull;
+  for (;;) {
+    if (my_cnt) {
+      int stop = 0;
+      i64 km = GR_KEY_NONE;
+      const i64 kp = q_walk<M, KIND, COUNT, true>(P, sv, need, k, me, my_lo, my_cnt, cc, sw, 0, wk, skj, wstar,
+                                                  &km, (unsigned)clock() + P.slice, &stop);
+      key = kp < key ? kp : key;
+      key_m = km < key_m ? km : key_m;
+      my_lo += (u64)stop;
+      my_cnt -= (u64)stop;
+    }
+    const unsigned busy = __ballot_sync(0xffffffffu, my_cnt != 0);
+    if (!busy) break;
+    if (busy == 0xffffffffu) continue;
+    u64 v = my_cnt;  // the busy lane with the most left gives it out
+    int src = lane;
+    for (int o = 16; o; o >>= 1) {
+      const u64 v2 = __shfl_xor_sync(0xffffffffu, v, o);
+      const int s2 = __shfl_xor_sync(0xffffffffu, src, o);
+      if (v2 > v || (v2 == v && s2 < src)) { v = v2; src = s2; }
+    }
+    const u64 dlo = __shfl_sync(0xffffffffu, my_lo, src);
+    const int nidle = 32 - __popc(busy);
+    if (v < (u64)P.split_min * (u64)(nidle + 1)) continue;
+    const u64 part = v / (u64)(nidle + 1);
+    if (lane == src) {
+      my_cnt = part;
+    } else if (!((busy >> lane) & 1u)) {
+      const int ir = __popc(~busy & ((1u << lane) - 1u));
+      my_lo = dlo + (u64)(ir + 1) * part;
+      my_cnt = ir + 1 == nidle ? v - (u64)nidle * part : part;
+    }
+  }
+}
+
 template <bool COUNT, int NTK, int KIND>
 __global__ void __launch_bounds__(NTK, COUNT ? 1 : ENUM_CTAS * NT / NTK) queue_kernel(const __grid_constant__ QParams P) {
   extern __shared__ u64 cls[];  // tables, then the staged clause records
@@ -1959,44 +2004,10 @@ __global__ void __launch_bounds__(NTK, COUNT ? 1 : ENUM_CTAS * NT / NTK) queue_k
         F2 *sH = (F2 *)stage;
         u64 *sP = stage + (size_t)2 * HREC * np;
         if (KIND == 1 && P.slice && staged && me <= 32) {  // (warp-uniform)
-          // the fused walk in time slices: a lane whose window outlasts a
-          // slice hands the rest out to the warp's idle lanes (every lane
-          // takes part, with or without a window of its own)
+          // (not above 32 variables: C3's exhaustive windows are uniformly
+          // busy, and slicing them measured 2.44 -> 3.49 ms)
           Clauses<u32> cc{(const u32 *)sP, sH, np, nn};
-          u64 my_lo = r_lo, my_cnt = (need && r_lo < ck) ? ((ck - r_lo) < L ? (ck - r_lo) : L) : 0ull;
-          for (;;) {
-            if (my_cnt) {
-              int stop = 0;
-              i64 km = GR_KEY_NONE;
-              const i64 kp = q_walk<u32, KIND, COUNT, true>(P, sv, need, k, me, my_lo, my_cnt, cc, s_w, 0, wk,
-                                                            s_skj, s_wstar, &km, (unsigned)clock() + P.slice, &stop);
-              key = kp < key ? kp : key;
-              key_m = km < key_m ? km : key_m;
-              my_lo += (u64)stop;
-              my_cnt -= (u64)stop;
-            }
-            const unsigned busy = __ballot_sync(0xffffffffu, my_cnt != 0);
-            if (!busy) break;
-            if (busy == 0xffffffffu) continue;
-            u64 v = my_cnt;  // the busy lane with the most left gives it out
-            int src = lane;
-            for (int o = 16; o; o >>= 1) {
-              const u64 v2 = __shfl_xor_sync(0xffffffffu, v, o);
-              const int s2 = __shfl_xor_sync(0xffffffffu, src, o);
-              if (v2 > v || (v2 == v && s2 < src)) { v = v2; src = s2; }
-            }
-            const u64 dlo = __shfl_sync(0xffffffffu, my_lo, src);
-            const int nidle = 32 - __popc(busy);
-            if (v < (u64)P.split_min * (u64)(nidle + 1)) continue;
-            const u64 part = v / (u64)(nidle + 1);
-            if (lane == src) {
-              my_cnt = part;
-            } else if (!((busy >> lane) & 1u)) {
-              const int ir = __popc(~busy & ((1u << lane) - 1u));
-              my_lo = dlo + (u64)(ir + 1) * part;
-              my_cnt = ir + 1 == nidle ? v - (u64)nidle * part : part;
-            }
-          }
+          q_sliced<u32, KIND, COUNT>(P, sv, need, k, me, r_lo, ck, L, cc, s_w, wk, s_skj, s_wstar, key, key_m);
         } else if (need && r_lo < ck) {
           const u64 cnt = (ck - r_lo) < L ? (ck - r_lo) : L;
           const int64_t lo = P.in[sv].off[b];
